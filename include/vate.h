@@ -1,0 +1,194 @@
+/*
+ * vate.h -- C ABI of the B200-native VATE hot path (libvate_b200.so).
+ *
+ * The reference package (slidecard, pure Python + numpy) has no native
+ * interface; its "plugin" boundary is the duck-typed pool protocol plus the
+ * estimator / pipeline functions.  Each entry point below names the reference
+ * symbol it replaces (paths relative to /root/reference/pkg/src/slidecard/).
+ * The Python host layer paper_1812_00282_b200/ binds these through ctypes and
+ * re-exposes the reference's names; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - Every function returns int: VATE_OK (0) or a negative code.  The text of
+ *     the last error on the calling thread is vate_last_error().
+ *     VATE_ECONFIG maps to slidecard's ConfigError (errors.py:9-10),
+ *     VATE_EVALUE to ValueError (precondition violations, e.g. pools.py:215-217),
+ *     VATE_ECUDA / VATE_ENOMEM to RuntimeError / MemoryError.
+ *   - A vate_pool owns one CUDA stream on one device; calls on one pool are
+ *     stream-ordered and must not be made concurrently from several threads.
+ *   - `where` says whether an input pointer is host memory (VATE_HOST) or
+ *     device memory on the pool's device (VATE_DEVICE).  Output pointers are
+ *     host memory unless the name ends in _dev.
+ *   - Plain pointers and sizes only; no torch or numpy types.
+ */
+#ifndef VATE_H
+#define VATE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VATE_ABI_VERSION 1
+
+enum vate_status {
+  VATE_OK = 0,
+  VATE_ECONFIG = -1, /* ConfigError: bad shape / config / snapshot      */
+  VATE_EVALUE = -2,  /* ValueError: precondition violated               */
+  VATE_ECUDA = -3,   /* CUDA runtime failure                            */
+  VATE_ENOMEM = -4   /* device or pinned allocation failed              */
+};
+
+enum vate_where { VATE_HOST = 0, VATE_DEVICE = 1 };
+enum vate_partition { VATE_TAIL = 0, VATE_LOWDEV = 1 }; /* pools.py:27-29 */
+
+typedef struct vate_pool vate_pool;   /* AtPool on one device               */
+typedef struct vate_hosts vate_hosts; /* SlidingHostSet on the same device  */
+
+/* ---- library ---------------------------------------------------------- */
+const char* vate_last_error(void);
+int vate_abi_version(void);
+int vate_device_count(int* n);
+
+/* ---- pool lifecycle: AtPool.__init__ (pools.py:72-100), make_pool
+ *      (pools.py:413-421), _validate_pool_shape (pools.py:57-64) --------- */
+int vate_pool_create(vate_pool** out, int c, int k, int partition, int device);
+int vate_pool_destroy(vate_pool* p);
+/* bact0 (pools.py:96), cell storage bytes (1, 2 or 4), the stream (cudaStream_t) */
+int vate_pool_info(const vate_pool* p, int32_t* bact0, int32_t* cell_bytes, void** stream);
+int vate_pool_sync(vate_pool* p);
+/* cumulative count of kernels this pool (and its registries) launched */
+int vate_pool_launches(const vate_pool* p, uint64_t* n);
+/* per-kernel CUDA-event timing (bench only): kind ids in vate_kernel_kind */
+int vate_pool_set_timing(vate_pool* p, int on);
+int vate_pool_timing(vate_pool* p, int kind, double* total_ms, uint64_t* launches);
+
+/* stream-ordered timestamps for benchmarking: mark(id) records CUDA event id
+ * (0..15) on the pool's stream; elapsed waits for both and returns ms. */
+int vate_mark(vate_pool* p, int id);
+int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
+
+enum vate_kernel_kind {
+  VATE_K_SCAN = 0,     /* record_pairs / set_many scatter      */
+  VATE_K_REGISTRY = 1, /* host-registry update / compaction    */
+  VATE_K_BITMAP = 2,   /* Z_p count + inactive bitmap          */
+  VATE_K_G0 = 3,       /* per-host g0 gather                   */
+  VATE_K_FINAL = 4,    /* estimate LUT + floor compaction      */
+  VATE_K_SWEEP = 5,    /* two-block maintenance                */
+  VATE_K_SORT = 6,     /* active-host radix sort               */
+  VATE_K_OTHER = 7,
+  VATE_K_COUNT = 8
+};
+
+/* ---- ingest ------------------------------------------------------------ */
+/* AtPool.set_many (pools.py:164-178): cells[idx] <- clock of idx's block.
+ * Indices >= 2^c fail with VATE_EVALUE (checked on the host for host input). */
+int vate_set_cells(vate_pool* p, const uint64_t* idx, uint64_t n, int where);
+
+/* record_pairs (estimator.py:102-104) = pair_cells (:96-99) + set_many, fused.
+ * g, cell_stream, group_stream are EstimatorConfig's (estimator.py:32-61).
+ * If hosts != NULL the distinct aips are also registered as last seen in
+ * slice t (SlidingHostSet.update, pipeline.py:50-52, called from
+ * Pipeline.process_slice pipeline.py:146-147). */
+int vate_scan_pairs(vate_pool* p, uint64_t g, uint64_t cell_stream, uint64_t group_stream,
+                    const uint64_t* aips, const uint64_t* bips, uint64_t n, int where,
+                    vate_hosts* hosts, int64_t t);
+/* Same, on packed 8-byte records {uint32 aip, uint32 bip}. */
+int vate_scan_packed(vate_pool* p, uint64_t g, uint64_t cell_stream, uint64_t group_stream,
+                     const uint32_t* pairs, uint64_t n, int where, vate_hosts* hosts,
+                     int64_t t);
+/* pair_cells (estimator.py:96-99) without touching the pool; c <= 32. */
+int vate_pair_cells(vate_pool* p, uint64_t g, int c, uint64_t cell_stream,
+                    uint64_t group_stream, const uint64_t* aips, const uint64_t* bips,
+                    uint64_t n, int where, uint64_t* out_cells);
+
+/* host_cells (estimator.py:107-111): all g cells of each host, host-major;
+ * out_cells holds n*g values. */
+int vate_host_cells(vate_pool* p, uint64_t g, int c, uint64_t cell_stream, const uint64_t* aips,
+                    uint64_t n, int where, uint64_t* out_cells);
+
+/* ---- maintenance: AtPool.advance_slice (pools.py:221-249) -------------- */
+/* blocks[0] = block now at clock 0, blocks[1] = block at clock k;
+ * maintained = cells visited, cleared = cells turned inactive. */
+int vate_advance(vate_pool* p, int32_t blocks[2], uint64_t* maintained, uint64_t* cleared);
+/* Stream-ordered variant: enqueue now, collect with vate_advance_result. */
+int vate_advance_async(vate_pool* p);
+int vate_advance_result(vate_pool* p, int32_t blocks[2], uint64_t* maintained,
+                        uint64_t* cleared);
+
+/* ---- queries ----------------------------------------------------------- */
+/* AtPool.count_inactive (pools.py:195-210); 1 <= k_prime <= k. */
+int vate_count_inactive(vate_pool* p, int k_prime, uint64_t* out);
+/* AtPool.inactive_mask (pools.py:187-193): out[i] = 1 if idx[i] inactive. */
+int vate_inactive_mask(vate_pool* p, const uint64_t* idx, uint64_t n, int k_prime,
+                       uint8_t* out, int where);
+/* PackedArray.get through AtPool.cells (bitpack.py:88-95). */
+int vate_get_cells(vate_pool* p, const uint64_t* idx, uint64_t n, uint32_t* out, int where);
+/* inactive_virtual_counts (estimator.py:114-123): g0 per host. */
+int vate_host_g0(vate_pool* p, uint64_t g, uint64_t cell_stream, const uint64_t* aips,
+                 uint64_t n, int k_prime, int32_t* g0, int where);
+
+/* ---- float path: reports_from_counts (estimator.py:138-162) ------------
+ * log_zv[j] = np.log(j == 0 ? 1/(2g) : j/g) for j in [0, g], computed by the
+ * host with numpy so the device reproduces numpy's logarithm bit for bit;
+ * set once per g.  log_zp is np.log of the clamped pool fraction. */
+int vate_set_log_table(vate_pool* p, uint64_t g, const double* log_zv);
+int vate_reports_from_counts(vate_pool* p, uint64_t g, const int32_t* g0, uint64_t n,
+                             uint64_t pool_inactive, double log_zp, double* est,
+                             double* z_v, uint8_t* saturated);
+
+/* ---- fused per-slice estimate: Pipeline._estimate (pipeline.py:120-138) -
+ * begin: sorted active hosts (SlidingHostSet.active, pipeline.py:54-58),
+ *        pool_inactive (count_inactive) and g0 of every active host are
+ *        computed on the device; returns once the host count and P are known
+ *        (the g0 gather may still be running).  nhosts == 0 means no report
+ *        and no P (pipeline.py:122-123).
+ * finish: estimates, z_v, saturation and the `estimate >= floor` filter
+ *        (pipeline.py:136-137) on the device; kept rows land in the host
+ *        arrays (capacity cap) in ascending host order. */
+int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                        int64_t t, int k_prime, uint64_t* nhosts, uint64_t* pool_inactive);
+/* begin for an explicit host list (ascending, no duplicates) instead of the
+ * registry's active set -- the aip-range split of a multi-GPU estimate. */
+int vate_estimate_begin_hosts(vate_pool* p, const uint64_t* hosts, uint64_t n, int where,
+                              uint64_t g, uint64_t cell_stream, int k_prime,
+                              uint64_t* pool_inactive);
+int vate_estimate_finish(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
+                         double floor, uint64_t* out_host, double* out_est,
+                         double* out_zv, uint8_t* out_sat, uint64_t cap, uint64_t* nkept);
+
+/* ---- snapshots: AtPool.snapshot_bytes / load (pools.py:261-298) -------- */
+int vate_snapshot_size(const vate_pool* p, uint64_t* nbytes);
+int vate_snapshot(vate_pool* p, uint8_t* buf, uint64_t cap, uint64_t* len);
+/* Restores payload + bact0 into a pool of the snapshot's (c, k, partition). */
+int vate_load(vate_pool* p, const uint8_t* buf, uint64_t len);
+
+/* ---- host registry: SlidingHostSet (pipeline.py:43-64) ------------------ */
+int vate_hosts_create(vate_hosts** out, vate_pool* p, int k);
+int vate_hosts_destroy(vate_hosts* h);
+int vate_hosts_update(vate_hosts* h, const uint64_t* aips, uint64_t n, int64_t t, int where);
+/* sorted hosts with last-seen > t - k_prime; *n = count (may exceed cap) */
+int vate_hosts_active(vate_hosts* h, int64_t t, int k_prime, uint64_t* out, uint64_t cap,
+                      uint64_t* n);
+/* drop hosts last seen at or before t - k (SlidingHostSet.prune) */
+int vate_hosts_prune(vate_hosts* h, int64_t t);
+int vate_hosts_size(vate_hosts* h, uint64_t* n);
+
+/* ---- multi-GPU replica merge ---------------------------
+ * Replicas share bact0 and hold identical cells at slice start, so a cell
+ * differs only if some replica set it this slice (value == its block clock).
+ * dirty: 1 bit per cell, words of 32 cells, (2^c + 31) / 32 uint32 words.
+ * merge: OR of nranks such bitmaps laid end to end; dirty cells take their
+ * block clock.  Both pointers are device memory (e.g. NCCL buffers). */
+int vate_dirty_bitmap(vate_pool* p, uint32_t* bitmap_dev);
+int vate_merge_dirty(vate_pool* p, const uint32_t* bitmaps_dev, int nranks);
+
+/* ---- synthetic traffic (bench / tests): oracle.synthetic_slice ---------- */
+int vate_synth_packets(vate_pool* p, int64_t t, uint64_t n, uint64_t hosts,
+                       uint64_t base_aip, uint64_t trace_seed, uint32_t* pairs_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VATE_H */

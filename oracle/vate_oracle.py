@@ -231,14 +231,24 @@ class OraclePool:
                               self.nblocks, self.sentinel, k_prime)
 
     def inactive_bits(self, k_prime: int) -> np.ndarray:
-        """Whole-pool inactive predicate, one bool per cell."""
+        """Whole-pool inactive predicate, one bool per cell (block by block)."""
         self._check_width(k_prime)
-        return self._inactive(self.cells, self.cell_clocks(), self.nblocks,
-                              self.sentinel, k_prime)
+        out = np.empty(self.size, dtype=bool)
+        for b, act in enumerate(self.clock(np.arange(self.nblocks)).tolist()):
+            lo, hi = self.block_range(b)
+            out[lo:hi] = self._inactive(self.cells[lo:hi], act, self.nblocks,
+                                        self.sentinel, k_prime)
+        return out
 
     def count_inactive(self, k_prime: int) -> int:
         """Pool-wide inactive count P (pools.py:195-210), by a full pass."""
-        return int(self.inactive_bits(k_prime).sum())
+        self._check_width(k_prime)
+        total = 0
+        for b, act in enumerate(self.clock(np.arange(self.nblocks)).tolist()):
+            lo, hi = self.block_range(b)
+            total += int(self._inactive(self.cells[lo:hi], act, self.nblocks,
+                                        self.sentinel, k_prime).sum())
+        return total
 
     # maintenance ------------------------------------------------------------
     def advance(self):
@@ -295,14 +305,21 @@ class OraclePool:
 
 
 def pack_cells(cells: np.ndarray, width: int) -> bytes:
-    """w-bit cells, LSB-first, into little-endian u64 words, zero pad (bitpack.py:26-78)."""
+    """w-bit cells, LSB-first, into little-endian u64 words, zero pad (bitpack.py:26-78).
+
+    Works in chunks of 2^20 cells (a whole number of u64 words) to bound memory.
+    """
     n = len(cells)
-    bits = ((cells.astype(np.uint64)[:, None] >> np.arange(width, dtype=np.uint64))
-            & np.uint64(1)).astype(np.uint8).reshape(-1)
     nwords = -(-n * width // 64)
     out = np.zeros(nwords * 8, dtype=np.uint8)
-    packed = np.packbits(bits, bitorder="little")
-    out[:len(packed)] = packed
+    chunk = 1 << 20
+    shifts = np.arange(width, dtype=np.uint32)
+    for lo in range(0, n, chunk):
+        part = cells[lo:lo + chunk].astype(np.uint32)
+        bits = ((part[:, None] >> shifts) & np.uint32(1)).astype(np.uint8).reshape(-1)
+        packed = np.packbits(bits, bitorder="little")
+        start = lo * width // 8
+        out[start:start + len(packed)] = packed
     return out.tobytes()
 
 

@@ -1,0 +1,426 @@
+// vate_estimate.cu -- the per-host estimate: g0 gather over the inactive
+// bitmap, the float path, the floor filter, and the fused per-slice driver.
+//
+// Reference: estimator.py:107-181 (host_cells, inactive_virtual_counts,
+// reports_from_counts, estimate_hosts), pipeline.py:120-138 (_estimate).
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "vate_internal.cuh"
+
+namespace vate {
+
+int build_bitmap(vate_pool* p, int k_prime);   // vate_pool.cu
+int check_width(vate_pool* p, int k_prime);    // vate_pool.cu
+
+// g0[h] = #{ j < g : bitmap bit of H(aip_h, j) is set }  (estimator.py:107-123)
+//
+// LPH lanes cooperate on one host.  Keys of one host differ only in the low
+// word, so ((aip<<32)|j)*phi + cs = base + j*phi with
+// base = ((uint32(aip) * uint32(phi)) << 32) + cs, and each lane walks its
+// slots with one 64-bit add.  The bitmap (2^c/8 bytes) stays L2-resident.
+template <int LPH>
+__global__ void __launch_bounds__(kThreads) k_g0(const uint64_t* __restrict__ hosts, uint64_t n,
+                                                 const uint32_t* __restrict__ bitmap,
+                                                 HashParams H, int32_t* __restrict__ g0) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & (LPH - 1);
+  const unsigned gmask = LPH == 32 ? 0xffffffffu : (((1u << LPH) - 1u) << (lane & ~(LPH - 1)));
+  const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / LPH;
+  const uint64_t step = (uint64_t)LPH * kPhi;
+  const uint64_t g = H.g;
+  for (uint64_t h = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPH; h < n; h += groups) {
+    const uint64_t aip = hosts[h];
+    uint64_t x = ((uint64_t)((uint32_t)aip * (uint32_t)kPhi) << 32) + H.cs + (uint64_t)sub * kPhi;
+    uint32_t cnt = 0;
+    uint64_t j = sub;
+    // four independent gathers in flight per lane
+    for (; j + 3 * LPH < g; j += 4 * LPH) {
+      const uint64_t c0 = mix64(x) & H.cmask;
+      const uint64_t c1 = mix64(x + step) & H.cmask;
+      const uint64_t c2 = mix64(x + 2 * step) & H.cmask;
+      const uint64_t c3 = mix64(x + 3 * step) & H.cmask;
+      const uint32_t w0 = __ldg(bitmap + (c0 >> 5));
+      const uint32_t w1 = __ldg(bitmap + (c1 >> 5));
+      const uint32_t w2 = __ldg(bitmap + (c2 >> 5));
+      const uint32_t w3 = __ldg(bitmap + (c3 >> 5));
+      cnt += ((w0 >> (c0 & 31)) & 1u) + ((w1 >> (c1 & 31)) & 1u) + ((w2 >> (c2 & 31)) & 1u) +
+             ((w3 >> (c3 & 31)) & 1u);
+      x += 4 * step;
+    }
+    for (; j < g; j += LPH) {
+      const uint64_t c0 = mix64(x) & H.cmask;
+      cnt += (__ldg(bitmap + (c0 >> 5)) >> (c0 & 31)) & 1u;
+      x += step;
+    }
+#pragma unroll
+    for (int o = LPH / 2; o; o >>= 1) cnt += __shfl_xor_sync(gmask, cnt, o);
+    if (sub == 0) g0[h] = (int32_t)cnt;
+  }
+}
+
+static int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H,
+                     int32_t* g0_dev) {
+  // lanes per host: the next power of two >= g, at most a warp
+  int lph = 1;
+  while (lph < 32 && (uint64_t)lph < H.g) lph <<= 1;
+  const uint64_t threads = n * (uint64_t)lph;
+  const uint32_t grid = grid_for(threads, kThreads, 148u * 64u);
+  const uint32_t* bm = p->bitmap.as<const uint32_t>();
+  switch (lph) {
+    case 1: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<1>, hosts_dev, n, bm, H, g0_dev); break;
+    case 2: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<2>, hosts_dev, n, bm, H, g0_dev); break;
+    case 4: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<4>, hosts_dev, n, bm, H, g0_dev); break;
+    case 8: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<8>, hosts_dev, n, bm, H, g0_dev); break;
+    case 16: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<16>, hosts_dev, n, bm, H, g0_dev); break;
+    default: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<32>, hosts_dev, n, bm, H, g0_dev); break;
+  }
+  return VATE_OK;
+}
+
+// The single float path (estimator.py:138-162), per host:
+//   z_v = g0/g;  raw = g * (log_zp - log_zv[g0]);  est = max(raw, 0)
+//   saturated = g0 == 0 | raw < 0 | P == 0
+// log_zv / log_zp come from numpy on the host (see vate.h), and the
+// subtraction and product are single IEEE roundings with no contraction, so
+// the results are bit-identical to the reference's numpy expression.
+struct FloatPath {
+  const double* lzv;
+  double lzp;
+  double gd;
+  int pool_empty;  // P == 0
+  double floor;    // keep iff floor <= 0 or est >= floor (pipeline.py:136-137)
+};
+
+__device__ __forceinline__ void float_path(int32_t g0, const FloatPath& F, double* est, double* zv,
+                                           uint8_t* sat, bool* keep) {
+  const double raw = __dmul_rn(F.gd, __dsub_rn(F.lzp, F.lzv[g0]));
+  *zv = __ddiv_rn((double)g0, F.gd);
+  *sat = (g0 == 0) | (raw < 0.0) | F.pool_empty;
+  *est = raw < 0.0 ? 0.0 : raw;
+  *keep = !(F.floor > 0.0) || *est >= F.floor;
+}
+
+constexpr int kFinTile = 1024;  // hosts per CTA in the filter passes (256 threads x 4)
+
+// Pass 1: per-tile kept counts (only when a floor is set).
+__global__ void __launch_bounds__(256) k_final_count(const int32_t* __restrict__ g0, uint64_t n,
+                                                     FloatPath F, unsigned* __restrict__ tile_cnt) {
+  __shared__ unsigned s;
+  if (threadIdx.x == 0) s = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kFinTile + threadIdx.x * 4;
+  unsigned local = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (base + q < n) {
+      double e, z;
+      uint8_t st;
+      bool keep;
+      float_path(g0[base + q], F, &e, &z, &st, &keep);
+      local += keep;
+    }
+  }
+  local = __reduce_add_sync(0xffffffffu, local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(&s, local);
+  __syncthreads();
+  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = s;
+}
+
+// Pass 2: exclusive scan of tile counts in one CTA; total -> *nsel.
+__global__ void __launch_bounds__(1024) k_final_scan(unsigned* __restrict__ tile_cnt, uint64_t ntiles,
+                                                     unsigned long long* nsel) {
+  __shared__ unsigned long long warp_tot[32];
+  __shared__ unsigned long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint64_t base = 0; base < ntiles; base += blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    const unsigned long long v = i < ntiles ? tile_cnt[i] : 0;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long w = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long u = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += u;
+      }
+      warp_tot[lane] = w;  // inclusive prefix over warps
+    }
+    __syncthreads();
+    const unsigned long long before = (wid ? warp_tot[wid - 1] : 0) + carry;
+    if (i < ntiles) tile_cnt[i] = (unsigned)(before + incl - v);
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = before + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *nsel = carry;
+}
+
+// Pass 3 (or the only pass without a floor): values for every host; kept
+// rows are written in host order at their stable compacted position.
+__global__ void __launch_bounds__(256) k_final_write(const uint64_t* __restrict__ hosts,
+                                                     const int32_t* __restrict__ g0, uint64_t n,
+                                                     FloatPath F, const unsigned* __restrict__ tile_off,
+                                                     uint64_t* __restrict__ out_host,
+                                                     double* __restrict__ out_est,
+                                                     double* __restrict__ out_zv,
+                                                     uint8_t* __restrict__ out_sat) {
+  __shared__ unsigned warp_tot[8];
+  const uint64_t base = (uint64_t)blockIdx.x * kFinTile + threadIdx.x * 4;
+  double e[4], z[4];
+  uint8_t st[4];
+  bool keep[4];
+  unsigned mine = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    keep[q] = false;
+    if (base + q < n) {
+      float_path(g0[base + q], F, &e[q], &z[q], &st[q], &keep[q]);
+      mine += keep[q];
+    }
+  }
+  uint64_t pos = base;
+  if (tile_off) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    unsigned before = 0;
+    for (int w = 0; w < wid; ++w) before += warp_tot[w];
+    pos = (uint64_t)tile_off[blockIdx.x] + before + incl - mine;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (keep[q]) {
+      out_host[pos] = hosts ? hosts[base + q] : 0;
+      out_est[pos] = e[q];
+      out_zv[pos] = z[q];
+      out_sat[pos] = st[q];
+      ++pos;
+    }
+  }
+}
+
+static int run_float_path(vate_pool* p, const uint64_t* hosts_dev, const int32_t* g0_dev,
+                          uint64_t n, FloatPath F, uint64_t* nkept) {
+  const uint64_t ntiles = (n + kFinTile - 1) / kFinTile;
+  int rc;
+  for (DevBuf* b : {&p->host_out, &p->est_out, &p->zv_out}) {
+    rc = b->ensure(n * 8 + 8);
+    if (rc) return rc;
+  }
+  rc = p->sat_out.ensure(n + 8);
+  if (rc) return rc;
+  const unsigned* tile_off = nullptr;
+  if (F.floor > 0.0) {
+    rc = p->flags.ensure(ntiles * 4 + 16);
+    if (rc) return rc;
+    VATE_LAUNCH(p, VATE_K_FINAL, (uint32_t)ntiles, 256, 0, k_final_count, g0_dev, n, F,
+                p->flags.as<unsigned>());
+    VATE_LAUNCH(p, VATE_K_FINAL, 1, 1024, 0, k_final_scan, p->flags.as<unsigned>(), ntiles,
+                p->d_ctr + C_NSEL);
+    VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_NSEL, p->d_ctr + C_NSEL, 8, cudaMemcpyDeviceToHost,
+                              p->stream));
+    tile_off = p->flags.as<const unsigned>();
+  }
+  VATE_LAUNCH(p, VATE_K_FINAL, (uint32_t)ntiles, 256, 0, k_final_write, hosts_dev, g0_dev, n, F,
+              tile_off, p->host_out.as<uint64_t>(), p->est_out.as<double>(), p->zv_out.as<double>(),
+              p->sat_out.as<uint8_t>());
+  if (F.floor > 0.0) {
+    rc = sync_small(p);
+    if (rc) return rc;
+    *nkept = p->h_ctr[C_NSEL];
+  } else {
+    *nkept = n;
+  }
+  return VATE_OK;
+}
+
+static int copy_rows_out(vate_pool* p, uint64_t m, bool with_hosts, uint64_t* out_host,
+                         double* out_est, double* out_zv, uint8_t* out_sat) {
+  if (m) {
+    if (with_hosts && out_host)
+      VATE_CUDA(cudaMemcpyAsync(out_host, p->host_out.ptr, m * 8, cudaMemcpyDeviceToHost, p->stream));
+    if (out_est)
+      VATE_CUDA(cudaMemcpyAsync(out_est, p->est_out.ptr, m * 8, cudaMemcpyDeviceToHost, p->stream));
+    if (out_zv)
+      VATE_CUDA(cudaMemcpyAsync(out_zv, p->zv_out.ptr, m * 8, cudaMemcpyDeviceToHost, p->stream));
+    if (out_sat)
+      VATE_CUDA(cudaMemcpyAsync(out_sat, p->sat_out.ptr, m, cudaMemcpyDeviceToHost, p->stream));
+  }
+  return sync_small(p);
+}
+
+static int float_params(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
+                        double floor, FloatPath* F) {
+  if (p->lzv_g != g || !p->lzv.ptr)
+    return set_error(VATE_EVALUE, "log table not set for g=" + std::to_string(g));
+  F->lzv = p->lzv.as<const double>();
+  F->lzp = log_zp;
+  F->gd = (double)g;
+  F->pool_empty = pool_inactive == 0;
+  F->floor = floor;
+  return VATE_OK;
+}
+
+}  // namespace vate
+
+using namespace vate;
+
+extern "C" {
+
+int vate_host_g0(vate_pool* p, uint64_t g, uint64_t cell_stream, const uint64_t* aips, uint64_t n,
+                 int k_prime, int32_t* g0, int where) {
+  int rc = enter(p);
+  if (rc) return rc;
+  rc = check_width(p, k_prime);
+  if (rc || n == 0) return rc;
+  if (g < 1 || g > p->L.size) return set_error(VATE_ECONFIG, "g must be in [1, 2^c]");
+  rc = build_bitmap(p, k_prime);
+  if (rc) return rc;
+  const void* d_aips;
+  rc = stage_in(p, p->in_a, aips, n * 8, where, &d_aips);
+  if (rc) return rc;
+  rc = p->g0.ensure(n * 4 + 4);
+  if (rc) return rc;
+  rc = launch_g0(p, (const uint64_t*)d_aips, n, make_hash(g, p->c, cell_stream, 0), p->g0.as<int32_t>());
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(g0, p->g0.ptr, n * 4, cudaMemcpyDeviceToHost, p->stream));
+  return sync_small(p);
+}
+
+int vate_set_log_table(vate_pool* p, uint64_t g, const double* log_zv) {
+  int rc = enter(p);
+  if (rc) return rc;
+  rc = p->lzv.ensure((g + 1) * 8);
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(p->lzv.ptr, log_zv, (g + 1) * 8, cudaMemcpyHostToDevice, p->stream));
+  rc = sync_small(p);
+  if (rc) return rc;
+  p->lzv_g = g;
+  return VATE_OK;
+}
+
+int vate_reports_from_counts(vate_pool* p, uint64_t g, const int32_t* g0, uint64_t n,
+                             uint64_t pool_inactive, double log_zp, double* est, double* z_v,
+                             uint8_t* saturated) {
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  for (uint64_t i = 0; i < n; ++i)
+    if (g0[i] < 0 || (uint64_t)g0[i] > g)
+      return set_error(VATE_EVALUE, "g0=" + std::to_string(g0[i]) + " outside [0, " + std::to_string(g) + "]");
+  FloatPath F;
+  rc = float_params(p, g, pool_inactive, log_zp, 0.0, &F);
+  if (rc) return rc;
+  const void* d_g0;
+  rc = stage_in(p, p->in_a, g0, n * 4, VATE_HOST, &d_g0);
+  if (rc) return rc;
+  uint64_t kept = 0;
+  rc = run_float_path(p, nullptr, (const int32_t*)d_g0, n, F, &kept);
+  if (rc) return rc;
+  return copy_rows_out(p, n, false, nullptr, est, z_v, saturated);
+}
+
+int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                        int64_t t, int k_prime, uint64_t* nhosts, uint64_t* pool_inactive) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (!hosts || hosts->pool != p) return set_error(VATE_EVALUE, "registry does not belong to pool");
+  rc = check_width(p, k_prime);
+  if (rc) return rc;
+  if (g < 1 || g > p->L.size) return set_error(VATE_ECONFIG, "g must be in [1, 2^c]");
+  p->est_n = 0;
+  uint64_t* keys = nullptr;
+  uint64_t n = 0;
+  rc = hosts_compact_active(hosts, t, k_prime, &keys, &n);  // pipeline.py:121
+  if (rc) return rc;
+  *nhosts = n;
+  *pool_inactive = 0;
+  if (n == 0) return VATE_OK;  // no hosts: no P, no reports (pipeline.py:122-123)
+  rc = build_bitmap(p, k_prime);  // P -> h_ctr[C_P], bitmap for the gather
+  if (rc) return rc;
+  VATE_CUDA(cudaEventRecord(p->ev_small, p->stream));
+  rc = p->g0.ensure(n * 4 + 4);
+  if (rc) return rc;
+  rc = launch_g0(p, keys, n, make_hash(g, p->c, cell_stream, 0), p->g0.as<int32_t>());
+  if (rc) return rc;
+  VATE_CUDA(cudaEventSynchronize(p->ev_small));  // P is known; the gather keeps running
+  *pool_inactive = p->h_ctr[C_P];
+  p->est_n = n;
+  p->est_kp = k_prime;
+  p->est_g = g;
+  return VATE_OK;
+}
+
+int vate_estimate_begin_hosts(vate_pool* p, const uint64_t* hosts, uint64_t n, int where,
+                              uint64_t g, uint64_t cell_stream, int k_prime,
+                              uint64_t* pool_inactive) {
+  int rc = enter(p);
+  if (rc) return rc;
+  rc = check_width(p, k_prime);
+  if (rc) return rc;
+  if (g < 1 || g > p->L.size) return set_error(VATE_ECONFIG, "g must be in [1, 2^c]");
+  p->est_n = 0;
+  *pool_inactive = 0;
+  rc = p->hosts_sorted.ensure(n * 8 + 8);
+  if (rc) return rc;
+  if (n) {
+    if (where == VATE_DEVICE)
+      VATE_CUDA(cudaMemcpyAsync(p->hosts_sorted.ptr, hosts, n * 8, cudaMemcpyDeviceToDevice, p->stream));
+    else
+      VATE_CUDA(cudaMemcpyAsync(p->hosts_sorted.ptr, hosts, n * 8, cudaMemcpyHostToDevice, p->stream));
+  }
+  rc = build_bitmap(p, k_prime);
+  if (rc) return rc;
+  VATE_CUDA(cudaEventRecord(p->ev_small, p->stream));
+  if (n) {
+    rc = p->g0.ensure(n * 4 + 4);
+    if (rc) return rc;
+    rc = launch_g0(p, p->hosts_sorted.as<uint64_t>(), n, make_hash(g, p->c, cell_stream, 0),
+                   p->g0.as<int32_t>());
+    if (rc) return rc;
+  }
+  VATE_CUDA(cudaEventSynchronize(p->ev_small));
+  *pool_inactive = p->h_ctr[C_P];
+  p->est_n = n;
+  p->est_kp = k_prime;
+  p->est_g = g;
+  return VATE_OK;
+}
+
+int vate_estimate_finish(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
+                         double floor, uint64_t* out_host, double* out_est, double* out_zv,
+                         uint8_t* out_sat, uint64_t cap, uint64_t* nkept) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (g != p->est_g) return set_error(VATE_EVALUE, "estimate_finish: g differs from begin");
+  const uint64_t n = p->est_n;
+  *nkept = 0;
+  if (n == 0) return VATE_OK;
+  FloatPath F;
+  rc = float_params(p, g, pool_inactive, log_zp, floor, &F);
+  if (rc) return rc;
+  uint64_t kept = 0;
+  rc = run_float_path(p, p->hosts_sorted.as<const uint64_t>(), p->g0.as<const int32_t>(), n, F, &kept);
+  if (rc) return rc;
+  *nkept = kept;
+  p->est_n = 0;
+  return copy_rows_out(p, kept < cap ? kept : cap, true, out_host, out_est, out_zv, out_sat);
+}
+
+}  // extern "C"

@@ -1,0 +1,381 @@
+// vate_hosts.cu -- the host registry on the device (SlidingHostSet,
+// pipeline.py:43-64): last-seen slice per host, the sorted active set of a
+// window, and pruning.
+//
+// Layout: open addressing with linear probing over 16-byte {key, last}
+// entries (one sector per probe), kept at load factor <= 1/2 by growing at
+// every drain.  Inserts that exceed the probe limit are parked in an
+// overflow list and re-inserted at the next drain, which every read of the
+// registry performs first, so no update is ever lost.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <string>
+
+#include "vate_internal.cuh"
+#include "vate_registry.cuh"
+
+namespace vate {
+
+enum HCtr { H_COUNT = 0, H_OVF = 1, H_SPECIAL = 2, H_MAXKEY = 3, H_NOUT = 4, H_N = 8 };
+
+RegRef make_ref(const vate_hosts* h, const DevBuf& table, uint64_t cap) {
+  RegRef R{};
+  R.table = table.as<RegEntry>();
+  R.mask = cap - 1;
+  R.count = h->d_count + H_COUNT;
+  R.ovf = h->ovf.as<RegEntry>();
+  R.ovf_n = h->d_count + H_OVF;
+  R.ovf_cap = h->ovf_cap;
+  R.special = reinterpret_cast<unsigned int*>(h->d_count + H_SPECIAL);
+  R.enabled = 1;
+  return R;
+}
+
+__global__ void k_insert_keys(const uint64_t* __restrict__ keys, uint64_t n, RegRef R,
+                              long long t) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    reg_insert(R, keys[i], t, false);
+}
+
+// Re-insert whole entries (rehash, overflow drain, prune rebuild).  n may live
+// on the device (n_dev) when the host has not read it back.
+__global__ void k_insert_entries(const RegEntry* __restrict__ src, uint64_t n,
+                                 const unsigned long long* n_dev, RegRef R, int skip_empty) {
+  const uint64_t total = n_dev ? *n_dev : n;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+    const RegEntry e = src[i];
+    if (skip_empty && e.key == kEmptyKey) continue;
+    reg_insert(R, e.key, e.last, true);
+  }
+}
+
+// Warp-aggregated append of the keys whose last-seen slice is > cut.
+__global__ void k_active(const RegEntry* __restrict__ table, uint64_t cap, int special,
+                         long long cut, uint64_t* __restrict__ out,
+                         unsigned long long* nout, unsigned long long* maxkey) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t total = cap + 1;
+  const int lane = threadIdx.x & 31;
+  unsigned long long kmax = 0;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < total; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    bool take = false;
+    unsigned long long key = 0;
+    if (i < total) {
+      const RegEntry e = table[i];
+      key = e.key;
+      take = (i < cap) ? (key != kEmptyKey && e.last > cut) : (special && e.last > cut);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (m) {
+      unsigned long long pos = 0;
+      if (lane == 0) pos = atomicAdd(nout, (unsigned long long)__popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, 0);
+      if (take) {
+        out[pos + __popc(m & ((1u << lane) - 1u))] = key;
+        kmax = key > kmax ? key : kmax;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, kmax, o);
+    kmax = other > kmax ? other : kmax;
+  }
+  if (lane == 0 && kmax) atomicMax(maxkey, kmax);
+}
+
+// Entries with last > horizon, appended (prune keeps them).
+__global__ void k_keep(const RegEntry* __restrict__ table, uint64_t cap, long long horizon,
+                       RegEntry* __restrict__ out, unsigned long long* nout) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap; i += stride) {
+    const RegEntry e = table[i];
+    if (e.key != kEmptyKey && e.last > horizon) out[atomicAdd(nout, 1ull)] = e;
+  }
+}
+
+static int ensure_table(DevBuf& buf, uint64_t cap, cudaStream_t s) {
+  int rc = buf.ensure((cap + 1) * sizeof(RegEntry));
+  if (rc) return rc;
+  VATE_CUDA(cudaMemsetAsync(buf.ptr, 0xFF, (cap + 1) * sizeof(RegEntry), s));
+  return VATE_OK;
+}
+
+static uint64_t pow2_at_least(uint64_t x) {
+  uint64_t c = 1;
+  while (c < x) c <<= 1;
+  return c;
+}
+
+int hosts_read_counters(vate_hosts* h, unsigned long long out[H_N]) {
+  vate_pool* p = h->pool;
+  VATE_CUDA(cudaMemcpyAsync(out, h->d_count, H_N * 8, cudaMemcpyDeviceToHost, p->stream));
+  VATE_CUDA(cudaStreamSynchronize(p->stream));
+  return VATE_OK;
+}
+
+int hosts_drain(vate_hosts* h) {
+  vate_pool* p = h->pool;
+  unsigned long long c[H_N];
+  int rc = hosts_read_counters(h, c);
+  if (rc) return rc;
+  const uint64_t count = c[H_COUNT], novf = c[H_OVF];
+  const bool special = (c[H_SPECIAL] & 0xFFFFFFFFull) != 0;
+  if (novf > h->ovf_cap)
+    return set_error(VATE_ECUDA, "host registry overflow list overran its capacity");
+  if (novf > 0 || count > h->cap / 2) {
+    const uint64_t new_cap = pow2_at_least(std::max<uint64_t>(h->cap, 4 * (count + novf) + 64));
+    // rehash the live table: copy entries out first (rebuild consumes `src`)
+    DevBuf old;
+    old.ptr = h->table.ptr;
+    old.bytes = h->table.bytes;
+    const uint64_t old_cap = h->cap;
+    h->table.ptr = nullptr;
+    h->table.bytes = 0;
+    // new table in h->table via scratch swap
+    rc = ensure_table(h->scratch, new_cap, p->stream);
+    if (rc) return rc;
+    VATE_CUDA(cudaMemcpyAsync(h->scratch.as<RegEntry>() + new_cap, old.as<RegEntry>() + old_cap,
+                              sizeof(RegEntry), cudaMemcpyDeviceToDevice, p->stream));
+    VATE_CUDA(cudaMemsetAsync(h->d_count + H_COUNT, 0, 8, p->stream));
+    VATE_CUDA(cudaMemsetAsync(h->d_count + H_OVF, 0, 8, p->stream));
+    unsigned long long one = special ? 1ull : 0ull;
+    VATE_CUDA(cudaMemcpyAsync(h->d_count + H_COUNT, &one, 8, cudaMemcpyHostToDevice, p->stream));
+    RegRef R = make_ref(h, h->scratch, new_cap);
+    VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(old_cap, kThreads, 148u * 16u), kThreads, 0,
+                k_insert_entries, old.as<RegEntry>(), old_cap, (const unsigned long long*)nullptr,
+                R, 1);
+    if (novf) {
+      // overflow entries go after the rehash; keep a copy since inserts may park again
+      DevBuf tmp;
+      rc = tmp.ensure(novf * sizeof(RegEntry));
+      if (rc) { old.release(); return rc; }
+      VATE_CUDA(cudaMemcpyAsync(tmp.ptr, h->ovf.ptr, novf * sizeof(RegEntry),
+                                cudaMemcpyDeviceToDevice, p->stream));
+      VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(novf, kThreads, 148u * 16u), kThreads, 0,
+                  k_insert_entries, tmp.as<RegEntry>(), novf, (const unsigned long long*)nullptr,
+                  R, 0);
+      VATE_CUDA(cudaStreamSynchronize(p->stream));
+      tmp.release();
+    }
+    VATE_CUDA(cudaStreamSynchronize(p->stream));
+    old.release();
+    h->table.ptr = h->scratch.ptr;
+    h->table.bytes = h->scratch.bytes;
+    h->scratch.ptr = nullptr;
+    h->scratch.bytes = 0;
+    h->cap = new_cap;
+    rc = hosts_read_counters(h, c);
+    if (rc) return rc;
+    if (c[H_OVF]) return hosts_drain(h);  // pathological: grow again
+  }
+  h->pending = 0;
+  h->count_hint = c[H_COUNT];
+  return VATE_OK;
+}
+
+int hosts_prepare_insert(vate_hosts* h, uint64_t n) {
+  if (h->pending + n > h->ovf_cap) {
+    if (h->pending) {
+      int rc = hosts_drain(h);
+      if (rc) return rc;
+    }
+    if (n > h->ovf_cap) {
+      int rc = h->ovf.ensure(n * sizeof(RegEntry));
+      if (rc) return rc;
+      h->ovf_cap = h->ovf.bytes / sizeof(RegEntry);
+    }
+  }
+  h->pending += n;
+  return VATE_OK;
+}
+
+static int sort_keys(vate_pool* p, uint64_t* in, uint64_t* out, uint64_t n, int end_bit) {
+  size_t bytes = 0;
+  VATE_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const unsigned long long*)in,
+                                           (unsigned long long*)out, (int64_t)n, 0, end_bit,
+                                           p->stream));
+  int rc = p->cub_tmp.ensure(bytes + 256);
+  if (rc) return rc;
+  cudaEvent_t ta = nullptr;
+  timing_begin(p, VATE_K_SORT, &ta);
+  VATE_CUDA(cub::DeviceRadixSort::SortKeys(p->cub_tmp.ptr, bytes, (const unsigned long long*)in,
+                                           (unsigned long long*)out, (int64_t)n, 0, end_bit,
+                                           p->stream));
+  timing_end(p, VATE_K_SORT, ta);
+  p->launches += 1 + (uint64_t)(end_bit + 7) / 8;  // histogram + one pass per 8-bit digit
+  return VATE_OK;
+}
+
+// Sorted keys with last > t - k' into pool->hosts_sorted.
+int hosts_compact_active(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev,
+                         uint64_t* n) {
+  vate_pool* p = h->pool;
+  int rc = hosts_drain(h);
+  if (rc) return rc;
+  const uint64_t count = h->count_hint;
+  rc = p->hosts_tmp.ensure((count + 1) * 8);
+  if (rc) return rc;
+  rc = p->hosts_sorted.ensure((count + 1) * 8);
+  if (rc) return rc;
+  VATE_CUDA(cudaMemsetAsync(h->d_count + H_MAXKEY, 0, 16, p->stream));
+  unsigned long long c[H_N];
+  VATE_CUDA(cudaMemcpyAsync(c, h->d_count, H_N * 8, cudaMemcpyDeviceToHost, p->stream));
+  VATE_CUDA(cudaStreamSynchronize(p->stream));
+  const int special = (c[H_SPECIAL] & 0xFFFFFFFFull) != 0;
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap + 1, kThreads, 148u * 16u), kThreads, 0,
+              k_active, h->table.as<const RegEntry>(), h->cap, special,
+              (long long)(t - k_prime), p->hosts_tmp.as<uint64_t>(), h->d_count + H_NOUT,
+              h->d_count + H_MAXKEY);
+  rc = hosts_read_counters(h, c);
+  if (rc) return rc;
+  *n = c[H_NOUT];
+  const unsigned long long maxkey = c[H_MAXKEY];
+  int end_bit = 64;
+  while (end_bit > 1 && !((maxkey >> (end_bit - 1)) & 1ull)) --end_bit;
+  if (*n > 1) {
+    rc = sort_keys(p, p->hosts_tmp.as<uint64_t>(), p->hosts_sorted.as<uint64_t>(), *n, end_bit);
+    if (rc) return rc;
+  } else if (*n == 1) {
+    VATE_CUDA(cudaMemcpyAsync(p->hosts_sorted.ptr, p->hosts_tmp.ptr, 8, cudaMemcpyDeviceToDevice,
+                              p->stream));
+  }
+  *keys_dev = p->hosts_sorted.as<uint64_t>();
+  return VATE_OK;
+}
+
+}  // namespace vate
+
+vate::RegRef vate_hosts::ref() const { return vate::make_ref(this, table, cap); }
+
+using namespace vate;
+
+extern "C" {
+
+int vate_hosts_create(vate_hosts** out, vate_pool* p, int k) {
+  if (!out) return set_error(VATE_EVALUE, "null output pointer");
+  *out = nullptr;
+  int rc = enter(p);
+  if (rc) return rc;
+  vate_hosts* h = new vate_hosts();
+  h->pool = p;
+  h->k = k;
+  h->cap = 1 << 12;
+  cudaError_t e = cudaMalloc(&h->d_count, H_N * 8);
+  if (e != cudaSuccess) {
+    delete h;
+    return cuda_fail(e, "cudaMalloc");
+  }
+  e = cudaMemsetAsync(h->d_count, 0, H_N * 8, p->stream);
+  if (e == cudaSuccess) rc = ensure_table(h->table, h->cap, p->stream);
+  else rc = cuda_fail(e, "cudaMemsetAsync");
+  if (rc == VATE_OK) {
+    rc = h->ovf.ensure(4096 * sizeof(RegEntry));
+    h->ovf_cap = h->ovf.bytes / sizeof(RegEntry);
+  }
+  if (rc == VATE_OK) rc = sync_small(p);
+  if (rc) {
+    vate_hosts_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return VATE_OK;
+}
+
+int vate_hosts_destroy(vate_hosts* h) {
+  if (!h) return VATE_OK;
+  cudaSetDevice(h->pool->device);
+  cudaStreamSynchronize(h->pool->stream);
+  h->table.release();
+  h->ovf.release();
+  h->scratch.release();
+  if (h->d_count) cudaFree(h->d_count);
+  delete h;
+  return VATE_OK;
+}
+
+int vate_hosts_update(vate_hosts* h, const uint64_t* aips, uint64_t n, int64_t t, int where) {
+  if (!h) return set_error(VATE_EVALUE, "null registry handle");
+  vate_pool* p = h->pool;
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  rc = hosts_prepare_insert(h, n);
+  if (rc) return rc;
+  const void* d_keys;
+  rc = stage_in(p, p->in_a, aips, n * 8, where, &d_keys);
+  if (rc) return rc;
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(n, kThreads, 148u * 16u), kThreads, 0, k_insert_keys,
+              (const uint64_t*)d_keys, n, h->ref(), (long long)t);
+  return VATE_OK;
+}
+
+int vate_hosts_active(vate_hosts* h, int64_t t, int k_prime, uint64_t* out, uint64_t cap,
+                      uint64_t* n) {
+  if (!h) return set_error(VATE_EVALUE, "null registry handle");
+  vate_pool* p = h->pool;
+  int rc = enter(p);
+  if (rc) return rc;
+  uint64_t* keys = nullptr;
+  rc = hosts_compact_active(h, t, k_prime, &keys, n);
+  if (rc) return rc;
+  const uint64_t m = *n < cap ? *n : cap;
+  if (m) VATE_CUDA(cudaMemcpyAsync(out, keys, m * 8, cudaMemcpyDeviceToHost, p->stream));
+  return sync_small(p);
+}
+
+int vate_hosts_prune(vate_hosts* h, int64_t t) {
+  if (!h) return set_error(VATE_EVALUE, "null registry handle");
+  vate_pool* p = h->pool;
+  int rc = enter(p);
+  if (rc) return rc;
+  rc = hosts_drain(h);
+  if (rc) return rc;
+  const long long horizon = (long long)(t - h->k);
+  // keep list -> fresh table of the same capacity
+  DevBuf keep;
+  rc = keep.ensure((h->count_hint + 1) * sizeof(RegEntry));
+  if (rc) return rc;
+  VATE_CUDA(cudaMemsetAsync(h->d_count + H_NOUT, 0, 8, p->stream));
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap, kThreads, 148u * 16u), kThreads, 0, k_keep,
+              h->table.as<const RegEntry>(), h->cap, horizon, keep.as<RegEntry>(),
+              h->d_count + H_NOUT);
+  // special entry: keep iff present and last > horizon
+  RegEntry special_entry;
+  unsigned long long c[H_N];
+  VATE_CUDA(cudaMemcpyAsync(&special_entry, h->table.as<RegEntry>() + h->cap, sizeof(RegEntry),
+                            cudaMemcpyDeviceToHost, p->stream));
+  rc = hosts_read_counters(h, c);
+  if (rc) { keep.release(); return rc; }
+  const bool special = (c[H_SPECIAL] & 0xFFFFFFFFull) != 0 && special_entry.last > horizon;
+  rc = ensure_table(h->table, h->cap, p->stream);
+  if (rc) { keep.release(); return rc; }
+  if (special) {
+    VATE_CUDA(cudaMemcpyAsync(h->table.as<RegEntry>() + h->cap, &special_entry, sizeof(RegEntry),
+                              cudaMemcpyHostToDevice, p->stream));
+  }
+  unsigned long long init[3] = {special ? 1ull : 0ull, 0ull, special ? 1ull : 0ull};
+  VATE_CUDA(cudaMemcpyAsync(h->d_count, init, 24, cudaMemcpyHostToDevice, p->stream));
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(c[H_NOUT], kThreads, 148u * 16u), kThreads, 0,
+              k_insert_entries, keep.as<const RegEntry>(), (uint64_t)c[H_NOUT],
+              (const unsigned long long*)nullptr, h->ref(), 1);
+  VATE_CUDA(cudaStreamSynchronize(p->stream));
+  keep.release();
+  h->count_hint = c[H_NOUT] + (special ? 1 : 0);
+  h->pending = 0;
+  return VATE_OK;
+}
+
+int vate_hosts_size(vate_hosts* h, uint64_t* n) {
+  if (!h) return set_error(VATE_EVALUE, "null registry handle");
+  int rc = enter(h->pool);
+  if (rc) return rc;
+  rc = hosts_drain(h);
+  if (rc) return rc;
+  *n = h->count_hint;
+  return VATE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,265 @@
+// vate_internal.cuh -- shared device helpers and the pool handle.
+//
+// Data layout in HBM:
+//   cells    : 2^c unpacked ATs, one uint8 (k <= 127), uint16 (k <= 32767) or
+//              uint32 (k = 32768) each.  The reference packs w-bit cells into
+//              u64 words (bitpack.py:26-56); unpacked cells make every scan
+//              write a plain byte/short store with no read-modify-write, and the
+//              ATP1 packed form is produced only for snapshots.
+//   bitmap   : 1 bit per cell, "inactive for k'" (pools.py:187-193), rebuilt
+//              per estimate; 2^c/8 bytes, L2-resident up to c = 29.
+//   registry : open-addressing table of {u64 aip, i64 last-seen slice}.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/vate.h"
+
+namespace vate {
+
+constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ull;   // hashing.py:18
+constexpr uint64_t kMul1 = 0xBF58476D1CE4E5B9ull;  // hashing.py:28
+constexpr uint64_t kMul2 = 0x94D049BB133111EBull;  // hashing.py:29
+constexpr uint64_t kEmptyKey = ~0ull;               // registry empty-slot marker
+constexpr int kMaxK = 1 << 15;                      // counters.py:27
+constexpr int kThreads = 256;
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// splitmix64 finalizer (hashing.py:25-30); u64 arithmetic wraps like numpy's.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= kMul1;
+  z ^= z >> 27;
+  z *= kMul2;
+  return z ^ (z >> 31);
+}
+
+// Exact x / d for any 64-bit x and d >= 1: q = hi64(x * floor((2^64-1)/d)) is
+// at most 2 below the true quotient; two conditional corrections fix it.
+struct DivU64 {
+  uint64_t d, m;
+};
+inline DivU64 make_div(uint64_t d) { return DivU64{d, d ? ~0ull / d : 0ull}; }
+__device__ __forceinline__ uint64_t div_u64(uint64_t x, DivU64 D, uint64_t* rem) {
+  uint64_t q = __umul64hi(x, D.m);
+  uint64_t r = x - q * D.d;
+  if (r >= D.d) { ++q; r -= D.d; }
+  if (r >= D.d) { ++q; r -= D.d; }
+  if (rem) *rem = r;
+  return q;
+}
+
+// EstimatorConfig hash parameters (estimator.py:32-61).
+struct HashParams {
+  uint64_t g;
+  DivU64 dg;
+  uint64_t gmask;      // g - 1 when g is a power of two
+  int gpow2;
+  uint64_t cs, gs;     // cell_stream, group_stream
+  uint64_t cmask;      // 2^c - 1
+};
+inline HashParams make_hash(uint64_t g, int c, uint64_t cs, uint64_t gs) {
+  HashParams H;
+  H.g = g;
+  H.dg = make_div(g);
+  H.gpow2 = (g & (g - 1)) == 0;
+  H.gmask = g - 1;
+  H.cs = cs;
+  H.gs = gs;
+  H.cmask = (c >= 64) ? ~0ull : ((1ull << c) - 1);
+  return H;
+}
+
+// BH(bip) = mix64(bip*phi + group_stream) mod g   (hashing.py:60-67)
+__device__ __forceinline__ uint64_t slot_of(uint64_t bip, const HashParams& H) {
+  uint64_t h = mix64(bip * kPhi + H.gs);
+  if (H.gpow2) return h & H.gmask;
+  uint64_t r;
+  div_u64(h, H.dg, &r);
+  return r;
+}
+// H(aip, slot) = mix64(((aip<<32)|slot)*phi + cell_stream) & (2^c-1)  (hashing.py:48-57)
+__device__ __forceinline__ uint64_t cell_of(uint64_t aip, uint64_t slot, const HashParams& H) {
+  return mix64(((aip << 32) | slot) * kPhi + H.cs) & H.cmask;
+}
+
+// Block layout of the 2k staggered-clock blocks (pools.py:80-95, :104-136).
+struct Layout {
+  uint64_t size;      // 2^c
+  uint32_t B;         // nblocks = 2k (also the sentinel value)
+  uint32_t k;
+  int part;           // 0 tail, 1 low-dev
+  DivU64 da;          // tail: a = S/(B-1); low-dev: a' = S/B
+  DivU64 da1;         // low-dev: a'+1
+  uint64_t split;     // low-dev: a'*(B-b'+1)
+  uint64_t narrow;    // low-dev: B-b'
+};
+
+__host__ __device__ __forceinline__ uint32_t clock_of(uint32_t bact0, uint32_t blk, uint32_t B) {
+  uint32_t s = bact0 + blk;
+  return s >= B ? s - B : s;
+}
+
+__device__ __forceinline__ uint32_t block_of(uint64_t i, const Layout& L) {
+  if (L.part == 0) {
+    uint64_t q = div_u64(i, L.da, nullptr);
+    return q < (uint64_t)(L.B - 1) ? (uint32_t)q : L.B - 1;
+  }
+  if (i < L.split) return (uint32_t)div_u64(i, L.da, nullptr);
+  return (uint32_t)div_u64(i + L.narrow, L.da1, nullptr);
+}
+
+__host__ __device__ __forceinline__ uint64_t block_start(uint32_t b, const Layout& L) {
+  if (b >= L.B) return L.size;
+  if (L.part == 0) return (uint64_t)b * L.da.d;
+  if (b < L.narrow) return (uint64_t)b * L.da.d;
+  return L.narrow * L.da.d + (uint64_t)(b - L.narrow) * L.da1.d;
+}
+
+// Inactive for width k' (pools.py:187-193): sentinel, or (act + 2k - v) mod 2k
+// >= k'.  For stored values above 2k (only reachable through a hand-made
+// snapshot) the reference's uint64 wraparound is reproduced exactly.
+__device__ __forceinline__ bool is_inactive(uint32_t v, uint32_t act, uint32_t B, uint32_t kp) {
+  if (v == B) return true;
+  uint32_t d;
+  if (v <= act) d = act - v;
+  else if (v < B) d = act + B - v;
+  else d = (uint32_t)(((uint64_t)act + B - (uint64_t)v) % B);
+  return d >= kp;
+}
+
+// Registry entry: one 16-byte sector-aligned record per host.
+struct __align__(16) RegEntry {
+  unsigned long long key;
+  long long last;
+};
+
+struct RegRef {
+  RegEntry* table;        // cap entries + 1 special entry (key == kEmptyKey)
+  uint64_t mask;          // cap - 1
+  unsigned long long* count;      // distinct keys stored
+  RegEntry* ovf;          // overflow list (probe limit hit)
+  unsigned long long* ovf_n;
+  uint64_t ovf_cap;
+  unsigned int* special;  // 1 if the special entry is present
+  int enabled;
+};
+
+// A growable device buffer (one stream per pool, so growth may sync).
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want);
+  void release();
+  template <typename T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+}  // namespace vate
+
+struct vate_hosts;
+
+struct vate_pool {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int c = 0, k = 0, partition = 0;
+  uint32_t width = 0;      // ats_bits(k) (counters.py:52-54)
+  int cell_bytes = 1;
+  vate::Layout L{};
+  uint32_t bact0 = 0;
+  void* cells = nullptr;
+
+  vate::DevBuf bitmap;      // (S+31)/32 words
+  vate::DevBuf in_a, in_b;  // staging for host inputs
+  vate::DevBuf out_buf;     // staging for device outputs
+  vate::DevBuf hosts_sorted, hosts_tmp, g0, flags, sel_idx, cub_tmp;
+  vate::DevBuf est_out, zv_out, sat_out, host_out;
+  vate::DevBuf lzv;         // log table, g+1 doubles
+  uint64_t lzv_g = 0;
+
+  unsigned long long* d_ctr = nullptr;  // device counters (see enum in .cu)
+  unsigned long long* h_ctr = nullptr;  // pinned mirror
+  cudaEvent_t ev_small = nullptr;
+  cudaEvent_t marks[16] = {nullptr};
+
+  // fused-estimate state between begin/finish
+  uint64_t est_n = 0;
+  int est_kp = 0;
+  uint64_t est_g = 0;
+
+  // pending async advance
+  bool adv_pending = false;
+  int32_t adv_blocks[2] = {0, 0};
+  uint64_t adv_maint = 0;
+
+  // instrumentation
+  uint64_t launches = 0;
+  bool timing = false;
+  struct Timed {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Timed> timed_pending;
+  std::vector<cudaEvent_t> event_pool;
+  double timed_ms[VATE_K_COUNT] = {0};
+  uint64_t timed_n[VATE_K_COUNT] = {0};
+};
+
+struct vate_hosts {
+  vate_pool* pool = nullptr;
+  int k = 1;
+  uint64_t cap = 0;
+  vate::DevBuf table, ovf, scratch;
+  unsigned long long* d_count = nullptr;  // [0] count, [1] ovf_n, [2] special flag, [3] maxkey
+  uint64_t ovf_cap = 0;
+  uint64_t pending = 0;    // registry inserts enqueued since the last drain
+  uint64_t count_hint = 0; // last count read back
+  vate::RegRef ref() const;
+};
+
+namespace vate {
+
+// error plumbing (thread-local message)
+int set_error(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+#define VATE_CUDA(call)                                  \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return ::vate::cuda_fail(_e, #call); \
+  } while (0)
+
+int enter(vate_pool* p);                  // cudaSetDevice + sticky-error check
+int stage_in(vate_pool* p, DevBuf& buf, const void* src, size_t bytes, int where,
+             const void** dev);           // host -> device staging
+int sync_small(vate_pool* p);             // wait for the stream
+void timing_begin(vate_pool* p, int kind, cudaEvent_t* a);
+void timing_end(vate_pool* p, int kind, cudaEvent_t a);
+int collect_timing(vate_pool* p);
+uint32_t grid_for(uint64_t work, uint32_t per_block, uint32_t cap_blocks = 148u * 64u);
+
+// counters in vate_pool::d_ctr
+enum Ctr { C_P = 0, C_CLEARED = 1, C_NSEL = 2, C_ERR = 3, C_N = 8 };
+
+// registry helpers (vate_hosts.cu)
+int hosts_drain(vate_hosts* h);
+int hosts_prepare_insert(vate_hosts* h, uint64_t n);
+int hosts_compact_active(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev,
+                         uint64_t* n);
+
+}  // namespace vate
+
+// RAII-free launch accounting: count every kernel, optionally time it.
+#define VATE_LAUNCH(p, kind, grid, block, smem, kernel, ...)               \
+  do {                                                                     \
+    cudaEvent_t _ta = nullptr;                                             \
+    ::vate::timing_begin((p), (kind), &_ta);                               \
+    kernel<<<(grid), (block), (smem), (p)->stream>>>(__VA_ARGS__);        \
+    (p)->launches++;                                                       \
+    ::vate::timing_end((p), (kind), _ta);                                  \
+    cudaError_t _le = cudaGetLastError();                                  \
+    if (_le != cudaSuccess) return ::vate::cuda_fail(_le, #kernel);        \
+  } while (0)

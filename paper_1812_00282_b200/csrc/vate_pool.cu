@@ -1,0 +1,1043 @@
+// vate_pool.cu -- the AT pool on the device: lifecycle, ingest scan,
+// two-block maintenance, whole-pool inactive bitmap / count, point queries,
+// ATP1 snapshots, replica merge and the synthetic packet generator.
+//
+// Reference: pools.py:67-298 (AtPool), estimator.py:96-104 (pair_cells /
+// record_pairs), bitpack.py:26-140 (the snapshot bit layout).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "vate_internal.cuh"
+#include "vate_registry.cuh"
+
+namespace vate {
+
+// ---------------------------------------------------------------------------
+// error plumbing, staging, timing
+// ---------------------------------------------------------------------------
+
+static thread_local std::string g_err;
+
+int set_error(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return set_error(e == cudaErrorMemoryAllocation ? VATE_ENOMEM : VATE_ECUDA,
+                   std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+int DevBuf::ensure(size_t want) {
+  if (want <= bytes && ptr) return VATE_OK;
+  size_t grow = std::max<size_t>(want, bytes + bytes / 2);
+  grow = (grow + 255) & ~size_t(255);
+  if (ptr) {
+    cudaError_t e = cudaFree(ptr);  // device-synchronising: safe for in-flight work
+    ptr = nullptr;
+    bytes = 0;
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFree");
+  }
+  cudaError_t e = cudaMalloc(&ptr, grow);
+  if (e != cudaSuccess) {
+    ptr = nullptr;
+    return cuda_fail(e, "cudaMalloc");
+  }
+  bytes = grow;
+  return VATE_OK;
+}
+
+void DevBuf::release() {
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  bytes = 0;
+}
+
+int enter(vate_pool* p) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  VATE_CUDA(cudaSetDevice(p->device));
+  return VATE_OK;
+}
+
+int stage_in(vate_pool* p, DevBuf& buf, const void* src, size_t bytes, int where,
+             const void** dev) {
+  if (where == VATE_DEVICE || bytes == 0) {
+    *dev = src;
+    return VATE_OK;
+  }
+  int rc = buf.ensure(bytes);
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, p->stream));
+  *dev = buf.ptr;
+  return VATE_OK;
+}
+
+int sync_small(vate_pool* p) {
+  VATE_CUDA(cudaStreamSynchronize(p->stream));
+  if (p->h_ctr && p->h_ctr[C_ERR]) {
+    p->h_ctr[C_ERR] = 0;
+    return set_error(VATE_EVALUE, "cell index outside the pool");
+  }
+  return VATE_OK;
+}
+
+static cudaEvent_t take_event(vate_pool* p) {
+  if (!p->event_pool.empty()) {
+    cudaEvent_t e = p->event_pool.back();
+    p->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void timing_begin(vate_pool* p, int kind, cudaEvent_t* a) {
+  (void)kind;
+  if (!p->timing) return;
+  *a = take_event(p);
+  cudaEventRecord(*a, p->stream);
+}
+
+void timing_end(vate_pool* p, int kind, cudaEvent_t a) {
+  if (!p->timing || !a) return;
+  cudaEvent_t b = take_event(p);
+  cudaEventRecord(b, p->stream);
+  p->timed_pending.push_back({kind, a, b});
+}
+
+int collect_timing(vate_pool* p) {
+  if (p->timed_pending.empty()) return VATE_OK;
+  VATE_CUDA(cudaStreamSynchronize(p->stream));
+  for (auto& t : p->timed_pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    p->timed_ms[t.kind] += ms;
+    p->timed_n[t.kind] += 1;
+    p->event_pool.push_back(t.a);
+    p->event_pool.push_back(t.b);
+  }
+  p->timed_pending.clear();
+  return VATE_OK;
+}
+
+uint32_t grid_for(uint64_t work, uint32_t per_block, uint32_t cap_blocks) {
+  uint64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap_blocks) g = cap_blocks;
+  return (uint32_t)g;
+}
+
+template <typename F>
+static int with_cell(int bytes, F f) {
+  switch (bytes) {
+    case 1: return f(uint8_t{});
+    case 2: return f(uint16_t{});
+    default: return f(uint32_t{});
+  }
+}
+
+__device__ __forceinline__ unsigned block_sum(unsigned v) {
+  __shared__ unsigned warp_sums[32];
+  v = __reduce_add_sync(0xffffffffu, v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) warp_sums[wid] = v;
+  __syncthreads();
+  unsigned total = 0;
+  if (wid == 0) {
+    total = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0u;
+    total = __reduce_add_sync(0xffffffffu, total);
+  }
+  return total;  // valid in thread 0
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void k_fill(T* cells, uint64_t n, T value) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    cells[i] = value;
+}
+
+// One packet: BH, H, block clock, store (pools.py:153-178 with
+// estimator.py:96-99).  Same-cell writers of a slice store the same clock, so
+// plain stores suffice -- no atomics, no read-modify-write.
+template <typename T, bool REG>
+__device__ __forceinline__ void scan_one(uint64_t aip, uint64_t bip, T* __restrict__ cells,
+                                         const HashParams& H, const Layout& L,
+                                         uint32_t bact0, const RegRef& R, long long t) {
+  const uint64_t cell = cell_of(aip, slot_of(bip, H), H);
+  const uint32_t act = clock_of(bact0, block_of(cell, L), L.B);
+  cells[cell] = (T)act;
+  if (REG) reg_insert(R, aip, t, false);
+}
+
+template <typename T, bool REG>
+__global__ void __launch_bounds__(kThreads) k_scan_packed16(
+    const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
+    Layout L, uint32_t bact0, RegRef R, long long t) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < npairs2; i += stride) {
+    const uint4 q = __ldcs(pairs2 + i);  // streamed once: evict-first
+    scan_one<T, REG>(q.x, q.y, cells, H, L, bact0, R, t);
+    scan_one<T, REG>(q.z, q.w, cells, H, L, bact0, R, t);
+  }
+}
+
+template <typename T, bool REG>
+__global__ void __launch_bounds__(kThreads) k_scan_packed8(
+    const uint2* __restrict__ pairs, uint64_t n, T* __restrict__ cells, HashParams H,
+    Layout L, uint32_t bact0, RegRef R, long long t) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint2 q = pairs[i];
+    scan_one<T, REG>(q.x, q.y, cells, H, L, bact0, R, t);
+  }
+}
+
+template <typename T, bool REG>
+__global__ void __launch_bounds__(kThreads) k_scan_u64(
+    const uint64_t* __restrict__ aips, const uint64_t* __restrict__ bips, uint64_t n,
+    T* __restrict__ cells, HashParams H, Layout L, uint32_t bact0, RegRef R, long long t) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    scan_one<T, REG>(__ldcs(aips + i), __ldcs(bips + i), cells, H, L, bact0, R, t);
+}
+
+__global__ void k_pair_cells(const uint64_t* __restrict__ aips,
+                             const uint64_t* __restrict__ bips, uint64_t n, HashParams H,
+                             uint64_t* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = cell_of(aips[i], slot_of(bips[i], H), H);
+}
+
+__global__ void k_host_cells(const uint64_t* __restrict__ aips, uint64_t n, uint64_t g,
+                             HashParams H, uint64_t* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * g; i += stride)
+    out[i] = cell_of(aips[i / g], i % g, H);
+}
+
+template <typename T>
+__global__ void k_set_cells(const uint64_t* __restrict__ idx, uint64_t n, T* __restrict__ cells,
+                            Layout L, uint32_t bact0, unsigned long long* err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t c = idx[i];
+    if (c >= L.size) {
+      *err = 1;
+      continue;
+    }
+    cells[c] = (T)clock_of(bact0, block_of(c, L), L.B);
+  }
+}
+
+// Two due blocks after the clock advance (pools.py:221-249, counters.py:113-127):
+// range 0 sits at clock 0 (stale: v <= k), range 1 at clock k (stale:
+// k <= v <= 2k-1 or v == 0).  Stale cells become the sentinel 2k.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_sweep(T* __restrict__ cells, uint64_t s0,
+                                                    uint64_t n0, uint64_t s1, uint64_t n1,
+                                                    uint32_t k, unsigned long long* cleared) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t total = n0 + n1;
+  const uint32_t B = 2 * k;
+  unsigned local = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+    const bool at_zero = i < n0;
+    const uint64_t c = at_zero ? s0 + i : s1 + (i - n0);
+    const uint32_t v = cells[c];
+    const bool stale = at_zero ? (v <= k) : ((v >= k && v <= B - 1) || v == 0);
+    if (stale) {
+      cells[c] = (T)B;
+      ++local;
+    }
+  }
+  const unsigned s = block_sum(local);
+  if (threadIdx.x == 0 && s) atomicAdd(cleared, (unsigned long long)s);
+}
+
+// 32 consecutive cells into registers with 16-byte loads (i0 is 32-aligned).
+template <typename T>
+__device__ __forceinline__ void load32(const T* __restrict__ p, uint32_t (&v)[32]) {
+  constexpr int NV = (int)sizeof(T) * 32 / 16;
+  uint4 r[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) r[q] = __ldcs(reinterpret_cast<const uint4*>(p) + q);
+  const T* e = reinterpret_cast<const T*>(r);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = e[j];
+}
+
+// Calls f(j, act) for the cells i0+j, j < cnt, walking block boundaries.
+template <typename F>
+__device__ __forceinline__ void for_word_clocks(uint64_t i0, uint32_t cnt, const Layout& L,
+                                                uint32_t bact0, F f) {
+  uint32_t b = block_of(i0, L);
+  uint64_t next = block_start(b + 1, L);
+  uint32_t act = clock_of(bact0, b, L.B);
+  if (i0 + cnt <= next) {
+#pragma unroll
+    for (uint32_t j = 0; j < 32; ++j)
+      if (j < cnt) f(j, act);
+    return;
+  }
+  for (uint32_t j = 0; j < cnt; ++j) {
+    while (i0 + j >= next) {
+      ++b;
+      next = block_start(b + 1, L);
+      act = (act + 1 == L.B) ? 0 : act + 1;
+    }
+    f(j, act);
+  }
+}
+
+// Whole-pool pass: inactive bitmap for width k' plus its popcount P
+// (count_inactive, pools.py:195-210; predicate pools.py:187-193).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells, Layout L,
+                                                     uint32_t bact0, uint32_t kp,
+                                                     uint32_t* __restrict__ bitmap,
+                                                     uint64_t nwords,
+                                                     unsigned long long* pool_inactive) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned local = 0;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
+    const uint64_t i0 = w * 32;
+    const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
+    uint32_t b = block_of(i0, L);
+    uint64_t next = block_start(b + 1, L);
+    uint32_t act = clock_of(bact0, b, L.B);
+    uint32_t bits = 0;
+    if (cnt == 32 && i0 + 32 <= next) {  // the whole word in one block: one clock
+      uint32_t v[32];
+      load32<T>(cells + i0, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) bits |= (uint32_t)is_inactive(v[j], act, L.B, kp) << j;
+    } else {  // block boundary (or pool end) inside the word
+      for (uint32_t j = 0; j < cnt; ++j) {
+        while (i0 + j >= next) {
+          ++b;
+          next = block_start(b + 1, L);
+          act = (act + 1 == L.B) ? 0 : act + 1;
+        }
+        bits |= (uint32_t)is_inactive(cells[i0 + j], act, L.B, kp) << j;
+      }
+    }
+    bitmap[w] = bits;
+    local += __popc(bits);
+  }
+  const unsigned s = block_sum(local);
+  if (threadIdx.x == 0 && s) atomicAdd(pool_inactive, (unsigned long long)s);
+}
+
+template <typename T>
+__global__ void k_mask(const T* __restrict__ cells, const uint64_t* __restrict__ idx, uint64_t n,
+                       Layout L, uint32_t bact0, uint32_t kp, uint8_t* __restrict__ out,
+                       unsigned long long* err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t c = idx[i];
+    if (c >= L.size) {
+      *err = 1;
+      out[i] = 0;
+      continue;
+    }
+    out[i] = is_inactive(cells[c], clock_of(bact0, block_of(c, L), L.B), L.B, kp);
+  }
+}
+
+template <typename T>
+__global__ void k_get(const T* __restrict__ cells, const uint64_t* __restrict__ idx, uint64_t n,
+                      uint64_t size, uint32_t* __restrict__ out, unsigned long long* err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t c = idx[i];
+    if (c >= size) {
+      *err = 1;
+      out[i] = 0;
+      continue;
+    }
+    out[i] = cells[c];
+  }
+}
+
+// ATP1 payload: cell i occupies bits [i*w, i*w+w) of a little-endian stream of
+// u64 words, LSB first; pad bits are zero (bitpack.py:26-78, pools.py:261-265).
+template <typename T>
+__global__ void k_pack(const T* __restrict__ cells, uint64_t size, uint32_t width,
+                       unsigned long long* __restrict__ words, uint64_t nwords) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
+    const uint64_t bit0 = w * 64;
+    const uint64_t i0 = bit0 / width;
+    const uint64_t i1 = umin64((bit0 + 63) / width, size - 1);
+    unsigned long long acc = 0;
+    for (uint64_t i = i0; i <= i1; ++i) {
+      const unsigned long long v = cells[i];
+      const long long sh = (long long)(i * width) - (long long)bit0;
+      acc |= sh >= 0 ? (v << sh) : (v >> (-sh));
+    }
+    words[w] = acc;
+  }
+}
+
+template <typename T>
+__global__ void k_unpack(const unsigned long long* __restrict__ words, uint64_t nwords,
+                         uint64_t size, uint32_t width, T* __restrict__ cells) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const unsigned long long mask = (1ull << width) - 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < size; i += stride) {
+    const uint64_t bit = i * width;
+    const uint64_t w0 = bit >> 6;
+    const uint32_t off = (uint32_t)(bit & 63);
+    unsigned long long v = words[w0] >> off;
+    if (off + width > 64 && w0 + 1 < nwords) v |= words[w0 + 1] << (64 - off);
+    cells[i] = (T)(v & mask);
+  }
+}
+
+// Replica merge, step 1: bit per cell, set iff the cell holds its block's
+// current clock, i.e. was set in this slice (maintenance leaves no cell at its
+// own clock: ats_preserve, counters.py:92-110).
+template <typename T>
+__global__ void k_dirty(const T* __restrict__ cells, Layout L, uint32_t bact0,
+                        uint32_t* __restrict__ bitmap, uint64_t nwords) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
+    const uint64_t i0 = w * 32;
+    const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
+    uint32_t bits = 0;
+    for_word_clocks(i0, cnt, L, bact0, [&](uint32_t j, uint32_t act) {
+      bits |= (uint32_t)((uint32_t)cells[i0 + j] == act) << j;
+    });
+    bitmap[w] = bits;
+  }
+}
+
+// Replica merge, step 2: OR of every rank's dirty bitmap; dirty cells take
+// their block clock.  Equals the newest-timestamp max of SURVEY.md §8e.
+template <typename T>
+__global__ void k_merge(T* __restrict__ cells, Layout L, uint32_t bact0,
+                        const uint32_t* __restrict__ bitmaps, uint64_t nwords, int nranks) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
+    uint32_t bits = 0;
+    for (int r = 0; r < nranks; ++r) bits |= bitmaps[(uint64_t)r * nwords + w];
+    if (!bits) continue;
+    const uint64_t i0 = w * 32;
+    const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
+    for_word_clocks(i0, cnt, L, bact0, [&](uint32_t j, uint32_t act) {
+      if ((bits >> j) & 1u) cells[i0 + j] = (T)act;
+    });
+  }
+}
+
+// Synthetic packets; must equal oracle/vate_oracle.py:synthetic_slice.
+constexpr uint64_t kSynthSalt = 0x51ED270B27C4DF1Dull;
+constexpr uint64_t kSynthHostSalt = 0xA5A5A5A5A5A5A5A5ull;
+constexpr uint64_t kSynthPeerSalt = 0x3C6EF372FE94F82Bull;
+
+__global__ void k_synth(long long t, uint64_t n, DivU64 dh, uint64_t base_aip, uint64_t stream,
+                        uint2* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t hi = ((uint64_t)t & 0xFFFFFFFFull) << 32;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t x = mix64(stream + (hi + i) * kPhi);
+    uint64_t rank;
+    div_u64(x, dh, &rank);
+    const uint32_t r = (uint32_t)(mix64(rank ^ kSynthHostSalt) >> 40);
+    const uint32_t lz = min(__clz(r) - 8, 12);
+    const uint32_t npeers = 1u + (r & 7u) + (1u << lz);
+    const uint32_t j = (uint32_t)((x >> 32) % npeers);
+    const uint32_t bip = (uint32_t)mix64((rank << 20) ^ (uint64_t)j ^ kSynthPeerSalt);
+    out[i] = make_uint2((uint32_t)(rank + base_aip), bip);
+  }
+}
+
+}  // namespace vate
+
+using namespace vate;
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+namespace vate {
+// Build the k' inactive bitmap and enqueue P into h_ctr[C_P] (not synced).
+int build_bitmap(vate_pool* p, int k_prime) {
+  const uint64_t nwords = (p->L.size + 31) / 32;
+  int rc = p->bitmap.ensure(nwords * 4 + 16);
+  if (rc) return rc;
+  VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_P, 0, 8, p->stream));
+  rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_BITMAP, grid_for(nwords, kThreads, 148u * 32u), kThreads, 0,
+                k_bitmap<T>, (const T*)p->cells, p->L, p->bact0, (uint32_t)k_prime,
+                p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P);
+    return VATE_OK;
+  });
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_P, p->d_ctr + C_P, 8, cudaMemcpyDeviceToHost, p->stream));
+  return VATE_OK;
+}
+
+int check_width(vate_pool* p, int k_prime) {
+  if (k_prime < 1 || k_prime > p->k)
+    return set_error(VATE_EVALUE, "k'=" + std::to_string(k_prime) + " outside [1, " +
+                                      std::to_string(p->k) + "]");
+  return VATE_OK;
+}
+}  // namespace vate
+
+extern "C" {
+
+const char* vate_last_error(void) { return vate::g_err.c_str(); }
+int vate_abi_version(void) { return VATE_ABI_VERSION; }
+
+int vate_device_count(int* n) {
+  VATE_CUDA(cudaGetDeviceCount(n));
+  return VATE_OK;
+}
+
+int vate_pool_create(vate_pool** out, int c, int k, int partition, int device) {
+  if (!out) return set_error(VATE_EVALUE, "null output pointer");
+  *out = nullptr;
+  // _validate_pool_shape (pools.py:57-64) and AtPool.__init__ (pools.py:72-95)
+  if (k < 1 || k > kMaxK)
+    return set_error(VATE_ECONFIG, "k must be in [1, 32768], got " + std::to_string(k));
+  if (c > 32) return set_error(VATE_ECONFIG, "c must be at most 32, got " + std::to_string(c));
+  if (c < 1 || (1ull << c) < 2ull * (uint64_t)k)
+    return set_error(VATE_ECONFIG, "pool of 2^" + std::to_string(c) +
+                                       " cells cannot hold 2k=" + std::to_string(2 * k) +
+                                       " non-empty blocks");
+  if (partition != VATE_TAIL && partition != VATE_LOWDEV)
+    return set_error(VATE_ECONFIG, "unknown partition method");
+  const uint64_t S = 1ull << c;
+  const uint32_t B = 2u * (uint32_t)k;
+  Layout L{};
+  L.size = S;
+  L.B = B;
+  L.k = (uint32_t)k;
+  L.part = partition;
+  if (partition == VATE_TAIL) {
+    const uint64_t a = S / (B - 1), b = S % (B - 1);
+    if (b == 0)
+      return set_error(VATE_ECONFIG,
+                       "tail partition leaves the last block empty for c=" + std::to_string(c) +
+                           ", k=" + std::to_string(k) + "; use the 'low-dev' partition");
+    L.da = make_div(a);
+    L.da1 = make_div(a);
+  } else {
+    const uint64_t a2 = S / B, b2 = S % B;
+    L.da = make_div(a2);
+    L.da1 = make_div(a2 + 1);
+    L.split = a2 * (B - b2 + 1);
+    L.narrow = B - b2;
+  }
+  vate_pool* p = new vate_pool();
+  p->device = device;
+  p->c = c;
+  p->k = k;
+  p->partition = partition;
+  p->width = 32u - (uint32_t)__builtin_clz(B);  // (2k).bit_length()
+  p->cell_bytes = p->width <= 8 ? 1 : (p->width <= 16 ? 2 : 4);
+  p->L = L;
+  int rc = VATE_OK;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&p->cells, S * (uint64_t)p->cell_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_ctr, C_N * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMallocHost(&p->h_ctr, C_N * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_small, cudaEventDisableTiming);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(p->d_ctr, 0, C_N * sizeof(unsigned long long), p->stream);
+  if (e != cudaSuccess) rc = cuda_fail(e, "vate_pool_create");
+  if (rc == VATE_OK) {
+    memset(p->h_ctr, 0, C_N * sizeof(unsigned long long));
+    // every cell starts at the sentinel 2k (ats_init, counters.py:57-59)
+    rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
+      using T = decltype(tag);
+      VATE_LAUNCH(p, VATE_K_OTHER, grid_for(S, kThreads), kThreads, 0, k_fill<T>, (T*)p->cells,
+                  S, (T)B);
+      return VATE_OK;
+    });
+  }
+  if (rc == VATE_OK) rc = sync_small(p);
+  if (rc != VATE_OK) {
+    vate_pool_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return VATE_OK;
+}
+
+int vate_pool_destroy(vate_pool* p) {
+  if (!p) return VATE_OK;
+  cudaSetDevice(p->device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  for (DevBuf* b : {&p->bitmap, &p->in_a, &p->in_b, &p->out_buf, &p->hosts_sorted, &p->hosts_tmp,
+                    &p->g0, &p->flags, &p->sel_idx, &p->cub_tmp, &p->est_out, &p->zv_out,
+                    &p->sat_out, &p->host_out, &p->lzv})
+    b->release();
+  if (p->cells) cudaFree(p->cells);
+  if (p->d_ctr) cudaFree(p->d_ctr);
+  if (p->h_ctr) cudaFreeHost(p->h_ctr);
+  if (p->ev_small) cudaEventDestroy(p->ev_small);
+  for (auto& t : p->timed_pending) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : p->event_pool) cudaEventDestroy(e);
+  for (auto e : p->marks)
+    if (e) cudaEventDestroy(e);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+  return VATE_OK;
+}
+
+int vate_pool_info(const vate_pool* p, int32_t* bact0, int32_t* cell_bytes, void** stream) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  if (bact0) *bact0 = (int32_t)p->bact0;
+  if (cell_bytes) *cell_bytes = p->cell_bytes;
+  if (stream) *stream = (void*)p->stream;
+  return VATE_OK;
+}
+
+int vate_pool_sync(vate_pool* p) {
+  int rc = enter(p);
+  if (rc) return rc;
+  return sync_small(p);
+}
+
+int vate_pool_launches(const vate_pool* p, uint64_t* n) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  *n = p->launches;
+  return VATE_OK;
+}
+
+int vate_pool_set_timing(vate_pool* p, int on) {
+  int rc = enter(p);
+  if (rc) return rc;
+  rc = collect_timing(p);
+  if (rc) return rc;
+  p->timing = on != 0;
+  for (int i = 0; i < VATE_K_COUNT; ++i) {
+    p->timed_ms[i] = 0;
+    p->timed_n[i] = 0;
+  }
+  return VATE_OK;
+}
+
+int vate_pool_timing(vate_pool* p, int kind, double* total_ms, uint64_t* launches) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (kind < 0 || kind >= VATE_K_COUNT) return set_error(VATE_EVALUE, "bad kernel kind");
+  rc = collect_timing(p);
+  if (rc) return rc;
+  *total_ms = p->timed_ms[kind];
+  *launches = p->timed_n[kind];
+  return VATE_OK;
+}
+
+int vate_mark(vate_pool* p, int id) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (id < 0 || id >= 16) return set_error(VATE_EVALUE, "mark id outside [0, 16)");
+  if (!p->marks[id]) VATE_CUDA(cudaEventCreate(&p->marks[id]));
+  VATE_CUDA(cudaEventRecord(p->marks[id], p->stream));
+  return VATE_OK;
+}
+
+int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (id0 < 0 || id0 >= 16 || id1 < 0 || id1 >= 16 || !p->marks[id0] || !p->marks[id1])
+    return set_error(VATE_EVALUE, "unrecorded mark");
+  VATE_CUDA(cudaEventSynchronize(p->marks[id1]));
+  float f = 0.f;
+  VATE_CUDA(cudaEventElapsedTime(&f, p->marks[id0], p->marks[id1]));
+  *ms = f;
+  return VATE_OK;
+}
+
+// ---- ingest -----------------------------------------------------------------
+
+int vate_set_cells(vate_pool* p, const uint64_t* idx, uint64_t n, int where) {
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  if (where == VATE_HOST) {
+    for (uint64_t i = 0; i < n; ++i)
+      if (idx[i] >= p->L.size)
+        return set_error(VATE_EVALUE, "cell index " + std::to_string(idx[i]) + " outside [0, " +
+                                          std::to_string(p->L.size) + ")");
+  }
+  const void* d_idx;
+  rc = stage_in(p, p->in_a, idx, n * 8, where, &d_idx);
+  if (rc) return rc;
+  return with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_SCAN, grid_for(n, kThreads), kThreads, 0, k_set_cells<T>,
+                (const uint64_t*)d_idx, n, (T*)p->cells, p->L, p->bact0, p->d_ctr + C_ERR);
+    return VATE_OK;
+  });
+}
+
+static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const uint64_t* bips,
+                       const uint32_t* pairs, uint64_t n, int where, vate_hosts* hosts,
+                       int64_t t) {
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  if (H.g < 1 || H.g > p->L.size) return set_error(VATE_ECONFIG, "g must be in [1, 2^c]");
+  RegRef R{};
+  if (hosts) {
+    if (hosts->pool != p) return set_error(VATE_EVALUE, "host registry belongs to another pool");
+    rc = hosts_prepare_insert(hosts, n);
+    if (rc) return rc;
+    R = hosts->ref();
+  }
+  const uint32_t grid = grid_for(n, kThreads, 148u * 16u);
+  if (pairs) {
+    const void* d_pairs;
+    rc = stage_in(p, p->in_a, pairs, n * 8, where, &d_pairs);
+    if (rc) return rc;
+    const bool aligned16 = ((uintptr_t)d_pairs & 15u) == 0;
+    return with_cell(p->cell_bytes, [&](auto tag) -> int {
+      using T = decltype(tag);
+      if (aligned16 && n >= 2) {
+        if (hosts)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
+                      (long long)t);
+        else
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, false>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
+                      (long long)t);
+        if (n & 1) {
+          const uint2* last = (const uint2*)d_pairs + (n - 1);
+          if (hosts)
+            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, true>), last, 1,
+                        (T*)p->cells, H, p->L, p->bact0, R, (long long)t);
+          else
+            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, false>), last, 1,
+                        (T*)p->cells, H, p->L, p->bact0, R, (long long)t);
+        }
+      } else {
+        if (hosts)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, true>),
+                      (const uint2*)d_pairs, n, (T*)p->cells, H, p->L, p->bact0, R,
+                      (long long)t);
+        else
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, false>),
+                      (const uint2*)d_pairs, n, (T*)p->cells, H, p->L, p->bact0, R,
+                      (long long)t);
+      }
+      return VATE_OK;
+    });
+  }
+  const void *d_a, *d_b;
+  rc = stage_in(p, p->in_a, aips, n * 8, where, &d_a);
+  if (rc) return rc;
+  rc = stage_in(p, p->in_b, bips, n * 8, where, &d_b);
+  if (rc) return rc;
+  return with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    if (hosts)
+      VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_u64<T, true>), (const uint64_t*)d_a,
+                  (const uint64_t*)d_b, n, (T*)p->cells, H, p->L, p->bact0, R, (long long)t);
+    else
+      VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_u64<T, false>), (const uint64_t*)d_a,
+                  (const uint64_t*)d_b, n, (T*)p->cells, H, p->L, p->bact0, R, (long long)t);
+    return VATE_OK;
+  });
+}
+
+int vate_scan_pairs(vate_pool* p, uint64_t g, uint64_t cell_stream, uint64_t group_stream,
+                    const uint64_t* aips, const uint64_t* bips, uint64_t n, int where,
+                    vate_hosts* hosts, int64_t t) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  return scan_common(p, make_hash(g, p->c, cell_stream, group_stream), aips, bips, nullptr, n,
+                     where, hosts, t);
+}
+
+int vate_scan_packed(vate_pool* p, uint64_t g, uint64_t cell_stream, uint64_t group_stream,
+                     const uint32_t* pairs, uint64_t n, int where, vate_hosts* hosts,
+                     int64_t t) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  return scan_common(p, make_hash(g, p->c, cell_stream, group_stream), nullptr, nullptr, pairs,
+                     n, where, hosts, t);
+}
+
+int vate_pair_cells(vate_pool* p, uint64_t g, int c, uint64_t cell_stream,
+                    uint64_t group_stream, const uint64_t* aips, const uint64_t* bips,
+                    uint64_t n, int where, uint64_t* out_cells) {
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  if (c < 1 || c > 32 || g < 1 || g > (1ull << c))
+    return set_error(VATE_ECONFIG, "bad g/c for pair_cells");
+  const void *d_a, *d_b;
+  rc = stage_in(p, p->in_a, aips, n * 8, where, &d_a);
+  if (rc) return rc;
+  rc = stage_in(p, p->in_b, bips, n * 8, where, &d_b);
+  if (rc) return rc;
+  rc = p->out_buf.ensure(n * 8);
+  if (rc) return rc;
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(n, kThreads), kThreads, 0, k_pair_cells,
+              (const uint64_t*)d_a, (const uint64_t*)d_b, n, make_hash(g, c, cell_stream, group_stream),
+              p->out_buf.as<uint64_t>());
+  VATE_CUDA(cudaMemcpyAsync(out_cells, p->out_buf.ptr, n * 8, cudaMemcpyDeviceToHost, p->stream));
+  return sync_small(p);
+}
+
+int vate_host_cells(vate_pool* p, uint64_t g, int c, uint64_t cell_stream, const uint64_t* aips,
+                    uint64_t n, int where, uint64_t* out_cells) {
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  if (c < 1 || c > 32 || g < 1 || g > (1ull << c))
+    return set_error(VATE_ECONFIG, "bad g/c for host_cells");
+  const void* d_a;
+  rc = stage_in(p, p->in_a, aips, n * 8, where, &d_a);
+  if (rc) return rc;
+  rc = p->out_buf.ensure(n * g * 8);
+  if (rc) return rc;
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(n * g, kThreads), kThreads, 0, k_host_cells,
+              (const uint64_t*)d_a, n, g, make_hash(g, c, cell_stream, 0), p->out_buf.as<uint64_t>());
+  VATE_CUDA(cudaMemcpyAsync(out_cells, p->out_buf.ptr, n * g * 8, cudaMemcpyDeviceToHost, p->stream));
+  return sync_small(p);
+}
+
+// ---- maintenance --------------------------------------------------------------
+
+int vate_advance_async(vate_pool* p) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (p->adv_pending) return set_error(VATE_EVALUE, "previous advance not collected");
+  const uint32_t B = p->L.B, k = p->L.k;
+  p->bact0 = (p->bact0 + 1) % B;  // pools.py:228
+  const uint32_t z = (B - p->bact0) % B, q = (k + B - p->bact0) % B;  // pools.py:231-232
+  const uint64_t s0 = block_start(z, p->L), e0 = block_start(z + 1, p->L);
+  const uint64_t s1 = block_start(q, p->L), e1 = block_start(q + 1, p->L);
+  p->adv_blocks[0] = (int32_t)z;
+  p->adv_blocks[1] = (int32_t)q;
+  p->adv_maint = (e0 - s0) + (e1 - s1);
+  VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_CLEARED, 0, 8, p->stream));
+  rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_SWEEP, grid_for(p->adv_maint, kThreads, 148u * 8u), kThreads, 0,
+                k_sweep<T>, (T*)p->cells, s0, e0 - s0, s1, e1 - s1, k, p->d_ctr + C_CLEARED);
+    return VATE_OK;
+  });
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_CLEARED, p->d_ctr + C_CLEARED, 8, cudaMemcpyDeviceToHost,
+                            p->stream));
+  p->adv_pending = true;
+  return VATE_OK;
+}
+
+int vate_advance_result(vate_pool* p, int32_t blocks[2], uint64_t* maintained,
+                        uint64_t* cleared) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (!p->adv_pending) return set_error(VATE_EVALUE, "no advance pending");
+  rc = sync_small(p);
+  if (rc) return rc;
+  p->adv_pending = false;
+  if (blocks) {
+    blocks[0] = p->adv_blocks[0];
+    blocks[1] = p->adv_blocks[1];
+  }
+  if (maintained) *maintained = p->adv_maint;
+  if (cleared) *cleared = p->h_ctr[C_CLEARED];
+  return VATE_OK;
+}
+
+int vate_advance(vate_pool* p, int32_t blocks[2], uint64_t* maintained, uint64_t* cleared) {
+  int rc = vate_advance_async(p);
+  if (rc) return rc;
+  return vate_advance_result(p, blocks, maintained, cleared);
+}
+
+// ---- queries ------------------------------------------------------------------
+
+
+int vate_count_inactive(vate_pool* p, int k_prime, uint64_t* out) {
+  int rc = enter(p);
+  if (rc) return rc;
+  rc = check_width(p, k_prime);
+  if (rc) return rc;
+  rc = build_bitmap(p, k_prime);
+  if (rc) return rc;
+  rc = sync_small(p);
+  if (rc) return rc;
+  *out = p->h_ctr[C_P];
+  return VATE_OK;
+}
+
+int vate_inactive_mask(vate_pool* p, const uint64_t* idx, uint64_t n, int k_prime, uint8_t* out,
+                       int where) {
+  int rc = enter(p);
+  if (rc) return rc;
+  rc = check_width(p, k_prime);
+  if (rc || n == 0) return rc;
+  const void* d_idx;
+  rc = stage_in(p, p->in_a, idx, n * 8, where, &d_idx);
+  if (rc) return rc;
+  rc = p->out_buf.ensure(n);
+  if (rc) return rc;
+  rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(n, kThreads), kThreads, 0, k_mask<T>, (const T*)p->cells,
+                (const uint64_t*)d_idx, n, p->L, p->bact0, (uint32_t)k_prime,
+                p->out_buf.as<uint8_t>(), p->d_ctr + C_ERR);
+    return VATE_OK;
+  });
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_ERR, p->d_ctr + C_ERR, 8, cudaMemcpyDeviceToHost, p->stream));
+  VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_ERR, 0, 8, p->stream));
+  VATE_CUDA(cudaMemcpyAsync(out, p->out_buf.ptr, n, cudaMemcpyDeviceToHost, p->stream));
+  return sync_small(p);
+}
+
+int vate_get_cells(vate_pool* p, const uint64_t* idx, uint64_t n, uint32_t* out, int where) {
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  const void* d_idx;
+  rc = stage_in(p, p->in_a, idx, n * 8, where, &d_idx);
+  if (rc) return rc;
+  rc = p->out_buf.ensure(n * 4);
+  if (rc) return rc;
+  rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(n, kThreads), kThreads, 0, k_get<T>, (const T*)p->cells,
+                (const uint64_t*)d_idx, n, p->L.size, p->out_buf.as<uint32_t>(), p->d_ctr + C_ERR);
+    return VATE_OK;
+  });
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_ERR, p->d_ctr + C_ERR, 8, cudaMemcpyDeviceToHost, p->stream));
+  VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_ERR, 0, 8, p->stream));
+  VATE_CUDA(cudaMemcpyAsync(out, p->out_buf.ptr, n * 4, cudaMemcpyDeviceToHost, p->stream));
+  return sync_small(p);
+}
+
+// ---- snapshots ----------------------------------------------------------------
+
+static uint64_t payload_words(const vate_pool* p) {
+  return (p->L.size * p->width + 63) / 64;  // bitpack.py:36
+}
+
+int vate_snapshot_size(const vate_pool* p, uint64_t* nbytes) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  *nbytes = 16 + 8 * payload_words(p);
+  return VATE_OK;
+}
+
+int vate_snapshot(vate_pool* p, uint8_t* buf, uint64_t cap, uint64_t* len) {
+  int rc = enter(p);
+  if (rc) return rc;
+  const uint64_t nwords = payload_words(p), need = 16 + 8 * nwords;
+  if (len) *len = need;
+  if (cap < need) return set_error(VATE_EVALUE, "snapshot buffer too small");
+  // header <4sBBHH6x>: magic, c, partition, k, bact0 (pools.py:32, :261-265)
+  memset(buf, 0, 16);
+  memcpy(buf, "ATP1", 4);
+  buf[4] = (uint8_t)p->c;
+  buf[5] = (uint8_t)p->partition;
+  buf[6] = (uint8_t)(p->k & 0xFF);
+  buf[7] = (uint8_t)((p->k >> 8) & 0xFF);
+  buf[8] = (uint8_t)(p->bact0 & 0xFF);
+  buf[9] = (uint8_t)((p->bact0 >> 8) & 0xFF);
+  rc = p->out_buf.ensure(nwords * 8);
+  if (rc) return rc;
+  rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(nwords, kThreads), kThreads, 0, k_pack<T>,
+                (const T*)p->cells, p->L.size, p->width, p->out_buf.as<unsigned long long>(), nwords);
+    return VATE_OK;
+  });
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(buf + 16, p->out_buf.ptr, nwords * 8, cudaMemcpyDeviceToHost, p->stream));
+  return sync_small(p);
+}
+
+int vate_load(vate_pool* p, const uint8_t* buf, uint64_t len) {
+  int rc = enter(p);
+  if (rc) return rc;
+  // pools.py:271-298
+  if (len < 16) return set_error(VATE_ECONFIG, "pool snapshot is truncated");
+  if (memcmp(buf, "ATP1", 4) != 0) return set_error(VATE_ECONFIG, "not a pool snapshot");
+  const int c = buf[4], part = buf[5];
+  const int k = buf[6] | (buf[7] << 8);
+  const uint32_t bact0 = buf[8] | (buf[9] << 8);
+  if (part > 1) return set_error(VATE_ECONFIG, "snapshot has unknown partition code " + std::to_string(part));
+  if (c != p->c || k != p->k || part != p->partition)
+    return set_error(VATE_ECONFIG, "snapshot shape differs from this pool");
+  if (bact0 >= p->L.B)
+    return set_error(VATE_ECONFIG, "snapshot clock " + std::to_string(bact0) + " out of range");
+  const uint64_t nwords = payload_words(p);
+  if (len - 16 != nwords * 8)
+    return set_error(VATE_ECONFIG, "snapshot payload is " + std::to_string(len - 16) +
+                                       " bytes, expected " + std::to_string(nwords * 8));
+  rc = p->in_a.ensure(nwords * 8 + 8);
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(p->in_a.ptr, buf + 16, nwords * 8, cudaMemcpyHostToDevice, p->stream));
+  rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(p->L.size, kThreads), kThreads, 0, k_unpack<T>,
+                p->in_a.as<const unsigned long long>(), nwords, p->L.size, p->width, (T*)p->cells);
+    return VATE_OK;
+  });
+  if (rc) return rc;
+  rc = sync_small(p);
+  if (rc) return rc;
+  p->bact0 = bact0;
+  return VATE_OK;
+}
+
+// ---- replica merge --------------------------------------------------------------
+
+int vate_dirty_bitmap(vate_pool* p, uint32_t* bitmap_dev) {
+  int rc = enter(p);
+  if (rc) return rc;
+  const uint64_t nwords = (p->L.size + 31) / 32;
+  return with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(nwords, kThreads), kThreads, 0, k_dirty<T>,
+                (const T*)p->cells, p->L, p->bact0, bitmap_dev, nwords);
+    return VATE_OK;
+  });
+}
+
+int vate_merge_dirty(vate_pool* p, const uint32_t* bitmaps_dev, int nranks) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (nranks < 1) return set_error(VATE_EVALUE, "nranks must be >= 1");
+  const uint64_t nwords = (p->L.size + 31) / 32;
+  return with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(nwords, kThreads), kThreads, 0, k_merge<T>, (T*)p->cells,
+                p->L, p->bact0, bitmaps_dev, nwords, nranks);
+    return VATE_OK;
+  });
+}
+
+// ---- synthetic traffic ------------------------------------------------------------
+
+int vate_synth_packets(vate_pool* p, int64_t t, uint64_t n, uint64_t hosts, uint64_t base_aip,
+                       uint64_t trace_seed, uint32_t* pairs_dev) {
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  if (hosts < 1) return set_error(VATE_EVALUE, "hosts must be >= 1");
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(n, kThreads), kThreads, 0, k_synth, (long long)t, n,
+              make_div(hosts), base_aip, mix64(trace_seed ^ kSynthSalt), (uint2*)pairs_dev);
+  return VATE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// vate_registry.cuh -- device-side insert into the host registry.
+//
+// SlidingHostSet.update (pipeline.py:50-52) sets last[aip] = t for every
+// distinct aip of a slice.  On the device every packet probes the table; all
+// writers of one call store the same t, so plain stores are race-free.  Keys
+// are u64 (the reference keeps arbitrary Python ints, estimator.py:67-81).
+#pragma once
+
+#include "vate_internal.cuh"
+
+namespace vate {
+
+constexpr uint64_t kRegSalt = 0x2545F4914F6CDD1Dull;
+constexpr int kMaxProbe = 64;
+
+__device__ __forceinline__ void reg_touch(RegEntry* e, long long t, bool use_max) {
+  if (use_max) {
+    atomicMax(&e->last, t);
+  } else if (*((volatile long long*)&e->last) != t) {
+    e->last = t;
+  }
+}
+
+// Insert-or-touch.  use_max is only used when draining the overflow list,
+// where entries of several calls meet (identical to overwrite whenever slice
+// indices are non-decreasing, as Pipeline.run feeds them).
+__device__ __forceinline__ void reg_insert(const RegRef& R, uint64_t key, long long t,
+                                           bool use_max) {
+  if (key == kEmptyKey) {  // the one key that collides with the empty marker
+    RegEntry* e = R.table + (R.mask + 1);
+    if (atomicExch(R.special, 1u) == 0u) atomicAdd(R.count, 1ull);
+    reg_touch(e, t, use_max);
+    return;
+  }
+  uint64_t h = mix64(key ^ kRegSalt) & R.mask;
+#pragma unroll 1
+  for (int probe = 0; probe < kMaxProbe; ++probe) {
+    RegEntry* e = R.table + h;
+    unsigned long long k = *((volatile unsigned long long*)&e->key);
+    if (k == key) {
+      reg_touch(e, t, use_max);
+      return;
+    }
+    if (k == kEmptyKey) {
+      unsigned long long prev = atomicCAS(&e->key, kEmptyKey, key);
+      if (prev == kEmptyKey) {
+        atomicAdd(R.count, 1ull);
+        reg_touch(e, t, use_max);
+        return;
+      }
+      if (prev == key) {
+        reg_touch(e, t, use_max);
+        return;
+      }
+    }
+    h = (h + 1) & R.mask;
+  }
+  // probe limit: park it; the host drains (grows + reinserts) before any read
+  unsigned long long slot = atomicAdd(R.ovf_n, 1ull);
+  if (slot < R.ovf_cap) {
+    R.ovf[slot].key = key;
+    R.ovf[slot].last = t;
+  }
+}
+
+}  // namespace vate

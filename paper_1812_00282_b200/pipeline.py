@@ -1,0 +1,202 @@
+"""Slice driver over the device pool (reference: pipeline.py).
+
+Each slice runs the reference's three ordered phases (pipeline.py:142-160):
+scan (hash + scatter the slice's pairs, register their hosts), estimate (the
+sorted active hosts, Z_p, g0 per host, the float path, the floor filter) and
+maintain (advance the clocks, sweep the two due blocks), then prunes the host
+registry every k slices.  All three phases are CUDA kernels on the pool's
+stream; stream order gives the hard barriers between them (SURVEY.md §7 hard
+part 4).  ``workers`` is accepted for signature compatibility; the device path
+has no host thread fan-out and its output never depended on it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import VATE_DEVICE, VATE_HOST, check, lib, ptr
+from .estimator import (EstimatorConfig, HostReports, _check_pool_cfg, _ensure_log_table,
+                        _u64, context_pool, log_zp)
+from .pools import AtPool, MaintenanceReport
+
+SCAN_CHUNK = 1 << 15  # pipeline.py:26 (the device scan takes a whole slice at once)
+
+
+@dataclass(frozen=True)
+class SliceStats:
+    """Timing and maintenance accounting for one processed slice (pipeline.py:30-40)."""
+
+    slice_index: int
+    pairs: int
+    scan_us: int
+    estimate_us: int
+    maintain_us: int
+    cells_maintained: int
+    cells_cleared: int
+
+
+class SlidingHostSet:
+    """Hosts seen recently, with the slice each was last seen in (pipeline.py:43-64).
+
+    Lives on the device next to ``pool`` (or a private context pool).
+    """
+
+    def __init__(self, k: int, pool: AtPool | None = None, device: int = 0):
+        self.k = k
+        self._pool = pool if pool is not None else context_pool(device)
+        h = C.c_void_p()
+        check(lib.vate_hosts_create(C.byref(h), self._pool.handle, k))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.vate_hosts_destroy(h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def update(self, aips, t: int) -> None:
+        a = _u64(aips)
+        if a.size:
+            check(lib.vate_hosts_update(self._h, ptr(a), a.size, t, VATE_HOST))
+
+    def __len__(self) -> int:
+        n = C.c_uint64()
+        check(lib.vate_hosts_size(self._h, C.byref(n)))
+        return n.value
+
+    def active(self, t: int, k_prime: int) -> np.ndarray:
+        """Sorted hosts seen within the last k' slices."""
+        out = np.empty(len(self), dtype=np.uint64)
+        n = C.c_uint64()
+        check(lib.vate_hosts_active(self._h, t, k_prime, ptr(out), out.size, C.byref(n)))
+        return out[: n.value]
+
+    def prune(self, t: int) -> None:
+        check(lib.vate_hosts_prune(self._h, t))
+
+
+class Pipeline:
+    """Runs one device pool and estimator layout over a sliced pair stream."""
+
+    def __init__(self, pool: AtPool, cfg: EstimatorConfig, k_prime: int, floor: float = 0.0,
+                 workers: int = 1):
+        if not 1 <= k_prime <= pool.k:
+            raise ValueError(f"k'={k_prime} outside [1, {pool.k}]")
+        if workers < 1:
+            raise ValueError(f"workers must be at least 1, got {workers}")
+        _check_pool_cfg(pool, cfg)
+        self.pool = pool
+        self.cfg = cfg
+        self.k_prime = k_prime
+        self.floor = floor
+        self.workers = workers
+        self.hosts = SlidingHostSet(pool.k, pool=pool)
+        self.total_maintained = 0
+        self.total_cleared = 0
+        _ensure_log_table(pool, cfg.g)
+
+    def close(self) -> None:
+        if self.hosts is not None:
+            self.hosts.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+    # --- phases --------------------------------------------------------------------
+    def _scan(self, aips, bips) -> int:
+        a, b = _u64(aips), _u64(bips)
+        if a.shape != b.shape:
+            raise ValueError("aips and bips must have the same length")
+        if a.size:
+            check(lib.vate_scan_pairs(self.pool.handle, self.cfg.g, self.cfg.cell_stream,
+                                      self.cfg.group_stream, ptr(a), ptr(b), a.size, VATE_HOST,
+                                      self.hosts.handle, self._t))
+        return a.size
+
+    def scan_packed(self, t: int, pairs, n: int, on_device: bool) -> None:
+        """Scan packed {u32 aip, u32 bip} records and register their hosts in slice t."""
+        check(lib.vate_scan_packed(self.pool.handle, self.cfg.g, self.cfg.cell_stream,
+                                   self.cfg.group_stream, int(pairs), int(n),
+                                   VATE_DEVICE if on_device else VATE_HOST,
+                                   self.hosts.handle, t))
+
+    def estimate_soa(self, t: int, out=None) -> HostReports | None:
+        """The estimate phase (pipeline.py:120-138) as arrays; None without hosts.
+
+        ``out`` may supply preallocated (pinned) host arrays
+        (host u64, estimate f64, z_v f64, saturated u8) of equal capacity.
+        """
+        nh, p = C.c_uint64(), C.c_uint64()
+        check(lib.vate_estimate_begin(self.pool.handle, self.hosts.handle, self.cfg.g,
+                                      self.cfg.cell_stream, t, self.k_prime, C.byref(nh),
+                                      C.byref(p)))
+        n = nh.value
+        if n == 0:
+            return None
+        lzp, z_p = log_zp(p.value, self.pool.size)
+        if out is None or len(out[0]) < n:
+            out = (np.empty(n, np.uint64), np.empty(n, np.float64), np.empty(n, np.float64),
+                   np.empty(n, np.uint8))
+        host, est, zv, sat = out
+        kept = C.c_uint64()
+        check(lib.vate_estimate_finish(self.pool.handle, self.cfg.g, p.value, lzp,
+                                       float(self.floor), ptr(host), ptr(est), ptr(zv), ptr(sat),
+                                       len(host), C.byref(kept)))
+        m = kept.value
+        self.last_pool_inactive = p.value
+        self.last_active = n
+        return HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool), z_p,
+                           t - self.k_prime + 1, self.k_prime)
+
+    def _maintain(self, t: int) -> MaintenanceReport:
+        rep = self.pool.advance_slice()
+        self.total_maintained += rep.cells_maintained
+        self.total_cleared += rep.cells_cleared
+        if t % max(1, self.pool.k) == 0:
+            self.hosts.prune(t)
+        return rep
+
+    # --- driving ---------------------------------------------------------------------
+    def process_slice_soa(self, t: int, aips, bips, out=None):
+        """All three phases for slice t; returns (HostReports | None, SliceStats)."""
+        t0 = time.perf_counter_ns()
+        self._t = t
+        n = self._scan(aips, bips)
+        t1 = time.perf_counter_ns()
+        reports = self.estimate_soa(t, out)
+        t2 = time.perf_counter_ns()
+        rep = self._maintain(t)
+        t3 = time.perf_counter_ns()
+        stats = SliceStats(t, n, (t1 - t0) // 1000, (t2 - t1) // 1000, (t3 - t2) // 1000,
+                           rep.cells_maintained, rep.cells_cleared)
+        self.last_maintenance = rep
+        return reports, stats
+
+    def process_slice(self, t: int, aips, bips):
+        """Run all three phases for slice t; returns (reports, stats) (pipeline.py:142-160)."""
+        soa, stats = self.process_slice_soa(t, aips, bips)
+        return ([] if soa is None else soa.to_list()), stats
+
+    def run(self, sliced):
+        """Process a (slice, aips, bips) stream; yields (t, reports, stats)."""
+        for t, aips, bips in sliced:
+            reports, stats = self.process_slice(t, aips, bips)
+            yield t, reports, stats

@@ -1,0 +1,452 @@
+"""CUDA path vs the oracle and the reference goldens (B200 only).
+
+Bar: bit-exact for every integer / byte / index result (cells, snapshots,
+P, g0, host sets, maintenance reports); the floats of the estimate are
+compared bit-for-bit against the oracle run on the same machine (same numpy)
+and within rel 1e-12 against the goldens recorded in the build container
+(the north star allows 1e-6).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from _golden import PIPE_NAMES, PipeCase, load
+from oracle import vate_oracle as vo
+
+pytestmark = pytest.mark.gpu
+
+vb = pytest.importorskip("paper_1812_00282_b200")
+
+REL = 1e-12   # float tolerance against goldens made on another machine's numpy
+
+
+def _cfgs(spec):
+    cfg = vb.EstimatorConfig(spec["g"], spec["c"], spec["k"], seed=spec["seed"],
+                             partition=spec["part"])
+    ocfg = vo.OracleConfig(spec["g"], spec["c"], spec["k"], seed=spec["seed"],
+                           partition=spec["part"])
+    return cfg, ocfg
+
+
+# --- hashing ------------------------------------------------------------------------
+
+def test_pair_cells_matches_reference_hashes():
+    kat = load("hash_kats.npz")
+    # pair_cells = cell_index(aip, group_index(bip)); check both halves via goldens
+    for si, seed in enumerate(kat["seeds"]):
+        for c in (5, 20, 28, 32):
+            g = 1024 if c >= 10 else 32
+            cfg = vb.EstimatorConfig(g, c, 2, seed=int(seed))
+            got = vb.pair_cells(cfg, kat["aips"], kat["bips"])
+            want = vo.OracleConfig(g, c, 2, seed=int(seed)).pair_cells(kat["aips"], kat["bips"])
+            assert np.array_equal(got, want), (seed, c)
+
+
+def test_host_cells_matches_reference_hashes():
+    kat = load("hash_kats.npz")
+    cfg = vb.EstimatorConfig(1000, 24, 2, seed=7)
+    aips = kat["aips"][:64]
+    got = vb.host_cells(cfg, aips)
+    want = vo.OracleConfig(1000, 24, 2, seed=7).host_cells(aips)
+    assert np.array_equal(got, want)
+
+
+def test_non_power_of_two_group_counts():
+    kat = load("hash_kats.npz")
+    for g in (1, 3, 1000, (1 << 20) + 7):
+        cfg = vb.EstimatorConfig(g, 24, 2, seed=1)
+        got = vb.pair_cells(cfg, kat["aips"], kat["bips"])
+        want = vo.OracleConfig(g, 24, 2, seed=1).pair_cells(kat["aips"], kat["bips"])
+        assert np.array_equal(got, want), g
+
+
+# --- whole pipelines against the reference goldens ---------------------------------
+
+@pytest.mark.parametrize("name", PIPE_NAMES)
+def test_pipeline_matches_reference_goldens(name):
+    case = PipeCase(name)
+    spec = case.spec
+    cfg, ocfg = _cfgs(spec)
+    pool = cfg.build_pool()
+    pipe = vb.Pipeline(pool, cfg, spec["kp"], floor=spec["floor"])
+    opipe = vo.OraclePipeline(ocfg, spec["kp"], floor=spec["floor"])
+    for s, (t, aips, bips) in enumerate(case.slices()):
+        got, stats = pipe.process_slice_soa(t, aips, bips)
+        want = opipe.process_slice(t, aips, bips)
+        assert stats.pairs == len(aips)
+        if len(case.live[s]) == 0:
+            assert got is None and want.reports is None
+        else:
+            assert pipe.last_active == len(case.live[s])
+            assert pipe.last_pool_inactive == case.p[s], (name, t)
+            # host set after the floor: identical to the reference
+            assert np.array_equal(got.host, case.kept[s]), (name, t)
+            # floats: bit-identical to the oracle on this machine ...
+            assert np.array_equal(got.estimate, want.reports.estimate), (name, t)
+            assert np.array_equal(got.z_v, want.reports.z_v), (name, t)
+            assert np.array_equal(got.saturated, want.reports.saturated), (name, t)
+            assert got.z_p == want.reports.z_p == case.zp[s]
+            # ... and within REL of the reference's recorded floats
+            keep = np.isin(case.live[s], case.kept[s])
+            np.testing.assert_allclose(got.estimate, case.est[s][keep], rtol=REL, atol=0)
+            assert np.array_equal(got.z_v, case.zv[s][keep])
+        m = pipe.last_maintenance
+        assert (m.blocks, m.cells_maintained, m.cells_cleared) == \
+            (tuple(case.blocks[s]), case.maintained[s], case.cleared[s]), (name, t)
+        assert pool.bact0 == case.bact0[s]
+        snap = pool.snapshot_bytes()
+        assert hashlib.sha256(snap).hexdigest() == case.snap_sha[s], (name, t)
+    if case.final_snapshot:
+        assert pool.snapshot_bytes() == case.final_snapshot
+    pipe.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1_small", "kprime_floor", "g1000_big_keys"])
+def test_list_api_matches_oracle(name):
+    case = PipeCase(name)
+    spec = case.spec
+    cfg, ocfg = _cfgs(spec)
+    pipe = vb.Pipeline(cfg.build_pool(), cfg, spec["kp"], floor=spec["floor"])
+    opipe = vo.OraclePipeline(ocfg, spec["kp"], floor=spec["floor"])
+    for t, aips, bips in case.slices()[:8]:
+        reports, _ = pipe.process_slice(t, aips, bips)
+        want = opipe.process_slice(t, aips, bips).reports
+        if want is None:
+            assert reports == []
+            continue
+        assert [r.host for r in reports] == want.host.tolist()
+        assert [r.estimate for r in reports] == want.estimate.tolist()
+        assert all(r.window_start == t - spec["kp"] + 1 and r.k_prime == spec["kp"]
+                   for r in reports)
+        assert all(r.slice_end == t for r in reports)
+    pipe.close()
+
+
+def test_appendix_b_digest():
+    ab = load("appendix_b.npz")
+    cfg = vb.EstimatorConfig(g=1024, c=20, k=10, seed=0)
+    pool = cfg.build_pool()
+    rng = np.random.default_rng(0)
+    for t in range(25):
+        a = (0x0A000000 + rng.integers(0, 10_000, 100_000)).astype(np.uint64)
+        b = rng.integers(1, 2 ** 32, 100_000).astype(np.uint64)
+        vb.record_pairs(pool, cfg, a, b)
+        if t == 24:
+            assert pool.count_inactive(10) == 422445
+            reps = vb.estimate_hosts(pool, cfg, ab["hosts24"], 24, 10)
+            np.testing.assert_allclose([r.estimate for r in reps], ab["est24"], rtol=REL)
+            assert [r.z_v for r in reps] == ab["zv24"].tolist()
+        rep = pool.advance_slice()
+    assert pool.bact0 == 5
+    assert rep == vb.MaintenanceReport((15, 5), 110376, 27266)
+    snap = pool.snapshot_bytes()
+    assert len(snap) == 655_376
+    assert hashlib.sha256(snap).hexdigest() == \
+        "75f3db138a48c85aee504bafe7d088f4c34cf81ae10c423c21d2d4049a621a24"
+
+
+# --- the pool protocol against a brute-force model (test_pools.py:120-149) ---------
+
+@pytest.mark.parametrize("partition", ["tail", "low-dev"])
+@pytest.mark.parametrize("k", [1, 4, 9, 70, 130])
+def test_pool_matches_brute_force(partition, k):
+    if partition == "tail" and k == 1:
+        partition = "low-dev"
+    c = 9 if k < 70 else 12
+    pool = vb.AtPool(c, k, partition)
+    size = pool.size
+    rng = np.random.default_rng(100 * k + 7)
+    last_set = {}
+    everything = np.arange(size, dtype=np.uint64)
+    widths = sorted({1, max(1, k // 2), k})
+    for t in range(min(20 * k + 15, 300)):
+        idx = rng.integers(0, size, size=25).astype(np.uint64)   # duplicates allowed
+        pool.set_many(idx)
+        for i in idx.tolist():
+            last_set[i] = t
+        one = int(rng.integers(0, size))
+        pool.set_one(one)
+        last_set[one] = t
+        for w in widths:
+            mask = pool.inactive_mask(everything, w)
+            want = np.array([i not in last_set or t - last_set[i] >= w for i in range(size)])
+            assert np.array_equal(mask, want), f"slice {t} width {w}"
+            assert pool.count_inactive(w) == int(want.sum())
+        for i in (0, one, size - 1):
+            assert pool.check_one(i, k) == (i in last_set and t - last_set[i] < k)
+        pool.advance_slice()
+
+
+def test_pool_errors():
+    pool = vb.AtPool(7, 4)
+    with pytest.raises(ValueError):
+        pool.count_inactive(0)
+    with pytest.raises(ValueError):
+        pool.count_inactive(5)
+    with pytest.raises(ValueError):
+        pool.check_one(200, 2)
+    with pytest.raises(ValueError):
+        pool.set_many(np.array([128], dtype=np.uint64))
+    with pytest.raises(ValueError):
+        pool.inactive_mask(np.array([5000], dtype=np.uint64), 2)
+    with pytest.raises(vb.ConfigError):
+        vb.make_pool("dr", 7, 4)
+    with pytest.raises(vb.ConfigError):
+        vb.make_pool("hll", 7, 4)
+    # the pool keeps working after a rejected call
+    pool.set_many(np.array([3], dtype=np.uint64))
+    assert pool.check_one(3, 1)
+
+
+def test_two_blocks_maintained_per_slice():
+    pool = vb.AtPool(10, 6)
+    k, cycle = pool.k, pool.nblocks
+    per_cell = np.zeros(pool.size, dtype=np.int64)
+    for step in range(2 * cycle):
+        rep = pool.advance_slice()
+        assert len(rep.blocks) == 2 and rep.blocks[0] != rep.blocks[1]
+        assert pool.block_act(rep.blocks[0]) == 0
+        assert pool.block_act(rep.blocks[1]) == k
+        span = 0
+        for bi in rep.blocks:
+            lo, hi = pool.block_range(bi)
+            per_cell[lo:hi] += 1
+            span += hi - lo
+        assert rep.cells_maintained == span <= 2 * pool.max_block_size
+        if (step + 1) % cycle == 0:
+            assert np.all(per_cell == 2)
+            per_cell[:] = 0
+
+
+def test_cell_widths_and_memory():
+    assert vb.AtPool(10, 300).bits_per_counter == 10
+    assert vb.AtPool(10, 300).cell_bytes == 2
+    assert vb.AtPool(10, 127).cell_bytes == 1
+    assert vb.AtPool(17, 1 << 15, "low-dev").cell_bytes == 4
+    p = vb.AtPool(20, 300)
+    assert p.packed_bytes == (-(-(1 << 20) * 10 // 64) + 1) * 8 + 16   # test_pools.py:249-254
+
+
+# --- snapshots ------------------------------------------------------------------------
+
+def test_snapshot_load_of_reference_bytes(tmp_path):
+    snap = load("snapshot_c8k9.npz")
+    blob = snap["blob"].tobytes()
+    path = tmp_path / "pool.snap"
+    path.write_bytes(blob)
+    pool = vb.AtPool.load(path)
+    assert pool.snapshot_bytes() == blob
+    assert pool.count_inactive(9) == int(snap["count9"])
+    opool = vo.OraclePool.from_snapshot(blob)
+    pool.advance_slice()
+    opool.advance()
+    assert pool.snapshot_bytes() == opool.snapshot_bytes()
+    for bad in (b"XXXX" + blob[4:], blob[:8], blob[:-8]):
+        path.write_bytes(bad)
+        with pytest.raises(vb.ConfigError):
+            vb.AtPool.load(path)
+
+
+@pytest.mark.parametrize("c,k,part", [(10, 4, "tail"), (12, 300, "tail"), (9, 33, "low-dev"),
+                                      (17, 1 << 15, "low-dev"), (3, 2, "tail")])
+def test_snapshot_roundtrip_all_cell_widths(c, k, part):
+    pool = vb.AtPool(c, k, part)
+    opool = vo.OraclePool(c, k, part)
+    rng = np.random.default_rng(c * k)
+    for _ in range(min(3 * k, 40)):
+        idx = rng.integers(0, pool.size, size=max(1, pool.size // 7)).astype(np.uint64)
+        pool.set_many(idx)
+        opool.set_cells(idx)
+        pool.advance_slice()
+        opool.advance()
+    blob = pool.snapshot_bytes()
+    assert blob == opool.snapshot_bytes()
+    back = vb.AtPool.from_bytes(blob)
+    assert back.snapshot_bytes() == blob
+    assert back.count_inactive(k) == pool.count_inactive(k) == opool.count_inactive(k)
+
+
+# --- estimator entry points ---------------------------------------------------------
+
+def test_estimate_hosts_arbitrary_order_and_duplicates():
+    cfg = vb.EstimatorConfig(512, 16, 8, seed=4)
+    ocfg = vo.OracleConfig(512, 16, 8, seed=4)
+    pool = cfg.build_pool()
+    opool = vo.OraclePool(16, 8)
+    rng = np.random.default_rng(9)
+    a = rng.integers(0, 500, 20000).astype(np.uint64)
+    b = rng.integers(0, 1 << 40, 20000).astype(np.uint64)
+    vb.record_pairs(pool, cfg, a, b)
+    opool.set_cells(ocfg.pair_cells(a, b))
+    hosts = np.array([7, 3, 7, 499, 0, 1 << 45, 3], dtype=np.uint64)
+    got = vb.estimate_hosts_soa(pool, cfg, hosts, 5, 8)
+    want = vo.estimate_soa(opool, ocfg, hosts, 5, 8)
+    assert np.array_equal(got.host, hosts)
+    assert np.array_equal(got.estimate, want.estimate)
+    assert np.array_equal(vb.inactive_virtual_counts(pool, cfg, hosts, 3),
+                          vo.host_g0(opool, ocfg, hosts, 3))
+    r = vb.estimate_host(pool, cfg, 7, 5, 8)
+    assert r.estimate == got.estimate[0] and r.host == 7
+
+
+def test_reports_from_counts_edge_cases():
+    kat = load("estimator_kats.npz")
+    for i in range(int(kat["n"][0])):
+        g, c, p = (int(x) for x in kat[f"c{i}_meta"])
+        cfg = vb.EstimatorConfig(g, c, 8)
+        g0 = kat[f"c{i}_g0"]
+        rep = vb.reports_from_counts_soa(cfg, np.arange(len(g0)), g0, p, 10, 8)
+        ocfg = vo.OracleConfig(g, c, 8)
+        want = vo.reports_soa(ocfg, np.arange(len(g0)), g0, p, 10, 8)
+        assert np.array_equal(rep.estimate, want.estimate), (g, c, p)
+        assert np.array_equal(rep.z_v, want.z_v) and np.array_equal(rep.saturated, want.saturated)
+        np.testing.assert_allclose(rep.estimate, kat[f"c{i}_est"], rtol=REL, atol=0)
+    with pytest.raises(ValueError):
+        vb.reports_from_counts(vb.EstimatorConfig(64, 10, 4), [1], [65], 10, 0, 1)
+
+
+def test_duplicate_pairs_and_order_do_not_matter():
+    cfg = vb.EstimatorConfig(128, 12, 4, seed=3)
+    rng = np.random.default_rng(4)
+    aips = rng.integers(0, 30, size=2000).astype(np.uint64)
+    bips = rng.integers(0, 5000, size=2000).astype(np.uint64)
+    perm = rng.permutation(2000)
+    a_pool, b_pool = cfg.build_pool(), cfg.build_pool()
+    vb.record_pairs(a_pool, cfg, aips, bips)
+    vb.record_pairs(b_pool, cfg, np.concatenate([aips[perm], aips]),
+                    np.concatenate([bips[perm], bips]))
+    assert a_pool.snapshot_bytes() == b_pool.snapshot_bytes()
+
+
+def test_packed_scan_equals_u64_scan():
+    cfg = vb.EstimatorConfig(1024, 20, 10, seed=0)
+    p1, p2 = cfg.build_pool(), cfg.build_pool()
+    rng = np.random.default_rng(2)
+    for n in (1, 2, 3, 1001, 65536):
+        a = rng.integers(0, 1 << 32, n, dtype=np.uint64)
+        b = rng.integers(0, 1 << 32, n, dtype=np.uint64)
+        vb.record_pairs(p1, cfg, a, b)
+        vb.record_packed(p2, cfg, np.stack([a, b], axis=1).astype(np.uint32))
+        assert p1.snapshot_bytes() == p2.snapshot_bytes(), n
+        p1.advance_slice()
+        p2.advance_slice()
+
+
+# --- host registry (test_pipeline.py:100-125) ----------------------------------------
+
+def test_host_registry_window():
+    reg = vb.SlidingHostSet(4)
+    reg.update(np.array([1, 2], dtype=np.uint64), 0)
+    reg.update(np.array([3], dtype=np.uint64), 2)
+    assert list(reg.active(2, 3)) == [1, 2, 3]
+    assert list(reg.active(2, 1)) == [3]
+    assert list(reg.active(4, 4)) == [3]
+    reg.prune(6)
+    assert list(reg.active(6, 4)) == []
+    assert len(reg) == 0
+
+
+def test_host_registry_growth_matches_dict():
+    reg = vb.SlidingHostSet(50)
+    ref = vo.OracleHosts(50)
+    rng = np.random.default_rng(5)
+    for t in range(60):
+        n = int(rng.integers(0, 200_000))
+        keys = rng.integers(0, 1 << 20, n).astype(np.uint64)
+        if t % 7 == 3:
+            keys = np.concatenate([keys, [np.uint64((1 << 64) - 1), np.uint64(0)]])
+        if t % 5 == 1:
+            keys = rng.integers(0, 1 << 64, n, dtype=np.uint64)
+        reg.update(keys, t)
+        ref.update(keys, t)
+        kp = 1 + t % 50
+        assert np.array_equal(reg.active(t, kp), ref.active(t, kp)), t
+        if t % 50 == 0:
+            reg.prune(t)
+            ref.prune(t)
+        assert len(reg) == len(ref.last)
+
+
+def test_hosts_age_out_of_reports():
+    cfg = vb.EstimatorConfig(64, 12, 6, seed=6)
+    quiet = np.empty(0, dtype=np.uint64)
+    peers = np.arange(100, 130, dtype=np.uint64)
+    sliced = [(0, np.full(30, 9, dtype=np.uint64), peers)]
+    sliced += [(t, quiet, quiet) for t in range(1, 5)]
+    with vb.Pipeline(cfg.build_pool(), cfg, 2, floor=0.0) as pipe:
+        seen = {t: [r.host for r in reports] for t, reports, _ in pipe.run(iter(sliced))}
+    assert seen == {0: [9], 1: [9], 2: [], 3: [], 4: []}
+
+
+def test_pipeline_rejects_bad_args():
+    cfg = vb.EstimatorConfig(64, 10, 4)
+    pool = cfg.build_pool()
+    for kp, workers in ((0, 1), (5, 1), (4, 0)):
+        with pytest.raises(ValueError):
+            vb.Pipeline(pool, cfg, kp, workers=workers)
+
+
+# --- full BASELINE sizes: size-independent properties ---------------------------------
+
+def _sample_hosts(pipe_hosts, n, seed):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(pipe_hosts, size=min(n, len(pipe_hosts)), replace=False))
+
+
+@pytest.mark.parametrize("c,k,hosts,pkts,slices", [(24, 60, 1_000_000, 5_000_000, 8),
+                                                   (26, 60, 1_000_000, 5_000_000, 4)])
+def test_full_size_u8_pipeline_against_oracle(c, k, hosts, pkts, slices):
+    """BASELINE cfg 2/3 shapes: snapshot, P, the active host count and g0 of sampled
+    hosts equal the oracle replaying the same synthetic packets."""
+    cfg = vb.EstimatorConfig(1024, c, k)
+    ocfg = vo.OracleConfig(1024, c, k)
+    pool = cfg.build_pool()
+    pipe = vb.Pipeline(pool, cfg, k)
+    opool = vo.OraclePool(c, k)
+    seen = set()
+    for t in range(slices):
+        a, b = vo.synthetic_slice(t, pkts, hosts)
+        got, _ = pipe.process_slice_soa(t, a, b)
+        opool.set_cells(ocfg.pair_cells(a, b))
+        seen.update(np.unique(a).tolist())
+        assert pipe.last_active == len(seen)
+        assert pipe.last_pool_inactive == opool.count_inactive(k)
+        assert np.all(np.diff(got.host.astype(np.int64)) > 0)
+        sample = _sample_hosts(got.host, 3000, t)
+        idx = np.searchsorted(got.host, sample)
+        want = vo.reports_soa(ocfg, sample, vo.host_g0(opool, ocfg, sample, k),
+                              pipe.last_pool_inactive, t, k)
+        assert np.array_equal(got.estimate[idx], want.estimate)
+        due, visited, cleared = opool.advance()
+        m = pipe.last_maintenance
+        assert (m.blocks, m.cells_maintained, m.cells_cleared) == (due, visited, cleared)
+    assert hashlib.sha256(pool.snapshot_bytes()).digest() == \
+        hashlib.sha256(opool.snapshot_bytes()).digest()
+
+
+def test_full_size_u16_pool_c28_k300():
+    """BASELINE cfg 4 shape (512 MiB of u16 cells, beyond L2): P, sampled cells and
+    sampled g0 equal the oracle replaying the same packets."""
+    c, k = 28, 300
+    cfg = vb.EstimatorConfig(1024, c, k)
+    ocfg = vo.OracleConfig(1024, c, k)
+    pool = cfg.build_pool()
+    assert pool.cell_bytes == 2
+    pipe = vb.Pipeline(pool, cfg, k)
+    opool = vo.OraclePool(c, k)
+    for t in range(3):
+        a, b = vo.synthetic_slice(t, 2_000_000, 1_000_000)
+        got, _ = pipe.process_slice_soa(t, a, b)
+        opool.set_cells(ocfg.pair_cells(a, b))
+        assert pipe.last_pool_inactive == opool.count_inactive(k)
+        sample = _sample_hosts(got.host, 1000, t)
+        idx = np.searchsorted(got.host, sample)
+        want = vo.reports_soa(ocfg, sample, vo.host_g0(opool, ocfg, sample, k),
+                              pipe.last_pool_inactive, t, k)
+        assert np.array_equal(got.estimate[idx], want.estimate)
+        due, visited, cleared = opool.advance()
+        assert pipe.last_maintenance.cells_cleared == cleared
+        cells = np.random.default_rng(t).integers(0, 1 << c, 100_000, dtype=np.uint64)
+        assert np.array_equal(pool.cells.get(cells), opool.cells[cells.astype(np.int64)])
