@@ -200,6 +200,7 @@ def run_gpu(args, rank, world, local_rank):
     pool = cfg.build_pool(device=dev)
     pipe = vb.Pipeline(pool, cfg, w["k_prime"], floor=w["floor"])
     h = pool.handle
+    check(lib.vate_pool_set_option(h, 0, ("auto", "gather", "smem").index(args.g0_kernel)))
     n = w["packets"]
     slice_bytes = n * 8
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -222,13 +223,13 @@ def run_gpu(args, rank, world, local_rank):
 
     def step(t, on_device):
         src = dring[t % ring].data_ptr() if on_device else hring[t % ring].data_ptr()
-        pipe.scan_packed(t, src, n, on_device)
         if merger is not None:
+            pipe.scan_packed(t, src, n, on_device)
             merger.merge()
             rep = merger.estimate(pipe, t, outs)
+            pipe._maintain(t)
         else:
-            rep = pipe.estimate_soa(t, outs)
-        pipe._maintain(t)
+            rep = pipe.step_packed(t, src, n, on_device, outs)
         return 0 if rep is None else len(rep)
 
     t = 0
@@ -335,6 +336,7 @@ def run_gpu(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": slice_bytes,
                 "d2h_bytes_per_step": int(e2e_rows / args.steps * 25)},
         "gpu_launches": int(launches),
+        "g0_kernel": args.g0_kernel,
         "clocks": clocks.summary(),
     }
     if cpu_mean is not None:
@@ -382,6 +384,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("vate", "reference"), default="vate")
+    ap.add_argument("--g0-kernel", choices=("auto", "gather", "smem"), default="auto",
+                    help="g0 gather variant (VATE_OPT_G0)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be at least 3")

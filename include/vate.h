@@ -69,6 +69,11 @@ int vate_pool_timing(vate_pool* p, int kind, double* total_ms, uint64_t* launche
 int vate_mark(vate_pool* p, int id);
 int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
 
+/* tuning switches (bench / tests): VATE_OPT_G0 = 0 auto, 1 L2-gather kernel,
+ * 2 shared-memory / cluster-DSMEM kernel (c <= 24 only). */
+enum vate_option { VATE_OPT_G0 = 0 };
+int vate_pool_set_option(vate_pool* p, int option, int64_t value);
+
 enum vate_kernel_kind {
   VATE_K_SCAN = 0,     /* record_pairs / set_many scatter      */
   VATE_K_REGISTRY = 1, /* host-registry update / compaction    */

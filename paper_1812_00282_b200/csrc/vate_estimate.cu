@@ -3,6 +3,7 @@
 //
 // Reference: estimator.py:107-181 (host_cells, inactive_virtual_counts,
 // reports_from_counts, estimate_hosts), pipeline.py:120-138 (_estimate).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -60,6 +61,132 @@ __global__ void __launch_bounds__(kThreads) k_g0(const uint64_t* __restrict__ ho
   }
 }
 
+// The same gather with the inactive bitmap in shared memory.  For c <= 20 one
+// CTA holds the whole bitmap (<= 128 KB); for 20 < c <= 24 a thread-block
+// cluster of 2^(c-20) CTAs holds it, 128 KB per CTA, and a gather of cell x
+// reads word (x mod 2^20)/32 of CTA x >> 20 through distributed shared memory
+// (mapa + ld.shared::cluster).  Random 4-byte LDGs are bound by the L1TEX
+// wavefront rate (one 128-B line per cycle per SM); shared-memory loads are
+// bound by bank conflicts instead.
+__device__ __forceinline__ uint32_t ld_dsmem(uint32_t local_addr, uint32_t rank) {
+  uint32_t remote, v;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
+  asm("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote));
+  return v;
+}
+
+constexpr int kDsmemLog2Bits = 20;  // bits held per CTA (128 KB)
+constexpr int kDsmemThreads = 1024;
+
+template <int LPH, bool CLUSTER>
+__global__ void __launch_bounds__(kDsmemThreads, 1) k_g0_smem(
+    const uint64_t* __restrict__ hosts, uint64_t n, const uint32_t* __restrict__ bitmap,
+    uint32_t words_per_cta, HashParams H, int32_t* __restrict__ g0) {
+  extern __shared__ uint4 smem4[];
+  namespace cg = cooperative_groups;
+  uint32_t rank = 0;
+  if (CLUSTER) rank = cg::this_cluster().block_rank();
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(bitmap + (uint64_t)rank * words_per_cta);
+    for (uint32_t i = threadIdx.x; i < words_per_cta / 4; i += blockDim.x) smem4[i] = __ldcg(src + i);
+    const uint32_t* s1 = bitmap + (uint64_t)rank * words_per_cta;
+    for (uint32_t i = (words_per_cta / 4) * 4 + threadIdx.x; i < words_per_cta; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(smem4)[i] = s1[i];
+  }
+  if (CLUSTER) cg::this_cluster().sync();
+  else __syncthreads();
+  const uint32_t* sbits = reinterpret_cast<const uint32_t*>(smem4);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sbits);
+  const uint64_t local_mask = (1ull << kDsmemLog2Bits) - 1;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & (LPH - 1);
+  const unsigned gmask = LPH == 32 ? 0xffffffffu : (((1u << LPH) - 1u) << (lane & ~(LPH - 1)));
+  const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / LPH;
+  const uint64_t step = (uint64_t)LPH * kPhi;
+  const uint64_t g = H.g;
+  auto bit = [&](uint64_t c) -> uint32_t {
+    uint32_t w;
+    if (CLUSTER) w = ld_dsmem(sbase + (uint32_t)((c & local_mask) >> 5) * 4u,
+                              (uint32_t)(c >> kDsmemLog2Bits));
+    else w = sbits[c >> 5];
+    return (w >> (c & 31)) & 1u;
+  };
+  for (uint64_t h = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPH; h < n; h += groups) {
+    const uint64_t aip = hosts[h];
+    uint64_t x = ((uint64_t)((uint32_t)aip * (uint32_t)kPhi) << 32) + H.cs + (uint64_t)sub * kPhi;
+    uint32_t cnt = 0;
+    uint64_t j = sub;
+    for (; j + 3 * LPH < g; j += 4 * LPH) {
+      const uint64_t c0 = mix64(x) & H.cmask;
+      const uint64_t c1 = mix64(x + step) & H.cmask;
+      const uint64_t c2 = mix64(x + 2 * step) & H.cmask;
+      const uint64_t c3 = mix64(x + 3 * step) & H.cmask;
+      cnt += bit(c0) + bit(c1) + bit(c2) + bit(c3);
+      x += 4 * step;
+    }
+    for (; j < g; j += LPH) {
+      cnt += bit(mix64(x) & H.cmask);
+      x += step;
+    }
+#pragma unroll
+    for (int o = LPH / 2; o; o >>= 1) cnt += __shfl_xor_sync(gmask, cnt, o);
+    if (sub == 0) g0[h] = (int32_t)cnt;
+  }
+  if (CLUSTER) cg::this_cluster().sync();  // peers may still read this CTA's bits
+}
+
+template <int LPH>
+static int launch_g0_smem(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H,
+                          int32_t* g0_dev) {
+  const uint64_t nbits = p->L.size;
+  const uint32_t cs = nbits > (1ull << kDsmemLog2Bits) ? (uint32_t)(nbits >> kDsmemLog2Bits) : 1u;
+  const uint32_t words = (uint32_t)((nbits / cs + 31) / 32);
+  const size_t smem = ((size_t)words * 4 + 15) & ~size_t(15);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.blockDim = dim3(kDsmemThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = p->stream;
+  if (cs > 1) {
+    auto kern = k_g0_smem<LPH, true>;
+    VATE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (cs > 8) VATE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (p->dsmem_clusters < 0) {
+      int nc = 0;
+      cfg.gridDim = dim3(cs);
+      VATE_CUDA(cudaOccupancyMaxActiveClusters(&nc, kern, &cfg));
+      p->dsmem_clusters = nc;
+    }
+    if (p->dsmem_clusters < 1) return set_error(VATE_ECUDA, "no room for a DSMEM cluster");
+    cfg.gridDim = dim3((uint32_t)p->dsmem_clusters * cs);
+    cudaEvent_t ta = nullptr;
+    timing_begin(p, VATE_K_G0, &ta);
+    VATE_CUDA(cudaLaunchKernelEx(&cfg, kern, hosts_dev, n, p->bitmap.as<const uint32_t>(), words, H,
+                                 g0_dev));
+    timing_end(p, VATE_K_G0, ta);
+  } else {
+    auto kern = k_g0_smem<LPH, false>;
+    VATE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+    cfg.gridDim = dim3((uint32_t)sms);
+    cfg.numAttrs = 0;
+    cudaEvent_t ta = nullptr;
+    timing_begin(p, VATE_K_G0, &ta);
+    VATE_CUDA(cudaLaunchKernelEx(&cfg, kern, hosts_dev, n, p->bitmap.as<const uint32_t>(), words, H,
+                                 g0_dev));
+    timing_end(p, VATE_K_G0, ta);
+  }
+  p->launches++;
+  return VATE_OK;
+}
+
 static int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H,
                      int32_t* g0_dev) {
   // lanes per host: the next power of two >= g, at most a warp
@@ -68,6 +195,19 @@ static int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashPa
   const uint64_t threads = n * (uint64_t)lph;
   const uint32_t grid = grid_for(threads, kThreads, 148u * 64u);
   const uint32_t* bm = p->bitmap.as<const uint32_t>();
+  // the smem/DSMEM gather needs the whole bitmap in <= 16 CTAs of 128 KB
+  const bool smem_ok = p->c <= kDsmemLog2Bits + 4 && p->c >= 5;
+  const bool use_smem = smem_ok && (p->opt_g0 == 2 || (p->opt_g0 == 0 && p->c <= kDsmemLog2Bits + 4));
+  if (use_smem) {
+    switch (lph) {
+      case 1: return launch_g0_smem<1>(p, hosts_dev, n, H, g0_dev);
+      case 2: return launch_g0_smem<2>(p, hosts_dev, n, H, g0_dev);
+      case 4: return launch_g0_smem<4>(p, hosts_dev, n, H, g0_dev);
+      case 8: return launch_g0_smem<8>(p, hosts_dev, n, H, g0_dev);
+      case 16: return launch_g0_smem<16>(p, hosts_dev, n, H, g0_dev);
+      default: return launch_g0_smem<32>(p, hosts_dev, n, H, g0_dev);
+    }
+  }
   switch (lph) {
     case 1: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<1>, hosts_dev, n, bm, H, g0_dev); break;
     case 2: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<2>, hosts_dev, n, bm, H, g0_dev); break;
@@ -345,22 +485,26 @@ int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t ce
   if (rc) return rc;
   if (g < 1 || g > p->L.size) return set_error(VATE_ECONFIG, "g must be in [1, 2^c]");
   p->est_n = 0;
+  // one host round trip per estimate: Z_p (bitmap pass) and the active-set
+  // compaction are both enqueued, then their counters are read together
+  rc = build_bitmap(p, k_prime);  // P -> h_ctr[C_P]; the bitmap feeds the gather
+  if (rc) return rc;
+  rc = hosts_active_launch(hosts, t, k_prime);  // pipeline.py:121
+  if (rc) return rc;
+  rc = sync_small(p);
+  if (rc) return rc;
   uint64_t* keys = nullptr;
   uint64_t n = 0;
-  rc = hosts_compact_active(hosts, t, k_prime, &keys, &n);  // pipeline.py:121
+  rc = hosts_active_finish(hosts, t, k_prime, &keys, &n);
   if (rc) return rc;
   *nhosts = n;
   *pool_inactive = 0;
-  if (n == 0) return VATE_OK;  // no hosts: no P, no reports (pipeline.py:122-123)
-  rc = build_bitmap(p, k_prime);  // P -> h_ctr[C_P], bitmap for the gather
-  if (rc) return rc;
-  VATE_CUDA(cudaEventRecord(p->ev_small, p->stream));
+  if (n == 0) return VATE_OK;  // no hosts: no report (pipeline.py:122-123)
+  *pool_inactive = p->h_ctr[C_P];
   rc = p->g0.ensure(n * 4 + 4);
   if (rc) return rc;
   rc = launch_g0(p, keys, n, make_hash(g, p->c, cell_stream, 0), p->g0.as<int32_t>());
   if (rc) return rc;
-  VATE_CUDA(cudaEventSynchronize(p->ev_small));  // P is known; the gather keeps running
-  *pool_inactive = p->h_ctr[C_P];
   p->est_n = n;
   p->est_kp = k_prime;
   p->est_g = g;

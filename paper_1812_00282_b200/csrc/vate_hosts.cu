@@ -51,33 +51,63 @@ __global__ void k_insert_entries(const RegEntry* __restrict__ src, uint64_t n,
   }
 }
 
-// Warp-aggregated append of the keys whose last-seen slice is > cut.
-__global__ void k_active(const RegEntry* __restrict__ table, uint64_t cap, int special,
-                         long long cut, uint64_t* __restrict__ out,
-                         unsigned long long* nout, unsigned long long* maxkey) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+// Keys whose last-seen slice is > cut, appended in arbitrary order (the caller
+// sorts).  Each CTA handles tiles of 1024 entries (4 per thread) and reserves
+// its output range with one atomic per tile.
+constexpr int kActTile = 1024;
+__global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ table, uint64_t cap,
+                                                const unsigned long long* special, long long cut,
+                                                uint64_t* __restrict__ out,
+                                                unsigned long long* nout,
+                                                unsigned long long* maxkey) {
+  __shared__ unsigned warp_tot[8];
+  __shared__ unsigned long long base_s;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t total = cap + 1;
-  const int lane = threadIdx.x & 31;
+  const bool special_present = (*special & 0xFFFFFFFFull) != 0;
   unsigned long long kmax = 0;
-  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < total; base += stride) {
-    const uint64_t i = base + threadIdx.x;
-    bool take = false;
-    unsigned long long key = 0;
-    if (i < total) {
-      const RegEntry e = table[i];
-      key = e.key;
-      take = (i < cap) ? (key != kEmptyKey && e.last > cut) : (special && e.last > cut);
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, take);
-    if (m) {
-      unsigned long long pos = 0;
-      if (lane == 0) pos = atomicAdd(nout, (unsigned long long)__popc(m));
-      pos = __shfl_sync(0xffffffffu, pos, 0);
-      if (take) {
-        out[pos + __popc(m & ((1u << lane) - 1u))] = key;
-        kmax = key > kmax ? key : kmax;
+  for (uint64_t tile = (uint64_t)blockIdx.x * kActTile; tile < total;
+       tile += (uint64_t)gridDim.x * kActTile) {
+    const uint64_t i0 = tile + threadIdx.x * 4;
+    unsigned long long key[4];
+    unsigned mine = 0, take = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = i0 + q;
+      key[q] = 0;
+      if (i < total) {
+        const RegEntry e = table[i];
+        const bool tk = (i < cap) ? (e.key != kEmptyKey && e.last > cut)
+                                  : (special_present && e.last > cut);
+        if (tk) {
+          key[q] = e.key;
+          take |= 1u << q;
+          ++mine;
+          kmax = e.key > kmax ? e.key : kmax;
+        }
       }
     }
+    unsigned incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned tot = 0;
+      for (int w = 0; w < 8; ++w) tot += warp_tot[w];
+      base_s = tot ? atomicAdd(nout, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    unsigned before = 0;
+    for (int w = 0; w < wid; ++w) before += warp_tot[w];
+    unsigned long long pos = base_s + before + incl - mine;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if ((take >> q) & 1u) out[pos++] = key[q];
+    __syncthreads();
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -112,8 +142,9 @@ static uint64_t pow2_at_least(uint64_t x) {
 
 int hosts_read_counters(vate_hosts* h, unsigned long long out[H_N]) {
   vate_pool* p = h->pool;
-  VATE_CUDA(cudaMemcpyAsync(out, h->d_count, H_N * 8, cudaMemcpyDeviceToHost, p->stream));
+  VATE_CUDA(cudaMemcpyAsync(h->h_count, h->d_count, H_N * 8, cudaMemcpyDeviceToHost, p->stream));
   VATE_CUDA(cudaStreamSynchronize(p->stream));
+  for (int i = 0; i < H_N; ++i) out[i] = h->h_count[i];
   return VATE_OK;
 }
 
@@ -210,30 +241,44 @@ static int sort_keys(vate_pool* p, uint64_t* in, uint64_t* out, uint64_t n, int 
   return VATE_OK;
 }
 
-// Sorted keys with last > t - k' into pool->hosts_sorted.
-int hosts_compact_active(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev,
-                         uint64_t* n) {
+// Launch the active-set compaction; counters land in h_count after a sync.
+int hosts_active_launch(vate_hosts* h, int64_t t, int k_prime) {
   vate_pool* p = h->pool;
-  int rc = hosts_drain(h);
+  int rc;
+  if (h->needs_grow) {
+    rc = hosts_drain(h);
+    if (rc) return rc;
+    h->needs_grow = false;
+  }
+  rc = p->hosts_tmp.ensure((h->cap + 2) * 8);
   if (rc) return rc;
-  const uint64_t count = h->count_hint;
-  rc = p->hosts_tmp.ensure((count + 1) * 8);
-  if (rc) return rc;
-  rc = p->hosts_sorted.ensure((count + 1) * 8);
+  rc = p->hosts_sorted.ensure((h->cap + 2) * 8);
   if (rc) return rc;
   VATE_CUDA(cudaMemsetAsync(h->d_count + H_MAXKEY, 0, 16, p->stream));
-  unsigned long long c[H_N];
-  VATE_CUDA(cudaMemcpyAsync(c, h->d_count, H_N * 8, cudaMemcpyDeviceToHost, p->stream));
-  VATE_CUDA(cudaStreamSynchronize(p->stream));
-  const int special = (c[H_SPECIAL] & 0xFFFFFFFFull) != 0;
-  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap + 1, kThreads, 148u * 16u), kThreads, 0,
-              k_active, h->table.as<const RegEntry>(), h->cap, special,
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap + 1, kActTile, 148u * 8u), 256, 0, k_active,
+              h->table.as<const RegEntry>(), h->cap, h->d_count + H_SPECIAL,
               (long long)(t - k_prime), p->hosts_tmp.as<uint64_t>(), h->d_count + H_NOUT,
               h->d_count + H_MAXKEY);
-  rc = hosts_read_counters(h, c);
-  if (rc) return rc;
-  *n = c[H_NOUT];
-  const unsigned long long maxkey = c[H_MAXKEY];
+  VATE_CUDA(cudaMemcpyAsync(h->h_count, h->d_count, H_N * 8, cudaMemcpyDeviceToHost, p->stream));
+  return VATE_OK;
+}
+
+// After the caller's sync: handle parked inserts, then sort the active keys.
+int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev, uint64_t* n) {
+  vate_pool* p = h->pool;
+  int rc;
+  if (h->h_count[H_OVF]) {  // inserts hit the probe limit: grow, re-insert, recompute
+    rc = hosts_drain(h);
+    if (rc) return rc;
+    rc = hosts_active_launch(h, t, k_prime);
+    if (rc) return rc;
+    VATE_CUDA(cudaStreamSynchronize(p->stream));
+  }
+  h->pending = 0;
+  h->count_hint = h->h_count[H_COUNT];
+  if (h->count_hint > h->cap / 2) h->needs_grow = true;
+  *n = h->h_count[H_NOUT];
+  const unsigned long long maxkey = h->h_count[H_MAXKEY];
   int end_bit = 64;
   while (end_bit > 1 && !((maxkey >> (end_bit - 1)) & 1ull)) --end_bit;
   if (*n > 1) {
@@ -245,6 +290,15 @@ int hosts_compact_active(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_
   }
   *keys_dev = p->hosts_sorted.as<uint64_t>();
   return VATE_OK;
+}
+
+// Sorted keys with last > t - k' into pool->hosts_sorted.
+int hosts_compact_active(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev,
+                         uint64_t* n) {
+  int rc = hosts_active_launch(h, t, k_prime);
+  if (rc) return rc;
+  VATE_CUDA(cudaStreamSynchronize(h->pool->stream));
+  return hosts_active_finish(h, t, k_prime, keys_dev, n);
 }
 
 }  // namespace vate
@@ -265,6 +319,7 @@ int vate_hosts_create(vate_hosts** out, vate_pool* p, int k) {
   h->k = k;
   h->cap = 1 << 12;
   cudaError_t e = cudaMalloc(&h->d_count, H_N * 8);
+  if (e == cudaSuccess) e = cudaMallocHost(&h->h_count, H_N * 8);
   if (e != cudaSuccess) {
     delete h;
     return cuda_fail(e, "cudaMalloc");
@@ -293,6 +348,7 @@ int vate_hosts_destroy(vate_hosts* h) {
   h->ovf.release();
   h->scratch.release();
   if (h->d_count) cudaFree(h->d_count);
+  if (h->h_count) cudaFreeHost(h->h_count);
   delete h;
   return VATE_OK;
 }

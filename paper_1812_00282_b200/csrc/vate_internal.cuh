@@ -196,6 +196,10 @@ struct vate_pool {
   int32_t adv_blocks[2] = {0, 0};
   uint64_t adv_maint = 0;
 
+  // options
+  int opt_g0 = 0;
+  int dsmem_clusters = -1;   // cached max active clusters for the DSMEM gather (-1 unknown)
+
   // instrumentation
   uint64_t launches = 0;
   bool timing = false;
@@ -214,10 +218,12 @@ struct vate_hosts {
   int k = 1;
   uint64_t cap = 0;
   vate::DevBuf table, ovf, scratch;
-  unsigned long long* d_count = nullptr;  // [0] count, [1] ovf_n, [2] special flag, [3] maxkey
+  unsigned long long* d_count = nullptr;  // [0] count, [1] ovf_n, [2] special flag, [3] maxkey, [4] nout
+  unsigned long long* h_count = nullptr;  // pinned mirror of d_count
   uint64_t ovf_cap = 0;
   uint64_t pending = 0;    // registry inserts enqueued since the last drain
   uint64_t count_hint = 0; // last count read back
+  bool needs_grow = false; // load factor passed 1/2: grow at the next drain point
   vate::RegRef ref() const;
 };
 
@@ -249,6 +255,9 @@ int hosts_drain(vate_hosts* h);
 int hosts_prepare_insert(vate_hosts* h, uint64_t n);
 int hosts_compact_active(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev,
                          uint64_t* n);
+// split form: launch (no sync; counters -> pinned), the caller syncs, finish sorts
+int hosts_active_launch(vate_hosts* h, int64_t t, int k_prime);
+int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev, uint64_t* n);
 
 }  // namespace vate
 

@@ -166,28 +166,66 @@ __global__ void k_fill(T* cells, uint64_t n, T value) {
     cells[i] = value;
 }
 
-// One packet: BH, H, block clock, store (pools.py:153-178 with
-// estimator.py:96-99).  Same-cell writers of a slice store the same clock, so
-// plain stores suffice -- no atomics, no read-modify-write.
-template <typename T, bool REG>
-__device__ __forceinline__ void scan_one(uint64_t aip, uint64_t bip, T* __restrict__ cells,
-                                         const HashParams& H, const Layout& L,
-                                         uint32_t bact0, const RegRef& R, long long t) {
-  const uint64_t cell = cell_of(aip, slot_of(bip, H), H);
-  const uint32_t act = clock_of(bact0, block_of(cell, L), L.B);
-  cells[cell] = (T)act;
-  if (REG) reg_insert(R, aip, t, false);
+// A batch of U packets per thread: BH, H, block clock, store (pools.py:153-178
+// with estimator.py:96-99), then the host-registry touch.  Same-cell writers
+// of a slice store the same clock, so plain stores suffice -- no atomics, no
+// read-modify-write.  The registry step issues all U first-probe loads (one
+// 16-byte sector each) before resolving any, so a thread keeps U independent
+// requests in flight; only misses take the probing insert.
+template <typename T, bool REG, int U>
+__device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint64_t (&bip)[U],
+                                           int m, T* __restrict__ cells, const HashParams& H,
+                                           const Layout& L, uint32_t bact0, const RegRef& R,
+                                           long long t) {
+#pragma unroll
+  for (int q = 0; q < U; ++q) {
+    if (q < m) {
+      const uint64_t cell = cell_of(aip[q], slot_of(bip[q], H), H);
+      cells[cell] = (T)clock_of(bact0, block_of(cell, L), L.B);
+    }
+  }
+  if (REG) {
+    uint64_t slot[U];
+    RegEntry e[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      slot[q] = mix64(aip[q] ^ kRegSalt) & R.mask;
+      if (q < m) e[q] = R.table[slot[q]];
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      if (q >= m) continue;
+      if (e[q].key == aip[q] && aip[q] != kEmptyKey) {
+        if (e[q].last != t) R.table[slot[q]].last = t;
+      } else {
+        reg_insert(R, aip[q], t, false);
+      }
+    }
+  }
 }
 
 template <typename T, bool REG>
 __global__ void __launch_bounds__(kThreads) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
     Layout L, uint32_t bact0, RegRef R, long long t) {
+  constexpr int V = 2;  // uint4 loads (2 packets each) per thread per iteration
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < npairs2; i += stride) {
-    const uint4 q = __ldcs(pairs2 + i);  // streamed once: evict-first
-    scan_one<T, REG>(q.x, q.y, cells, H, L, bact0, R, t);
-    scan_one<T, REG>(q.z, q.w, cells, H, L, bact0, R, t);
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (; i < npairs2; i += V * stride) {
+    uint64_t a[2 * V], b[2 * V];
+    int m = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const uint64_t j = i + v * stride;
+      if (j < npairs2) {
+        const uint4 q = __ldcs(pairs2 + j);  // streamed once: evict-first
+        a[2 * v] = q.x; b[2 * v] = q.y; a[2 * v + 1] = q.z; b[2 * v + 1] = q.w;
+        m += 2;
+      } else {
+        a[2 * v] = b[2 * v] = a[2 * v + 1] = b[2 * v + 1] = 0;
+      }
+    }
+    scan_batch<T, REG, 2 * V>(a, b, m, cells, H, L, bact0, R, t);
   }
 }
 
@@ -198,7 +236,8 @@ __global__ void __launch_bounds__(kThreads) k_scan_packed8(
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint2 q = pairs[i];
-    scan_one<T, REG>(q.x, q.y, cells, H, L, bact0, R, t);
+    const uint64_t a[1] = {q.x}, b[1] = {q.y};
+    scan_batch<T, REG, 1>(a, b, 1, cells, H, L, bact0, R, t);
   }
 }
 
@@ -206,9 +245,23 @@ template <typename T, bool REG>
 __global__ void __launch_bounds__(kThreads) k_scan_u64(
     const uint64_t* __restrict__ aips, const uint64_t* __restrict__ bips, uint64_t n,
     T* __restrict__ cells, HashParams H, Layout L, uint32_t bact0, RegRef R, long long t) {
+  constexpr int U = 4;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    scan_one<T, REG>(__ldcs(aips + i), __ldcs(bips + i), cells, H, L, bact0, R, t);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += U * stride) {
+    uint64_t a[U], b[U];
+    int m = 0;
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const uint64_t j = i + q * stride;
+      a[q] = b[q] = 0;
+      if (j < n) {
+        a[q] = __ldcs(aips + j);
+        b[q] = __ldcs(bips + j);
+        m = q + 1;
+      }
+    }
+    scan_batch<T, REG, U>(a, b, m, cells, H, L, bact0, R, t);
+  }
 }
 
 __global__ void k_pair_cells(const uint64_t* __restrict__ aips,
@@ -646,6 +699,15 @@ int vate_pool_timing(vate_pool* p, int kind, double* total_ms, uint64_t* launche
   *total_ms = p->timed_ms[kind];
   *launches = p->timed_n[kind];
   return VATE_OK;
+}
+
+int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  if (option == VATE_OPT_G0 && value >= 0 && value <= 2) {
+    p->opt_g0 = (int)value;
+    return VATE_OK;
+  }
+  return set_error(VATE_EVALUE, "unknown option or value");
 }
 
 int vate_mark(vate_pool* p, int id) {

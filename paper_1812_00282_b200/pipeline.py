@@ -138,17 +138,23 @@ class Pipeline:
                                    VATE_DEVICE if on_device else VATE_HOST,
                                    self.hosts.handle, t))
 
-    def estimate_soa(self, t: int, out=None) -> HostReports | None:
+    def estimate_soa(self, t: int, out=None, advance: bool = False) -> HostReports | None:
         """The estimate phase (pipeline.py:120-138) as arrays; None without hosts.
 
         ``out`` may supply preallocated (pinned) host arrays
         (host u64, estimate f64, z_v f64, saturated u8) of equal capacity.
+        With ``advance=True`` the slice advance is enqueued right after the g0
+        gather (it touches cells, the float path does not), so the float path
+        and the sweep share one host round trip; collect it with _collect().
         """
         nh, p = C.c_uint64(), C.c_uint64()
         check(lib.vate_estimate_begin(self.pool.handle, self.hosts.handle, self.cfg.g,
                                       self.cfg.cell_stream, t, self.k_prime, C.byref(nh),
                                       C.byref(p)))
+        if advance:
+            check(lib.vate_advance_async(self.pool.handle))
         n = nh.value
+        self.last_active = n
         if n == 0:
             return None
         lzp, z_p = log_zp(p.value, self.pool.size)
@@ -162,16 +168,33 @@ class Pipeline:
                                        len(host), C.byref(kept)))
         m = kept.value
         self.last_pool_inactive = p.value
-        self.last_active = n
         return HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool), z_p,
                            t - self.k_prime + 1, self.k_prime)
 
-    def _maintain(self, t: int) -> MaintenanceReport:
-        rep = self.pool.advance_slice()
+    def _collect(self, t: int) -> MaintenanceReport:
+        """Finish an advance enqueued by estimate_soa(advance=True); prune every k."""
+        blocks = (C.c_int32 * 2)()
+        maint, cleared = C.c_uint64(), C.c_uint64()
+        check(lib.vate_advance_result(self.pool.handle, blocks, C.byref(maint), C.byref(cleared)))
+        rep = MaintenanceReport((blocks[0], blocks[1]), maint.value, cleared.value)
+        return self._account(t, rep)
+
+    def _account(self, t: int, rep: MaintenanceReport) -> MaintenanceReport:
         self.total_maintained += rep.cells_maintained
         self.total_cleared += rep.cells_cleared
         if t % max(1, self.pool.k) == 0:
             self.hosts.prune(t)
+        self.last_maintenance = rep
+        return rep
+
+    def _maintain(self, t: int) -> MaintenanceReport:
+        return self._account(t, self.pool.advance_slice())
+
+    def step_packed(self, t: int, pairs, n: int, on_device: bool, out=None):
+        """One slice from packed records: scan, estimate (+ advance overlapped), prune."""
+        self.scan_packed(t, pairs, n, on_device)
+        rep = self.estimate_soa(t, out, advance=True)
+        self._collect(t)
         return rep
 
     # --- driving ---------------------------------------------------------------------
@@ -187,7 +210,6 @@ class Pipeline:
         t3 = time.perf_counter_ns()
         stats = SliceStats(t, n, (t1 - t0) // 1000, (t2 - t1) // 1000, (t3 - t2) // 1000,
                            rep.cells_maintained, rep.cells_cleared)
-        self.last_maintenance = rep
         return reports, stats
 
     def process_slice(self, t: int, aips, bips):

@@ -450,3 +450,29 @@ def test_full_size_u16_pool_c28_k300():
         assert pipe.last_maintenance.cells_cleared == cleared
         cells = np.random.default_rng(t).integers(0, 1 << c, 100_000, dtype=np.uint64)
         assert np.array_equal(pool.cells.get(cells), opool.cells[cells.astype(np.int64)])
+
+
+# --- both g0 gather kernels (global-memory L2 gather, shared/DSMEM gather) ------------
+
+@pytest.mark.parametrize("c,g", [(5, 32), (12, 64), (20, 1024), (21, 1000), (23, 7), (24, 1024)])
+def test_g0_kernels_agree_with_oracle(c, g):
+    from paper_1812_00282_b200._lib import check, lib
+    k = 8
+    cfg = vb.EstimatorConfig(g, c, k, seed=c)
+    ocfg = vo.OracleConfig(g, c, k, seed=c)
+    pool = cfg.build_pool()
+    opool = vo.OraclePool(c, k)
+    rng = np.random.default_rng(c)
+    for t in range(6):
+        a = rng.integers(0, 3000, 200_000).astype(np.uint64)
+        b = rng.integers(0, 1 << 32, 200_000).astype(np.uint64)
+        vb.record_pairs(pool, cfg, a, b)
+        opool.set_cells(ocfg.pair_cells(a, b))
+        pool.advance_slice()
+        opool.advance()
+    hosts = np.arange(0, 3000, 3, dtype=np.uint64)
+    want = vo.host_g0(opool, ocfg, hosts, 5)
+    for opt in (1, 2, 0):
+        check(lib.vate_pool_set_option(pool.handle, 0, opt))
+        got = vb.inactive_virtual_counts(pool, cfg, hosts, 5)
+        assert np.array_equal(got, want), (c, g, opt)
