@@ -197,7 +197,9 @@ static int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashPa
   const uint32_t* bm = p->bitmap.as<const uint32_t>();
   // the smem/DSMEM gather needs the whole bitmap in <= 16 CTAs of 128 KB
   const bool smem_ok = p->c <= kDsmemLog2Bits + 4 && p->c >= 5;
-  const bool use_smem = smem_ok && (p->opt_g0 == 2 || (p->opt_g0 == 0 && p->c <= kDsmemLog2Bits + 4));
+  // auto: only when one CTA holds the whole bitmap (c <= 20); the cluster/DSMEM
+  // form measured 4x slower than the L2 gather on B200 (profiles/)
+  const bool use_smem = smem_ok && (p->opt_g0 == 2 || (p->opt_g0 == 0 && p->c <= kDsmemLog2Bits));
   if (use_smem) {
     switch (lph) {
       case 1: return launch_g0_smem<1>(p, hosts_dev, n, H, g0_dev);

@@ -157,8 +157,14 @@ int hosts_drain(vate_hosts* h) {
   const bool special = (c[H_SPECIAL] & 0xFFFFFFFFull) != 0;
   if (novf > h->ovf_cap)
     return set_error(VATE_ECUDA, "host registry overflow list overran its capacity");
-  if (novf > 0 || count > h->cap / 2) {
-    const uint64_t new_cap = pow2_at_least(std::max<uint64_t>(h->cap, 4 * (count + novf) + 64));
+  // Grow on parked inserts or load > 1/2; shrink when load < 1/16.  The parked
+  // list repeats a key once per packet, so it only forces "at least double";
+  // the recursion below grows again if re-insertion still overflows.
+  const bool shrink = novf == 0 && h->cap > (1u << 16) && count * 16 < h->cap;
+  if (novf > 0 || count > h->cap / 2 || shrink) {
+    uint64_t new_cap = pow2_at_least(4 * count + 64);
+    if (novf > 0 || count > h->cap / 2) new_cap = std::max<uint64_t>(new_cap, 2 * h->cap);
+    new_cap = std::max<uint64_t>(new_cap, 1u << 12);
     // rehash the live table: copy entries out first (rebuild consumes `src`)
     DevBuf old;
     old.ptr = h->table.ptr;
@@ -276,7 +282,8 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
   }
   h->pending = 0;
   h->count_hint = h->h_count[H_COUNT];
-  if (h->count_hint > h->cap / 2) h->needs_grow = true;
+  if (h->count_hint > h->cap / 2 || (h->cap > (1u << 16) && h->count_hint * 16 < h->cap))
+    h->needs_grow = true;
   *n = h->h_count[H_NOUT];
   const unsigned long long maxkey = h->h_count[H_MAXKEY];
   int end_bit = 64;
