@@ -201,6 +201,7 @@ def run_gpu(args, rank, world, local_rank):
     pipe = vb.Pipeline(pool, cfg, w["k_prime"], floor=w["floor"])
     h = pool.handle
     check(lib.vate_pool_set_option(h, 0, ("auto", "gather", "smem").index(args.g0_kernel)))
+    pool.set_option("incremental", 1 if args.incremental == "on" else 0)
     n = w["packets"]
     slice_bytes = n * 8
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -250,6 +251,7 @@ def run_gpu(args, rank, world, local_rank):
     pool.set_timing(False)
     barrier()
     launches0 = pool.launches()
+    inc0 = pool.inc_stats()
     with ClockSampler(dev) as clocks:
         check(lib.vate_mark(h, 0))
         rows = 0
@@ -262,6 +264,7 @@ def run_gpu(args, rank, world, local_rank):
         check(lib.vate_mark_elapsed(h, 0, 1, C.byref(ms)))
         dev_ms = ms.value
         launches = pool.launches() - launches0
+        inc1 = pool.inc_stats()
 
         # --- per-kernel breakdown (separate pass, CUDA events around each launch) -----
         pool.set_timing(True)
@@ -337,6 +340,13 @@ def run_gpu(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(e2e_rows / args.steps * 25)},
         "gpu_launches": int(launches),
         "g0_kernel": args.g0_kernel,
+        "incremental": {"enabled": args.incremental == "on",
+                        **{k: inc1[k] - inc0[k] for k in ("rebuilds", "delta_slices",
+                                                          "refresh_slices", "full_slices")},
+                        "last_delta_cells": inc1["last_delta_cells"],
+                        "last_delta_work": inc1["last_delta_work"],
+                        "last_misses": inc1["last_misses"],
+                        "hosts_indexed": inc1["hosts_indexed"]},
         "clocks": clocks.summary(),
     }
     if cpu_mean is not None:
@@ -386,6 +396,8 @@ def main():
     ap.add_argument("--impl", choices=("vate", "reference"), default="vate")
     ap.add_argument("--g0-kernel", choices=("auto", "gather", "smem"), default="auto",
                     help="g0 gather variant (VATE_OPT_G0)")
+    ap.add_argument("--incremental", choices=("on", "off"), default="on",
+                    help="exact incremental g0 through the inverse index (VATE_OPT_INCREMENTAL)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be at least 3")

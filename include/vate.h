@@ -70,9 +70,14 @@ int vate_mark(vate_pool* p, int id);
 int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
 
 /* tuning switches (bench / tests): VATE_OPT_G0 = 0 auto, 1 L2-gather kernel,
- * 2 shared-memory / cluster-DSMEM kernel (c <= 24 only). */
-enum vate_option { VATE_OPT_G0 = 0 };
+ * 2 shared-memory / cluster-DSMEM kernel (c <= 24 only).  VATE_OPT_INCREMENTAL
+ * = 1 (default) lets the fused estimate update g0 through an inverse index
+ * (exact), 0 recomputes every g0 by a full gather. */
+enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1 };
 int vate_pool_set_option(vate_pool* p, int option, int64_t value);
+/* incremental-estimate counters: [rebuilds, delta slices, refresh slices, full
+ * slices, last delta cells, last delta work, last misses, hosts indexed] */
+int vate_pool_inc_stats(const vate_pool* p, uint64_t out[8]);
 
 enum vate_kernel_kind {
   VATE_K_SCAN = 0,     /* record_pairs / set_many scatter      */

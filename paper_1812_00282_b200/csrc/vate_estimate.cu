@@ -21,10 +21,15 @@ int check_width(vate_pool* p, int k_prime);    // vate_pool.cu
 // word, so ((aip<<32)|j)*phi + cs = base + j*phi with
 // base = ((uint32(aip) * uint32(phi)) << 32) + cs, and each lane walks its
 // slots with one 64-bit add.  The bitmap (2^c/8 bytes) stays L2-resident.
-template <int LPH>
+// LIST: gather only the hosts hosts[idx[i]], i < min(*count, n) (the misses of
+// the incremental path), writing g0[idx[i]].
+template <int LPH, bool LIST = false>
 __global__ void __launch_bounds__(kThreads) k_g0(const uint64_t* __restrict__ hosts, uint64_t n,
                                                  const uint32_t* __restrict__ bitmap,
-                                                 HashParams H, int32_t* __restrict__ g0) {
+                                                 HashParams H, int32_t* __restrict__ g0,
+                                                 const uint32_t* __restrict__ idx = nullptr,
+                                                 const unsigned long long* count = nullptr) {
+  if (LIST) n = umin64(n, *count);
   const int lane = threadIdx.x & 31;
   const int sub = lane & (LPH - 1);
   const unsigned gmask = LPH == 32 ? 0xffffffffu : (((1u << LPH) - 1u) << (lane & ~(LPH - 1)));
@@ -32,7 +37,8 @@ __global__ void __launch_bounds__(kThreads) k_g0(const uint64_t* __restrict__ ho
   const uint64_t step = (uint64_t)LPH * kPhi;
   const uint64_t g = H.g;
   for (uint64_t h = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / LPH; h < n; h += groups) {
-    const uint64_t aip = hosts[h];
+    const uint64_t hi = LIST ? idx[h] : h;
+    const uint64_t aip = hosts[hi];
     uint64_t x = ((uint64_t)((uint32_t)aip * (uint32_t)kPhi) << 32) + H.cs + (uint64_t)sub * kPhi;
     uint32_t cnt = 0;
     uint64_t j = sub;
@@ -57,7 +63,7 @@ __global__ void __launch_bounds__(kThreads) k_g0(const uint64_t* __restrict__ ho
     }
 #pragma unroll
     for (int o = LPH / 2; o; o >>= 1) cnt += __shfl_xor_sync(gmask, cnt, o);
-    if (sub == 0) g0[h] = (int32_t)cnt;
+    if (sub == 0) g0[hi] = (int32_t)cnt;
   }
 }
 
@@ -187,8 +193,8 @@ static int launch_g0_smem(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, H
   return VATE_OK;
 }
 
-static int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H,
-                     int32_t* g0_dev) {
+int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H,
+              int32_t* g0_dev) {
   // lanes per host: the next power of two >= g, at most a warp
   int lph = 1;
   while (lph < 32 && (uint64_t)lph < H.g) lph <<= 1;
@@ -217,6 +223,25 @@ static int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashPa
     case 8: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<8>, hosts_dev, n, bm, H, g0_dev); break;
     case 16: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<16>, hosts_dev, n, bm, H, g0_dev); break;
     default: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, k_g0<32>, hosts_dev, n, bm, H, g0_dev); break;
+  }
+  return VATE_OK;
+}
+
+int launch_g0_list(vate_pool* p, const uint64_t* hosts_dev, const uint32_t* idx_dev,
+                   const unsigned long long* count_dev, uint64_t cap, HashParams H,
+                   int32_t* g0_dev) {
+  int lph = 1;
+  while (lph < 32 && (uint64_t)lph < H.g) lph <<= 1;
+  // the count lives on the device: size the grid for a modest list, grid-stride beyond
+  const uint32_t grid = grid_for(umin64(cap, 1u << 16) * (uint64_t)lph, kThreads, 148u * 16u);
+  const uint32_t* bm = p->bitmap.as<const uint32_t>();
+  switch (lph) {
+    case 1: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<1, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
+    case 2: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<2, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
+    case 4: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<4, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
+    case 8: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<8, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
+    case 16: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<16, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
+    default: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<32, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
   }
   return VATE_OK;
 }
@@ -489,7 +514,13 @@ int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t ce
   p->est_n = 0;
   // one host round trip per estimate: Z_p (bitmap pass) and the active-set
   // compaction are both enqueued, then their counters are read together
+  // misses of the previous incremental estimate (visible since its finish sync)
+  if (p->inc.valid && p->inc.last_n && p->h_ctr[C_MISS] * 20 > p->inc.last_n)
+    p->inc.want_rebuild = true;
+  p->h_ctr[C_MISS] = 0;
   rc = build_bitmap(p, k_prime);  // P -> h_ctr[C_P]; the bitmap feeds the gather
+  if (rc) return rc;
+  rc = inc_launch_delta(p, g, cell_stream, k_prime);  // flipped cells vs the last estimate
   if (rc) return rc;
   rc = hosts_active_launch(hosts, t, k_prime);  // pipeline.py:121
   if (rc) return rc;
@@ -501,11 +532,12 @@ int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t ce
   if (rc) return rc;
   *nhosts = n;
   *pool_inactive = 0;
-  if (n == 0) return VATE_OK;  // no hosts: no report (pipeline.py:122-123)
+  if (n == 0) {  // no hosts: no report (pipeline.py:122-123); the index stays as it was
+    p->inc.delta_launched = false;
+    return VATE_OK;
+  }
   *pool_inactive = p->h_ctr[C_P];
-  rc = p->g0.ensure(n * 4 + 4);
-  if (rc) return rc;
-  rc = launch_g0(p, keys, n, make_hash(g, p->c, cell_stream, 0), p->g0.as<int32_t>());
+  rc = inc_compute_g0(p, keys, n, make_hash(g, p->c, cell_stream, 0), k_prime);
   if (rc) return rc;
   p->est_n = n;
   p->est_kp = k_prime;

@@ -1,0 +1,250 @@
+// vate_incremental.cu -- exact incremental g0 for the fused per-slice estimate.
+//
+// g0(h) = #{ j < g : inactive(H(h, j)) } (estimator.py:114-123) is recomputed
+// from scratch by the reference every slice: H*g hashed gathers (1.02 G at 1M
+// hosts).  Between consecutive slices only the cells whose inactive bit flipped
+// can change any g0, and in steady traffic that is a tiny fraction of the pool
+// (DESIGN.md §4b measures ~0.07% per slice on the cfg-2 trace).  So:
+//
+//   * an inverse index (CSR: off[cell] .. off[cell+1] -> host ids) over a host
+//     set X holds every (host, slot) pair once, duplicates included;
+//   * g0x[i] is g0 of X[i] for the previous bitmap bprev;
+//   * per slice: delta = bitmap XOR bprev; each flipped cell adds +-1 to the g0x
+//     of every (host, slot) pair that maps to it; hosts of the active set found
+//     in X read g0x, the rest ("misses", e.g. new hosts) take the full gather.
+//
+// All integer arithmetic: the result equals the full recompute exactly, which
+// the GPU parity tests check slice by slice against the oracle.  When the delta
+// touches more than 1/4 of a full recompute, g0x is refreshed by one full
+// gather over X instead; X is rebuilt from the active set when misses exceed
+// 5% or X grows past twice the active set.
+#include <cub/device/device_scan.cuh>
+
+#include <string>
+
+#include "vate_internal.cuh"
+
+namespace vate {
+
+__device__ __forceinline__ uint64_t host_base(uint64_t aip, const HashParams& H) {
+  return ((uint64_t)((uint32_t)aip * (uint32_t)kPhi) << 32) + H.cs;  // ((aip<<32)*phi + cs)
+}
+
+// entries per cell over all (host, slot) pairs of X
+__global__ void k_inc_count(const uint64_t* __restrict__ X, uint64_t total, DivU64 dg,
+                            HashParams H, uint32_t* __restrict__ cnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+    uint64_t j;
+    const uint64_t h = div_u64(i, dg, &j);
+    const uint64_t cell = mix64(host_base(X[h], H) + j * kPhi) & H.cmask;
+    atomicAdd(cnt + cell, 1u);
+  }
+}
+
+__global__ void k_inc_fill(const uint64_t* __restrict__ X, uint64_t total, DivU64 dg, HashParams H,
+                           uint32_t* __restrict__ cursor, uint32_t* __restrict__ ent) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+    uint64_t j;
+    const uint64_t h = div_u64(i, dg, &j);
+    const uint64_t cell = mix64(host_base(X[h], H) + j * kPhi) & H.cmask;
+    ent[atomicAdd(cursor + cell, 1u)] = (uint32_t)h;
+  }
+}
+
+// Flipped cells of (bnew XOR bold) -> list of cell | (now_inactive << 32),
+// with the number of index entries they touch.
+__global__ void k_inc_delta(const uint32_t* __restrict__ bnew, const uint32_t* __restrict__ bold,
+                            uint64_t nwords, const uint32_t* __restrict__ off,
+                            unsigned long long* __restrict__ list, uint64_t cap,
+                            unsigned long long* count, unsigned long long* work) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
+    const uint32_t nb = bnew[w];
+    uint32_t x = nb ^ bold[w];
+    if (!x) continue;
+    unsigned long long pos = atomicAdd(count, (unsigned long long)__popc(x));
+    unsigned long long wsum = 0;
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      const uint64_t cell = w * 32 + b;
+      wsum += off[cell + 1] - off[cell];
+      if (pos < cap) list[pos] = cell | ((unsigned long long)((nb >> b) & 1u) << 32);
+      ++pos;
+    }
+    atomicAdd(work, wsum);
+  }
+}
+
+// One warp per flipped cell: +1 to every pair that became inactive, -1 otherwise.
+__global__ void k_inc_apply(const unsigned long long* __restrict__ list,
+                            const unsigned long long* count, uint64_t cap,
+                            const uint32_t* __restrict__ off, const uint32_t* __restrict__ ent,
+                            int32_t* __restrict__ g0x) {
+  const uint64_t n = umin64(*count, cap);
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const unsigned long long v = list[i];
+    const uint64_t cell = v & 0xFFFFFFFFull;
+    const int d = (v >> 32) ? 1 : -1;
+    const uint32_t e1 = off[cell + 1];
+    for (uint32_t e = off[cell] + lane; e < e1; e += 32) atomicAdd(g0x + ent[e], d);
+  }
+}
+
+// Sorted active hosts A -> g0 from the index where present, else a miss.
+__global__ void k_inc_lookup(const uint64_t* __restrict__ A, uint64_t n,
+                             const uint64_t* __restrict__ X, uint64_t m,
+                             const int32_t* __restrict__ g0x, int32_t* __restrict__ g0,
+                             uint32_t* __restrict__ miss, unsigned long long* nmiss) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t a = A[i];
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (X[mid] < a) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < m && X[lo] == a) g0[i] = g0x[lo];
+    else miss[atomicAdd(nmiss, 1ull)] = (uint32_t)i;
+  }
+}
+
+void inc_release(vate_pool* p) {
+  IncIndex& I = p->inc;
+  for (DevBuf* b : {&I.X, &I.g0x, &I.off, &I.ent, &I.cursor, &I.bprev, &I.dlist, &I.miss, &I.scan_tmp})
+    b->release();
+  I.valid = false;
+  I.m = 0;
+}
+
+static void swap_buf(DevBuf& a, DevBuf& b) {
+  std::swap(a.ptr, b.ptr);
+  std::swap(a.bytes, b.bytes);
+}
+
+// Enqueue the delta of the fresh bitmap against bprev (before the estimate's
+// host round trip, so its counts arrive with P and the registry counters).
+int inc_launch_delta(vate_pool* p, uint64_t g, uint64_t cs, int kp) {
+  IncIndex& I = p->inc;
+  I.delta_launched = false;
+  if (!p->opt_inc || !I.valid || I.want_rebuild || I.g != g || I.cs != cs || I.kp != kp)
+    return VATE_OK;
+  const uint64_t nwords = (p->L.size + 31) / 32;
+  VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_DCNT, 0, 16, p->stream));
+  VATE_LAUNCH(p, VATE_K_G0, grid_for(nwords, kThreads, 148u * 16u), kThreads, 0, k_inc_delta,
+              p->bitmap.as<const uint32_t>(), I.bprev.as<const uint32_t>(), nwords,
+              I.off.as<const uint32_t>(), I.dlist.as<unsigned long long>(), I.dlist_cap,
+              p->d_ctr + C_DCNT, p->d_ctr + C_DWORK);
+  VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_DCNT, p->d_ctr + C_DCNT, 16, cudaMemcpyDeviceToHost,
+                            p->stream));
+  I.delta_launched = true;
+  return VATE_OK;
+}
+
+// Build the inverse index over X = hosts (sorted, n), with g0x = g0_dev (already
+// computed on the current bitmap), and take the current bitmap as bprev.
+static int inc_rebuild(vate_pool* p, const uint64_t* hosts, uint64_t n, HashParams H, int kp,
+                       const int32_t* g0_dev) {
+  IncIndex& I = p->inc;
+  I.valid = false;
+  const uint64_t total = n * H.g;
+  const uint64_t S = p->L.size, nwords = (S + 31) / 32;
+  if (n == 0 || total >= (1ull << 32)) return VATE_OK;  // u32 offsets only
+  // memory: ent 4*total, off/cursor 4*(S+1) each; keep a quarter of free memory spare
+  size_t free_b = 0, tot_b = 0;
+  VATE_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+  const uint64_t need = 4 * total + 8 * (S + 2) + 8 * n * 2 + 4 * nwords;
+  if (need + tot_b / 4 > free_b + I.ent.bytes + I.off.bytes + I.cursor.bytes) return VATE_OK;
+  int rc;
+  if ((rc = I.X.ensure(n * 8 + 8)) || (rc = I.g0x.ensure(n * 4 + 4)) ||
+      (rc = I.off.ensure((S + 2) * 4)) || (rc = I.cursor.ensure((S + 2) * 4)) ||
+      (rc = I.ent.ensure(total * 4 + 4)) || (rc = I.bprev.ensure(nwords * 4 + 16)) ||
+      (rc = I.miss.ensure(n * 4 + 4)))
+    return rc;
+  I.dlist_cap = S / 8 + 1024;
+  if ((rc = I.dlist.ensure(I.dlist_cap * 8))) return rc;
+  VATE_CUDA(cudaMemcpyAsync(I.X.ptr, hosts, n * 8, cudaMemcpyDeviceToDevice, p->stream));
+  VATE_CUDA(cudaMemcpyAsync(I.g0x.ptr, g0_dev, n * 4, cudaMemcpyDeviceToDevice, p->stream));
+  VATE_CUDA(cudaMemsetAsync(I.cursor.ptr, 0, (S + 1) * 4, p->stream));
+  const DivU64 dg = make_div(H.g);
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(total, kThreads, 148u * 32u), kThreads, 0, k_inc_count,
+              I.X.as<const uint64_t>(), total, dg, H, I.cursor.as<uint32_t>());
+  size_t tmp = 0;
+  VATE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, I.cursor.as<uint32_t>(),
+                                          I.off.as<uint32_t>(), (int64_t)(S + 1), p->stream));
+  if ((rc = I.scan_tmp.ensure(tmp + 256))) return rc;
+  VATE_CUDA(cub::DeviceScan::ExclusiveSum(I.scan_tmp.ptr, tmp, I.cursor.as<uint32_t>(),
+                                          I.off.as<uint32_t>(), (int64_t)(S + 1), p->stream));
+  p->launches += 2;
+  VATE_CUDA(cudaMemcpyAsync(I.cursor.ptr, I.off.ptr, (S + 1) * 4, cudaMemcpyDeviceToDevice,
+                            p->stream));
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(total, kThreads, 148u * 32u), kThreads, 0, k_inc_fill,
+              I.X.as<const uint64_t>(), total, dg, H, I.cursor.as<uint32_t>(),
+              I.ent.as<uint32_t>());
+  VATE_CUDA(cudaMemcpyAsync(I.bprev.ptr, p->bitmap.ptr, nwords * 4, cudaMemcpyDeviceToDevice,
+                            p->stream));
+  I.m = n;
+  I.g = H.g;
+  I.cs = H.cs;
+  I.kp = kp;
+  I.valid = true;
+  I.want_rebuild = false;
+  I.rebuilds++;
+  return VATE_OK;
+}
+
+// g0 of the sorted active hosts into p->g0 (after the estimate's round trip).
+int inc_compute_g0(vate_pool* p, const uint64_t* hosts, uint64_t n, HashParams H, int kp) {
+  IncIndex& I = p->inc;
+  int rc;
+  if ((rc = p->g0.ensure(n * 4 + 4))) return rc;
+  const bool same_req = I.req_g == H.g && I.req_cs == H.cs && I.req_kp == kp;
+  I.req_g = H.g;
+  I.req_cs = H.cs;
+  I.req_kp = kp;
+  if (I.delta_launched) {
+    I.delta_launched = false;
+    const uint64_t dcells = p->h_ctr[C_DCNT], dwork = p->h_ctr[C_DWORK];
+    I.last_delta_cells = dcells;
+    I.last_delta_work = dwork;
+    if (dcells <= I.dlist_cap && dwork <= n * H.g / 4) {
+      VATE_LAUNCH(p, VATE_K_G0, grid_for(umin64(dcells, 1u << 20) * 32 + 32, kThreads, 148u * 16u),
+                  kThreads, 0, k_inc_apply, I.dlist.as<const unsigned long long>(),
+                  p->d_ctr + C_DCNT, I.dlist_cap, I.off.as<const uint32_t>(),
+                  I.ent.as<const uint32_t>(), I.g0x.as<int32_t>());
+      I.delta_slices++;
+    } else {  // too much churn for the delta: refresh every host of X in one gather
+      if ((rc = launch_g0(p, I.X.as<const uint64_t>(), I.m, H, I.g0x.as<int32_t>()))) return rc;
+      I.refresh_slices++;
+    }
+    if ((rc = I.miss.ensure(n * 4 + 4))) return rc;
+    VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_MISS, 0, 8, p->stream));
+    VATE_LAUNCH(p, VATE_K_G0, grid_for(n, kThreads, 148u * 16u), kThreads, 0, k_inc_lookup, hosts, n,
+                I.X.as<const uint64_t>(), I.m, I.g0x.as<const int32_t>(), p->g0.as<int32_t>(),
+                I.miss.as<uint32_t>(), p->d_ctr + C_MISS);
+    if ((rc = launch_g0_list(p, hosts, I.miss.as<const uint32_t>(), p->d_ctr + C_MISS, n, H,
+                             p->g0.as<int32_t>())))
+      return rc;
+    VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_MISS, p->d_ctr + C_MISS, 8, cudaMemcpyDeviceToHost,
+                              p->stream));
+    swap_buf(p->bitmap, I.bprev);  // g0x now matches this slice's bitmap
+    I.last_n = n;
+    if (I.m > 2 * n) I.want_rebuild = true;
+    return VATE_OK;
+  }
+  // full recompute; then (re)build the index over this active set
+  if ((rc = launch_g0(p, hosts, n, H, p->g0.as<int32_t>()))) return rc;
+  I.full_slices++;
+  if (p->opt_inc && (same_req || !I.valid)) {
+    if ((rc = inc_rebuild(p, hosts, n, H, kp, p->g0.as<const int32_t>()))) return rc;
+  }
+  I.last_n = n;
+  return VATE_OK;
+}
+
+}  // namespace vate

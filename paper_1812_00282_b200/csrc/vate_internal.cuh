@@ -163,6 +163,27 @@ struct DevBuf {
 
 struct vate_hosts;
 
+namespace vate {
+// Incremental g0 state (vate_incremental.cu): an inverse index cell -> host
+// slots over a host set X, g0 of every host of X for the previous inactive
+// bitmap, and that bitmap.  Invariant: g0x[i] == #inactive slots of X[i] in bprev.
+struct IncIndex {
+  bool valid = false;
+  uint64_t g = 0, cs = 0;
+  int kp = 0;
+  uint64_t m = 0;                         // hosts in X
+  DevBuf X, g0x, off, ent, cursor, bprev, dlist, miss, scan_tmp;
+  uint64_t dlist_cap = 0;
+  bool delta_launched = false;
+  bool want_rebuild = false;
+  uint64_t last_n = 0;                    // active hosts of the previous estimate
+  uint64_t req_g = 0, req_cs = 0;         // previous request (rebuild on repeat)
+  int req_kp = 0;
+  uint64_t rebuilds = 0, delta_slices = 0, refresh_slices = 0, full_slices = 0;
+  uint64_t last_delta_cells = 0, last_delta_work = 0, last_misses = 0;
+};
+}  // namespace vate
+
 struct vate_pool {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -198,6 +219,8 @@ struct vate_pool {
 
   // options
   int opt_g0 = 0;
+  int opt_inc = 1;            // incremental g0 through the inverse index
+  vate::IncIndex inc;
   int dsmem_clusters = -1;   // cached max active clusters for the DSMEM gather (-1 unknown)
 
   // instrumentation
@@ -248,7 +271,16 @@ int collect_timing(vate_pool* p);
 uint32_t grid_for(uint64_t work, uint32_t per_block, uint32_t cap_blocks = 148u * 64u);
 
 // counters in vate_pool::d_ctr
-enum Ctr { C_P = 0, C_CLEARED = 1, C_NSEL = 2, C_ERR = 3, C_N = 8 };
+enum Ctr { C_P = 0, C_CLEARED = 1, C_NSEL = 2, C_ERR = 3, C_DCNT = 4, C_DWORK = 5, C_MISS = 6,
+           C_N = 8 };
+
+// estimate helpers (vate_estimate.cu / vate_incremental.cu)
+int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H, int32_t* g0_dev);
+int launch_g0_list(vate_pool* p, const uint64_t* hosts_dev, const uint32_t* idx_dev,
+                   const unsigned long long* count_dev, uint64_t cap, HashParams H, int32_t* g0_dev);
+int inc_launch_delta(vate_pool* p, uint64_t g, uint64_t cs, int kp);
+int inc_compute_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H, int kp);
+void inc_release(vate_pool* p);
 
 // registry helpers (vate_hosts.cu)
 int hosts_drain(vate_hosts* h);

@@ -641,6 +641,7 @@ int vate_pool_destroy(vate_pool* p) {
                     &p->g0, &p->flags, &p->sel_idx, &p->cub_tmp, &p->est_out, &p->zv_out,
                     &p->sat_out, &p->host_out, &p->lzv})
     b->release();
+  inc_release(p);
   if (p->cells) cudaFree(p->cells);
   if (p->d_ctr) cudaFree(p->d_ctr);
   if (p->h_ctr) cudaFreeHost(p->h_ctr);
@@ -707,7 +708,21 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_g0 = (int)value;
     return VATE_OK;
   }
+  if (option == VATE_OPT_INCREMENTAL && (value == 0 || value == 1)) {
+    p->opt_inc = (int)value;
+    if (!value) p->inc.valid = false;
+    return VATE_OK;
+  }
   return set_error(VATE_EVALUE, "unknown option or value");
+}
+
+int vate_pool_inc_stats(const vate_pool* p, uint64_t out[8]) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  const IncIndex& I = p->inc;
+  const uint64_t v[8] = {I.rebuilds, I.delta_slices, I.refresh_slices, I.full_slices,
+                         I.last_delta_cells, I.last_delta_work, I.last_misses, I.valid ? I.m : 0};
+  for (int i = 0; i < 8; ++i) out[i] = v[i];
+  return VATE_OK;
 }
 
 int vate_mark(vate_pool* p, int id) {

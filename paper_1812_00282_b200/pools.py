@@ -297,6 +297,19 @@ class AtPool(BlockLayout):
         check(lib.vate_pool_launches(self._h, C.byref(n)))
         return n.value
 
+    def set_option(self, option: str, value: int) -> None:
+        """Tuning switches: 'g0_kernel' (0 auto, 1 gather, 2 smem) and 'incremental' (0/1)."""
+        check(lib.vate_pool_set_option(self._h, ("g0_kernel", "incremental").index(option),
+                                       int(value)))
+
+    def inc_stats(self) -> dict:
+        """Counters of the incremental estimate."""
+        out = (C.c_uint64 * 8)()
+        check(lib.vate_pool_inc_stats(self._h, out))
+        keys = ("rebuilds", "delta_slices", "refresh_slices", "full_slices",
+                "last_delta_cells", "last_delta_work", "last_misses", "hosts_indexed")
+        return dict(zip(keys, list(out)))
+
     def set_timing(self, on: bool) -> None:
         check(lib.vate_pool_set_timing(self._h, int(on)))
 

@@ -476,3 +476,78 @@ def test_g0_kernels_agree_with_oracle(c, g):
         check(lib.vate_pool_set_option(pool.handle, 0, opt))
         got = vb.inactive_virtual_counts(pool, cfg, hosts, 5)
         assert np.array_equal(got, want), (c, g, opt)
+
+
+# --- incremental g0 (inverse index) vs full recompute vs oracle ---------------------
+
+def test_incremental_estimate_paths_match_oracle():
+    """Host churn (misses -> rebuild), a burst that flips most cells (refresh
+    path) and quiet slices (pure delta) -- every slice equals the oracle, and the
+    run exercises each path of the incremental estimate."""
+    cfg = vb.EstimatorConfig(256, 16, 8, seed=12)
+    ocfg = vo.OracleConfig(256, 16, 8, seed=12)
+    pool = cfg.build_pool()
+    pipe = vb.Pipeline(pool, cfg, 6)
+    opipe = vo.OraclePipeline(ocfg, 6)
+    rng = np.random.default_rng(3)
+    for t in range(40):
+        base = 1000 * (t // 12)                      # new host population every 12 slices
+        n = 3000
+        a = (base + rng.integers(0, 400, n)).astype(np.uint64)
+        b = rng.integers(0, 40, n).astype(np.uint64)  # few peers: a steady, low-churn pool
+        if t == 20:                                   # one burst that sets most of the pool
+            a = np.concatenate([a, rng.integers(0, 400, 400_000).astype(np.uint64)])
+            b = np.concatenate([b, rng.integers(0, 1 << 32, 400_000).astype(np.uint64)])
+        got, _ = pipe.process_slice_soa(t, a, b)
+        want = opipe.process_slice(t, a, b)
+        assert np.array_equal(got.host, want.reports.host), t
+        assert np.array_equal(got.estimate, want.reports.estimate), t
+        assert pipe.last_pool_inactive == want.pool_inactive, t
+    st = pool.inc_stats()
+    assert st["rebuilds"] >= 2 and st["delta_slices"] >= 20 and st["refresh_slices"] >= 1, st
+    pipe.close()
+
+
+def test_incremental_survives_outside_pool_changes():
+    """set_many / load between estimates are just more flipped cells."""
+    cfg = vb.EstimatorConfig(128, 14, 6, seed=5)
+    ocfg = vo.OracleConfig(128, 14, 6, seed=5)
+    pool = cfg.build_pool()
+    pipe = vb.Pipeline(pool, cfg, 6)
+    opipe = vo.OraclePipeline(ocfg, 6)
+    rng = np.random.default_rng(8)
+    for t in range(15):
+        a = rng.integers(0, 200, 2000).astype(np.uint64)
+        b = rng.integers(0, 30, 2000).astype(np.uint64)
+        if t == 7:
+            extra = rng.integers(0, 1 << 14, 500).astype(np.uint64)
+            pool.set_many(extra)
+            opipe.pool.set_cells(extra)
+        if t == 11:
+            blob = pool.snapshot_bytes()
+            pool.set_many(rng.integers(0, 1 << 14, 3000).astype(np.uint64))
+            check_blob = vb.AtPool.from_bytes(blob)   # reload the saved state in place
+            from paper_1812_00282_b200._lib import lib, ptr
+            arr = np.frombuffer(blob, dtype=np.uint8)
+            assert lib.vate_load(pool.handle, ptr(arr), arr.size) == 0
+            assert check_blob.snapshot_bytes() == pool.snapshot_bytes()
+        got, _ = pipe.process_slice_soa(t, a, b)
+        want = opipe.process_slice(t, a, b)
+        assert np.array_equal(got.estimate, want.reports.estimate), t
+    assert pool.inc_stats()["delta_slices"] >= 10
+    pipe.close()
+
+
+def test_incremental_off_equals_on():
+    cfg = vb.EstimatorConfig(1024, 20, 10, seed=0)
+    p_on, p_off = cfg.build_pool(), cfg.build_pool()
+    p_off.set_option("incremental", 0)
+    a_on, a_off = vb.Pipeline(p_on, cfg, 10), vb.Pipeline(p_off, cfg, 10)
+    from oracle import vate_oracle as vo2
+    for t in range(30):
+        a, b = vo2.synthetic_slice(t, 200_000, 20_000)
+        r1, _ = a_on.process_slice_soa(t, a, b)
+        r2, _ = a_off.process_slice_soa(t, a, b)
+        assert np.array_equal(r1.host, r2.host) and np.array_equal(r1.estimate, r2.estimate)
+    assert p_on.inc_stats()["delta_slices"] >= 25
+    assert p_off.inc_stats()["delta_slices"] == 0
