@@ -12,7 +12,7 @@ tail partition, seed 0, floor 0 (every active host's report is produced):
     -> maintain (advance clocks, sweep the two due blocks), prune every k.
 
 `value`  = packets / device time of K steps with packets resident in HBM
-           (a ring of distinct slices larger than L2, so inputs are not L2-hot).
+           (every slice distinct and pre-generated, 40 MB each: inputs are not L2-hot).
 `e2e`    = the same K steps through the public API from pinned HOST packet
            buffers: H2D of every slice's packets + D2H of every report row.
 The pool (16 MiB) is L2-resident by design across steps; it is state, not input.
@@ -175,8 +175,8 @@ def _config(w, world):
             "g": w["g"], "hosts": w["hosts"], "packets_per_slice_per_gpu": w["packets"],
             "floor": w["floor"], "partition": w["partition"], "seed": w["seed"],
             "parallelism": f"dp{world}" if world > 1 else "single",
-            "l2": "packet ring of distinct slices > 2x L2 (inputs not L2-hot); the 16 MiB "
-                  "pool stays L2-resident by design"}
+            "l2": "every slice distinct (40 MB each, pre-generated, >> L2: inputs not "
+                  "L2-hot); the 16 MiB pool stays L2-resident by design"}
 
 
 # ----------------------------------------------------------------------------------
@@ -204,16 +204,26 @@ def run_gpu(args, rank, world, local_rank):
     pool.set_option("incremental", 1 if args.incremental == "on" else 0)
     n = w["packets"]
     slice_bytes = n * 8
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    ring = max(4, -(-2 * l2 // slice_bytes) + 1)
     torch.cuda.set_device(dev)
-    dring = torch.empty((ring, n, 2), dtype=torch.int32, device=f"cuda:{dev}")
-    for r in range(ring):
-        check(lib.vate_synth_packets(h, r + 1000 * rank, n, w["hosts"], w["base_aip"],
-                                     w["seed"], dring[r].data_ptr()))
+    # Every slice of the run is distinct (no ring reuse): a repeated slice would
+    # re-set only cells that are already active and hide the real per-slice churn
+    # of the inactive bitmap.  Slices are generated on the device before the timed
+    # regions (k_synth == oracle.synthetic_slice), 40 MB each, >> L2 in total.
+    t_base = 1000 * rank
+    prefill = 2 * w["k"]
+    n_dev = args.warmup + 2 * args.steps
+    scratch = torch.empty((n, 2), dtype=torch.int32, device=f"cuda:{dev}")
+    dslices = torch.empty((n_dev, n, 2), dtype=torch.int32, device=f"cuda:{dev}")
+    for i in range(n_dev):
+        check(lib.vate_synth_packets(h, t_base + prefill + i, n, w["hosts"], w["base_aip"],
+                                     w["seed"], dslices[i].data_ptr()))
+    hslices = torch.empty((args.steps, n, 2), dtype=torch.int32, pin_memory=True)
+    for i in range(args.steps):
+        check(lib.vate_synth_packets(h, t_base + prefill + n_dev + i, n, w["hosts"], w["base_aip"],
+                                     w["seed"], scratch.data_ptr()))
+        pool.synchronize()
+        hslices[i].copy_(scratch)
     pool.synchronize()
-    hring = torch.empty((ring, n, 2), dtype=torch.int32, pin_memory=True)
-    hring.copy_(dring)
     nh_cap = w["hosts"] + 16
     outs = (torch.empty(nh_cap, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64),
             torch.empty(nh_cap, dtype=torch.float64, pin_memory=True).numpy(),
@@ -222,8 +232,7 @@ def run_gpu(args, rank, world, local_rank):
 
     merger = _Merger(pool, world, dist, torch) if world > 1 else None
 
-    def step(t, on_device):
-        src = dring[t % ring].data_ptr() if on_device else hring[t % ring].data_ptr()
+    def step(t, src, on_device):
         if merger is not None:
             pipe.scan_packed(t, src, n, on_device)
             merger.merge()
@@ -234,12 +243,16 @@ def run_gpu(args, rank, world, local_rank):
         return 0 if rep is None else len(rep)
 
     t = 0
-    for _ in range(2 * w["k"]):          # fill the window: every block swept twice
-        step(t, True)
+    for _ in range(prefill):             # fill the window: every block swept twice
+        check(lib.vate_synth_packets(h, t_base + t, n, w["hosts"], w["base_aip"], w["seed"],
+                                     scratch.data_ptr()))
+        step(t, scratch.data_ptr(), True)
         t += 1
+    di = 0
     for _ in range(args.warmup):
-        step(t, True)
+        step(t, dslices[di].data_ptr(), True)
         t += 1
+        di += 1
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -256,8 +269,9 @@ def run_gpu(args, rank, world, local_rank):
         check(lib.vate_mark(h, 0))
         rows = 0
         for _ in range(args.steps):
-            rows += step(t, True)
+            rows += step(t, dslices[di].data_ptr(), True)
             t += 1
+            di += 1
         check(lib.vate_mark(h, 1))
         barrier()
         ms = C.c_double()
@@ -269,8 +283,9 @@ def run_gpu(args, rank, world, local_rank):
         # --- per-kernel breakdown (separate pass, CUDA events around each launch) -----
         pool.set_timing(True)
         for _ in range(args.steps):
-            step(t, True)
+            step(t, dslices[di].data_ptr(), True)
             t += 1
+            di += 1
         barrier()
         kt = {kind: pool.kernel_time(kind) for kind in _lib.KERNEL_KINDS}
         pool.set_timing(False)
@@ -279,8 +294,8 @@ def run_gpu(args, rank, world, local_rank):
         barrier()
         e0 = time.perf_counter()
         e2e_rows = 0
-        for _ in range(args.steps):
-            e2e_rows += step(t, False)
+        for i in range(args.steps):
+            e2e_rows += step(t, hslices[i].data_ptr(), False)
             t += 1
         barrier()
         e2e_s = time.perf_counter() - e0
@@ -391,7 +406,7 @@ class _Merger:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("vate", "reference"), default="vate")
     ap.add_argument("--g0-kernel", choices=("auto", "gather", "smem"), default="auto",
