@@ -225,21 +225,31 @@ def run_gpu(args, rank, world, local_rank):
         hslices[i].copy_(scratch)
     pool.synchronize()
     nh_cap = w["hosts"] + 16
-    outs = (torch.empty(nh_cap, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64),
-            torch.empty(nh_cap, dtype=torch.float64, pin_memory=True).numpy(),
-            torch.empty(nh_cap, dtype=torch.float64, pin_memory=True).numpy(),
-            torch.empty(nh_cap, dtype=torch.uint8, pin_memory=True).numpy())
+
+    def pinned_outs():
+        return (torch.empty(nh_cap, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64),
+                torch.empty(nh_cap, dtype=torch.float64, pin_memory=True).numpy(),
+                torch.empty(nh_cap, dtype=torch.float64, pin_memory=True).numpy(),
+                torch.empty(nh_cap, dtype=torch.uint8, pin_memory=True).numpy())
+    out_sets = (pinned_outs(), pinned_outs())   # reports double-buffered across slices
+    outs = out_sets[0]
 
     merger = _Merger(pool, world, dist, torch) if world > 1 else None
 
     def step(t, src, on_device):
+        """One slice; report rows of slice t land in out_sets[t % 2] asynchronously."""
         if merger is not None:
             pipe.scan_packed(t, src, n, on_device)
             merger.merge()
-            rep = merger.estimate(pipe, t, outs)
+            rep = merger.estimate(pipe, t, out_sets[t % 2])
             pipe._maintain(t)
         else:
-            rep = pipe.step_packed(t, src, n, on_device, outs)
+            rep = pipe.step_packed(t, src, n, on_device, out_sets[t % 2], wait=False)
+        return 0 if rep is None else len(rep)
+
+    def step_host(t, i):
+        """e2e slice from pinned host packets; slice i+1's H2D overlaps slice i."""
+        rep = pipe.step_staged(t, staged[i % 2], n, out_sets[t % 2], wait=False)
         return 0 if rep is None else len(rep)
 
     t = 0
@@ -255,6 +265,7 @@ def run_gpu(args, rank, world, local_rank):
         di += 1
 
     def barrier():
+        pipe.wait_reports()
         torch.cuda.synchronize(dev)
         pool.synchronize()
         if dist is not None:
@@ -294,8 +305,12 @@ def run_gpu(args, rank, world, local_rank):
         barrier()
         e0 = time.perf_counter()
         e2e_rows = 0
+        staged = [None, None]
+        staged[0] = pipe.stage_packed(hslices[0].data_ptr(), n)
         for i in range(args.steps):
-            e2e_rows += step(t, hslices[i].data_ptr(), False)
+            if i + 1 < args.steps:
+                staged[(i + 1) % 2] = pipe.stage_packed(hslices[i + 1].data_ptr(), n)
+            e2e_rows += step_host(t, i)
             t += 1
         barrier()
         e2e_s = time.perf_counter() - e0

@@ -108,6 +108,13 @@ int vate_scan_pairs(vate_pool* p, uint64_t g, uint64_t cell_stream, uint64_t gro
 int vate_scan_packed(vate_pool* p, uint64_t g, uint64_t cell_stream, uint64_t group_stream,
                      const uint32_t* pairs, uint64_t n, int where, vate_hosts* hosts,
                      int64_t t);
+/* H2D prefetch: stage packed records from (pinned) host memory on the pool's
+ * copy stream into one of two device buffers (*slot), overlapping the
+ * current slice's kernels; vate_scan_staged scans a staged buffer once its
+ * copy has landed (stream-ordered, no host wait). */
+int vate_stage_packed(vate_pool* p, const uint32_t* pairs, uint64_t n, int* slot);
+int vate_scan_staged(vate_pool* p, uint64_t g, uint64_t cell_stream, uint64_t group_stream,
+                     int slot, uint64_t n, vate_hosts* hosts, int64_t t);
 /* pair_cells (estimator.py:96-99) without touching the pool; c <= 32. */
 int vate_pair_cells(vate_pool* p, uint64_t g, int c, uint64_t cell_stream,
                     uint64_t group_stream, const uint64_t* aips, const uint64_t* bips,
@@ -167,6 +174,14 @@ int vate_estimate_begin_hosts(vate_pool* p, const uint64_t* hosts, uint64_t n, i
 int vate_estimate_finish(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
                          double floor, uint64_t* out_host, double* out_est,
                          double* out_zv, uint8_t* out_sat, uint64_t cap, uint64_t* nkept);
+
+/* async form: the report rows are copied on the pool's D2H stream (double-
+ * buffered), overlapping the next slice; *nkept is final on return, the host
+ * arrays are complete after vate_estimate_wait. */
+int vate_estimate_finish_async(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
+                               double floor, uint64_t* out_host, double* out_est,
+                               double* out_zv, uint8_t* out_sat, uint64_t cap, uint64_t* nkept);
+int vate_estimate_wait(vate_pool* p);
 
 /* ---- snapshots: AtPool.snapshot_bytes / load (pools.py:261-298) -------- */
 int vate_snapshot_size(const vate_pool* p, uint64_t* nbytes);

@@ -55,6 +55,8 @@ _SIGS = {
     "vate_set_cells": ([_p, _p, _u64, _int], _int),
     "vate_scan_pairs": ([_p, _u64, _u64, _u64, _p, _p, _u64, _int, _p, _i64], _int),
     "vate_scan_packed": ([_p, _u64, _u64, _u64, _p, _u64, _int, _p, _i64], _int),
+    "vate_stage_packed": ([_p, _p, _u64, C.POINTER(_int)], _int),
+    "vate_scan_staged": ([_p, _u64, _u64, _u64, _int, _u64, _p, _i64], _int),
     "vate_pair_cells": ([_p, _u64, _int, _u64, _u64, _p, _p, _u64, _int, _p], _int),
     "vate_host_cells": ([_p, _u64, _int, _u64, _p, _u64, _int, _p], _int),
     "vate_advance": ([_p, _pi32, _pu64, _pu64], _int),
@@ -69,6 +71,8 @@ _SIGS = {
     "vate_estimate_begin": ([_p, _p, _u64, _u64, _i64, _int, _pu64, _pu64], _int),
     "vate_estimate_begin_hosts": ([_p, _p, _u64, _int, _u64, _u64, _int, _pu64], _int),
     "vate_estimate_finish": ([_p, _u64, _u64, _dbl, _dbl, _p, _p, _p, _p, _u64, _pu64], _int),
+    "vate_estimate_finish_async": ([_p, _u64, _u64, _dbl, _dbl, _p, _p, _p, _p, _u64, _pu64], _int),
+    "vate_estimate_wait": ([_p], _int),
     "vate_snapshot_size": ([_p, _pu64], _int),
     "vate_snapshot": ([_p, _p, _u64, _pu64], _int),
     "vate_load": ([_p, _p, _u64], _int),

@@ -383,15 +383,17 @@ __global__ void __launch_bounds__(256) k_final_write(const uint64_t* __restrict_
   }
 }
 
+// Writes report set `slot`; the D2H that last read that set must be done first.
 static int run_float_path(vate_pool* p, const uint64_t* hosts_dev, const int32_t* g0_dev,
-                          uint64_t n, FloatPath F, uint64_t* nkept) {
+                          uint64_t n, FloatPath F, int slot, uint64_t* nkept) {
   const uint64_t ntiles = (n + kFinTile - 1) / kFinTile;
   int rc;
-  for (DevBuf* b : {&p->host_out, &p->est_out, &p->zv_out}) {
+  VATE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_d2h[slot], 0));
+  for (DevBuf* b : {&p->host_out[slot], &p->est_out[slot], &p->zv_out[slot]}) {
     rc = b->ensure(n * 8 + 8);
     if (rc) return rc;
   }
-  rc = p->sat_out.ensure(n + 8);
+  rc = p->sat_out[slot].ensure(n + 8);
   if (rc) return rc;
   const unsigned* tile_off = nullptr;
   if (F.floor > 0.0) {
@@ -406,8 +408,8 @@ static int run_float_path(vate_pool* p, const uint64_t* hosts_dev, const int32_t
     tile_off = p->flags.as<const unsigned>();
   }
   VATE_LAUNCH(p, VATE_K_FINAL, (uint32_t)ntiles, 256, 0, k_final_write, hosts_dev, g0_dev, n, F,
-              tile_off, p->host_out.as<uint64_t>(), p->est_out.as<double>(), p->zv_out.as<double>(),
-              p->sat_out.as<uint8_t>());
+              tile_off, p->host_out[slot].as<uint64_t>(), p->est_out[slot].as<double>(),
+              p->zv_out[slot].as<double>(), p->sat_out[slot].as<uint8_t>());
   if (F.floor > 0.0) {
     rc = sync_small(p);
     if (rc) return rc;
@@ -418,19 +420,30 @@ static int run_float_path(vate_pool* p, const uint64_t* hosts_dev, const int32_t
   return VATE_OK;
 }
 
-static int copy_rows_out(vate_pool* p, uint64_t m, bool with_hosts, uint64_t* out_host,
+// Report rows of set `slot` -> host, on the D2H stream once the float path is
+// done; overlaps the next slice's kernels.  ev_d2h[slot] marks completion.
+static int copy_rows_out(vate_pool* p, int slot, uint64_t m, bool with_hosts, uint64_t* out_host,
                          double* out_est, double* out_zv, uint8_t* out_sat) {
+  VATE_CUDA(cudaEventRecord(p->ev_fin[slot], p->stream));
+  VATE_CUDA(cudaStreamWaitEvent(p->d2h_stream, p->ev_fin[slot], 0));
   if (m) {
+    cudaStream_t s = p->d2h_stream;
     if (with_hosts && out_host)
-      VATE_CUDA(cudaMemcpyAsync(out_host, p->host_out.ptr, m * 8, cudaMemcpyDeviceToHost, p->stream));
+      VATE_CUDA(cudaMemcpyAsync(out_host, p->host_out[slot].ptr, m * 8, cudaMemcpyDeviceToHost, s));
     if (out_est)
-      VATE_CUDA(cudaMemcpyAsync(out_est, p->est_out.ptr, m * 8, cudaMemcpyDeviceToHost, p->stream));
+      VATE_CUDA(cudaMemcpyAsync(out_est, p->est_out[slot].ptr, m * 8, cudaMemcpyDeviceToHost, s));
     if (out_zv)
-      VATE_CUDA(cudaMemcpyAsync(out_zv, p->zv_out.ptr, m * 8, cudaMemcpyDeviceToHost, p->stream));
+      VATE_CUDA(cudaMemcpyAsync(out_zv, p->zv_out[slot].ptr, m * 8, cudaMemcpyDeviceToHost, s));
     if (out_sat)
-      VATE_CUDA(cudaMemcpyAsync(out_sat, p->sat_out.ptr, m, cudaMemcpyDeviceToHost, p->stream));
+      VATE_CUDA(cudaMemcpyAsync(out_sat, p->sat_out[slot].ptr, m, cudaMemcpyDeviceToHost, s));
   }
-  return sync_small(p);
+  VATE_CUDA(cudaEventRecord(p->ev_d2h[slot], p->d2h_stream));
+  return VATE_OK;
+}
+
+static int wait_rows(vate_pool* p, int slot) {
+  VATE_CUDA(cudaEventSynchronize(p->ev_d2h[slot]));
+  return VATE_OK;
 }
 
 static int float_params(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
@@ -498,9 +511,13 @@ int vate_reports_from_counts(vate_pool* p, uint64_t g, const int32_t* g0, uint64
   rc = stage_in(p, p->in_a, g0, n * 4, VATE_HOST, &d_g0);
   if (rc) return rc;
   uint64_t kept = 0;
-  rc = run_float_path(p, nullptr, (const int32_t*)d_g0, n, F, &kept);
+  const int slot = p->out_slot;
+  p->out_slot ^= 1;
+  rc = run_float_path(p, nullptr, (const int32_t*)d_g0, n, F, slot, &kept);
   if (rc) return rc;
-  return copy_rows_out(p, n, false, nullptr, est, z_v, saturated);
+  rc = copy_rows_out(p, slot, n, false, nullptr, est, z_v, saturated);
+  if (rc) return rc;
+  return wait_rows(p, slot);
 }
 
 int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
@@ -555,6 +572,7 @@ int vate_estimate_begin_hosts(vate_pool* p, const uint64_t* hosts, uint64_t n, i
   if (g < 1 || g > p->L.size) return set_error(VATE_ECONFIG, "g must be in [1, 2^c]");
   p->est_n = 0;
   *pool_inactive = 0;
+  p->sorted_owner = nullptr;  // hosts_sorted no longer holds a registry's active set
   rc = p->hosts_sorted.ensure(n * 8 + 8);
   if (rc) return rc;
   if (n) {
@@ -581,9 +599,10 @@ int vate_estimate_begin_hosts(vate_pool* p, const uint64_t* hosts, uint64_t n, i
   return VATE_OK;
 }
 
-int vate_estimate_finish(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
-                         double floor, uint64_t* out_host, double* out_est, double* out_zv,
-                         uint8_t* out_sat, uint64_t cap, uint64_t* nkept) {
+static int estimate_finish_impl(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
+                                double floor, uint64_t* out_host, double* out_est,
+                                double* out_zv, uint8_t* out_sat, uint64_t cap, uint64_t* nkept,
+                                bool wait) {
   int rc = enter(p);
   if (rc) return rc;
   if (g != p->est_g) return set_error(VATE_EVALUE, "estimate_finish: g differs from begin");
@@ -594,11 +613,37 @@ int vate_estimate_finish(vate_pool* p, uint64_t g, uint64_t pool_inactive, doubl
   rc = float_params(p, g, pool_inactive, log_zp, floor, &F);
   if (rc) return rc;
   uint64_t kept = 0;
-  rc = run_float_path(p, p->hosts_sorted.as<const uint64_t>(), p->g0.as<const int32_t>(), n, F, &kept);
+  const int slot = p->out_slot;
+  p->out_slot ^= 1;
+  rc = run_float_path(p, p->hosts_sorted.as<const uint64_t>(), p->g0.as<const int32_t>(), n, F,
+                      slot, &kept);
   if (rc) return rc;
   *nkept = kept;
   p->est_n = 0;
-  return copy_rows_out(p, kept < cap ? kept : cap, true, out_host, out_est, out_zv, out_sat);
+  rc = copy_rows_out(p, slot, kept < cap ? kept : cap, true, out_host, out_est, out_zv, out_sat);
+  if (rc || !wait) return rc;
+  return wait_rows(p, slot);
+}
+
+int vate_estimate_finish(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
+                         double floor, uint64_t* out_host, double* out_est, double* out_zv,
+                         uint8_t* out_sat, uint64_t cap, uint64_t* nkept) {
+  return estimate_finish_impl(p, g, pool_inactive, log_zp, floor, out_host, out_est, out_zv,
+                              out_sat, cap, nkept, true);
+}
+
+int vate_estimate_finish_async(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
+                               double floor, uint64_t* out_host, double* out_est,
+                               double* out_zv, uint8_t* out_sat, uint64_t cap, uint64_t* nkept) {
+  return estimate_finish_impl(p, g, pool_inactive, log_zp, floor, out_host, out_est, out_zv,
+                              out_sat, cap, nkept, false);
+}
+
+int vate_estimate_wait(vate_pool* p) {
+  int rc = enter(p);
+  if (rc) return rc;
+  VATE_CUDA(cudaStreamSynchronize(p->d2h_stream));
+  return VATE_OK;
 }
 
 }  // extern "C"

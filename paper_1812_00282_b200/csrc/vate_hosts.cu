@@ -16,7 +16,7 @@
 
 namespace vate {
 
-enum HCtr { H_COUNT = 0, H_OVF = 1, H_SPECIAL = 2, H_MAXKEY = 3, H_NOUT = 4, H_N = 8 };
+enum HCtr { H_COUNT = 0, H_OVF = 1, H_SPECIAL = 2, H_MAXKEY = 3, H_NOUT = 4, H_CHANGES = 5, H_N = 8 };
 
 RegRef make_ref(const vate_hosts* h, const DevBuf& table, uint64_t cap) {
   RegRef R{};
@@ -55,17 +55,23 @@ __global__ void k_insert_entries(const RegEntry* __restrict__ src, uint64_t n,
 // sorts).  Each CTA handles tiles of 1024 entries (4 per thread) and reserves
 // its output range with one atomic per tile.
 constexpr int kActTile = 1024;
+// member[i] remembers whether slot i was in the previous compaction's set; the
+// number of slots whose membership flipped tells the host whether last slice's
+// sorted list can be reused (exactly) instead of sorting again.
 __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ table, uint64_t cap,
                                                 const unsigned long long* special, long long cut,
                                                 uint64_t* __restrict__ out,
                                                 unsigned long long* nout,
-                                                unsigned long long* maxkey) {
+                                                unsigned long long* maxkey,
+                                                uint8_t* __restrict__ member,
+                                                unsigned long long* changes) {
   __shared__ unsigned warp_tot[8];
   __shared__ unsigned long long base_s;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t total = cap + 1;
   const bool special_present = (*special & 0xFFFFFFFFull) != 0;
   unsigned long long kmax = 0;
+  unsigned flips = 0;
   for (uint64_t tile = (uint64_t)blockIdx.x * kActTile; tile < total;
        tile += (uint64_t)gridDim.x * kActTile) {
     const uint64_t i0 = tile + threadIdx.x * 4;
@@ -79,6 +85,10 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
         const RegEntry e = table[i];
         const bool tk = (i < cap) ? (e.key != kEmptyKey && e.last > cut)
                                   : (special_present && e.last > cut);
+        if ((member[i] != 0) != tk) {
+          member[i] = tk;
+          ++flips;
+        }
         if (tk) {
           key[q] = e.key;
           take |= 1u << q;
@@ -115,6 +125,8 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
     kmax = other > kmax ? other : kmax;
   }
   if (lane == 0 && kmax) atomicMax(maxkey, kmax);
+  flips = __reduce_add_sync(0xffffffffu, flips);
+  if (lane == 0 && flips) atomicAdd(changes, (unsigned long long)flips);
 }
 
 // Entries with last > horizon, appended (prune keeps them).
@@ -205,6 +217,7 @@ int hosts_drain(vate_hosts* h) {
     h->scratch.ptr = nullptr;
     h->scratch.bytes = 0;
     h->cap = new_cap;
+    h->member_valid = false;  // slots moved
     rc = hosts_read_counters(h, c);
     if (rc) return rc;
     if (c[H_OVF]) return hosts_drain(h);  // pathological: grow again
@@ -258,13 +271,20 @@ int hosts_active_launch(vate_hosts* h, int64_t t, int k_prime) {
   }
   rc = p->hosts_tmp.ensure((h->cap + 2) * 8);
   if (rc) return rc;
+  if (p->hosts_sorted.bytes < (h->cap + 2) * 8) p->sorted_owner = nullptr;  // realloc loses it
   rc = p->hosts_sorted.ensure((h->cap + 2) * 8);
   if (rc) return rc;
-  VATE_CUDA(cudaMemsetAsync(h->d_count + H_MAXKEY, 0, 16, p->stream));
+  if (!h->member_valid || h->member.bytes < h->cap + 1) {
+    rc = h->member.ensure(h->cap + 1);
+    if (rc) return rc;
+    VATE_CUDA(cudaMemsetAsync(h->member.ptr, 0, h->cap + 1, p->stream));
+    h->member_valid = false;  // first compaction after a (re)layout always sorts
+  }
+  VATE_CUDA(cudaMemsetAsync(h->d_count + H_MAXKEY, 0, 24, p->stream));
   VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap + 1, kActTile, 148u * 8u), 256, 0, k_active,
               h->table.as<const RegEntry>(), h->cap, h->d_count + H_SPECIAL,
               (long long)(t - k_prime), p->hosts_tmp.as<uint64_t>(), h->d_count + H_NOUT,
-              h->d_count + H_MAXKEY);
+              h->d_count + H_MAXKEY, h->member.as<uint8_t>(), h->d_count + H_CHANGES);
   VATE_CUDA(cudaMemcpyAsync(h->h_count, h->d_count, H_N * 8, cudaMemcpyDeviceToHost, p->stream));
   return VATE_OK;
 }
@@ -285,6 +305,15 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
   if (h->count_hint > h->cap / 2 || (h->cap > (1u << 16) && h->count_hint * 16 < h->cap))
     h->needs_grow = true;
   *n = h->h_count[H_NOUT];
+  *keys_dev = p->hosts_sorted.as<uint64_t>();
+  // same membership as the last compaction, whose sorted list is still in place
+  const bool reuse = h->member_valid && h->h_count[H_CHANGES] == 0 && p->sorted_owner == h &&
+                     p->sorted_n == *n;
+  h->member_valid = true;
+  if (reuse) {
+    p->sorts_skipped++;
+    return VATE_OK;
+  }
   const unsigned long long maxkey = h->h_count[H_MAXKEY];
   int end_bit = 64;
   while (end_bit > 1 && !((maxkey >> (end_bit - 1)) & 1ull)) --end_bit;
@@ -295,7 +324,8 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
     VATE_CUDA(cudaMemcpyAsync(p->hosts_sorted.ptr, p->hosts_tmp.ptr, 8, cudaMemcpyDeviceToDevice,
                               p->stream));
   }
-  *keys_dev = p->hosts_sorted.as<uint64_t>();
+  p->sorted_owner = h;
+  p->sorted_n = *n;
   return VATE_OK;
 }
 
@@ -351,7 +381,9 @@ int vate_hosts_destroy(vate_hosts* h) {
   if (!h) return VATE_OK;
   cudaSetDevice(h->pool->device);
   cudaStreamSynchronize(h->pool->stream);
+  if (h->pool->sorted_owner == h) h->pool->sorted_owner = nullptr;
   h->table.release();
+  h->member.release();
   h->ovf.release();
   h->scratch.release();
   if (h->d_count) cudaFree(h->d_count);
@@ -426,6 +458,7 @@ int vate_hosts_prune(vate_hosts* h, int64_t t) {
               (const unsigned long long*)nullptr, h->ref(), 1);
   VATE_CUDA(cudaStreamSynchronize(p->stream));
   keep.release();
+  h->member_valid = false;  // slots moved
   h->count_hint = c[H_NOUT] + (special ? 1 : 0);
   h->pending = 0;
   return VATE_OK;

@@ -198,7 +198,13 @@ struct vate_pool {
   vate::DevBuf in_a, in_b;  // staging for host inputs
   vate::DevBuf out_buf;     // staging for device outputs
   vate::DevBuf hosts_sorted, hosts_tmp, g0, flags, sel_idx, cub_tmp;
-  vate::DevBuf est_out, zv_out, sat_out, host_out;
+  vate::DevBuf est_out[2], zv_out[2], sat_out[2], host_out[2];  // double-buffered reports
+  int out_slot = 0;
+  vate::DevBuf stage[2];    // double-buffered packet staging (H2D prefetch)
+  int stage_slot = 0;
+  cudaStream_t d2h_stream = nullptr, h2d_stream = nullptr;
+  cudaEvent_t ev_fin[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   vate::DevBuf lzv;         // log table, g+1 doubles
   uint64_t lzv_g = 0;
 
@@ -220,6 +226,9 @@ struct vate_pool {
   // options
   int opt_g0 = 0;
   int opt_inc = 1;            // incremental g0 through the inverse index
+  const void* sorted_owner = nullptr;  // registry whose active set hosts_sorted holds
+  uint64_t sorted_n = 0;
+  uint64_t sorts_skipped = 0;
   vate::IncIndex inc;
   int dsmem_clusters = -1;   // cached max active clusters for the DSMEM gather (-1 unknown)
 
@@ -247,6 +256,8 @@ struct vate_hosts {
   uint64_t pending = 0;    // registry inserts enqueued since the last drain
   uint64_t count_hint = 0; // last count read back
   bool needs_grow = false; // load factor passed 1/2: grow at the next drain point
+  vate::DevBuf member;     // u8 per slot: in the active set of the last compaction
+  bool member_valid = false;
   vate::RegRef ref() const;
 };
 

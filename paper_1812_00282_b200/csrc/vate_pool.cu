@@ -611,6 +611,12 @@ int vate_pool_create(vate_pool** out, int c, int k, int partition, int device) {
   if (e == cudaSuccess) e = cudaMalloc(&p->d_ctr, C_N * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMallocHost(&p->h_ctr, C_N * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_small, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    for (cudaEvent_t* ev : {&p->ev_fin[i], &p->ev_d2h[i], &p->ev_h2d[i], &p->ev_used[i]})
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  }
   if (e == cudaSuccess)
     e = cudaMemsetAsync(p->d_ctr, 0, C_N * sizeof(unsigned long long), p->stream);
   if (e != cudaSuccess) rc = cuda_fail(e, "vate_pool_create");
@@ -637,10 +643,19 @@ int vate_pool_destroy(vate_pool* p) {
   if (!p) return VATE_OK;
   cudaSetDevice(p->device);
   if (p->stream) cudaStreamSynchronize(p->stream);
+  if (p->d2h_stream) cudaStreamSynchronize(p->d2h_stream);
+  if (p->h2d_stream) cudaStreamSynchronize(p->h2d_stream);
   for (DevBuf* b : {&p->bitmap, &p->in_a, &p->in_b, &p->out_buf, &p->hosts_sorted, &p->hosts_tmp,
-                    &p->g0, &p->flags, &p->sel_idx, &p->cub_tmp, &p->est_out, &p->zv_out,
-                    &p->sat_out, &p->host_out, &p->lzv})
+                    &p->g0, &p->flags, &p->sel_idx, &p->cub_tmp, &p->lzv})
     b->release();
+  for (int i = 0; i < 2; ++i) {
+    for (DevBuf* b : {&p->est_out[i], &p->zv_out[i], &p->sat_out[i], &p->host_out[i], &p->stage[i]})
+      b->release();
+    for (cudaEvent_t ev : {p->ev_fin[i], p->ev_d2h[i], p->ev_h2d[i], p->ev_used[i]})
+      if (ev) cudaEventDestroy(ev);
+  }
+  if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
+  if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
   inc_release(p);
   if (p->cells) cudaFree(p->cells);
   if (p->d_ctr) cudaFree(p->d_ctr);
@@ -669,6 +684,8 @@ int vate_pool_info(const vate_pool* p, int32_t* bact0, int32_t* cell_bytes, void
 int vate_pool_sync(vate_pool* p) {
   int rc = enter(p);
   if (rc) return rc;
+  VATE_CUDA(cudaStreamSynchronize(p->h2d_stream));
+  VATE_CUDA(cudaStreamSynchronize(p->d2h_stream));
   return sync_small(p);
 }
 
@@ -851,6 +868,37 @@ int vate_scan_packed(vate_pool* p, uint64_t g, uint64_t cell_stream, uint64_t gr
   if (!p) return set_error(VATE_EVALUE, "null pool handle");
   return scan_common(p, make_hash(g, p->c, cell_stream, group_stream), nullptr, nullptr, pairs,
                      n, where, hosts, t);
+}
+
+int vate_stage_packed(vate_pool* p, const uint32_t* pairs, uint64_t n, int* slot) {
+  int rc = enter(p);
+  if (rc) return rc;
+  const int s = p->stage_slot;
+  p->stage_slot ^= 1;
+  if (p->stage[s].bytes < n * 8) {
+    VATE_CUDA(cudaEventSynchronize(p->ev_used[s]));
+    rc = p->stage[s].ensure(n * 8 + 16);
+    if (rc) return rc;
+  }
+  VATE_CUDA(cudaStreamWaitEvent(p->h2d_stream, p->ev_used[s], 0));  // last scan of this buffer
+  if (n) VATE_CUDA(cudaMemcpyAsync(p->stage[s].ptr, pairs, n * 8, cudaMemcpyHostToDevice, p->h2d_stream));
+  VATE_CUDA(cudaEventRecord(p->ev_h2d[s], p->h2d_stream));
+  *slot = s;
+  return VATE_OK;
+}
+
+int vate_scan_staged(vate_pool* p, uint64_t g, uint64_t cell_stream, uint64_t group_stream,
+                     int slot, uint64_t n, vate_hosts* hosts, int64_t t) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (slot < 0 || slot > 1 || p->stage[slot].bytes < n * 8)
+    return set_error(VATE_EVALUE, "bad staging slot");
+  VATE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_h2d[slot], 0));
+  rc = scan_common(p, make_hash(g, p->c, cell_stream, group_stream), nullptr, nullptr,
+                   (const uint32_t*)p->stage[slot].ptr, n, VATE_DEVICE, hosts, t);
+  if (rc) return rc;
+  VATE_CUDA(cudaEventRecord(p->ev_used[slot], p->stream));
+  return VATE_OK;
 }
 
 int vate_pair_cells(vate_pool* p, uint64_t g, int c, uint64_t cell_stream,

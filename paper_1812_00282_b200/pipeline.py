@@ -138,7 +138,8 @@ class Pipeline:
                                    VATE_DEVICE if on_device else VATE_HOST,
                                    self.hosts.handle, t))
 
-    def estimate_soa(self, t: int, out=None, advance: bool = False) -> HostReports | None:
+    def estimate_soa(self, t: int, out=None, advance: bool = False,
+                     wait: bool = True) -> HostReports | None:
         """The estimate phase (pipeline.py:120-138) as arrays; None without hosts.
 
         ``out`` may supply preallocated (pinned) host arrays
@@ -146,6 +147,9 @@ class Pipeline:
         With ``advance=True`` the slice advance is enqueued right after the g0
         gather (it touches cells, the float path does not), so the float path
         and the sweep share one host round trip; collect it with _collect().
+        With ``wait=False`` the report rows are copied on the pool's D2H stream
+        while the caller moves on (double-buffered): the arrays are complete
+        after ``wait_reports()``; alternate two ``out`` sets between slices.
         """
         nh, p = C.c_uint64(), C.c_uint64()
         check(lib.vate_estimate_begin(self.pool.handle, self.hosts.handle, self.cfg.g,
@@ -163,9 +167,9 @@ class Pipeline:
                    np.empty(n, np.uint8))
         host, est, zv, sat = out
         kept = C.c_uint64()
-        check(lib.vate_estimate_finish(self.pool.handle, self.cfg.g, p.value, lzp,
-                                       float(self.floor), ptr(host), ptr(est), ptr(zv), ptr(sat),
-                                       len(host), C.byref(kept)))
+        finish = lib.vate_estimate_finish if wait else lib.vate_estimate_finish_async
+        check(finish(self.pool.handle, self.cfg.g, p.value, lzp, float(self.floor), ptr(host),
+                     ptr(est), ptr(zv), ptr(sat), len(host), C.byref(kept)))
         m = kept.value
         self.last_pool_inactive = p.value
         return HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool), z_p,
@@ -190,10 +194,29 @@ class Pipeline:
     def _maintain(self, t: int) -> MaintenanceReport:
         return self._account(t, self.pool.advance_slice())
 
-    def step_packed(self, t: int, pairs, n: int, on_device: bool, out=None):
+    def wait_reports(self) -> None:
+        """Block until every report row enqueued with wait=False is in host memory."""
+        check(lib.vate_estimate_wait(self.pool.handle))
+
+    def stage_packed(self, pairs_host_ptr: int, n: int) -> int:
+        """Start the H2D copy of a slice's packed records (pinned host memory) on the
+        pool's copy stream; returns the staging slot for step_staged."""
+        slot = C.c_int()
+        check(lib.vate_stage_packed(self.pool.handle, int(pairs_host_ptr), int(n), C.byref(slot)))
+        return slot.value
+
+    def step_packed(self, t: int, pairs, n: int, on_device: bool, out=None, wait: bool = True):
         """One slice from packed records: scan, estimate (+ advance overlapped), prune."""
         self.scan_packed(t, pairs, n, on_device)
-        rep = self.estimate_soa(t, out, advance=True)
+        rep = self.estimate_soa(t, out, advance=True, wait=wait)
+        self._collect(t)
+        return rep
+
+    def step_staged(self, t: int, slot: int, n: int, out=None, wait: bool = True):
+        """One slice from a staged buffer (see stage_packed)."""
+        check(lib.vate_scan_staged(self.pool.handle, self.cfg.g, self.cfg.cell_stream,
+                                   self.cfg.group_stream, slot, int(n), self.hosts.handle, t))
+        rep = self.estimate_soa(t, out, advance=True, wait=wait)
         self._collect(t)
         return rep
 

@@ -551,3 +551,28 @@ def test_incremental_off_equals_on():
         assert np.array_equal(r1.host, r2.host) and np.array_equal(r1.estimate, r2.estimate)
     assert p_on.inc_stats()["delta_slices"] >= 25
     assert p_off.inc_stats()["delta_slices"] == 0
+
+
+def test_active_set_reuse_is_exact():
+    """The registry reuses last slice's sorted active list only when no host
+    entered or left; interleave quiet slices with joins, departures, k' changes
+    and a second registry on the same pool."""
+    pool = vb.AtPool(12, 6)
+    reg = vb.SlidingHostSet(6, pool=pool)
+    other = vb.SlidingHostSet(6, pool=pool)
+    ref = vo.OracleHosts(6)
+    rng = np.random.default_rng(21)
+    keys = rng.integers(0, 1 << 40, 500).astype(np.uint64)
+    for t in range(40):
+        if t % 9 == 4:
+            batch = rng.integers(0, 1 << 40, 50).astype(np.uint64)      # joins
+        elif t % 9 == 7:
+            batch = np.empty(0, dtype=np.uint64)                       # departures age out
+        else:
+            batch = keys                                               # quiet
+        reg.update(batch, t)
+        ref.update(batch, t)
+        other.update(keys[:10], t)
+        for kp in (6, 6, 3, 6):
+            assert np.array_equal(reg.active(t, kp), ref.active(t, kp)), (t, kp)
+        assert len(other.active(t, 6)) == 10
