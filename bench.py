@@ -375,7 +375,7 @@ def run_gpu(args, rank, world, local_rank):
                                                           "refresh_slices", "full_slices")},
                         "last_delta_cells": inc1["last_delta_cells"],
                         "last_delta_work": inc1["last_delta_work"],
-                        "last_misses": inc1["last_misses"],
+                        "identity_slices": inc1["identity_slices"] - inc0["identity_slices"],
                         "hosts_indexed": inc1["hosts_indexed"]},
         "clocks": clocks.summary(),
     }

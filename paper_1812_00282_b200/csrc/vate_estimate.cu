@@ -12,7 +12,6 @@
 
 namespace vate {
 
-int build_bitmap(vate_pool* p, int k_prime);   // vate_pool.cu
 int check_width(vate_pool* p, int k_prime);    // vate_pool.cu
 
 // g0[h] = #{ j < g : bitmap bit of H(aip_h, j) is set }  (estimator.py:107-123)
@@ -531,13 +530,21 @@ int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t ce
   p->est_n = 0;
   // one host round trip per estimate: Z_p (bitmap pass) and the active-set
   // compaction are both enqueued, then their counters are read together
-  // misses of the previous incremental estimate (visible since its finish sync)
-  if (p->inc.valid && p->inc.last_n && p->h_ctr[C_MISS] * 20 > p->inc.last_n)
-    p->inc.want_rebuild = true;
+  // misses of the previous incremental lookup (visible since its finish sync)
+  IncIndex& I = p->inc;
+  if (I.lookup_pending) {
+    I.lookup_pending = false;
+    I.last_misses = p->h_ctr[C_MISS];
+    if (I.valid && I.last_n && I.last_misses * 20 > I.last_n) I.want_rebuild = true;
+    if (I.valid && I.last_misses == 0 && I.m == I.last_n) {  // that active list == X
+      I.identity_ok = true;
+      I.identity_version = I.lookup_version;
+    }
+  }
   p->h_ctr[C_MISS] = 0;
-  rc = build_bitmap(p, k_prime);  // P -> h_ctr[C_P]; the bitmap feeds the gather
-  if (rc) return rc;
-  rc = inc_launch_delta(p, g, cell_stream, k_prime);  // flipped cells vs the last estimate
+  // P -> h_ctr[C_P]; the bitmap feeds the gather; with a live inverse index the
+  // same pass lists the cells whose bit flipped since the last estimate
+  rc = build_bitmap(p, k_prime, inc_delta_ready(p, g, cell_stream, k_prime));
   if (rc) return rc;
   rc = hosts_active_launch(hosts, t, k_prime);  // pipeline.py:121
   if (rc) return rc;
@@ -573,6 +580,8 @@ int vate_estimate_begin_hosts(vate_pool* p, const uint64_t* hosts, uint64_t n, i
   p->est_n = 0;
   *pool_inactive = 0;
   p->sorted_owner = nullptr;  // hosts_sorted no longer holds a registry's active set
+  p->sorted_version++;
+  p->g0_src = nullptr;
   rc = p->hosts_sorted.ensure(n * 8 + 8);
   if (rc) return rc;
   if (n) {
@@ -615,8 +624,8 @@ static int estimate_finish_impl(vate_pool* p, uint64_t g, uint64_t pool_inactive
   uint64_t kept = 0;
   const int slot = p->out_slot;
   p->out_slot ^= 1;
-  rc = run_float_path(p, p->hosts_sorted.as<const uint64_t>(), p->g0.as<const int32_t>(), n, F,
-                      slot, &kept);
+  rc = run_float_path(p, p->hosts_sorted.as<const uint64_t>(),
+                      p->g0_src ? p->g0_src : p->g0.as<const int32_t>(), n, F, slot, &kept);
   if (rc) return rc;
   *nkept = kept;
   p->est_n = 0;

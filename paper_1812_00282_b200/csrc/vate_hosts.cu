@@ -326,6 +326,7 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
   }
   p->sorted_owner = h;
   p->sorted_n = *n;
+  p->sorted_version++;
   return VATE_OK;
 }
 

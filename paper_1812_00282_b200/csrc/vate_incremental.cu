@@ -53,31 +53,6 @@ __global__ void k_inc_fill(const uint64_t* __restrict__ X, uint64_t total, DivU6
   }
 }
 
-// Flipped cells of (bnew XOR bold) -> list of cell | (now_inactive << 32),
-// with the number of index entries they touch.
-__global__ void k_inc_delta(const uint32_t* __restrict__ bnew, const uint32_t* __restrict__ bold,
-                            uint64_t nwords, const uint32_t* __restrict__ off,
-                            unsigned long long* __restrict__ list, uint64_t cap,
-                            unsigned long long* count, unsigned long long* work) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
-    const uint32_t nb = bnew[w];
-    uint32_t x = nb ^ bold[w];
-    if (!x) continue;
-    unsigned long long pos = atomicAdd(count, (unsigned long long)__popc(x));
-    unsigned long long wsum = 0;
-    while (x) {
-      const int b = __ffs(x) - 1;
-      x &= x - 1;
-      const uint64_t cell = w * 32 + b;
-      wsum += off[cell + 1] - off[cell];
-      if (pos < cap) list[pos] = cell | ((unsigned long long)((nb >> b) & 1u) << 32);
-      ++pos;
-    }
-    atomicAdd(work, wsum);
-  }
-}
-
 // One warp per flipped cell: +1 to every pair that became inactive, -1 otherwise.
 __global__ void k_inc_apply(const unsigned long long* __restrict__ list,
                             const unsigned long long* count, uint64_t cap,
@@ -127,23 +102,13 @@ static void swap_buf(DevBuf& a, DevBuf& b) {
   std::swap(a.bytes, b.bytes);
 }
 
-// Enqueue the delta of the fresh bitmap against bprev (before the estimate's
-// host round trip, so its counts arrive with P and the registry counters).
-int inc_launch_delta(vate_pool* p, uint64_t g, uint64_t cs, int kp) {
+// Whether the coming bitmap pass should also emit the delta against bprev
+// (index live and built for these parameters).
+bool inc_delta_ready(vate_pool* p, uint64_t g, uint64_t cs, int kp) {
   IncIndex& I = p->inc;
-  I.delta_launched = false;
-  if (!p->opt_inc || !I.valid || I.want_rebuild || I.g != g || I.cs != cs || I.kp != kp)
-    return VATE_OK;
-  const uint64_t nwords = (p->L.size + 31) / 32;
-  VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_DCNT, 0, 16, p->stream));
-  VATE_LAUNCH(p, VATE_K_G0, grid_for(nwords, kThreads, 148u * 16u), kThreads, 0, k_inc_delta,
-              p->bitmap.as<const uint32_t>(), I.bprev.as<const uint32_t>(), nwords,
-              I.off.as<const uint32_t>(), I.dlist.as<unsigned long long>(), I.dlist_cap,
-              p->d_ctr + C_DCNT, p->d_ctr + C_DWORK);
-  VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_DCNT, p->d_ctr + C_DCNT, 16, cudaMemcpyDeviceToHost,
-                            p->stream));
-  I.delta_launched = true;
-  return VATE_OK;
+  I.delta_launched = p->opt_inc && I.valid && !I.want_rebuild && I.g == g && I.cs == cs &&
+                     I.kp == kp;
+  return I.delta_launched;
 }
 
 // Build the inverse index over X = hosts (sorted, n), with g0x = g0_dev (already
@@ -195,6 +160,8 @@ static int inc_rebuild(vate_pool* p, const uint64_t* hosts, uint64_t n, HashPara
   I.valid = true;
   I.want_rebuild = false;
   I.rebuilds++;
+  I.identity_ok = true;  // X is exactly this active list
+  I.identity_version = p->sorted_version;
   return VATE_OK;
 }
 
@@ -222,16 +189,25 @@ int inc_compute_g0(vate_pool* p, const uint64_t* hosts, uint64_t n, HashParams H
       if ((rc = launch_g0(p, I.X.as<const uint64_t>(), I.m, H, I.g0x.as<int32_t>()))) return rc;
       I.refresh_slices++;
     }
-    if ((rc = I.miss.ensure(n * 4 + 4))) return rc;
-    VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_MISS, 0, 8, p->stream));
-    VATE_LAUNCH(p, VATE_K_G0, grid_for(n, kThreads, 148u * 16u), kThreads, 0, k_inc_lookup, hosts, n,
-                I.X.as<const uint64_t>(), I.m, I.g0x.as<const int32_t>(), p->g0.as<int32_t>(),
-                I.miss.as<uint32_t>(), p->d_ctr + C_MISS);
-    if ((rc = launch_g0_list(p, hosts, I.miss.as<const uint32_t>(), p->d_ctr + C_MISS, n, H,
-                             p->g0.as<int32_t>())))
-      return rc;
-    VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_MISS, p->d_ctr + C_MISS, 8, cudaMemcpyDeviceToHost,
-                              p->stream));
+    if (I.identity_ok && I.identity_version == p->sorted_version && I.m == n) {
+      p->g0_src = I.g0x.as<const int32_t>();  // the active list is X itself
+      I.identity_slices++;
+    } else {
+      I.identity_ok = false;
+      if ((rc = I.miss.ensure(n * 4 + 4))) return rc;
+      VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_MISS, 0, 8, p->stream));
+      VATE_LAUNCH(p, VATE_K_G0, grid_for(n, kThreads, 148u * 16u), kThreads, 0, k_inc_lookup, hosts,
+                  n, I.X.as<const uint64_t>(), I.m, I.g0x.as<const int32_t>(), p->g0.as<int32_t>(),
+                  I.miss.as<uint32_t>(), p->d_ctr + C_MISS);
+      if ((rc = launch_g0_list(p, hosts, I.miss.as<const uint32_t>(), p->d_ctr + C_MISS, n, H,
+                               p->g0.as<int32_t>())))
+        return rc;
+      VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_MISS, p->d_ctr + C_MISS, 8, cudaMemcpyDeviceToHost,
+                                p->stream));
+      I.lookup_pending = true;
+      I.lookup_version = p->sorted_version;
+      p->g0_src = p->g0.as<const int32_t>();
+    }
     swap_buf(p->bitmap, I.bprev);  // g0x now matches this slice's bitmap
     I.last_n = n;
     if (I.m > 2 * n) I.want_rebuild = true;
@@ -239,6 +215,7 @@ int inc_compute_g0(vate_pool* p, const uint64_t* hosts, uint64_t n, HashParams H
   }
   // full recompute; then (re)build the index over this active set
   if ((rc = launch_g0(p, hosts, n, H, p->g0.as<int32_t>()))) return rc;
+  p->g0_src = p->g0.as<const int32_t>();
   I.full_slices++;
   if (p->opt_inc && (same_req || !I.valid)) {
     if ((rc = inc_rebuild(p, hosts, n, H, kp, p->g0.as<const int32_t>()))) return rc;

@@ -181,6 +181,12 @@ struct IncIndex {
   int req_kp = 0;
   uint64_t rebuilds = 0, delta_slices = 0, refresh_slices = 0, full_slices = 0;
   uint64_t last_delta_cells = 0, last_delta_work = 0, last_misses = 0;
+  // identity fast path: the active list equals X (same sorted version), so g0x
+  // *is* the g0 array and no lookup is needed
+  bool identity_ok = false;
+  uint64_t identity_version = 0, lookup_version = 0;
+  bool lookup_pending = false;
+  uint64_t identity_slices = 0;
 };
 }  // namespace vate
 
@@ -229,6 +235,9 @@ struct vate_pool {
   const void* sorted_owner = nullptr;  // registry whose active set hosts_sorted holds
   uint64_t sorted_n = 0;
   uint64_t sorts_skipped = 0;
+  uint64_t sorted_version = 1;         // bumps whenever hosts_sorted changes content
+  const int32_t* g0_src = nullptr;     // g0 array the float path reads (p->g0 or inc.g0x)
+  cudaEvent_t ev_adv = nullptr;        // advance counters landed in h_ctr
   vate::IncIndex inc;
   int dsmem_clusters = -1;   // cached max active clusters for the DSMEM gather (-1 unknown)
 
@@ -263,6 +272,8 @@ struct vate_hosts {
 
 namespace vate {
 
+int build_bitmap(vate_pool* p, int k_prime, bool with_delta = false);
+
 // error plumbing (thread-local message)
 int set_error(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
@@ -289,7 +300,7 @@ enum Ctr { C_P = 0, C_CLEARED = 1, C_NSEL = 2, C_ERR = 3, C_DCNT = 4, C_DWORK = 
 int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H, int32_t* g0_dev);
 int launch_g0_list(vate_pool* p, const uint64_t* hosts_dev, const uint32_t* idx_dev,
                    const unsigned long long* count_dev, uint64_t cap, HashParams H, int32_t* g0_dev);
-int inc_launch_delta(vate_pool* p, uint64_t g, uint64_t cs, int kp);
+bool inc_delta_ready(vate_pool* p, uint64_t g, uint64_t cs, int kp);
 int inc_compute_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H, int kp);
 void inc_release(vate_pool* p);
 

@@ -353,14 +353,63 @@ __device__ __forceinline__ void for_word_clocks(uint64_t i0, uint32_t cnt, const
   }
 }
 
+// Active bits of 32 cells that share one clock, SIMD-in-register for u8/u16
+// cells: a cell is active iff its value lies in the cyclic interval
+// [act-k'+1, act] (mod 2k) -- the predicate of pools.py:187-193 for values
+// <= 2k.  Returns false if a value exceeds 2k (only a hand-made snapshot can
+// hold one); the caller then takes the exact scalar path.
+template <typename T>
+__device__ __forceinline__ bool active_bits_simd(const uint4 (&r)[(int)sizeof(T) * 2], uint32_t act,
+                                                 uint32_t B, uint32_t kp, uint32_t* active) {
+  const int lo = (int)act - (int)kp + 1;
+  const uint32_t* x = reinterpret_cast<const uint32_t*>(r);
+  uint32_t bits = 0, bad = 0;
+  if (sizeof(T) == 1) {
+    const uint32_t B4 = B * 0x01010101u, A4 = act * 0x01010101u;
+    const uint32_t L4 = (uint32_t)(lo >= 0 ? lo : lo + (int)B) * 0x01010101u;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      bad |= __vcmpgtu4(x[q], B4);
+      const uint32_t m = lo >= 0 ? (__vcmpgeu4(x[q], L4) & __vcmpleu4(x[q], A4))
+                                 : (__vcmpleu4(x[q], A4) | (__vcmpgeu4(x[q], L4) & __vcmpltu4(x[q], B4)));
+      bits |= (((m & 0x01010101u) * 0x01020408u) >> 24) << (4 * q);
+    }
+  } else {
+    const uint32_t B2 = B * 0x00010001u, A2 = act * 0x00010001u;
+    const uint32_t L2 = (uint32_t)(lo >= 0 ? lo : lo + (int)B) * 0x00010001u;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      bad |= __vcmpgtu2(x[q], B2);
+      const uint32_t m = lo >= 0 ? (__vcmpgeu2(x[q], L2) & __vcmpleu2(x[q], A2))
+                                 : (__vcmpleu2(x[q], A2) | (__vcmpgeu2(x[q], L2) & __vcmpltu2(x[q], B2)));
+      bits |= ((m & 1u) | ((m >> 15) & 2u)) << (2 * q);
+    }
+  }
+  *active = bits;
+  return bad == 0;
+}
+
 // Whole-pool pass: inactive bitmap for width k' plus its popcount P
-// (count_inactive, pools.py:195-210; predicate pools.py:187-193).
+// (count_inactive, pools.py:195-210; predicate pools.py:187-193).  With
+// `bprev` set it also emits the cells whose bit flipped against the previous
+// estimate's bitmap (the incremental g0 delta, vate_incremental.cu), so the
+// delta costs no second pass.
+struct DeltaOut {
+  const uint32_t* bprev;       // nullptr: no delta
+  const uint32_t* off;         // inverse-index offsets
+  unsigned long long* list;    // cell | (now_inactive << 32)
+  uint64_t cap;
+  unsigned long long* count;
+  unsigned long long* work;
+};
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells, Layout L,
                                                      uint32_t bact0, uint32_t kp,
                                                      uint32_t* __restrict__ bitmap,
                                                      uint64_t nwords,
-                                                     unsigned long long* pool_inactive) {
+                                                     unsigned long long* pool_inactive,
+                                                     DeltaOut D) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   unsigned local = 0;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
@@ -370,12 +419,28 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
     uint64_t next = block_start(b + 1, L);
     uint32_t act = clock_of(bact0, b, L.B);
     uint32_t bits = 0;
+    bool done = false;
     if (cnt == 32 && i0 + 32 <= next) {  // the whole word in one block: one clock
-      uint32_t v[32];
-      load32<T>(cells + i0, v);
+      if (sizeof(T) <= 2) {
+        uint4 r[(int)sizeof(T) * 2];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) bits |= (uint32_t)is_inactive(v[j], act, L.B, kp) << j;
-    } else {  // block boundary (or pool end) inside the word
+        for (int q = 0; q < (int)sizeof(T) * 2; ++q)
+          r[q] = __ldcs(reinterpret_cast<const uint4*>(cells + i0) + q);
+        uint32_t active;
+        if (active_bits_simd<T>(r, act, L.B, kp, &active)) {
+          bits = ~active;
+          done = true;
+        }
+      }
+      if (!done) {
+        uint32_t v[32];
+        load32<T>(cells + i0, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) bits |= (uint32_t)is_inactive(v[j], act, L.B, kp) << j;
+        done = true;
+      }
+    }
+    if (!done) {  // block boundary (or pool end) inside the word
       for (uint32_t j = 0; j < cnt; ++j) {
         while (i0 + j >= next) {
           ++b;
@@ -387,6 +452,22 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
     }
     bitmap[w] = bits;
     local += __popc(bits);
+    if (D.bprev) {
+      uint32_t x = bits ^ D.bprev[w];
+      if (x) {
+        unsigned long long pos = atomicAdd(D.count, (unsigned long long)__popc(x));
+        unsigned long long wsum = 0;
+        while (x) {
+          const int j = __ffs(x) - 1;
+          x &= x - 1;
+          const uint64_t cell = i0 + j;
+          wsum += D.off[cell + 1] - D.off[cell];
+          if (pos < D.cap) D.list[pos] = cell | ((unsigned long long)((bits >> j) & 1u) << 32);
+          ++pos;
+        }
+        atomicAdd(D.work, wsum);
+      }
+    }
   }
   const unsigned s = block_sum(local);
   if (threadIdx.x == 0 && s) atomicAdd(pool_inactive, (unsigned long long)s);
@@ -526,20 +607,32 @@ using namespace vate;
 
 namespace vate {
 // Build the k' inactive bitmap and enqueue P into h_ctr[C_P] (not synced).
-int build_bitmap(vate_pool* p, int k_prime) {
+int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
   const uint64_t nwords = (p->L.size + 31) / 32;
   int rc = p->bitmap.ensure(nwords * 4 + 16);
   if (rc) return rc;
   VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_P, 0, 8, p->stream));
+  DeltaOut D{};
+  if (with_delta) {
+    IncIndex& I = p->inc;
+    VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_DCNT, 0, 16, p->stream));
+    D = DeltaOut{I.bprev.as<const uint32_t>(), I.off.as<const uint32_t>(),
+                 I.dlist.as<unsigned long long>(), I.dlist_cap, p->d_ctr + C_DCNT,
+                 p->d_ctr + C_DWORK};
+  }
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
     VATE_LAUNCH(p, VATE_K_BITMAP, grid_for(nwords, kThreads, 148u * 32u), kThreads, 0,
                 k_bitmap<T>, (const T*)p->cells, p->L, p->bact0, (uint32_t)k_prime,
-                p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P);
+                p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D);
     return VATE_OK;
   });
   if (rc) return rc;
+  // P (and the delta counts) reach the host with the estimate's one round trip
   VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_P, p->d_ctr + C_P, 8, cudaMemcpyDeviceToHost, p->stream));
+  if (with_delta)
+    VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_DCNT, p->d_ctr + C_DCNT, 16, cudaMemcpyDeviceToHost,
+                              p->stream));
   return VATE_OK;
 }
 
@@ -611,6 +704,7 @@ int vate_pool_create(vate_pool** out, int c, int k, int partition, int device) {
   if (e == cudaSuccess) e = cudaMalloc(&p->d_ctr, C_N * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMallocHost(&p->h_ctr, C_N * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_small, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_adv, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
@@ -661,6 +755,7 @@ int vate_pool_destroy(vate_pool* p) {
   if (p->d_ctr) cudaFree(p->d_ctr);
   if (p->h_ctr) cudaFreeHost(p->h_ctr);
   if (p->ev_small) cudaEventDestroy(p->ev_small);
+  if (p->ev_adv) cudaEventDestroy(p->ev_adv);
   for (auto& t : p->timed_pending) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
@@ -737,7 +832,7 @@ int vate_pool_inc_stats(const vate_pool* p, uint64_t out[8]) {
   if (!p) return set_error(VATE_EVALUE, "null pool handle");
   const IncIndex& I = p->inc;
   const uint64_t v[8] = {I.rebuilds, I.delta_slices, I.refresh_slices, I.full_slices,
-                         I.last_delta_cells, I.last_delta_work, I.last_misses, I.valid ? I.m : 0};
+                         I.last_delta_cells, I.last_delta_work, I.identity_slices, I.valid ? I.m : 0};
   for (int i = 0; i < 8; ++i) out[i] = v[i];
   return VATE_OK;
 }
@@ -963,6 +1058,7 @@ int vate_advance_async(vate_pool* p) {
   if (rc) return rc;
   VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_CLEARED, p->d_ctr + C_CLEARED, 8, cudaMemcpyDeviceToHost,
                             p->stream));
+  VATE_CUDA(cudaEventRecord(p->ev_adv, p->stream));
   p->adv_pending = true;
   return VATE_OK;
 }
@@ -972,8 +1068,7 @@ int vate_advance_result(vate_pool* p, int32_t blocks[2], uint64_t* maintained,
   int rc = enter(p);
   if (rc) return rc;
   if (!p->adv_pending) return set_error(VATE_EVALUE, "no advance pending");
-  rc = sync_small(p);
-  if (rc) return rc;
+  VATE_CUDA(cudaEventSynchronize(p->ev_adv));  // only the sweep's counter, not later work
   p->adv_pending = false;
   if (blocks) {
     blocks[0] = p->adv_blocks[0];

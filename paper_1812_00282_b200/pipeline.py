@@ -107,6 +107,7 @@ class Pipeline:
         self.hosts = SlidingHostSet(pool.k, pool=pool)
         self.total_maintained = 0
         self.total_cleared = 0
+        self._deferred_t = None   # slice whose advance result is still to be collected
         _ensure_log_table(pool, cfg.g)
 
     def close(self) -> None:
@@ -155,6 +156,9 @@ class Pipeline:
         check(lib.vate_estimate_begin(self.pool.handle, self.hosts.handle, self.cfg.g,
                                       self.cfg.cell_stream, t, self.k_prime, C.byref(nh),
                                       C.byref(p)))
+        if self._deferred_t is not None:   # last slice's sweep finished before this sync
+            self._collect(self._deferred_t)
+            self._deferred_t = None
         if advance:
             check(lib.vate_advance_async(self.pool.handle))
         n = nh.value
@@ -195,8 +199,12 @@ class Pipeline:
         return self._account(t, self.pool.advance_slice())
 
     def wait_reports(self) -> None:
-        """Block until every report row enqueued with wait=False is in host memory."""
+        """Block until every report row enqueued with wait=False is in host memory
+        and every deferred slice advance is accounted."""
         check(lib.vate_estimate_wait(self.pool.handle))
+        if self._deferred_t is not None:
+            self._collect(self._deferred_t)
+            self._deferred_t = None
 
     def stage_packed(self, pairs_host_ptr: int, n: int) -> int:
         """Start the H2D copy of a slice's packed records (pinned host memory) on the
@@ -206,19 +214,27 @@ class Pipeline:
         return slot.value
 
     def step_packed(self, t: int, pairs, n: int, on_device: bool, out=None, wait: bool = True):
-        """One slice from packed records: scan, estimate (+ advance overlapped), prune."""
+        """One slice from packed records: scan, estimate (+ advance overlapped), prune.
+
+        wait=False streams: report rows land asynchronously (see estimate_soa) and
+        the advance report of slice t is collected during slice t+1's estimate
+        (its one host round trip), so a slice costs a single host sync."""
         self.scan_packed(t, pairs, n, on_device)
+        return self._estimate_advance(t, out, wait)
+
+    def _estimate_advance(self, t: int, out, wait: bool):
         rep = self.estimate_soa(t, out, advance=True, wait=wait)
-        self._collect(t)
+        if wait:
+            self._collect(t)
+        else:
+            self._deferred_t = t
         return rep
 
     def step_staged(self, t: int, slot: int, n: int, out=None, wait: bool = True):
         """One slice from a staged buffer (see stage_packed)."""
         check(lib.vate_scan_staged(self.pool.handle, self.cfg.g, self.cfg.cell_stream,
                                    self.cfg.group_stream, slot, int(n), self.hosts.handle, t))
-        rep = self.estimate_soa(t, out, advance=True, wait=wait)
-        self._collect(t)
-        return rep
+        return self._estimate_advance(t, out, wait)
 
     # --- driving ---------------------------------------------------------------------
     def process_slice_soa(self, t: int, aips, bips, out=None):

@@ -307,7 +307,7 @@ class AtPool(BlockLayout):
         out = (C.c_uint64 * 8)()
         check(lib.vate_pool_inc_stats(self._h, out))
         keys = ("rebuilds", "delta_slices", "refresh_slices", "full_slices",
-                "last_delta_cells", "last_delta_work", "last_misses", "hosts_indexed")
+                "last_delta_cells", "last_delta_work", "identity_slices", "hosts_indexed")
         return dict(zip(keys, list(out)))
 
     def set_timing(self, on: bool) -> None:

