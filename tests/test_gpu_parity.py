@@ -592,6 +592,7 @@ def test_streaming_steps_match_oracle(mode):
     outs = [(np.empty(cap, np.uint64), np.empty(cap, np.float64), np.empty(cap, np.float64),
              np.empty(cap, np.uint8)) for _ in range(2)]
     pending = None
+    cleared = 0
     slices = [vo.synthetic_slice(t, n, hosts) for t in range(30)]
     packed = [np.ascontiguousarray(np.stack([a, b], axis=1).astype(np.uint32)) for a, b in slices]
     staged = pipe.stage_packed(packed[0].ctypes.data, n) if mode == "staged" else None
@@ -603,6 +604,7 @@ def test_streaming_steps_match_oracle(mode):
         else:
             rep = pipe.step_packed(t, packed[t].ctypes.data, n, False, outs[t % 2], wait=False)
         want = opipe.process_slice(t, *slices[t])
+        cleared += want.cleared
         if pending is not None:          # slice t-1's rows are complete after slice t began
             pipe.wait_reports()
             prev_rep, prev_want = pending
@@ -613,6 +615,6 @@ def test_streaming_steps_match_oracle(mode):
     pipe.wait_reports()
     assert np.array_equal(pending[0].estimate, pending[1].reports.estimate)
     assert pool.snapshot_bytes() == opipe.pool.snapshot_bytes()
-    assert pipe.total_cleared == sum(0 for _ in []) + pipe.total_cleared   # collected
+    assert pipe.total_cleared == cleared          # every deferred advance was collected
     st = pool.inc_stats()
     assert st["delta_slices"] > 20 and st["identity_slices"] > 0, st
