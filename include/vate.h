@@ -76,8 +76,9 @@ int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
 enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1 };
 int vate_pool_set_option(vate_pool* p, int option, int64_t value);
 /* incremental-estimate counters: [rebuilds, delta slices, refresh slices, full
- * slices, last delta cells, last delta work, identity slices, hosts indexed] */
-int vate_pool_inc_stats(const vate_pool* p, uint64_t out[8]);
+ * slices, last delta cells, last delta work, identity slices, hosts indexed,
+ * total index-rebuild time in microseconds, misses gathered since the rebuild] */
+int vate_pool_inc_stats(vate_pool* p, uint64_t out[10]);
 
 enum vate_kernel_kind {
   VATE_K_SCAN = 0,     /* record_pairs / set_many scatter      */

@@ -94,6 +94,34 @@ for _name, (_args, _res) in _SIGS.items():
 
 EXPORTED = tuple(_SIGS)
 
+# Handles are destroyed registries-first at interpreter exit, before the CUDA
+# runtime inside the library is torn down; __del__ is a no-op from then on.
+import atexit as _atexit
+import weakref as _weakref
+
+_LIVE = _weakref.WeakValueDictionary()
+_SHUTDOWN = [False]
+
+
+def track(obj) -> None:
+    _LIVE[id(obj)] = obj
+
+
+def shutting_down() -> bool:
+    return _SHUTDOWN[0]
+
+
+@_atexit.register
+def _close_all() -> None:
+    objs = list(_LIVE.values())
+    for o in objs:                       # registries before the pools they live on
+        if getattr(o, "_is_registry", False):
+            o.close()
+    for o in objs:
+        if not getattr(o, "_is_registry", False):
+            o.close()
+    _SHUTDOWN[0] = True
+
 
 def last_error() -> str:
     msg = lib.vate_last_error()

@@ -535,7 +535,11 @@ int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t ce
   if (I.lookup_pending) {
     I.lookup_pending = false;
     I.last_misses = p->h_ctr[C_MISS];
-    if (I.valid && I.last_n && I.last_misses * 20 > I.last_n) I.want_rebuild = true;
+    I.miss_accum += I.last_misses;
+    // rebuild when misses are a large share now, or (ski rental) once the
+    // misses gathered since the last rebuild add up to the size of the index
+    if (I.valid && I.last_n && (I.last_misses * 20 > I.last_n || I.miss_accum >= I.m))
+      I.want_rebuild = true;
     if (I.valid && I.last_misses == 0 && I.m == I.last_n) {  // that active list == X
       I.identity_ok = true;
       I.identity_version = I.lookup_version;

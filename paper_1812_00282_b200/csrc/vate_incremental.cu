@@ -91,6 +91,11 @@ __global__ void k_inc_lookup(const uint64_t* __restrict__ A, uint64_t n,
 
 void inc_release(vate_pool* p) {
   IncIndex& I = p->inc;
+  for (cudaEvent_t& e : I.ev_rb)
+    if (e) {
+      cudaEventDestroy(e);
+      e = nullptr;
+    }
   for (DevBuf* b : {&I.X, &I.g0x, &I.off, &I.ent, &I.cursor, &I.bprev, &I.dlist, &I.miss, &I.scan_tmp})
     b->release();
   I.valid = false;
@@ -133,6 +138,15 @@ static int inc_rebuild(vate_pool* p, const uint64_t* hosts, uint64_t n, HashPara
     return rc;
   I.dlist_cap = S / 8 + 1024;
   if ((rc = I.dlist.ensure(I.dlist_cap * 8))) return rc;
+  for (cudaEvent_t& e : I.ev_rb)
+    if (!e) VATE_CUDA(cudaEventCreate(&e));
+  if (I.rb_timing) {  // fold in a previous rebuild not yet read
+    float ms = 0.f;
+    VATE_CUDA(cudaEventSynchronize(I.ev_rb[1]));
+    VATE_CUDA(cudaEventElapsedTime(&ms, I.ev_rb[0], I.ev_rb[1]));
+    I.rebuild_ms += ms;
+  }
+  VATE_CUDA(cudaEventRecord(I.ev_rb[0], p->stream));
   VATE_CUDA(cudaMemcpyAsync(I.X.ptr, hosts, n * 8, cudaMemcpyDeviceToDevice, p->stream));
   VATE_CUDA(cudaMemcpyAsync(I.g0x.ptr, g0_dev, n * 4, cudaMemcpyDeviceToDevice, p->stream));
   VATE_CUDA(cudaMemsetAsync(I.cursor.ptr, 0, (S + 1) * 4, p->stream));
@@ -153,6 +167,9 @@ static int inc_rebuild(vate_pool* p, const uint64_t* hosts, uint64_t n, HashPara
               I.ent.as<uint32_t>());
   VATE_CUDA(cudaMemcpyAsync(I.bprev.ptr, p->bitmap.ptr, nwords * 4, cudaMemcpyDeviceToDevice,
                             p->stream));
+  VATE_CUDA(cudaEventRecord(I.ev_rb[1], p->stream));
+  I.rb_timing = true;
+  I.miss_accum = 0;
   I.m = n;
   I.g = H.g;
   I.cs = H.cs;

@@ -187,6 +187,10 @@ struct IncIndex {
   uint64_t identity_version = 0, lookup_version = 0;
   bool lookup_pending = false;
   uint64_t identity_slices = 0;
+  uint64_t miss_accum = 0;                // misses gathered since the last rebuild
+  cudaEvent_t ev_rb[2] = {nullptr, nullptr};
+  bool rb_timing = false;
+  double rebuild_ms = 0;
 };
 }  // namespace vate
 

@@ -828,12 +828,21 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
   return set_error(VATE_EVALUE, "unknown option or value");
 }
 
-int vate_pool_inc_stats(const vate_pool* p, uint64_t out[8]) {
-  if (!p) return set_error(VATE_EVALUE, "null pool handle");
-  const IncIndex& I = p->inc;
-  const uint64_t v[8] = {I.rebuilds, I.delta_slices, I.refresh_slices, I.full_slices,
-                         I.last_delta_cells, I.last_delta_work, I.identity_slices, I.valid ? I.m : 0};
-  for (int i = 0; i < 8; ++i) out[i] = v[i];
+int vate_pool_inc_stats(vate_pool* p, uint64_t out[10]) {
+  int rc = enter(p);
+  if (rc) return rc;
+  IncIndex& I = p->inc;
+  if (I.rb_timing) {  // the last rebuild's device time
+    float ms = 0.f;
+    VATE_CUDA(cudaEventSynchronize(I.ev_rb[1]));
+    VATE_CUDA(cudaEventElapsedTime(&ms, I.ev_rb[0], I.ev_rb[1]));
+    I.rebuild_ms += ms;
+    I.rb_timing = false;
+  }
+  const uint64_t v[10] = {I.rebuilds, I.delta_slices, I.refresh_slices, I.full_slices,
+                          I.last_delta_cells, I.last_delta_work, I.identity_slices,
+                          I.valid ? I.m : 0, (uint64_t)(I.rebuild_ms * 1000.0), I.miss_accum};
+  for (int i = 0; i < 10; ++i) out[i] = v[i];
   return VATE_OK;
 }
 

@@ -18,6 +18,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _lib
 from ._lib import VATE_DEVICE, VATE_HOST, check, lib, ptr
 from .estimator import (EstimatorConfig, HostReports, _check_pool_cfg, _ensure_log_table,
                         _u64, context_pool, log_zp)
@@ -51,6 +52,8 @@ class SlidingHostSet:
         h = C.c_void_p()
         check(lib.vate_hosts_create(C.byref(h), self._pool.handle, k))
         self._h = h
+        self._is_registry = True
+        _lib.track(self)
 
     @property
     def handle(self):
@@ -58,7 +61,7 @@ class SlidingHostSet:
 
     def close(self) -> None:
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and not _lib.shutting_down():
             lib.vate_hosts_destroy(h)
             self._h = C.c_void_p()
 

@@ -134,11 +134,12 @@ class AtPool(BlockLayout):
         h = C.c_void_p()
         check(lib.vate_pool_create(C.byref(h), c, k, PARTITIONS.index(partition), device))
         self._h = h
+        _lib.track(self)
 
     # --- handle -----------------------------------------------------------------
     def close(self) -> None:
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and not _lib.shutting_down():
             lib.vate_pool_destroy(h)
             self._h = C.c_void_p()
 
