@@ -376,7 +376,9 @@ def run_gpu(args, rank, world, local_rank):
                         "last_delta_cells": inc1["last_delta_cells"],
                         "last_delta_work": inc1["last_delta_work"],
                         "identity_slices": inc1["identity_slices"] - inc0["identity_slices"],
-                        "hosts_indexed": inc1["hosts_indexed"]},
+                        "hosts_indexed": inc1["hosts_indexed"],
+                        "rebuild_ms_total_run": inc1["rebuild_us_total"] / 1e3,
+                        "misses_since_rebuild": inc1["miss_accum"]},
         "clocks": clocks.summary(),
     }
     if cpu_mean is not None:
