@@ -306,11 +306,16 @@ def run_gpu(args, rank, world, local_rank):
         e0 = time.perf_counter()
         e2e_rows = 0
         staged = [None, None]
+        host_ms = {"stage": 0.0, "step": 0.0}
         staged[0] = pipe.stage_packed(hslices[0].data_ptr(), n)
         for i in range(args.steps):
+            a = time.perf_counter()
             if i + 1 < args.steps:
                 staged[(i + 1) % 2] = pipe.stage_packed(hslices[i + 1].data_ptr(), n)
+            b = time.perf_counter()
             e2e_rows += step_host(t, i)
+            host_ms["stage"] += (b - a) * 1e3
+            host_ms["step"] += (time.perf_counter() - b) * 1e3
             t += 1
         barrier()
         e2e_s = time.perf_counter() - e0
@@ -367,7 +372,8 @@ def run_gpu(args, rank, world, local_rank):
                      "traffic": None,
                      "algorithmic_bytes_per_launch": alg_bytes[dom]},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": slice_bytes,
-                "d2h_bytes_per_step": int(e2e_rows / args.steps * 25)},
+                "d2h_bytes_per_step": int(e2e_rows / args.steps * 25),
+                "host_ms_per_step": {k: v / args.steps for k, v in host_ms.items()}},
         "gpu_launches": int(launches),
         "g0_kernel": args.g0_kernel,
         "incremental": {"enabled": args.incremental == "on",

@@ -11,8 +11,8 @@ pool = cfg.build_pool()
 pipe = vb.Pipeline(pool, cfg, 60)
 n = 5_000_000
 scratch = torch.empty((n, 2), dtype=torch.int32, device="cuda:0")
-hs = torch.empty((8, n, 2), dtype=torch.int32, pin_memory=True)
-for i in range(8):
+hs = torch.empty((int(os.environ.get("NSL", "8")), n, 2), dtype=torch.int32, pin_memory=True)
+for i in range(hs.shape[0]):
     check(lib.vate_synth_packets(pool.handle, 500 + i, n, 1_000_000, 0x0A000000, 0, scratch.data_ptr()))
     pool.synchronize()
     hs[i].copy_(scratch)
@@ -36,9 +36,10 @@ for mode in ("staged", "hostptr", "device"):
     staged[0] = pipe.stage_packed(hs[0].data_ptr(), n)
     pool.synchronize()
     for i in range(8):
+        i = i * (hs.shape[0] // 8)
         a = time.perf_counter()
         if mode == "staged":
-            if i + 1 < 8:
+            if i + 1 < hs.shape[0]:
                 staged[(i + 1) % 2] = pipe.stage_packed(hs[i + 1].data_ptr(), n)
             b = time.perf_counter()
             pipe.step_staged(t, staged[i % 2], n, outs[t % 2], wait=False)
