@@ -537,8 +537,10 @@ int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t ce
     I.last_misses = p->h_ctr[C_MISS];
     I.miss_accum += I.last_misses;
     // rebuild when misses are a large share now, or (ski rental) once the
-    // misses gathered since the last rebuild add up to the size of the index
-    if (I.valid && I.last_n && (I.last_misses * 20 > I.last_n || I.miss_accum >= I.m))
+    // gathers spent on misses since the last rebuild match a rebuild's cost:
+    // a rebuild measures ~20 full recomputes (count + fill passes over m*g
+    // pairs with atomics, profiles/), so the break-even is 16-24 x m misses
+    if (I.valid && I.last_n && (I.last_misses * 20 > I.last_n || I.miss_accum >= 16 * I.m))
       I.want_rebuild = true;
     if (I.valid && I.last_misses == 0 && I.m == I.last_n) {  // that active list == X
       I.identity_ok = true;
