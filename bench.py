@@ -276,7 +276,10 @@ def run_gpu(args, rank, world, local_rank):
     barrier()
     launches0 = pool.launches()
     inc0 = pool.inc_stats()
+    profile_region = os.environ.get("VATE_PROFILE_REGION") == "1"
     with ClockSampler(dev) as clocks:
+        if profile_region:
+            check(lib.vate_profiler(1))
         check(lib.vate_mark(h, 0))
         rows = 0
         for _ in range(args.steps):
@@ -285,6 +288,8 @@ def run_gpu(args, rank, world, local_rank):
             di += 1
         check(lib.vate_mark(h, 1))
         barrier()
+        if profile_region:
+            check(lib.vate_profiler(0))
         ms = C.c_double()
         check(lib.vate_mark_elapsed(h, 0, 1, C.byref(ms)))
         dev_ms = ms.value

@@ -71,21 +71,38 @@ __global__ void k_inc_apply(const unsigned long long* __restrict__ list,
 }
 
 // Sorted active hosts A -> g0 from the index where present, else a miss.
+// Both lists are ascending, so each thread takes a run of kRun consecutive
+// hosts: one binary search places the first, the rest advance linearly
+// (typically one step per host), falling back to a search on long gaps.
+constexpr int kRun = 8;
 __global__ void k_inc_lookup(const uint64_t* __restrict__ A, uint64_t n,
                              const uint64_t* __restrict__ X, uint64_t m,
                              const int32_t* __restrict__ g0x, int32_t* __restrict__ g0,
                              uint32_t* __restrict__ miss, unsigned long long* nmiss) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint64_t a = A[i];
-    uint64_t lo = 0, hi = m;
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (X[mid] < a) lo = mid + 1;
-      else hi = mid;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kRun;
+  for (uint64_t i0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kRun; i0 < n; i0 += stride) {
+    uint64_t lo = 0;
+    bool placed = false;
+    for (int r = 0; r < kRun && i0 + r < n; ++r) {
+      const uint64_t i = i0 + r;
+      const uint64_t a = A[i];
+      int walked = 0;
+      while (placed && lo < m && X[lo] < a && walked < 16) {
+        ++lo;
+        ++walked;
+      }
+      if (!placed || (lo < m && X[lo] < a)) {  // first host of the run, or a long gap
+        uint64_t hi = m;
+        while (lo < hi) {
+          const uint64_t mid = (lo + hi) >> 1;
+          if (X[mid] < a) lo = mid + 1;
+          else hi = mid;
+        }
+        placed = true;
+      }
+      if (lo < m && X[lo] == a) g0[i] = g0x[lo];
+      else miss[atomicAdd(nmiss, 1ull)] = (uint32_t)i;
     }
-    if (lo < m && X[lo] == a) g0[i] = g0x[lo];
-    else miss[atomicAdd(nmiss, 1ull)] = (uint32_t)i;
   }
 }
 
@@ -213,7 +230,8 @@ int inc_compute_g0(vate_pool* p, const uint64_t* hosts, uint64_t n, HashParams H
       I.identity_ok = false;
       if ((rc = I.miss.ensure(n * 4 + 4))) return rc;
       VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_MISS, 0, 8, p->stream));
-      VATE_LAUNCH(p, VATE_K_G0, grid_for(n, kThreads, 148u * 16u), kThreads, 0, k_inc_lookup, hosts,
+      VATE_LAUNCH(p, VATE_K_G0, grid_for((n + kRun - 1) / kRun, kThreads, 148u * 16u), kThreads, 0,
+                  k_inc_lookup, hosts,
                   n, I.X.as<const uint64_t>(), I.m, I.g0x.as<const int32_t>(), p->g0.as<int32_t>(),
                   I.miss.as<uint32_t>(), p->d_ctr + C_MISS);
       if ((rc = launch_g0_list(p, hosts, I.miss.as<const uint32_t>(), p->d_ctr + C_MISS, n, H,

@@ -4,6 +4,7 @@
 //
 // Reference: pools.py:67-298 (AtPool), estimator.py:96-104 (pair_cells /
 // record_pairs), bitpack.py:26-140 (the snapshot bit layout).
+#include <cuda_profiler_api.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -204,11 +205,10 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
   }
 }
 
-template <typename T, bool REG>
+template <typename T, bool REG, int V = 2>  // V uint4 loads (2 packets each) per iteration
 __global__ void __launch_bounds__(kThreads) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
     Layout L, uint32_t bact0, RegRef R, long long t) {
-  constexpr int V = 2;  // uint4 loads (2 packets each) per thread per iteration
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   for (; i < npairs2; i += V * stride) {
@@ -820,6 +820,10 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_g0 = (int)value;
     return VATE_OK;
   }
+  if (option == VATE_OPT_SCAN_V && (value == 2 || value == 4)) {
+    p->opt_scan_v = (int)value;
+    return VATE_OK;
+  }
   if (option == VATE_OPT_INCREMENTAL && (value == 0 || value == 1)) {
     p->opt_inc = (int)value;
     if (!value) p->inc.valid = false;
@@ -843,6 +847,11 @@ int vate_pool_inc_stats(vate_pool* p, uint64_t out[10]) {
                           I.last_delta_cells, I.last_delta_work, I.identity_slices,
                           I.valid ? I.m : 0, (uint64_t)(I.rebuild_ms * 1000.0), I.miss_accum};
   for (int i = 0; i < 10; ++i) out[i] = v[i];
+  return VATE_OK;
+}
+
+int vate_profiler(int on) {
+  VATE_CUDA(on ? cudaProfilerStart() : cudaProfilerStop());
   return VATE_OK;
 }
 
@@ -911,7 +920,11 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     return with_cell(p->cell_bytes, [&](auto tag) -> int {
       using T = decltype(tag);
       if (aligned16 && n >= 2) {
-        if (hosts)
+        if (hosts && p->opt_scan_v == 4)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 4>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
+                      (long long)t);
+        else if (hosts)
           VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
                       (long long)t);

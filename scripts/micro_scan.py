@@ -14,13 +14,15 @@ for i in range(12):
     check(lib.vate_synth_packets(pool.handle, i, n, 1_000_000, 0x0A000000, 0, bufs[i].data_ptr()))
 for t in range(12):   # fill the registry
     pipe.step_packed(t, bufs[t].data_ptr(), n, True)
-pool.set_timing(True)
-for rep in range(3):
-    for t in range(12):
-        check(lib.vate_scan_packed(pool.handle, cfg.g, cfg.cell_stream, cfg.group_stream,
-                                   bufs[t].data_ptr(), n, 1, pipe.hosts.handle, 100 + t))
-ms, k = pool.kernel_time("scan")
-print("scan+registry ms/launch", ms / k)
+for v in (2, 4, 2, 4):
+    pool.set_option("scan_v", v)
+    pool.set_timing(False); pool.set_timing(True)
+    for rep in range(3):
+        for t in range(12):
+            check(lib.vate_scan_packed(pool.handle, cfg.g, cfg.cell_stream, cfg.group_stream,
+                                       bufs[t].data_ptr(), n, 1, pipe.hosts.handle, 100 + t))
+    ms, k = pool.kernel_time("scan")
+    print("scan+registry V", v, "ms/launch", ms / k)
 pool.set_timing(False); pool.set_timing(True)
 for rep in range(3):
     for t in range(12):

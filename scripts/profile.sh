@@ -1,8 +1,8 @@
 # ncu evidence for the bench workload (1 GPU): launch list + full captures of the top kernels
 mkdir -p gpurun_out
 # every launch of a few timed steps with its device time (cold, serialised: compare SHARES)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 1300 -c 150 --csv \
-   --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 > gpurun_out/ncu_launch_run.log 2>&1
+VATE_PROFILE_REGION=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+   python bench.py --steps 10 --warmup 3 > gpurun_out/launches.csv 2> gpurun_out/ncu_launch_run.log
 echo "launches rc=$?"
 # incremental path kernels (default bench), one capture each, after the prefill
 for K in k_scan_packed16 k_bitmap k_inc_apply k_inc_lookup k_final_write k_active k_g0; do
