@@ -217,8 +217,9 @@ def run_gpu(args, rank, world, local_rank):
     for i in range(n_dev):
         check(lib.vate_synth_packets(h, t_base + prefill + i, n, w["hosts"], w["base_aip"],
                                      w["seed"], dslices[i].data_ptr()))
-    hslices = torch.empty((args.steps, n, 2), dtype=torch.int32, pin_memory=True)
-    for i in range(args.steps):
+    n_host = args.warmup + args.steps
+    hslices = torch.empty((n_host, n, 2), dtype=torch.int32, pin_memory=True)
+    for i in range(n_host):
         check(lib.vate_synth_packets(h, t_base + prefill + n_dev + i, n, w["hosts"], w["base_aip"],
                                      w["seed"], scratch.data_ptr()))
         pool.synchronize()
@@ -244,12 +245,12 @@ def run_gpu(args, rank, world, local_rank):
             rep = merger.estimate(pipe, t, out_sets[t % 2])
             pipe._maintain(t)
         else:
-            rep = pipe.step_packed(t, src, n, on_device, out_sets[t % 2], wait=False)
+            rep = pipe.step_fast(t, src, n, "device" if on_device else "host", out_sets[t % 2])
         return 0 if rep is None else len(rep)
 
     def step_host(t, i):
         """e2e slice from pinned host packets; slice i+1's H2D overlaps slice i."""
-        rep = pipe.step_staged(t, staged[i % 2], n, out_sets[t % 2], wait=False)
+        rep = pipe.step_fast(t, staged[i % 2], n, "staged", out_sets[t % 2])
         return 0 if rep is None else len(rep)
 
     t = 0
@@ -307,15 +308,20 @@ def run_gpu(args, rank, world, local_rank):
         pool.set_timing(False)
 
         # --- end to end from pinned host buffers (e2e) --------------------------------
+        # e2e warm-up: W host-fed slices (PCIe link and staging buffers warm)
+        staged = [None, None]
+        staged[0] = pipe.stage_packed(hslices[0].data_ptr(), n)
+        for i in range(args.warmup):
+            staged[(i + 1) % 2] = pipe.stage_packed(hslices[i + 1].data_ptr(), n)
+            step_host(t, i)
+            t += 1
         barrier()
         e0 = time.perf_counter()
         e2e_rows = 0
-        staged = [None, None]
         host_ms = {"stage": 0.0, "step": 0.0}
-        staged[0] = pipe.stage_packed(hslices[0].data_ptr(), n)
-        for i in range(args.steps):
+        for i in range(args.warmup, n_host):
             a = time.perf_counter()
-            if i + 1 < args.steps:
+            if i + 1 < n_host:
                 staged[(i + 1) % 2] = pipe.stage_packed(hslices[i + 1].data_ptr(), n)
             b = time.perf_counter()
             e2e_rows += step_host(t, i)

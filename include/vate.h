@@ -40,7 +40,7 @@ enum vate_status {
   VATE_ENOMEM = -4   /* device or pinned allocation failed              */
 };
 
-enum vate_where { VATE_HOST = 0, VATE_DEVICE = 1 };
+enum vate_where { VATE_HOST = 0, VATE_DEVICE = 1, VATE_STAGED = 2 };
 enum vate_partition { VATE_TAIL = 0, VATE_LOWDEV = 1 }; /* pools.py:27-29 */
 
 typedef struct vate_pool vate_pool;   /* AtPool on one device               */
@@ -187,6 +187,27 @@ int vate_estimate_finish_async(vate_pool* p, uint64_t g, uint64_t pool_inactive,
                                double floor, uint64_t* out_host, double* out_est,
                                double* out_zv, uint8_t* out_sat, uint64_t cap, uint64_t* nkept);
 int vate_estimate_wait(vate_pool* p);
+
+/* ---- one whole slice (pipeline.py:142-160) in one call, streaming form ---
+ * scan (pairs: host/device pointer, or the staging slot when where ==
+ * VATE_STAGED) -> estimate begin -> the slice's single host round trip ->
+ * the previous slice's advance result (collected into res->prev_*) -> g0 ->
+ * advance (enqueued) -> float path + async D2H of the report rows (complete
+ * after vate_estimate_wait or the next call's round trip).
+ * log_zp_table[P] = np.log(clamped P / 2^c) for P in [0, 2^c] (numpy-made,
+ * estimator.py:148-151).  The advance of this slice is collected by the next
+ * call or by vate_advance_result. */
+typedef struct vate_step_result {
+  uint64_t nhosts, nkept, pool_inactive;
+  int32_t prev_collected;
+  int32_t prev_blocks[2];
+  uint64_t prev_maintained, prev_cleared;
+} vate_step_result;
+int vate_slice_step(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                    uint64_t group_stream, const uint32_t* pairs, uint64_t n, int where,
+                    int64_t t, int k_prime, double floor, const double* log_zp_table,
+                    uint64_t* out_host, double* out_est, double* out_zv, uint8_t* out_sat,
+                    uint64_t cap, vate_step_result* res);
 
 /* ---- snapshots: AtPool.snapshot_bytes / load (pools.py:261-298) -------- */
 int vate_snapshot_size(const vate_pool* p, uint64_t* nbytes);

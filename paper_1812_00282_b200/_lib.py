@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvate_b200.so")
 
 VATE_OK, VATE_ECONFIG, VATE_EVALUE, VATE_ECUDA, VATE_ENOMEM = 0, -1, -2, -3, -4
-VATE_HOST, VATE_DEVICE = 0, 1
+VATE_HOST, VATE_DEVICE, VATE_STAGED = 0, 1, 2
 KERNEL_KINDS = ("scan", "registry", "bitmap", "g0", "final", "sweep", "sort", "other")
 
 if not os.path.exists(LIB_PATH):
@@ -26,6 +26,13 @@ if not os.path.exists(LIB_PATH):
         "paper_1812_00282_b200/csrc)")
 
 lib = C.CDLL(LIB_PATH)
+
+class StepResult(C.Structure):
+    """vate_step_result (include/vate.h)."""
+    _fields_ = [("nhosts", C.c_uint64), ("nkept", C.c_uint64), ("pool_inactive", C.c_uint64),
+                ("prev_collected", C.c_int32), ("prev_blocks", C.c_int32 * 2),
+                ("prev_maintained", C.c_uint64), ("prev_cleared", C.c_uint64)]
+
 
 _p = C.c_void_p
 _u64 = C.c_uint64
@@ -74,6 +81,8 @@ _SIGS = {
     "vate_estimate_finish": ([_p, _u64, _u64, _dbl, _dbl, _p, _p, _p, _p, _u64, _pu64], _int),
     "vate_estimate_finish_async": ([_p, _u64, _u64, _dbl, _dbl, _p, _p, _p, _p, _u64, _pu64], _int),
     "vate_estimate_wait": ([_p], _int),
+    "vate_slice_step": ([_p, _p, _u64, _u64, _u64, _p, _u64, _int, _i64, _int, _dbl, _p,
+                         _p, _p, _p, _p, _u64, C.POINTER(StepResult)], _int),
     "vate_snapshot_size": ([_p, _pu64], _int),
     "vate_snapshot": ([_p, _p, _u64, _pu64], _int),
     "vate_load": ([_p, _p, _u64], _int),

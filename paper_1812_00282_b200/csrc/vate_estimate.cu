@@ -6,6 +6,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <string>
 
 #include "vate_internal.cuh"
@@ -519,20 +520,27 @@ int vate_reports_from_counts(vate_pool* p, uint64_t g, const int32_t* g0, uint64
   return wait_rows(p, slot);
 }
 
-int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
-                        int64_t t, int k_prime, uint64_t* nhosts, uint64_t* pool_inactive) {
-  int rc = enter(p);
-  if (rc) return rc;
+// The estimate in two halves around its single host round trip.
+// enqueue: the bitmap pass (P, and the flipped cells when the index is live)
+// and the active-set compaction; their counters are copied to pinned memory.
+static int begin_enqueue(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                         int64_t t, int k_prime) {
   if (!hosts || hosts->pool != p) return set_error(VATE_EVALUE, "registry does not belong to pool");
-  rc = check_width(p, k_prime);
+  int rc = check_width(p, k_prime);
   if (rc) return rc;
   if (g < 1 || g > p->L.size) return set_error(VATE_ECONFIG, "g must be in [1, 2^c]");
   p->est_n = 0;
-  // one host round trip per estimate: Z_p (bitmap pass) and the active-set
-  // compaction are both enqueued, then their counters are read together
-  // misses of the previous incremental lookup (visible since its finish sync)
+  rc = build_bitmap(p, k_prime, inc_delta_ready(p, g, cell_stream, k_prime));
+  if (rc) return rc;
+  return hosts_active_launch(hosts, t, k_prime);  // pipeline.py:121
+}
+
+// complete (after the caller's sync): the sorted active set, P, and g0 of
+// every active host (incremental or full); the g0 kernels are left running.
+static int begin_complete(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                          int64_t t, int k_prime, uint64_t* nhosts, uint64_t* pool_inactive) {
   IncIndex& I = p->inc;
-  if (I.lookup_pending) {
+  if (I.lookup_pending) {  // misses of the previous lookup (landed before this sync)
     I.lookup_pending = false;
     I.last_misses = p->h_ctr[C_MISS];
     I.miss_accum += I.last_misses;
@@ -547,23 +555,14 @@ int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t ce
       I.identity_version = I.lookup_version;
     }
   }
-  p->h_ctr[C_MISS] = 0;
-  // P -> h_ctr[C_P]; the bitmap feeds the gather; with a live inverse index the
-  // same pass lists the cells whose bit flipped since the last estimate
-  rc = build_bitmap(p, k_prime, inc_delta_ready(p, g, cell_stream, k_prime));
-  if (rc) return rc;
-  rc = hosts_active_launch(hosts, t, k_prime);  // pipeline.py:121
-  if (rc) return rc;
-  rc = sync_small(p);
-  if (rc) return rc;
   uint64_t* keys = nullptr;
   uint64_t n = 0;
-  rc = hosts_active_finish(hosts, t, k_prime, &keys, &n);
+  int rc = hosts_active_finish(hosts, t, k_prime, &keys, &n);
   if (rc) return rc;
   *nhosts = n;
   *pool_inactive = 0;
   if (n == 0) {  // no hosts: no report (pipeline.py:122-123); the index stays as it was
-    p->inc.delta_launched = false;
+    I.delta_launched = false;
     return VATE_OK;
   }
   *pool_inactive = p->h_ctr[C_P];
@@ -573,6 +572,17 @@ int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t ce
   p->est_kp = k_prime;
   p->est_g = g;
   return VATE_OK;
+}
+
+int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                        int64_t t, int k_prime, uint64_t* nhosts, uint64_t* pool_inactive) {
+  int rc = enter(p);
+  if (rc) return rc;
+  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime);
+  if (rc) return rc;
+  rc = sync_small(p);
+  if (rc) return rc;
+  return begin_complete(p, hosts, g, cell_stream, t, k_prime, nhosts, pool_inactive);
 }
 
 int vate_estimate_begin_hosts(vate_pool* p, const uint64_t* hosts, uint64_t n, int where,
@@ -652,6 +662,48 @@ int vate_estimate_finish_async(vate_pool* p, uint64_t g, uint64_t pool_inactive,
                                double* out_zv, uint8_t* out_sat, uint64_t cap, uint64_t* nkept) {
   return estimate_finish_impl(p, g, pool_inactive, log_zp, floor, out_host, out_est, out_zv,
                               out_sat, cap, nkept, false);
+}
+
+int vate_slice_step(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                    uint64_t group_stream, const uint32_t* pairs, uint64_t n, int where,
+                    int64_t t, int k_prime, double floor, const double* log_zp_table,
+                    uint64_t* out_host, double* out_est, double* out_zv, uint8_t* out_sat,
+                    uint64_t cap, vate_step_result* res) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (!res || !log_zp_table) return set_error(VATE_EVALUE, "null result or log table");
+  memset(res, 0, sizeof(*res));
+  // scan (pipeline.py:144-147)
+  if (where == VATE_STAGED) {
+    rc = vate_scan_staged(p, g, cell_stream, group_stream, (int)(uintptr_t)pairs, n, hosts, t);
+  } else if (n) {
+    rc = vate_scan_packed(p, g, cell_stream, group_stream, pairs, n, where, hosts, t);
+  }
+  if (rc) return rc;
+  // estimate, first half; then the slice's one host round trip
+  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime);
+  if (rc) return rc;
+  rc = sync_small(p);
+  if (rc) return rc;
+  if (p->adv_pending) {  // the previous slice's sweep finished before this sync
+    res->prev_collected = 1;
+    rc = vate_advance_result(p, res->prev_blocks, &res->prev_maintained, &res->prev_cleared);
+    if (rc) return rc;
+  }
+  uint64_t nh = 0, pin = 0;
+  rc = begin_complete(p, hosts, g, cell_stream, t, k_prime, &nh, &pin);
+  if (rc) return rc;
+  res->nhosts = nh;
+  res->pool_inactive = pin;
+  // maintenance may run before the float path: it touches cells, not g0
+  rc = vate_advance_async(p);
+  if (rc) return rc;
+  if (nh == 0) return VATE_OK;
+  uint64_t kept = 0;
+  rc = vate_estimate_finish_async(p, g, pin, log_zp_table[pin], floor, out_host, out_est, out_zv,
+                                  out_sat, cap, &kept);
+  res->nkept = kept;
+  return rc;
 }
 
 int vate_estimate_wait(vate_pool* p) {

@@ -124,6 +124,25 @@ def log_zp(pool_inactive: int, pool_size: int):
     return float(np.log(zp_clamped)), float(z_p)
 
 
+_LZP_CACHE: dict = {}
+LZP_TABLE_MAX_C = 26   # 2^26+1 doubles = 512 MiB; larger pools take log_zp per slice
+
+
+def log_zp_table(c: int):
+    """np.log of the clamped pool fraction for every P in [0, 2^c] (estimator.py:148-151),
+    elementwise identical to log_zp(P, 2^c); None above LZP_TABLE_MAX_C."""
+    if c > LZP_TABLE_MAX_C:
+        return None
+    tab = _LZP_CACHE.get(c)
+    if tab is None:
+        size = 1 << c
+        zp = np.arange(size + 1, dtype=np.int64) / np.float64(size)
+        zp[0] = 1.0 / (2 * size)
+        tab = np.ascontiguousarray(np.log(zp))
+        _LZP_CACHE[c] = tab
+    return tab
+
+
 def _ensure_log_table(pool: AtPool, g: int) -> None:
     if getattr(pool, "_lzv_g", None) != g:
         tab = log_zv_table(g)

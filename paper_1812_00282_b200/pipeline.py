@@ -21,7 +21,7 @@ import numpy as np
 from . import _lib
 from ._lib import VATE_DEVICE, VATE_HOST, check, lib, ptr
 from .estimator import (EstimatorConfig, HostReports, _check_pool_cfg, _ensure_log_table,
-                        _u64, context_pool, log_zp)
+                        _u64, context_pool, log_zp, log_zp_table)
 from .pools import AtPool, MaintenanceReport
 
 SCAN_CHUNK = 1 << 15  # pipeline.py:26 (the device scan takes a whole slice at once)
@@ -232,6 +232,39 @@ class Pipeline:
         else:
             self._deferred_t = t
         return rep
+
+    def step_fast(self, t: int, pairs: int, n: int, where: str, out):
+        """One whole slice in a single library call (vate_slice_step), streaming.
+
+        ``pairs`` is a device pointer (where='device'), a host pointer
+        ('host') or a staging slot from stage_packed ('staged').  Report rows
+        land asynchronously in ``out`` (alternate two sets); the advance of
+        slice t is accounted during the next call or wait_reports()."""
+        tab = getattr(self, "_lzp_tab", None)
+        if tab is None:
+            tab = self._lzp_tab = log_zp_table(self.pool.c)
+            if tab is None:
+                raise ValueError("step_fast needs c <= 26; use step_packed")
+        host, est, zv, sat = out
+        res = _lib.StepResult()
+        where_code = {"host": VATE_HOST, "device": VATE_DEVICE, "staged": _lib.VATE_STAGED}[where]
+        check(lib.vate_slice_step(self.pool.handle, self.hosts.handle, self.cfg.g,
+                                  self.cfg.cell_stream, self.cfg.group_stream, int(pairs), int(n),
+                                  where_code, t, self.k_prime, float(self.floor), ptr(tab),
+                                  ptr(host), ptr(est), ptr(zv), ptr(sat), len(host),
+                                  C.byref(res)))
+        if res.prev_collected:
+            self._account(self._deferred_t, MaintenanceReport(
+                (res.prev_blocks[0], res.prev_blocks[1]), res.prev_maintained, res.prev_cleared))
+        self._deferred_t = t
+        self.last_active = res.nhosts
+        if res.nhosts == 0:
+            return None
+        self.last_pool_inactive = res.pool_inactive
+        m = res.nkept
+        return HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool),
+                           res.pool_inactive / float(self.pool.size), t - self.k_prime + 1,
+                           self.k_prime)
 
     def step_staged(self, t: int, slot: int, n: int, out=None, wait: bool = True):
         """One slice from a staged buffer (see stage_packed)."""

@@ -578,7 +578,7 @@ def test_active_set_reuse_is_exact():
         assert len(other.active(t, 6)) == 10
 
 
-@pytest.mark.parametrize("mode", ["streamed", "staged"])
+@pytest.mark.parametrize("mode", ["streamed", "staged", "fast-device", "fast-staged"])
 def test_streaming_steps_match_oracle(mode):
     """The bench's paths: packed records, async report D2H (double-buffered),
     the advance collected one slice late, and (staged) H2D prefetch."""
@@ -595,12 +595,21 @@ def test_streaming_steps_match_oracle(mode):
     cleared = 0
     slices = [vo.synthetic_slice(t, n, hosts) for t in range(30)]
     packed = [np.ascontiguousarray(np.stack([a, b], axis=1).astype(np.uint32)) for a, b in slices]
-    staged = pipe.stage_packed(packed[0].ctypes.data, n) if mode == "staged" else None
+    staged = pipe.stage_packed(packed[0].ctypes.data, n) if "staged" in mode else None
+    import torch
+    dev = [torch.from_numpy(x.view(np.int32)).cuda() for x in packed] if mode == "fast-device" else None
+    torch.cuda.synchronize()
     for t in range(30):
         if mode == "staged":
             nxt = pipe.stage_packed(packed[t + 1].ctypes.data, n) if t + 1 < 30 else None
             rep = pipe.step_staged(t, staged, n, outs[t % 2], wait=False)
             staged = nxt
+        elif mode == "fast-staged":
+            nxt = pipe.stage_packed(packed[t + 1].ctypes.data, n) if t + 1 < 30 else None
+            rep = pipe.step_fast(t, staged, n, "staged", outs[t % 2])
+            staged = nxt
+        elif mode == "fast-device":
+            rep = pipe.step_fast(t, dev[t].data_ptr(), n, "device", outs[t % 2])
         else:
             rep = pipe.step_packed(t, packed[t].ctypes.data, n, False, outs[t % 2], wait=False)
         want = opipe.process_slice(t, *slices[t])

@@ -114,3 +114,14 @@ def test_float_path_decomposition_on_pipeline_goldens():
             assert np.array_equal(est, case.est[s]), (name, s)
             assert np.array_equal(zv, case.zv[s]) and np.array_equal(sat, case.sat[s])
             assert zp == case.zp[s]
+
+
+def test_log_zp_table_equals_scalar_path():
+    """The per-pool table the one-call slice step indexes by P equals log_zp(P)."""
+    from paper_1812_00282_b200.estimator import log_zp_table
+    tab = log_zp_table(18)
+    size = 1 << 18
+    rng = np.random.default_rng(0)
+    for p in np.concatenate([[0, 1, 2, size - 1, size], rng.integers(0, size + 1, 20_000)]):
+        assert tab[p] == log_zp(int(p), size)[0], p
+    assert log_zp_table(27) is None
