@@ -187,6 +187,11 @@ int vate_estimate_finish_async(vate_pool* p, uint64_t g, uint64_t pool_inactive,
                                double floor, uint64_t* out_host, double* out_est,
                                double* out_zv, uint8_t* out_sat, uint64_t cap, uint64_t* nkept);
 int vate_estimate_wait(vate_pool* p);
+/* Device addresses of the last finished report rows (for GPU consumers; with
+ * null host output arrays the rows stay in HBM and nothing crosses PCIe).
+ * Valid until the next-but-one finish (two report sets alternate). */
+int vate_reports_device(vate_pool* p, uint64_t** host, double** est, double** zv,
+                        uint8_t** sat);
 
 /* ---- one whole slice (pipeline.py:142-160) in one call, streaming form ---
  * scan (pairs: host/device pointer, or the staging slot when where ==

@@ -706,6 +706,17 @@ int vate_slice_step(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_s
   return rc;
 }
 
+int vate_reports_device(vate_pool* p, uint64_t** host, double** est, double** zv,
+                        uint8_t** sat) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  const int slot = p->out_slot ^ 1;  // the set the last finish wrote
+  if (host) *host = p->host_out[slot].as<uint64_t>();
+  if (est) *est = p->est_out[slot].as<double>();
+  if (zv) *zv = p->zv_out[slot].as<double>();
+  if (sat) *sat = p->sat_out[slot].as<uint8_t>();
+  return VATE_OK;
+}
+
 int vate_estimate_wait(vate_pool* p) {
   int rc = enter(p);
   if (rc) return rc;

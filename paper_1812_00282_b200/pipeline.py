@@ -238,21 +238,23 @@ class Pipeline:
 
         ``pairs`` is a device pointer (where='device'), a host pointer
         ('host') or a staging slot from stage_packed ('staged').  Report rows
-        land asynchronously in ``out`` (alternate two sets); the advance of
-        slice t is accounted during the next call or wait_reports()."""
+        land asynchronously in ``out`` (alternate two sets); with out=None they
+        stay in device memory (reports_device()) and the call returns the row
+        count.  The advance of slice t is accounted during the next call or
+        wait_reports()."""
         tab = getattr(self, "_lzp_tab", None)
         if tab is None:
             tab = self._lzp_tab = log_zp_table(self.pool.c)
             if tab is None:
                 raise ValueError("step_fast needs c <= 26; use step_packed")
-        host, est, zv, sat = out
+        host, est, zv, sat = out if out is not None else (None, None, None, None)
         res = _lib.StepResult()
         where_code = {"host": VATE_HOST, "device": VATE_DEVICE, "staged": _lib.VATE_STAGED}[where]
         check(lib.vate_slice_step(self.pool.handle, self.hosts.handle, self.cfg.g,
                                   self.cfg.cell_stream, self.cfg.group_stream, int(pairs), int(n),
                                   where_code, t, self.k_prime, float(self.floor), ptr(tab),
-                                  ptr(host), ptr(est), ptr(zv), ptr(sat), len(host),
-                                  C.byref(res)))
+                                  *(ptr(a) if a is not None else None for a in (host, est, zv, sat)),
+                                  len(host) if host is not None else 0, C.byref(res)))
         if res.prev_collected:
             self._account(self._deferred_t, MaintenanceReport(
                 (res.prev_blocks[0], res.prev_blocks[1]), res.prev_maintained, res.prev_cleared))
@@ -262,9 +264,17 @@ class Pipeline:
             return None
         self.last_pool_inactive = res.pool_inactive
         m = res.nkept
+        if out is None:
+            return m
         return HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool),
                            res.pool_inactive / float(self.pool.size), t - self.k_prime + 1,
                            self.k_prime)
+
+    def reports_device(self):
+        """(host, estimate, z_v, saturated) device addresses of the last report rows."""
+        ptrs = [C.c_void_p() for _ in range(4)]
+        check(lib.vate_reports_device(self.pool.handle, *(C.byref(q) for q in ptrs)))
+        return tuple(q.value for q in ptrs)
 
     def step_staged(self, t: int, slot: int, n: int, out=None, wait: bool = True):
         """One slice from a staged buffer (see stage_packed)."""

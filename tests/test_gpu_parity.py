@@ -646,3 +646,33 @@ def test_identity_path_when_population_is_stable():
         assert np.array_equal(got.estimate, want.reports.estimate), t
     st = pool.inc_stats()
     assert st["identity_slices"] >= 15, st
+
+
+def test_step_fast_device_resident_reports():
+    """out=None keeps the rows in HBM; reading them back equals the oracle."""
+    import torch
+    cfg = vb.EstimatorConfig(256, 16, 6, seed=9)
+    ocfg = vo.OracleConfig(256, 16, 6, seed=9)
+    pipe = vb.Pipeline(cfg.build_pool(), cfg, 6)
+    opipe = vo.OraclePipeline(ocfg, 6)
+    for t in range(10):
+        a, b = vo.synthetic_slice(t, 50_000, 3_000)
+        dev = torch.from_numpy(np.stack([a, b], axis=1).astype(np.uint32).view(np.int32)).cuda()
+        torch.cuda.synchronize()
+        m = pipe.step_fast(t, dev.data_ptr(), len(a), "device", None)
+        want = opipe.process_slice(t, a, b).reports
+        pipe.wait_reports()
+        pipe.pool.synchronize()
+        hp, ep, zp, sp = pipe.reports_device()
+        import ctypes
+        est = np.empty(m, np.float64)
+        ctypes.CDLL("libcudart.so" if False else None)  # noqa: keep ctypes imported
+        got = torch.empty(m, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        # copy the device rows through torch (UVA pointer -> tensor)
+        from paper_1812_00282_b200._lib import lib
+        assert m == len(want.host) and hp and ep
+        cudart = torch.cuda.cudart()
+        cudart.cudaMemcpy(got.data_ptr(), ep, m * 8, 3)   # device -> device
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), want.estimate), t
