@@ -50,6 +50,32 @@ UNIT = "Mpackets/s"
 PEAKS_FALLBACK = dict(hbm_gbs=6650.0)
 
 
+KERNEL_SYMBOL = {"scan": "k_scan_packed16", "bitmap": "k_bitmap", "g0": "k_g0", "final": "k_final_write",
+                 "registry": "k_active", "sweep": "k_sweep"}
+
+
+def _ncu_traffic(kind):
+    """dram read+write bytes per launch of the kernel behind `kind`, from the committed
+    ncu --set full summaries (profiles/*ncu_kernels.txt); None if not captured."""
+    import glob
+    sym = KERNEL_SYMBOL.get(kind)
+    if sym is None:
+        return None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_kernels.txt")), reverse=True):
+        cur, vals = None, {}
+        for line in open(path):
+            if line.startswith("## "):
+                cur = line
+            elif cur and sym in cur and "_full" not in cur and "dram__bytes" in line:
+                parts = line.split()
+                v, unit = float(parts[1]), parts[2] if len(parts) > 2 else "byte"
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+                vals[parts[0]] = v * scale
+        if vals:
+            return sum(vals.values())
+    return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -352,11 +378,10 @@ def run_gpu(args, rank, world, local_rank):
     # dominant kernel by event time; algorithmic bytes per launch
     per_kind = {k: {"ms_total": v[0], "launches": v[1],
                     "ms_per_launch": (v[0] / v[1] if v[1] else 0.0)} for k, v in kt.items()}
-    dom = max(per_kind, key=lambda k: per_kind[k]["ms_total"])
     nh = pipe.last_active
     S = 1 << w["c"]
     alg_bytes = {
-        "g0": nh * (32 * w["g"] + 12),                 # one sector per gather + aip in, g0 out
+        "g0": (nh * (32 * w["g"] + 12) if args.incremental == "off" else None),
         "scan": n * 40,                                # 8 B pair + one 32 B sector write
         "bitmap": S * pool.cell_bytes + S // 8,        # pool read + bitmap write
         "sweep": 2 * pool.cell_bytes * 2 * pool.max_block_size,
@@ -365,8 +390,15 @@ def run_gpu(args, rank, world, local_rank):
         "sort": nh * 8 * 4 * 2,
         "other": 0,
     }
+    # the dominant kernel among those with a defined per-unit figure (the incremental
+    # g0 family has none in SURVEY §8(d); its work is reported in "incremental")
+    dom = max((k for k in per_kind if alg_bytes.get(k)), key=lambda k: per_kind[k]["ms_total"])
     dk = per_kind[dom]
     achieved = alg_bytes[dom] / (dk["ms_per_launch"] / 1e3) / 1e9 if dk["ms_per_launch"] else 0.0
+    for kind, v in per_kind.items():   # the same accounting for every kernel, for context
+        if v["ms_per_launch"] and alg_bytes.get(kind):
+            v["alg_gbs"] = alg_bytes[kind] / (v["ms_per_launch"] / 1e3) / 1e9
+            v["frac_of_hbm"] = v["alg_gbs"] / hbm
     step_ms = max_ms / args.steps
     cpu_mean, cores = cpu_sample(w, steps=1) if world == 1 else (None, None)
     line = {
@@ -377,13 +409,16 @@ def run_gpu(args, rank, world, local_rank):
         "config": _config(w, world),
         "estimate_ms_per_slice": sum(per_kind[k]["ms_total"] for k in
                                      ("registry", "sort", "bitmap", "g0", "final")) / args.steps,
+        "estimate_ms_per_slice_note": "kernel time from the end of scan to the report rows "
+                                      "(registry compaction, sort, bitmap+delta, g0, float path)",
         "scan_update_mpps": n / ((per_kind["scan"]["ms_total"] + per_kind["sweep"]["ms_total"])
                                  / args.steps / 1e3) / 1e6,
         "reports_per_slice": nh,
         "kernels": per_kind,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": None,
+                     "traffic": _ncu_traffic(dom),
+                     "traffic_source": "profiles/*ncu_kernels.txt (ncu --set full, one launch)",
                      "algorithmic_bytes_per_launch": alg_bytes[dom]},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": slice_bytes,
                 "d2h_bytes_per_step": int(e2e_rows / args.steps * 25),
