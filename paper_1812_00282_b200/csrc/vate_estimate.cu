@@ -384,6 +384,27 @@ __global__ void __launch_bounds__(256) k_final_write(const uint64_t* __restrict_
 }
 
 // Writes report set `slot`; the D2H that last read that set must be done first.
+// No floor: every host is kept at its own position, so a plain grid-stride
+// loop gives fully coalesced loads and stores.
+__global__ void __launch_bounds__(256) k_final_all(const uint64_t* __restrict__ hosts,
+                                                   const int32_t* __restrict__ g0, uint64_t n,
+                                                   FloatPath F, uint64_t* __restrict__ out_host,
+                                                   double* __restrict__ out_est,
+                                                   double* __restrict__ out_zv,
+                                                   uint8_t* __restrict__ out_sat) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double e, z;
+    uint8_t st;
+    bool keep;
+    float_path(__ldcs(g0 + i), F, &e, &z, &st, &keep);
+    if (hosts) __stcs(out_host + i, __ldcs(hosts + i));
+    __stcs(out_est + i, e);
+    __stcs(out_zv + i, z);
+    out_sat[i] = st;
+  }
+}
+
 static int run_float_path(vate_pool* p, const uint64_t* hosts_dev, const int32_t* g0_dev,
                           uint64_t n, FloatPath F, int slot, uint64_t* nkept) {
   const uint64_t ntiles = (n + kFinTile - 1) / kFinTile;
@@ -407,9 +428,14 @@ static int run_float_path(vate_pool* p, const uint64_t* hosts_dev, const int32_t
                               p->stream));
     tile_off = p->flags.as<const unsigned>();
   }
-  VATE_LAUNCH(p, VATE_K_FINAL, (uint32_t)ntiles, 256, 0, k_final_write, hosts_dev, g0_dev, n, F,
-              tile_off, p->host_out[slot].as<uint64_t>(), p->est_out[slot].as<double>(),
-              p->zv_out[slot].as<double>(), p->sat_out[slot].as<uint8_t>());
+  if (tile_off)
+    VATE_LAUNCH(p, VATE_K_FINAL, (uint32_t)ntiles, 256, 0, k_final_write, hosts_dev, g0_dev, n, F,
+                tile_off, p->host_out[slot].as<uint64_t>(), p->est_out[slot].as<double>(),
+                p->zv_out[slot].as<double>(), p->sat_out[slot].as<uint8_t>());
+  else
+    VATE_LAUNCH(p, VATE_K_FINAL, grid_for(n, 256, 148u * 16u), 256, 0, k_final_all, hosts_dev,
+                g0_dev, n, F, p->host_out[slot].as<uint64_t>(), p->est_out[slot].as<double>(),
+                p->zv_out[slot].as<double>(), p->sat_out[slot].as<uint8_t>());
   if (F.floor > 0.0) {
     rc = sync_small(p);
     if (rc) return rc;

@@ -404,68 +404,84 @@ struct DeltaOut {
 };
 
 template <typename T>
+__device__ __forceinline__ uint32_t word_inactive_bits(const T* __restrict__ cells,
+                                                       const uint4 (&r)[(int)sizeof(T) * 2],
+                                                       uint64_t i0, uint32_t cnt, const Layout& L,
+                                                       uint32_t bact0, uint32_t kp) {
+  uint32_t b = block_of(i0, L);
+  uint64_t next = block_start(b + 1, L);
+  uint32_t act = clock_of(bact0, b, L.B);
+  if (cnt == 32 && i0 + 32 <= next) {  // the whole word in one block: one clock
+    if (sizeof(T) <= 2) {
+      uint32_t active;
+      if (active_bits_simd<T>(r, act, L.B, kp, &active)) return ~active;
+    }
+    const T* e = reinterpret_cast<const T*>(r);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) bits |= (uint32_t)is_inactive(e[j], act, L.B, kp) << j;
+    return bits;
+  }
+  uint32_t bits = 0;  // block boundary (or pool end) inside the word
+  for (uint32_t j = 0; j < cnt; ++j) {
+    while (i0 + j >= next) {
+      ++b;
+      next = block_start(b + 1, L);
+      act = (act + 1 == L.B) ? 0 : act + 1;
+    }
+    bits |= (uint32_t)is_inactive(cells[i0 + j], act, L.B, kp) << j;
+  }
+  return bits;
+}
+
+// kW words per thread per iteration: all their 16-byte loads are issued before
+// any predicate, for memory-level parallelism.
+template <typename T>
 __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells, Layout L,
                                                      uint32_t bact0, uint32_t kp,
                                                      uint32_t* __restrict__ bitmap,
                                                      uint64_t nwords,
                                                      unsigned long long* pool_inactive,
                                                      DeltaOut D) {
+  constexpr int kW = sizeof(T) == 1 ? 4 : 2;
+  constexpr int NV = (int)sizeof(T) * 2;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   unsigned local = 0;
-  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
-    const uint64_t i0 = w * 32;
-    const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
-    uint32_t b = block_of(i0, L);
-    uint64_t next = block_start(b + 1, L);
-    uint32_t act = clock_of(bact0, b, L.B);
-    uint32_t bits = 0;
-    bool done = false;
-    if (cnt == 32 && i0 + 32 <= next) {  // the whole word in one block: one clock
-      if (sizeof(T) <= 2) {
-        uint4 r[(int)sizeof(T) * 2];
+  for (uint64_t w0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w0 < nwords;
+       w0 += kW * stride) {
+    uint4 r[kW][NV];
 #pragma unroll
-        for (int q = 0; q < (int)sizeof(T) * 2; ++q)
-          r[q] = __ldcs(reinterpret_cast<const uint4*>(cells + i0) + q);
-        uint32_t active;
-        if (active_bits_simd<T>(r, act, L.B, kp, &active)) {
-          bits = ~active;
-          done = true;
-        }
-      }
-      if (!done) {
-        uint32_t v[32];
-        load32<T>(cells + i0, v);
+    for (int q = 0; q < kW; ++q) {
+      const uint64_t w = w0 + q * stride;
+      if (w < nwords && (w + 1) * 32 <= L.size) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) bits |= (uint32_t)is_inactive(v[j], act, L.B, kp) << j;
-        done = true;
+        for (int v = 0; v < NV; ++v) r[q][v] = __ldcs(reinterpret_cast<const uint4*>(cells + w * 32) + v);
       }
     }
-    if (!done) {  // block boundary (or pool end) inside the word
-      for (uint32_t j = 0; j < cnt; ++j) {
-        while (i0 + j >= next) {
-          ++b;
-          next = block_start(b + 1, L);
-          act = (act + 1 == L.B) ? 0 : act + 1;
+#pragma unroll
+    for (int q = 0; q < kW; ++q) {
+      const uint64_t w = w0 + q * stride;
+      if (w >= nwords) break;
+      const uint64_t i0 = w * 32;
+      const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
+      const uint32_t bits = word_inactive_bits<T>(cells, r[q], i0, cnt, L, bact0, kp);
+      bitmap[w] = bits;
+      local += __popc(bits);
+      if (D.bprev) {
+        uint32_t x = bits ^ D.bprev[w];
+        if (x) {
+          unsigned long long pos = atomicAdd(D.count, (unsigned long long)__popc(x));
+          unsigned long long wsum = 0;
+          while (x) {
+            const int j = __ffs(x) - 1;
+            x &= x - 1;
+            const uint64_t cell = i0 + j;
+            wsum += D.off[cell + 1] - D.off[cell];
+            if (pos < D.cap) D.list[pos] = cell | ((unsigned long long)((bits >> j) & 1u) << 32);
+            ++pos;
+          }
+          atomicAdd(D.work, wsum);
         }
-        bits |= (uint32_t)is_inactive(cells[i0 + j], act, L.B, kp) << j;
-      }
-    }
-    bitmap[w] = bits;
-    local += __popc(bits);
-    if (D.bprev) {
-      uint32_t x = bits ^ D.bprev[w];
-      if (x) {
-        unsigned long long pos = atomicAdd(D.count, (unsigned long long)__popc(x));
-        unsigned long long wsum = 0;
-        while (x) {
-          const int j = __ffs(x) - 1;
-          x &= x - 1;
-          const uint64_t cell = i0 + j;
-          wsum += D.off[cell + 1] - D.off[cell];
-          if (pos < D.cap) D.list[pos] = cell | ((unsigned long long)((bits >> j) & 1u) << 32);
-          ++pos;
-        }
-        atomicAdd(D.work, wsum);
       }
     }
   }
@@ -622,7 +638,7 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
   }
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
-    VATE_LAUNCH(p, VATE_K_BITMAP, grid_for(nwords, kThreads, 148u * 32u), kThreads, 0,
+    VATE_LAUNCH(p, VATE_K_BITMAP, grid_for((nwords + 3) / 4, kThreads, 148u * 32u), kThreads, 0,
                 k_bitmap<T>, (const T*)p->cells, p->L, p->bact0, (uint32_t)k_prime,
                 p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D);
     return VATE_OK;
