@@ -16,7 +16,7 @@
 
 namespace vate {
 
-enum HCtr { H_COUNT = 0, H_OVF = 1, H_SPECIAL = 2, H_MAXKEY = 3, H_NOUT = 4, H_CHANGES = 5, H_N = 8 };
+enum HCtr { H_COUNT = 0, H_OVF = 1, H_SPECIAL = 2, H_MAXKEY = 3, H_NOUT = 4, H_CHANGES = 5, H_NOUT2 = 6, H_N = 8 };
 
 RegRef make_ref(const vate_hosts* h, const DevBuf& table, uint64_t cap) {
   RegRef R{};
@@ -55,23 +55,79 @@ __global__ void k_insert_entries(const RegEntry* __restrict__ src, uint64_t n,
 // sorts).  Each CTA handles tiles of 1024 entries (4 per thread) and reserves
 // its output range with one atomic per tile.
 constexpr int kActTile = 1024;
-// member[i] remembers whether slot i was in the previous compaction's set; the
-// number of slots whose membership flipped tells the host whether last slice's
-// sorted list can be reused (exactly) instead of sorting again.
+
+// Pass 1 (every estimate): membership of every slot for the window (last > cut),
+// recorded in member[]; counts the active keys, the slots whose membership
+// flipped since the previous compaction, and the largest active key.  One
+// global atomic per CTA for each counter.
 __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ table, uint64_t cap,
                                                 const unsigned long long* special, long long cut,
-                                                uint64_t* __restrict__ out,
+                                                uint8_t* __restrict__ member,
                                                 unsigned long long* nout,
                                                 unsigned long long* maxkey,
-                                                uint8_t* __restrict__ member,
                                                 unsigned long long* changes) {
+  __shared__ unsigned s_n, s_flips;
+  __shared__ unsigned long long s_max;
+  if (threadIdx.x == 0) {
+    s_n = 0;
+    s_flips = 0;
+    s_max = 0;
+  }
+  __syncthreads();
+  const uint64_t total = cap + 1;
+  const bool special_present = (*special & 0xFFFFFFFFull) != 0;
+  unsigned long long kmax = 0;
+  unsigned mine = 0, flips = 0;
+  for (uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < total;
+       i0 += (uint64_t)gridDim.x * blockDim.x * 4) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = i0 + q;
+      if (i >= total) break;
+      const RegEntry e = table[i];
+      const bool tk = (i < cap) ? (e.key != kEmptyKey && e.last > cut)
+                                : (special_present && e.last > cut);
+      if ((member[i] != 0) != tk) {
+        member[i] = tk;
+        ++flips;
+      }
+      if (tk) {
+        ++mine;
+        kmax = e.key > kmax ? e.key : kmax;
+      }
+    }
+  }
+  mine = __reduce_add_sync(0xffffffffu, mine);
+  flips = __reduce_add_sync(0xffffffffu, flips);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, kmax, o);
+    kmax = other > kmax ? other : kmax;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mine) atomicAdd(&s_n, mine);
+    if (flips) atomicAdd(&s_flips, flips);
+    if (kmax) atomicMax(&s_max, kmax);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_n) atomicAdd(nout, (unsigned long long)s_n);
+    if (s_flips) atomicAdd(changes, (unsigned long long)s_flips);
+    if (s_max) atomicMax(maxkey, s_max);
+  }
+}
+
+// Pass 2 (only when membership changed): the member keys, appended in arbitrary
+// order (the caller sorts); one reservation per 1024-slot tile.
+__global__ void __launch_bounds__(256) k_active_keys(const RegEntry* __restrict__ table,
+                                                     uint64_t cap,
+                                                     const uint8_t* __restrict__ member,
+                                                     uint64_t* __restrict__ out,
+                                                     unsigned long long* nout) {
   __shared__ unsigned warp_tot[8];
   __shared__ unsigned long long base_s;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t total = cap + 1;
-  const bool special_present = (*special & 0xFFFFFFFFull) != 0;
-  unsigned long long kmax = 0;
-  unsigned flips = 0;
   for (uint64_t tile = (uint64_t)blockIdx.x * kActTile; tile < total;
        tile += (uint64_t)gridDim.x * kActTile) {
     const uint64_t i0 = tile + threadIdx.x * 4;
@@ -81,20 +137,10 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
     for (int q = 0; q < 4; ++q) {
       const uint64_t i = i0 + q;
       key[q] = 0;
-      if (i < total) {
-        const RegEntry e = table[i];
-        const bool tk = (i < cap) ? (e.key != kEmptyKey && e.last > cut)
-                                  : (special_present && e.last > cut);
-        if ((member[i] != 0) != tk) {
-          member[i] = tk;
-          ++flips;
-        }
-        if (tk) {
-          key[q] = e.key;
-          take |= 1u << q;
-          ++mine;
-          kmax = e.key > kmax ? e.key : kmax;
-        }
+      if (i < total && member[i]) {
+        key[q] = table[i].key;
+        take |= 1u << q;
+        ++mine;
       }
     }
     unsigned incl = mine;
@@ -119,14 +165,6 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
       if ((take >> q) & 1u) out[pos++] = key[q];
     __syncthreads();
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const unsigned long long other = __shfl_xor_sync(0xffffffffu, kmax, o);
-    kmax = other > kmax ? other : kmax;
-  }
-  if (lane == 0 && kmax) atomicMax(maxkey, kmax);
-  flips = __reduce_add_sync(0xffffffffu, flips);
-  if (lane == 0 && flips) atomicAdd(changes, (unsigned long long)flips);
 }
 
 // Entries with last > horizon, appended (prune keeps them).
@@ -280,11 +318,11 @@ int hosts_active_launch(vate_hosts* h, int64_t t, int k_prime) {
     VATE_CUDA(cudaMemsetAsync(h->member.ptr, 0, h->cap + 1, p->stream));
     h->member_valid = false;  // first compaction after a (re)layout always sorts
   }
-  VATE_CUDA(cudaMemsetAsync(h->d_count + H_MAXKEY, 0, 24, p->stream));
-  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap + 1, kActTile, 148u * 8u), 256, 0, k_active,
+  VATE_CUDA(cudaMemsetAsync(h->d_count + H_MAXKEY, 0, 32, p->stream));
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for((h->cap + 4) / 4, 256, 148u * 8u), 256, 0, k_active,
               h->table.as<const RegEntry>(), h->cap, h->d_count + H_SPECIAL,
-              (long long)(t - k_prime), p->hosts_tmp.as<uint64_t>(), h->d_count + H_NOUT,
-              h->d_count + H_MAXKEY, h->member.as<uint8_t>(), h->d_count + H_CHANGES);
+              (long long)(t - k_prime), h->member.as<uint8_t>(), h->d_count + H_NOUT,
+              h->d_count + H_MAXKEY, h->d_count + H_CHANGES);
   VATE_CUDA(cudaMemcpyAsync(h->h_count, h->d_count, H_N * 8, cudaMemcpyDeviceToHost, p->stream));
   return VATE_OK;
 }
@@ -313,6 +351,13 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
   if (reuse) {
     p->sorts_skipped++;
     return VATE_OK;
+  }
+  // membership changed: write the member keys (same predicate, from member[])
+  if (*n) {
+    VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap + 1, kActTile, 148u * 8u), 256, 0,
+                k_active_keys, h->table.as<const RegEntry>(), h->cap,
+                h->member.as<const uint8_t>(), p->hosts_tmp.as<uint64_t>(),
+                h->d_count + H_NOUT2);
   }
   const unsigned long long maxkey = h->h_count[H_MAXKEY];
   int end_bit = 64;

@@ -445,6 +445,15 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
                                                      DeltaOut D) {
   constexpr int kW = sizeof(T) == 1 ? 4 : 2;
   constexpr int NV = (int)sizeof(T) * 2;
+  constexpr unsigned kDeltaStage = 1024;
+  __shared__ unsigned long long s_delta[kDeltaStage];
+  __shared__ unsigned s_nd;
+  __shared__ unsigned long long s_work, s_base;
+  if (threadIdx.x == 0) {
+    s_nd = 0;
+    s_work = 0;
+  }
+  __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   unsigned local = 0;
   for (uint64_t w0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w0 < nwords;
@@ -469,21 +478,36 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
       local += __popc(bits);
       if (D.bprev) {
         uint32_t x = bits ^ D.bprev[w];
-        if (x) {
-          unsigned long long pos = atomicAdd(D.count, (unsigned long long)__popc(x));
+        if (x) {  // stage this CTA's flipped cells in shared memory
           unsigned long long wsum = 0;
           while (x) {
             const int j = __ffs(x) - 1;
             x &= x - 1;
             const uint64_t cell = i0 + j;
             wsum += D.off[cell + 1] - D.off[cell];
-            if (pos < D.cap) D.list[pos] = cell | ((unsigned long long)((bits >> j) & 1u) << 32);
-            ++pos;
+            const unsigned long long v = cell | ((unsigned long long)((bits >> j) & 1u) << 32);
+            const unsigned slot = atomicAdd(&s_nd, 1u);
+            if (slot < kDeltaStage) s_delta[slot] = v;
+            else {  // stage full: straight to the global list
+              const unsigned long long pos = atomicAdd(D.count, 1ull);
+              if (pos < D.cap) D.list[pos] = v;
+            }
           }
-          atomicAdd(D.work, wsum);
+          atomicAdd(&s_work, wsum);
         }
       }
     }
+  }
+  if (D.bprev) {  // one global reservation per CTA
+    __syncthreads();
+    const unsigned nd = s_nd < kDeltaStage ? s_nd : kDeltaStage;
+    if (threadIdx.x == 0) {
+      s_base = nd ? atomicAdd(D.count, (unsigned long long)nd) : 0ull;
+      if (s_work) atomicAdd(D.work, s_work);
+    }
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < nd; i += blockDim.x)
+      if (s_base + i < D.cap) D.list[s_base + i] = s_delta[i];
   }
   const unsigned s = block_sum(local);
   if (threadIdx.x == 0 && s) atomicAdd(pool_inactive, (unsigned long long)s);
