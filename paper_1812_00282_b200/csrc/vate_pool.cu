@@ -210,37 +210,27 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
   }
 }
 
-// V uint4 loads (2 packets each) per thread per iteration; the next
-// iteration's packets are loaded before this one's stores.
-template <typename T, bool REG, int V = 2>
+template <typename T, bool REG, int V = 2>  // V uint4 loads (2 packets each) per iteration
 __global__ void __launch_bounds__(kThreads) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
     Layout L, uint32_t bact0, RegRef R, long long t) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  uint4 cur[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const uint64_t j = i + v * stride;
-    cur[v] = j < npairs2 ? __ldcs(pairs2 + j) : make_uint4(0, 0, 0, 0);
-  }
   for (; i < npairs2; i += V * stride) {
-    uint4 nxt[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const uint64_t j = i + (V + v) * stride;
-      nxt[v] = j < npairs2 ? __ldcs(pairs2 + j) : make_uint4(0, 0, 0, 0);
-    }
     uint64_t a[2 * V], b[2 * V];
     int m = 0;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      a[2 * v] = cur[v].x; b[2 * v] = cur[v].y; a[2 * v + 1] = cur[v].z; b[2 * v + 1] = cur[v].w;
-      if (i + v * stride < npairs2) m += 2;
+      const uint64_t j = i + v * stride;
+      if (j < npairs2) {
+        const uint4 q = __ldcs(pairs2 + j);  // streamed once: evict-first
+        a[2 * v] = q.x; b[2 * v] = q.y; a[2 * v + 1] = q.z; b[2 * v + 1] = q.w;
+        m += 2;
+      } else {
+        a[2 * v] = b[2 * v] = a[2 * v + 1] = b[2 * v + 1] = 0;
+      }
     }
     scan_batch<T, REG, 2 * V>(a, b, m, cells, H, L, bact0, R, t);
-#pragma unroll
-    for (int v = 0; v < V; ++v) cur[v] = nxt[v];
   }
 }
 
