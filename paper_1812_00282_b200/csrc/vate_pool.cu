@@ -178,18 +178,6 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
                                            int m, T* __restrict__ cells, const HashParams& H,
                                            const Layout& L, uint32_t bact0, const RegRef& R,
                                            long long t) {
-  // registry probes first: their addresses depend on aip alone, and issuing
-  // them before the byte stores (which may alias anything) keeps U loads in
-  // flight while the cells are hashed and written
-  uint64_t slot[U];
-  RegEntry e[U];
-  if (REG) {
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      slot[q] = mix64(aip[q] ^ kRegSalt) & R.mask;
-      if (q < m) e[q] = R.table[slot[q]];
-    }
-  }
 #pragma unroll
   for (int q = 0; q < U; ++q) {
     if (q < m) {
@@ -198,6 +186,14 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
     }
   }
   if (REG) {
+    // all U first probes in flight before any is resolved (one 16-B sector each)
+    uint64_t slot[U];
+    RegEntry e[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      slot[q] = mix64(aip[q] ^ kRegSalt) & R.mask;
+      if (q < m) e[q] = R.table[slot[q]];
+    }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       if (q >= m) continue;
@@ -211,7 +207,7 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
 }
 
 template <typename T, bool REG, int V = 2>  // V uint4 loads (2 packets each) per iteration
-__global__ void __launch_bounds__(kThreads) k_scan_packed16(
+__global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
     Layout L, uint32_t bact0, RegRef R, long long t) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
