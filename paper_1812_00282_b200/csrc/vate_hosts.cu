@@ -211,9 +211,11 @@ int hosts_drain(vate_hosts* h) {
   // list repeats a key once per packet, so it only forces "at least double";
   // the recursion below grows again if re-insertion still overflows.
   const bool shrink = novf == 0 && h->cap > (1u << 16) && count * 16 < h->cap;
-  if (novf > 0 || count > h->cap / 2 || shrink) {
-    uint64_t new_cap = pow2_at_least(4 * count + 64);
-    if (novf > 0 || count > h->cap / 2) new_cap = std::max<uint64_t>(new_cap, 2 * h->cap);
+  // load kept <= 0.6: the table stays small enough to live in L2 next to the
+  // pool (every packet probes it once)
+  if (novf > 0 || count * 5 > h->cap * 3 || shrink) {
+    uint64_t new_cap = pow2_at_least(2 * count + 64);
+    if (novf > 0 || count * 5 > h->cap * 3) new_cap = std::max<uint64_t>(new_cap, 2 * h->cap);
     new_cap = std::max<uint64_t>(new_cap, 1u << 12);
     // rehash the live table: copy entries out first (rebuild consumes `src`)
     DevBuf old;
@@ -340,7 +342,7 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
   }
   h->pending = 0;
   h->count_hint = h->h_count[H_COUNT];
-  if (h->count_hint > h->cap / 2 || (h->cap > (1u << 16) && h->count_hint * 16 < h->cap))
+  if (h->count_hint * 5 > h->cap * 3 || (h->cap > (1u << 16) && h->count_hint * 16 < h->cap))
     h->needs_grow = true;
   *n = h->h_count[H_NOUT];
   *keys_dev = p->hosts_sorted.as<uint64_t>();
