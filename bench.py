@@ -42,9 +42,21 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = dict(name="cfg2-40Gbps-equivalent", c=24, k=60, k_prime=60, g=1024,
-                hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
-                base_aip=0x0A000000)
+WORKLOADS = {
+    # BASELINE.json configs[1] -- the headline (default)
+    "cfg2": dict(name="cfg2-40Gbps-equivalent", c=24, k=60, k_prime=60, g=1024,
+                 hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
+                 base_aip=0x0A000000),
+    # configs[0]: the reference's CPU-runnable shape (1M packets as 10 x 100k slices)
+    "cfg1": dict(name="cfg1-cpu-reference-shape", c=20, k=10, k_prime=10, g=1024,
+                 hosts=10_000, packets=100_000, seed=0, partition="tail", floor=0.0,
+                 base_aip=0x0A000000),
+    # configs[3]: long window, 512 MiB of u16 cells beyond L2
+    "cfg4": dict(name="cfg4-long-window-k300", c=28, k=300, k_prime=300, g=1024,
+                 hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
+                 base_aip=0x0A000000),
+}
+WORKLOAD = WORKLOADS["cfg2"]
 METRIC = "Mpackets/s AT scan+update (full slice: scan+estimate+maintain)"
 UNIT = "Mpackets/s"
 PEAKS_FALLBACK = dict(hbm_gbs=6650.0)
@@ -149,6 +161,7 @@ def cpu_sample(w, seconds_budget=20.0, workers=None, sample_packets=1_000_000,
     cfg = vo.OracleConfig(w["g"], w["c"], w["k"], seed=w["seed"], partition=w["partition"])
     pipe = vo.OraclePipeline(cfg, w["k_prime"], floor=w["floor"], workers=workers)
     per_step = []
+    sample_packets = min(sample_packets, w["packets"])
     for t in range(steps):
         a, b = vo.synthetic_slice(t, sample_packets, w["hosts"], w["base_aip"])
         t0 = time.perf_counter()
@@ -179,13 +192,14 @@ def run_reference(args, rank, world):
         cpu_sample(w, steps=1)
     mean, cores = cpu_sample(w, steps=args.steps)
     value = w["packets"] / mean["slice_s"] / 1e6
-    sample = (f"per step: scan of 1,000,000 of the slice's {w['packets']:,} packets and g0 of "
-              f"1,000 of its ~{w['hosts']:,} active hosts (both extrapolated), full-pool Z_p "
-              f"and the real two-block advance; oracle port with {cores} threads")
+    sample = (f"per step: scan of {min(1_000_000, w['packets']):,} of the slice's "
+              f"{w['packets']:,} packets and g0 of 1,000 of its ~{w['hosts']:,} active hosts "
+              f"(both extrapolated), full-pool Z_p and the real two-block advance; oracle port "
+              f"with {cores} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean["slice_s"] * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype(w),
         "data": "synthetic (oracle.synthetic_slice)",
         "config": _config(w, world),
         "estimate_ms_per_slice": mean["estimate_s"] * 1e3,
@@ -195,6 +209,11 @@ def run_reference(args, rank, world):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _dtype(w):
+    """Cell storage type of the pool (the arithmetic type of the path)."""
+    return "u8" if 2 * w["k"] <= 254 else ("u16" if 2 * w["k"] <= 65534 else "u32")
 
 
 def _config(w, world):
@@ -404,7 +423,7 @@ def run_gpu(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "scaling": "weak", "vs_baseline": None, "dtype": _dtype(w),
         "data": "synthetic (csrc k_synth == oracle.synthetic_slice)",
         "config": _config(w, world),
         "estimate_ms_per_slice": sum(per_kind[k]["ms_total"] for k in
@@ -440,8 +459,9 @@ def run_gpu(args, rank, world, local_rank):
         line["cpu_baseline"] = {
             "value": w["packets"] / cpu_mean["slice_s"] / 1e6, "unit": UNIT, "cores": cores,
             "kind": "port",
-            "sample": "one slice: scan of 1M of 5M packets, g0 of 1,000 of ~1M hosts "
-                      "(extrapolated), full Z_p and advance; numpy oracle, all host threads"}
+            "sample": f"one slice: scan of {min(1_000_000, w['packets']):,} of {w['packets']:,} "
+                      f"packets, g0 of 1,000 of ~{w['hosts']:,} hosts (extrapolated), full Z_p "
+                      f"and advance; numpy oracle, all host threads"}
     print(json.dumps(line), flush=True)
     _teardown(dist)
 
@@ -483,11 +503,15 @@ def main():
     ap.add_argument("--impl", choices=("vate", "reference"), default="vate")
     ap.add_argument("--g0-kernel", choices=("auto", "gather", "smem"), default="auto",
                     help="g0 gather variant (VATE_OPT_G0)")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2",
+                    help="workload shape (BASELINE.json configs); cfg2 is the headline")
     ap.add_argument("--incremental", choices=("on", "off"), default="on",
                     help="exact incremental g0 through the inverse index (VATE_OPT_INCREMENTAL)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be at least 3")
+    global WORKLOAD
+    WORKLOAD = WORKLOADS[args.config]
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

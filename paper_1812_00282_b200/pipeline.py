@@ -143,7 +143,7 @@ class Pipeline:
                                    self.hosts.handle, t))
 
     def estimate_soa(self, t: int, out=None, advance: bool = False,
-                     wait: bool = True) -> HostReports | None:
+                     wait: bool = True, keep_on_device: bool = False):
         """The estimate phase (pipeline.py:120-138) as arrays; None without hosts.
 
         ``out`` may supply preallocated (pinned) host arrays
@@ -169,6 +169,13 @@ class Pipeline:
         if n == 0:
             return None
         lzp, z_p = log_zp(p.value, self.pool.size)
+        if keep_on_device:   # rows stay in HBM (reports_device()); return the row count
+            kept = C.c_uint64()
+            check(lib.vate_estimate_finish_async(self.pool.handle, self.cfg.g, p.value, lzp,
+                                                 float(self.floor), None, None, None, None, 0,
+                                                 C.byref(kept)))
+            self.last_pool_inactive = p.value
+            return kept.value
         if out is None or len(out[0]) < n:
             out = (np.empty(n, np.uint64), np.empty(n, np.float64), np.empty(n, np.float64),
                    np.empty(n, np.uint8))
@@ -245,8 +252,17 @@ class Pipeline:
         tab = getattr(self, "_lzp_tab", None)
         if tab is None:
             tab = self._lzp_tab = log_zp_table(self.pool.c)
-            if tab is None:
-                raise ValueError("step_fast needs c <= 26; use step_packed")
+        if tab is None:   # pool too large for the table: same slice, log_zp per slice
+            if where == "staged":
+                check(lib.vate_scan_staged(self.pool.handle, self.cfg.g, self.cfg.cell_stream,
+                                           self.cfg.group_stream, int(pairs), int(n),
+                                           self.hosts.handle, t))
+            else:
+                self.scan_packed(t, pairs, n, where == "device")
+            rep = self.estimate_soa(t, out, advance=True, wait=False,
+                                    keep_on_device=out is None)
+            self._deferred_t = t
+            return rep
         host, est, zv, sat = out if out is not None else (None, None, None, None)
         res = _lib.StepResult()
         where_code = {"host": VATE_HOST, "device": VATE_DEVICE, "staged": _lib.VATE_STAGED}[where]
