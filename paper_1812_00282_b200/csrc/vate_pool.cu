@@ -365,7 +365,35 @@ __device__ __forceinline__ bool active_bits_simd(const uint4 (&r)[(int)sizeof(T)
   const int lo = (int)act - (int)kp + 1;
   const uint32_t* x = reinterpret_cast<const uint32_t*>(r);
   uint32_t bits = 0, bad = 0;
-  if (sizeof(T) == 1) {
+  if (sizeof(T) == 1 && B < 128) {
+    // Guard-bit SWAR: with every lane below 128, ((x | H) - y) & H flags the
+    // lanes where x >= y, and no borrow crosses a lane.  4 ops per 4 cells.
+    const uint32_t H = 0x80808080u;
+    const uint32_t AH = (act * 0x01010101u) | H;
+    const uint32_t L4 = (uint32_t)(lo >= 0 ? lo : lo + (int)B) * 0x01010101u;
+    const uint32_t B4 = B * 0x01010101u, Bp1 = (B + 1) * 0x01010101u;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t xh = x[q] | H;
+      bad |= (x[q] & H) | ((xh - Bp1) & H);  // a byte >= 128 or > 2k
+      const uint32_t ge_lo = (xh - L4) & H, le_act = (AH - x[q]) & H;
+      const uint32_t m = lo >= 0 ? (ge_lo & le_act) : (le_act | (ge_lo & ~((xh - B4) & H)));
+      bits |= ((((m >> 7) * 0x01020408u) >> 24) & 0xFu) << (4 * q);
+    }
+  } else if (sizeof(T) == 2 && B < 32768) {
+    const uint32_t H = 0x80008000u;
+    const uint32_t AH = (act * 0x00010001u) | H;
+    const uint32_t L2 = (uint32_t)(lo >= 0 ? lo : lo + (int)B) * 0x00010001u;
+    const uint32_t B2 = B * 0x00010001u, Bp1 = (B + 1) * 0x00010001u;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const uint32_t xh = x[q] | H;
+      bad |= (x[q] & H) | ((xh - Bp1) & H);
+      const uint32_t ge_lo = (xh - L2) & H, le_act = (AH - x[q]) & H;
+      const uint32_t m = lo >= 0 ? (ge_lo & le_act) : (le_act | (ge_lo & ~((xh - B2) & H)));
+      bits |= (((m >> 15) & 1u) | ((m >> 30) & 2u)) << (2 * q);
+    }
+  } else if (sizeof(T) == 1) {
     const uint32_t B4 = B * 0x01010101u, A4 = act * 0x01010101u;
     const uint32_t L4 = (uint32_t)(lo >= 0 ? lo : lo + (int)B) * 0x01010101u;
 #pragma unroll
@@ -376,15 +404,7 @@ __device__ __forceinline__ bool active_bits_simd(const uint4 (&r)[(int)sizeof(T)
       bits |= (((m & 0x01010101u) * 0x01020408u) >> 24) << (4 * q);
     }
   } else {
-    const uint32_t B2 = B * 0x00010001u, A2 = act * 0x00010001u;
-    const uint32_t L2 = (uint32_t)(lo >= 0 ? lo : lo + (int)B) * 0x00010001u;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      bad |= __vcmpgtu2(x[q], B2);
-      const uint32_t m = lo >= 0 ? (__vcmpgeu2(x[q], L2) & __vcmpleu2(x[q], A2))
-                                 : (__vcmpleu2(x[q], A2) | (__vcmpgeu2(x[q], L2) & __vcmpltu2(x[q], B2)));
-      bits |= ((m & 1u) | ((m >> 15) & 2u)) << (2 * q);
-    }
+    return false;  // 2k >= 32768: the exact scalar path
   }
   *active = bits;
   return bad == 0;

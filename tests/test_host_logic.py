@@ -125,3 +125,45 @@ def test_log_zp_table_equals_scalar_path():
     for p in np.concatenate([[0, 1, 2, size - 1, size], rng.integers(0, size + 1, 20_000)]):
         assert tab[p] == log_zp(int(p), size)[0], p
     assert log_zp_table(27) is None
+
+
+def _swar_active(vals, act, B, kp, lane_bits):
+    """Python restatement of active_bits_simd's guard-bit SWAR (csrc/vate_pool.cu)."""
+    n = 32 // lane_bits
+    mask32 = 0xFFFFFFFF
+    rep = sum(1 << (lane_bits * i) for i in range(n))
+    H = (1 << (lane_bits - 1)) * rep
+    lo = act - kp + 1
+    L = (lo if lo >= 0 else lo + B) * rep
+    AH = (act * rep) | H
+    Bx, Bp1 = B * rep, (B + 1) * rep
+    out, bad = [], 0
+    for w in range(0, len(vals), n):
+        x = sum(int(v) << (lane_bits * i) for i, v in enumerate(vals[w:w + n]))
+        xh = x | H
+        bad |= (x & H) | (((xh - Bp1) & mask32) & H)
+        ge_lo = ((xh - L) & mask32) & H
+        le_act = ((AH - x) & mask32) & H
+        m = (ge_lo & le_act) if lo >= 0 else (le_act | (ge_lo & ~(((xh - Bx) & mask32) & H)))
+        out += [bool((m >> (lane_bits * i + lane_bits - 1)) & 1) for i in range(n)]
+    return out, bad == 0
+
+
+@pytest.mark.parametrize("lane_bits,bmax", [(8, 127), (16, 700)])
+def test_swar_predicate_matches_scalar(lane_bits, bmax):
+    rng = np.random.default_rng(lane_bits)
+    for _ in range(300):
+        k = int(rng.integers(1, bmax // 2 + 1))
+        B = 2 * k
+        if B >= (1 << (lane_bits - 1)):
+            continue
+        act = int(rng.integers(0, B))
+        kp = int(rng.integers(1, k + 1))
+        vals = rng.integers(0, B + 1, 64)        # valid stored values incl. the sentinel
+        got, ok = _swar_active(vals.tolist(), act, B, kp, lane_bits)
+        assert ok
+        want = [(v != B) and ((act - v) % B) < kp for v in vals.tolist()]
+        assert got == want, (B, act, kp)
+        bad_vals = vals.copy()
+        bad_vals[3] = B + 1 + int(rng.integers(0, (1 << lane_bits) - B - 1))
+        assert not _swar_active(bad_vals.tolist(), act, B, kp, lane_bits)[1]
