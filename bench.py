@@ -446,7 +446,8 @@ def run_gpu(args, rank, world, local_rank):
         "g0_kernel": args.g0_kernel,
         "incremental": {"enabled": args.incremental == "on",
                         **{k: inc1[k] - inc0[k] for k in ("rebuilds", "delta_slices",
-                                                          "refresh_slices", "full_slices")},
+                                                          "refresh_slices", "full_slices",
+                                                          "extends")},
                         "last_delta_cells": inc1["last_delta_cells"],
                         "last_delta_work": inc1["last_delta_work"],
                         "identity_slices": inc1["identity_slices"] - inc0["identity_slices"],

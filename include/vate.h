@@ -77,8 +77,9 @@ enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 
 int vate_pool_set_option(vate_pool* p, int option, int64_t value);
 /* incremental-estimate counters: [rebuilds, delta slices, refresh slices, full
  * slices, last delta cells, last delta work, identity slices, hosts indexed,
- * total index-rebuild time in microseconds, misses gathered since the rebuild] */
-int vate_pool_inc_stats(vate_pool* p, uint64_t out[10]);
+ * total index-rebuild time in microseconds, misses gathered since the rebuild,
+ * extensions (previous misses merged into the index)] */
+int vate_pool_inc_stats(vate_pool* p, uint64_t out[11]);
 
 /* cudaProfilerStart/Stop, so `ncu --profile-from-start off` captures exactly a
  * timed region (bench.py with VATE_PROFILE_REGION=1). */

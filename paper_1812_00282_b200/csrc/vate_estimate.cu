@@ -570,12 +570,14 @@ static int begin_complete(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t 
     I.lookup_pending = false;
     I.last_misses = p->h_ctr[C_MISS];
     I.miss_accum += I.last_misses;
-    // rebuild when misses are a large share now, or (ski rental) once the
-    // gathers spent on misses since the last rebuild match a rebuild's cost:
-    // a rebuild measures ~20 full recomputes (count + fill passes over m*g
-    // pairs with atomics, profiles/), so the break-even is 16-24 x m misses
-    if (I.valid && I.last_n && (I.last_misses * 20 > I.last_n || I.miss_accum >= 16 * I.m))
-      I.want_rebuild = true;
+    I.extend_accum += I.last_misses;
+    // Policy (ski rental on measured costs, profiles/): the captured misses of
+    // the last lookup join X by a streaming CSR merge (~8 B per index entry)
+    // once the misses gathered since the last merge reach 1/4 of |X|
+    // (a miss costs g sector gathers, 32 B each); X is rebuilt from scratch only
+    // when most of the active set is new or X has gone stale (> 2x active).
+    if (I.valid && I.last_n && I.last_misses * 2 > I.last_n) I.want_rebuild = true;
+    else if (I.valid && I.last_misses && I.extend_accum * 4 >= I.m) I.want_extend = true;
     if (I.valid && I.last_misses == 0 && I.m == I.last_n) {  // that active list == X
       I.identity_ok = true;
       I.identity_version = I.lookup_version;

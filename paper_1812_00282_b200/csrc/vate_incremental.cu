@@ -18,6 +18,7 @@
 // touches more than 1/4 of a full recompute, g0x is refreshed by one full
 // gather over X instead; X is rebuilt from the active set when misses exceed
 // 5% or X grows past twice the active set.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <string>
@@ -106,6 +107,90 @@ __global__ void k_inc_lookup(const uint64_t* __restrict__ A, uint64_t n,
   }
 }
 
+// The hosts a lookup missed (positions in A) and their just-gathered g0, kept
+// so the next slice can merge them into X (their g0 matches bprev).
+__global__ void k_inc_capture(const uint64_t* __restrict__ A, const uint32_t* __restrict__ miss,
+                              const unsigned long long* nmiss, uint64_t cap,
+                              const int32_t* __restrict__ g0, uint64_t* __restrict__ yk,
+                              int32_t* __restrict__ yg) {
+  const uint64_t n = umin64(*nmiss, cap);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += stride) {
+    const uint32_t i = miss[j];
+    yk[j] = A[i];
+    yg[j] = g0[i];
+  }
+}
+
+__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* __restrict__ v, uint64_t n,
+                                                    uint64_t key) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (v[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Merge positions of X (m, sorted) and Y (y, sorted, disjoint from X) in X u Y.
+__global__ void k_ext_positions(const uint64_t* __restrict__ X, uint64_t m,
+                                const int32_t* __restrict__ g0x, const uint64_t* __restrict__ Ys,
+                                uint64_t y, const int32_t* __restrict__ Yg0s,
+                                uint32_t* __restrict__ remapX, uint32_t* __restrict__ posY,
+                                uint64_t* __restrict__ Xn, int32_t* __restrict__ g0xn) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m + y; i += stride) {
+    if (i < m) {
+      const uint64_t a = X[i];
+      const uint64_t p = i + lower_bound_u64(Ys, y, a);
+      remapX[i] = (uint32_t)p;
+      Xn[p] = a;
+      g0xn[p] = g0x[i];
+    } else {
+      const uint64_t j = i - m, b = Ys[j];
+      const uint64_t p = j + lower_bound_u64(X, m, b);
+      posY[j] = (uint32_t)p;
+      Xn[p] = b;
+      g0xn[p] = Yg0s[j];
+    }
+  }
+}
+
+__global__ void k_ext_offsets(const uint32_t* __restrict__ offX, const uint32_t* __restrict__ offY,
+                              uint64_t n, uint32_t* __restrict__ off2) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < n; c += stride)
+    off2[c] = offX[c] + offY[c];
+}
+
+// X's entries into the merged CSR (renumbered), one warp per run of cells.
+__global__ void k_ext_copy(const uint32_t* __restrict__ offX, const uint32_t* __restrict__ entX,
+                           const uint32_t* __restrict__ off2, const uint32_t* __restrict__ remapX,
+                           uint64_t ncells, uint32_t* __restrict__ ent2) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; c < ncells; c += warps) {
+    const uint32_t a = offX[c], b = offX[c + 1], d = off2[c];
+    for (uint32_t e = a + lane; e < b; e += 32) ent2[d + (e - a)] = remapX[entX[e]];
+  }
+}
+
+// Y's (host, slot) pairs after X's entries of each cell.
+__global__ void k_ext_fill_y(const uint64_t* __restrict__ Ys, uint64_t total, DivU64 dg,
+                             HashParams H, const uint32_t* __restrict__ offX,
+                             const uint32_t* __restrict__ off2, const uint32_t* __restrict__ posY,
+                             uint32_t* __restrict__ cursor, uint32_t* __restrict__ ent2) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+    uint64_t j;
+    const uint64_t h = div_u64(i, dg, &j);
+    const uint64_t cell = mix64(host_base(Ys[h], H) + j * kPhi) & H.cmask;
+    const uint32_t at = off2[cell] + (offX[cell + 1] - offX[cell]) + atomicAdd(cursor + cell, 1u);
+    ent2[at] = posY[h];
+  }
+}
+
 void inc_release(vate_pool* p) {
   IncIndex& I = p->inc;
   for (cudaEvent_t& e : I.ev_rb)
@@ -113,7 +198,9 @@ void inc_release(vate_pool* p) {
       cudaEventDestroy(e);
       e = nullptr;
     }
-  for (DevBuf* b : {&I.X, &I.g0x, &I.off, &I.ent, &I.cursor, &I.bprev, &I.dlist, &I.miss, &I.scan_tmp})
+  for (DevBuf* b : {&I.X, &I.g0x, &I.off, &I.ent, &I.cursor, &I.bprev, &I.dlist, &I.miss, &I.scan_tmp,
+                    &I.Ykeys, &I.Yg0, &I.Ys, &I.Yg0s, &I.remap, &I.posY, &I.Xn, &I.g0xn, &I.off2,
+                    &I.offY, &I.ent2, &I.sort_tmp})
     b->release();
   I.valid = false;
   I.m = 0;
@@ -187,6 +274,8 @@ static int inc_rebuild(vate_pool* p, const uint64_t* hosts, uint64_t n, HashPara
   VATE_CUDA(cudaEventRecord(I.ev_rb[1], p->stream));
   I.rb_timing = true;
   I.miss_accum = 0;
+  I.extend_accum = 0;
+  I.want_extend = false;
   I.m = n;
   I.g = H.g;
   I.cs = H.cs;
@@ -196,6 +285,66 @@ static int inc_rebuild(vate_pool* p, const uint64_t* hosts, uint64_t n, HashPara
   I.rebuilds++;
   I.identity_ok = true;  // X is exactly this active list
   I.identity_version = p->sorted_version;
+  return VATE_OK;
+}
+
+// Merge the y hosts captured by the previous lookup (Ykeys/Yg0, valid for
+// bprev) into X: sorted union, renumbered CSR with their (host, slot) pairs.
+// One streaming pass over the index (~8 B per entry) instead of a rebuild.
+static int inc_extend(vate_pool* p, uint64_t y, HashParams H) {
+  IncIndex& I = p->inc;
+  const uint64_t m = I.m, S = p->L.size, mn = m + y, total_new = mn * H.g;
+  if (y == 0 || total_new >= (1ull << 32)) return VATE_OK;
+  int rc;
+  if ((rc = I.Ys.ensure(y * 8 + 8)) || (rc = I.Yg0s.ensure(y * 4 + 4)) ||
+      (rc = I.remap.ensure(m * 4 + 4)) || (rc = I.posY.ensure(y * 4 + 4)) ||
+      (rc = I.Xn.ensure(mn * 8 + 8)) || (rc = I.g0xn.ensure(mn * 4 + 4)) ||
+      (rc = I.off2.ensure((S + 2) * 4)) || (rc = I.offY.ensure((S + 2) * 4)) ||
+      (rc = I.ent2.ensure(total_new * 4 + 4)) || (rc = I.miss.ensure(mn * 4 + 4)))
+    return rc;
+  size_t tmp = 0;
+  VATE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, I.Ykeys.as<const unsigned long long>(),
+                                            I.Ys.as<unsigned long long>(), I.Yg0.as<const int32_t>(),
+                                            I.Yg0s.as<int32_t>(), (int64_t)y, 0, 64, p->stream));
+  if ((rc = I.sort_tmp.ensure(tmp + 256))) return rc;
+  VATE_CUDA(cub::DeviceRadixSort::SortPairs(I.sort_tmp.ptr, tmp, I.Ykeys.as<const unsigned long long>(),
+                                            I.Ys.as<unsigned long long>(), I.Yg0.as<const int32_t>(),
+                                            I.Yg0s.as<int32_t>(), (int64_t)y, 0, 64, p->stream));
+  p->launches += 9;
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(mn, kThreads, 148u * 32u), kThreads, 0, k_ext_positions,
+              I.X.as<const uint64_t>(), m, I.g0x.as<const int32_t>(), I.Ys.as<const uint64_t>(), y,
+              I.Yg0s.as<const int32_t>(), I.remap.as<uint32_t>(), I.posY.as<uint32_t>(),
+              I.Xn.as<uint64_t>(), I.g0xn.as<int32_t>());
+  // Y's CSR offsets: count, scan; merged offsets = X's + Y's
+  const DivU64 dg = make_div(H.g);
+  VATE_CUDA(cudaMemsetAsync(I.cursor.ptr, 0, (S + 1) * 4, p->stream));
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(y * H.g, kThreads, 148u * 32u), kThreads, 0, k_inc_count,
+              I.Ys.as<const uint64_t>(), y * H.g, dg, H, I.cursor.as<uint32_t>());
+  tmp = 0;
+  VATE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, I.cursor.as<uint32_t>(), I.offY.as<uint32_t>(),
+                                          (int64_t)(S + 1), p->stream));
+  if ((rc = I.scan_tmp.ensure(tmp + 256))) return rc;
+  VATE_CUDA(cub::DeviceScan::ExclusiveSum(I.scan_tmp.ptr, tmp, I.cursor.as<uint32_t>(),
+                                          I.offY.as<uint32_t>(), (int64_t)(S + 1), p->stream));
+  p->launches += 2;
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(S + 1, kThreads, 148u * 32u), kThreads, 0, k_ext_offsets,
+              I.off.as<const uint32_t>(), I.offY.as<const uint32_t>(), S + 1, I.off2.as<uint32_t>());
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(S * 32, kThreads, 148u * 32u), kThreads, 0, k_ext_copy,
+              I.off.as<const uint32_t>(), I.ent.as<const uint32_t>(), I.off2.as<const uint32_t>(),
+              I.remap.as<const uint32_t>(), S, I.ent2.as<uint32_t>());
+  VATE_CUDA(cudaMemsetAsync(I.cursor.ptr, 0, (S + 1) * 4, p->stream));
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(y * H.g, kThreads, 148u * 32u), kThreads, 0, k_ext_fill_y,
+              I.Ys.as<const uint64_t>(), y * H.g, dg, H, I.off.as<const uint32_t>(),
+              I.off2.as<const uint32_t>(), I.posY.as<const uint32_t>(), I.cursor.as<uint32_t>(),
+              I.ent2.as<uint32_t>());
+  swap_buf(I.X, I.Xn);
+  swap_buf(I.g0x, I.g0xn);
+  swap_buf(I.off, I.off2);
+  swap_buf(I.ent, I.ent2);
+  I.m = mn;
+  I.identity_ok = false;
+  I.extend_accum = 0;
+  I.extends++;
   return VATE_OK;
 }
 
@@ -210,6 +359,10 @@ int inc_compute_g0(vate_pool* p, const uint64_t* hosts, uint64_t n, HashParams H
   I.req_kp = kp;
   if (I.delta_launched) {
     I.delta_launched = false;
+    if (I.want_extend) {  // last slice's misses join X before this slice's delta
+      I.want_extend = false;
+      if ((rc = inc_extend(p, I.last_misses, H))) return rc;
+    }
     const uint64_t dcells = p->h_ctr[C_DCNT], dwork = p->h_ctr[C_DWORK];
     I.last_delta_cells = dcells;
     I.last_delta_work = dwork;
@@ -237,6 +390,10 @@ int inc_compute_g0(vate_pool* p, const uint64_t* hosts, uint64_t n, HashParams H
       if ((rc = launch_g0_list(p, hosts, I.miss.as<const uint32_t>(), p->d_ctr + C_MISS, n, H,
                                p->g0.as<int32_t>())))
         return rc;
+      if ((rc = I.Ykeys.ensure(n * 8 + 8)) || (rc = I.Yg0.ensure(n * 4 + 4))) return rc;
+      VATE_LAUNCH(p, VATE_K_G0, grid_for(umin64(n, 1u << 16), kThreads, 148u * 8u), kThreads, 0,
+                  k_inc_capture, hosts, I.miss.as<const uint32_t>(), p->d_ctr + C_MISS, n,
+                  p->g0.as<const int32_t>(), I.Ykeys.as<uint64_t>(), I.Yg0.as<int32_t>());
       VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_MISS, p->d_ctr + C_MISS, 8, cudaMemcpyDeviceToHost,
                                 p->stream));
       I.lookup_pending = true;

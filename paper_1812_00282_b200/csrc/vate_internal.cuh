@@ -173,6 +173,10 @@ struct IncIndex {
   int kp = 0;
   uint64_t m = 0;                         // hosts in X
   DevBuf X, g0x, off, ent, cursor, bprev, dlist, miss, scan_tmp;
+  // extension (merge the previous slice's misses into X): staging + double buffers
+  DevBuf Ykeys, Yg0, Ys, Yg0s, remap, posY, Xn, g0xn, off2, offY, ent2, sort_tmp;
+  uint64_t extends = 0, extend_accum = 0;
+  bool want_extend = false;
   uint64_t dlist_cap = 0;
   bool delta_launched = false;
   bool want_rebuild = false;

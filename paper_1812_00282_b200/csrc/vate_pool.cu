@@ -893,7 +893,7 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
   return set_error(VATE_EVALUE, "unknown option or value");
 }
 
-int vate_pool_inc_stats(vate_pool* p, uint64_t out[10]) {
+int vate_pool_inc_stats(vate_pool* p, uint64_t out[11]) {
   int rc = enter(p);
   if (rc) return rc;
   IncIndex& I = p->inc;
@@ -904,10 +904,11 @@ int vate_pool_inc_stats(vate_pool* p, uint64_t out[10]) {
     I.rebuild_ms += ms;
     I.rb_timing = false;
   }
-  const uint64_t v[10] = {I.rebuilds, I.delta_slices, I.refresh_slices, I.full_slices,
+  const uint64_t v[11] = {I.rebuilds, I.delta_slices, I.refresh_slices, I.full_slices,
                           I.last_delta_cells, I.last_delta_work, I.identity_slices,
-                          I.valid ? I.m : 0, (uint64_t)(I.rebuild_ms * 1000.0), I.miss_accum};
-  for (int i = 0; i < 10; ++i) out[i] = v[i];
+                          I.valid ? I.m : 0, (uint64_t)(I.rebuild_ms * 1000.0), I.miss_accum,
+                          I.extends};
+  for (int i = 0; i < 11; ++i) out[i] = v[i];
   return VATE_OK;
 }
 

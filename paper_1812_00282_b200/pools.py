@@ -305,11 +305,11 @@ class AtPool(BlockLayout):
 
     def inc_stats(self) -> dict:
         """Counters of the incremental estimate."""
-        out = (C.c_uint64 * 10)()
+        out = (C.c_uint64 * 11)()
         check(lib.vate_pool_inc_stats(self._h, out))
         keys = ("rebuilds", "delta_slices", "refresh_slices", "full_slices",
                 "last_delta_cells", "last_delta_work", "identity_slices", "hosts_indexed",
-                "rebuild_us_total", "miss_accum")
+                "rebuild_us_total", "miss_accum", "extends")
         return dict(zip(keys, list(out)))
 
     def set_timing(self, on: bool) -> None:

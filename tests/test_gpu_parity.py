@@ -679,3 +679,27 @@ def test_step_fast_device_resident_reports():
                                  ctypes.c_size_t(m * 8), 2) == 0
         assert np.array_equal(est, want.estimate), t
         assert np.array_equal(host, want.host), t
+
+
+def test_incremental_extend_merges_new_hosts():
+    """A steady population plus a trickle of new hosts: the misses are merged
+    into the index (streaming CSR merge), after which the active list is X
+    again (identity path) -- every slice oracle-exact."""
+    cfg = vb.EstimatorConfig(256, 16, 20, seed=13)
+    ocfg = vo.OracleConfig(256, 16, 20, seed=13)
+    pool = cfg.build_pool()
+    pipe = vb.Pipeline(pool, cfg, 20)
+    opipe = vo.OraclePipeline(ocfg, 20)
+    rng = np.random.default_rng(6)
+    base = np.repeat(np.arange(1000, dtype=np.uint64), 3)
+    for t in range(60):
+        new = np.arange(1000 + 10 * t, 1010 + 10 * t, dtype=np.uint64) if t < 40 else \\
+            np.empty(0, dtype=np.uint64)
+        a = np.concatenate([base, new])
+        b = (rng.integers(0, 8, a.size).astype(np.uint64) + (a << np.uint64(3)))
+        got, _ = pipe.process_slice_soa(t, a, b)
+        want = opipe.process_slice(t, a, b)
+        assert np.array_equal(got.host, want.reports.host), t
+        assert np.array_equal(got.estimate, want.reports.estimate), t
+    st = pool.inc_stats()
+    assert st["extends"] >= 2 and st["rebuilds"] == 1 and st["identity_slices"] >= 5, st
