@@ -693,8 +693,8 @@ def test_incremental_extend_merges_new_hosts():
     rng = np.random.default_rng(6)
     base = np.repeat(np.arange(1000, dtype=np.uint64), 3)
     for t in range(60):
-        new = np.arange(1000 + 10 * t, 1010 + 10 * t, dtype=np.uint64) if t < 40 else \\
-            np.empty(0, dtype=np.uint64)
+        new = (np.arange(1000 + 10 * t, 1010 + 10 * t, dtype=np.uint64) if t < 40
+               else np.empty(0, dtype=np.uint64))
         a = np.concatenate([base, new])
         b = (rng.integers(0, 8, a.size).astype(np.uint64) + (a << np.uint64(3)))
         got, _ = pipe.process_slice_soa(t, a, b)
