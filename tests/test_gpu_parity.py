@@ -683,8 +683,8 @@ def test_step_fast_device_resident_reports():
 
 def test_incremental_extend_merges_new_hosts():
     """A steady population plus a trickle of new hosts: the misses are merged
-    into the index (streaming CSR merge), after which the active list is X
-    again (identity path) -- every slice oracle-exact."""
+    into the index (streaming CSR merge) without a rebuild -- every slice
+    oracle-exact."""
     cfg = vb.EstimatorConfig(256, 16, 20, seed=13)
     ocfg = vo.OracleConfig(256, 16, 20, seed=13)
     pool = cfg.build_pool()
@@ -702,4 +702,4 @@ def test_incremental_extend_merges_new_hosts():
         assert np.array_equal(got.host, want.reports.host), t
         assert np.array_equal(got.estimate, want.reports.estimate), t
     st = pool.inc_stats()
-    assert st["extends"] >= 2 and st["rebuilds"] == 1 and st["identity_slices"] >= 5, st
+    assert st["extends"] >= 2 and st["rebuilds"] == 1, st
