@@ -424,17 +424,26 @@ struct DeltaOut {
   unsigned long long* work;
 };
 
-// Exact scalar predicate for a word that crosses a block boundary, ends the
-// pool, or holds a stored value above 2k; kept out of line so the SIMD fast
-// path stays small in the instruction cache.
 template <typename T>
-__device__ __noinline__ uint32_t word_bits_slow(const T* __restrict__ cells, uint64_t i0,
-                                                uint32_t cnt, Layout L, uint32_t bact0,
-                                                uint32_t kp) {
+__device__ __forceinline__ uint32_t word_inactive_bits(const T* __restrict__ cells,
+                                                       const uint4 (&r)[(int)sizeof(T) * 2],
+                                                       uint64_t i0, uint32_t cnt, const Layout& L,
+                                                       uint32_t bact0, uint32_t kp) {
   uint32_t b = block_of(i0, L);
   uint64_t next = block_start(b + 1, L);
   uint32_t act = clock_of(bact0, b, L.B);
-  uint32_t bits = 0;
+  if (cnt == 32 && i0 + 32 <= next) {  // the whole word in one block: one clock
+    if (sizeof(T) <= 2) {
+      uint32_t active;
+      if (active_bits_simd<T>(r, act, L.B, kp, &active)) return ~active;
+    }
+    const T* e = reinterpret_cast<const T*>(r);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) bits |= (uint32_t)is_inactive(e[j], act, L.B, kp) << j;
+    return bits;
+  }
+  uint32_t bits = 0;  // block boundary (or pool end) inside the word
   for (uint32_t j = 0; j < cnt; ++j) {
     while (i0 + j >= next) {
       ++b;
@@ -444,19 +453,6 @@ __device__ __noinline__ uint32_t word_bits_slow(const T* __restrict__ cells, uin
     bits |= (uint32_t)is_inactive(cells[i0 + j], act, L.B, kp) << j;
   }
   return bits;
-}
-
-template <typename T>
-__device__ __forceinline__ uint32_t word_inactive_bits(const T* __restrict__ cells,
-                                                       const uint4 (&r)[(int)sizeof(T) * 2],
-                                                       uint64_t i0, uint32_t cnt, const Layout& L,
-                                                       uint32_t bact0, uint32_t kp) {
-  const uint32_t b = block_of(i0, L);
-  if (cnt == 32 && i0 + 32 <= block_start(b + 1, L) && sizeof(T) <= 2) {  // one clock
-    uint32_t active;
-    if (active_bits_simd<T>(r, clock_of(bact0, b, L.B), L.B, kp, &active)) return ~active;
-  }
-  return word_bits_slow<T>(cells, i0, cnt, L, bact0, kp);
 }
 
 // kW words per thread per iteration: all their 16-byte loads are issued before
