@@ -881,7 +881,7 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_g0 = (int)value;
     return VATE_OK;
   }
-  if (option == VATE_OPT_SCAN_V && (value == 2 || value == 4)) {
+  if (option == VATE_OPT_SCAN_V && (value == 1 || value == 2 || value == 4)) {
     p->opt_scan_v = (int)value;
     return VATE_OK;
   }
@@ -973,7 +973,8 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     if (rc) return rc;
     R = hosts->ref();
   }
-  const uint32_t grid = grid_for(n, kThreads, 148u * 16u);
+  const uint32_t grid = p->opt_scan_v == 1 ? grid_for((n + 1) / 2, kThreads, 148u * 64u)
+                                           : grid_for(n, kThreads, 148u * 16u);
   if (pairs) {
     const void* d_pairs;
     rc = stage_in(p, p->in_a, pairs, n * 8, where, &d_pairs);
@@ -982,7 +983,11 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     return with_cell(p->cell_bytes, [&](auto tag) -> int {
       using T = decltype(tag);
       if (aligned16 && n >= 2) {
-        if (hosts && p->opt_scan_v == 4)
+        if (hosts && p->opt_scan_v == 1)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 1>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
+                      (long long)t);
+        else if (hosts && p->opt_scan_v == 4)
           VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 4>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
                       (long long)t);

@@ -14,7 +14,7 @@ for i in range(12):
     check(lib.vate_synth_packets(pool.handle, i, n, 1_000_000, 0x0A000000, 0, bufs[i].data_ptr()))
 for t in range(12):   # fill the registry
     pipe.step_packed(t, bufs[t].data_ptr(), n, True)
-for v in (2, 4, 2, 4):
+for v in (2, 1, 4, 2, 1):
     pool.set_option("scan_v", v)
     pool.set_timing(False); pool.set_timing(True)
     for rep in range(3):
