@@ -95,6 +95,9 @@ _SIGS = {
     "vate_hosts_size": ([_p, _pu64], _int),
     "vate_dirty_bitmap": ([_p, _p], _int),
     "vate_merge_dirty": ([_p, _p, _int], _int),
+    "vate_trace_bucket": ([_p, _p, _u64, _int, _u64, _i64, _u64, _int, _p, _u64, _u64, _p,
+                           C.POINTER(_i64)], _int),
+    "vate_copy_device": ([_p, _p, _p, _u64], _int),
     "vate_synth_packets": ([_p, _i64, _u64, _u64, _u64, _u64, _p], _int),
 }
 

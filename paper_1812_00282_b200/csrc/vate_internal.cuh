@@ -303,7 +303,7 @@ uint32_t grid_for(uint64_t work, uint32_t per_block, uint32_t cap_blocks = 148u 
 
 // counters in vate_pool::d_ctr
 enum Ctr { C_P = 0, C_CLEARED = 1, C_NSEL = 2, C_ERR = 3, C_DCNT = 4, C_DWORK = 5, C_MISS = 6,
-           C_N = 8 };
+           C_TRACE = 7, C_N = 8 };
 
 // estimate helpers (vate_estimate.cu / vate_incremental.cu)
 int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H, int32_t* g0_dev);

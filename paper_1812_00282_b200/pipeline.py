@@ -313,6 +313,20 @@ class Pipeline:
                            rep.cells_maintained, rep.cells_cleared)
         return reports, stats
 
+    def process_packed(self, t: int, pairs_dev: int, n: int):
+        """All three phases for a slice of packed {u32 aip, u32 bip} records already
+        on the device (e.g. from traceio.DeviceSlices); (HostReports | None, SliceStats)."""
+        t0 = time.perf_counter_ns()
+        if n:
+            self.scan_packed(t, pairs_dev, n, True)
+        t1 = time.perf_counter_ns()
+        reports = self.estimate_soa(t)
+        t2 = time.perf_counter_ns()
+        rep = self._maintain(t)
+        t3 = time.perf_counter_ns()
+        return reports, SliceStats(t, n, (t1 - t0) // 1000, (t2 - t1) // 1000,
+                                   (t3 - t2) // 1000, rep.cells_maintained, rep.cells_cleared)
+
     def process_slice(self, t: int, aips, bips):
         """Run all three phases for slice t; returns (reports, stats) (pipeline.py:142-160)."""
         soa, stats = self.process_slice_soa(t, aips, bips)

@@ -231,6 +231,53 @@ def snapshot_blob():
                         count9=pool.count_inactive(9))
 
 
+def cli_goldens():
+    """The reference CLI on a small generated trace: the trace files and the
+    byte-exact CSV that `slidecard estimate` writes (cli.py:102-126)."""
+    import contextlib
+    import io
+    import tempfile
+
+    from slidecard import cli
+    d = tempfile.mkdtemp()
+    trace_txt, truth = os.path.join(d, "t.csv"), os.path.join(d, "truth.csv")
+    assert cli.main(["gen", "--out", trace_txt, "--truth", truth, "--hosts", "40",
+                     "--n-min", "20", "--n-max", "400", "--k-prime", "6", "--seed", "1"]) == 0
+    trace_bin = os.path.join(d, "t.bin")
+    assert cli.main(["gen", "--out", trace_bin, "--truth", truth, "--hosts", "40",
+                     "--n-min", "20", "--n-max", "400", "--k-prime", "6", "--seed", "1",
+                     "--format", "binary"]) == 0
+    out = {}
+    runs = {
+        "est_floor0": ["estimate", "--trace", trace_bin, "--format", "binary", "--c", "14",
+                       "--g", "256", "--k", "6", "--floor", "0", "--workers", "1"],
+        "est_default": ["estimate", "--trace", trace_txt, "--c", "16", "--g", "256", "--k", "8",
+                        "--k-prime", "5", "--workers", "1"],
+        "est_lowdev": ["estimate", "--trace", trace_bin, "--format", "binary", "--c", "12",
+                       "--g", "128", "--k", "6", "--partition", "low-dev", "--floor", "10",
+                       "--seed", "9", "--slice-us", "500000", "--workers", "1"],
+    }
+    for name, argv in runs.items():
+        path = os.path.join(d, name + ".csv")
+        assert cli.main(argv + ["--out", path]) == 0
+        out[name] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    ckpt = os.path.join(d, "pool.atp1")
+    assert cli.main(runs["est_floor0"] + ["--out", os.path.join(d, "x.csv"),
+                                          "--checkpoint", ckpt]) == 0
+    out["checkpoint"] = np.frombuffer(open(ckpt, "rb").read(), dtype=np.uint8)
+    bench = os.path.join(d, "bench.csv")
+    with contextlib.redirect_stderr(io.StringIO()):
+        assert cli.main(["bench", "--trace", trace_bin, "--format", "binary", "--c", "14",
+                         "--g", "256", "--k", "6", "--floor", "0", "--workers", "1",
+                         "--out", bench]) == 0
+    out["bench_cols"] = np.array([[int(x) for x in (line.split(",")[0], line.split(",")[4],
+                                                     line.split(",")[5])]
+                                  for line in open(bench).read().splitlines()[1:]])
+    out["trace_bin"] = np.frombuffer(open(trace_bin, "rb").read(), dtype=np.uint8)
+    out["trace_txt"] = np.frombuffer(open(trace_txt, "rb").read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "cli.npz"), **out)
+
+
 if __name__ == "__main__":
     hash_kats()
     layouts()
@@ -238,4 +285,5 @@ if __name__ == "__main__":
     snapshot_blob()
     appendix_b()
     pipelines()
+    cli_goldens()
     print("numpy", np.__version__)
