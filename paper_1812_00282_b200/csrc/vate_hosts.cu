@@ -167,13 +167,61 @@ __global__ void __launch_bounds__(256) k_active_keys(const RegEntry* __restrict_
   }
 }
 
-// Entries with last > horizon, appended (prune keeps them).
-__global__ void k_keep(const RegEntry* __restrict__ table, uint64_t cap, long long horizon,
-                       RegEntry* __restrict__ out, unsigned long long* nout) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap; i += stride) {
-    const RegEntry e = table[i];
-    if (e.key != kEmptyKey && e.last > horizon) out[atomicAdd(nout, 1ull)] = e;
+// Entries with last > horizon (prune keeps them), appended with one
+// reservation per 1024-slot tile; count_only just counts the expired ones.
+__global__ void __launch_bounds__(256) k_keep(const RegEntry* __restrict__ table, uint64_t cap,
+                                              long long horizon, RegEntry* __restrict__ out,
+                                              unsigned long long* nout, int count_only) {
+  __shared__ unsigned warp_tot[8];
+  __shared__ unsigned long long base_s;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned expired = 0;
+  for (uint64_t tile = (uint64_t)blockIdx.x * kActTile; tile < cap;
+       tile += (uint64_t)gridDim.x * kActTile) {
+    const uint64_t i0 = tile + threadIdx.x * 4;
+    RegEntry e[4];
+    unsigned take = 0, mine = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = i0 + q;
+      if (i < cap) {
+        e[q] = table[i];
+        if (e[q].key != kEmptyKey) {
+          if (e[q].last > horizon) {
+            take |= 1u << q;
+            ++mine;
+          } else {
+            ++expired;
+          }
+        }
+      }
+    }
+    if (count_only) continue;
+    unsigned incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned tot = 0;
+      for (int w = 0; w < 8; ++w) tot += warp_tot[w];
+      base_s = tot ? atomicAdd(nout, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    unsigned before = 0;
+    for (int w = 0; w < wid; ++w) before += warp_tot[w];
+    unsigned long long pos = base_s + before + incl - mine;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if ((take >> q) & 1u) out[pos++] = e[q];
+    __syncthreads();
+  }
+  if (count_only) {
+    expired = __reduce_add_sync(0xffffffffu, expired);
+    if (lane == 0 && expired) atomicAdd(nout, (unsigned long long)expired);
   }
 }
 
@@ -477,24 +525,34 @@ int vate_hosts_prune(vate_hosts* h, int64_t t) {
   rc = hosts_drain(h);
   if (rc) return rc;
   const long long horizon = (long long)(t - h->k);
-  // keep list -> fresh table of the same capacity
-  DevBuf keep;
-  rc = keep.ensure((h->count_hint + 1) * sizeof(RegEntry));
-  if (rc) return rc;
-  VATE_CUDA(cudaMemsetAsync(h->d_count + H_NOUT, 0, 8, p->stream));
-  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap, kThreads, 148u * 16u), kThreads, 0, k_keep,
-              h->table.as<const RegEntry>(), h->cap, horizon, keep.as<RegEntry>(),
-              h->d_count + H_NOUT);
-  // special entry: keep iff present and last > horizon
-  RegEntry special_entry;
+  // count the expired first: in steady traffic nothing expires and the table
+  // stays as it is (slots, membership flags and the sorted active list intact)
   unsigned long long c[H_N];
+  VATE_CUDA(cudaMemsetAsync(h->d_count + H_NOUT, 0, 8, p->stream));
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap, kActTile, 148u * 8u), 256, 0, k_keep,
+              h->table.as<const RegEntry>(), h->cap, horizon, (RegEntry*)nullptr,
+              h->d_count + H_NOUT, 1);
+  RegEntry special_entry;
   VATE_CUDA(cudaMemcpyAsync(&special_entry, h->table.as<RegEntry>() + h->cap, sizeof(RegEntry),
                             cudaMemcpyDeviceToHost, p->stream));
   rc = hosts_read_counters(h, c);
-  if (rc) { keep.release(); return rc; }
-  const bool special = (c[H_SPECIAL] & 0xFFFFFFFFull) != 0 && special_entry.last > horizon;
+  if (rc) return rc;
+  const bool special_present = (c[H_SPECIAL] & 0xFFFFFFFFull) != 0;
+  if (c[H_NOUT] == 0 && !(special_present && special_entry.last <= horizon)) return VATE_OK;
+  // keep list -> fresh table of the same capacity
+  DevBuf& keep = h->scratch;
+  rc = keep.ensure((h->count_hint + 1) * sizeof(RegEntry));
+  if (rc) return rc;
+  VATE_CUDA(cudaMemsetAsync(h->d_count + H_NOUT, 0, 8, p->stream));
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap, kActTile, 148u * 8u), 256, 0, k_keep,
+              h->table.as<const RegEntry>(), h->cap, horizon, keep.as<RegEntry>(),
+              h->d_count + H_NOUT, 0);
+  // special entry: keep iff present and last > horizon
+  rc = hosts_read_counters(h, c);
+  if (rc) return rc;
+  const bool special = special_present && special_entry.last > horizon;
   rc = ensure_table(h->table, h->cap, p->stream);
-  if (rc) { keep.release(); return rc; }
+  if (rc) return rc;
   if (special) {
     VATE_CUDA(cudaMemcpyAsync(h->table.as<RegEntry>() + h->cap, &special_entry, sizeof(RegEntry),
                               cudaMemcpyHostToDevice, p->stream));
@@ -505,7 +563,6 @@ int vate_hosts_prune(vate_hosts* h, int64_t t) {
               k_insert_entries, keep.as<const RegEntry>(), (uint64_t)c[H_NOUT],
               (const unsigned long long*)nullptr, h->ref(), 1);
   VATE_CUDA(cudaStreamSynchronize(p->stream));
-  keep.release();
   h->member_valid = false;  // slots moved
   h->count_hint = c[H_NOUT] + (special ? 1 : 0);
   h->pending = 0;
