@@ -703,3 +703,64 @@ def test_incremental_extend_merges_new_hosts():
         assert np.array_equal(got.estimate, want.reports.estimate), t
     st = pool.inc_stats()
     assert st["extends"] >= 2 and st["rebuilds"] == 1, st
+
+
+# --- the multi-GPU merge kernels, exercised with two replicas on one device --------
+
+def test_replica_merge_and_range_split_equal_one_pool():
+    """Two replica pools (the N=2 protocol of paper_1812_00282_b200.parallel, with
+    the NCCL all-gather replaced by a device concatenation): dirty bitmaps OR'ed
+    into both replicas reproduce the single pool's ATP1 bytes every slice, and the
+    aip-range-split estimate (vate_estimate_begin_hosts) concatenates to the
+    single pipeline's reports."""
+    import ctypes as C
+
+    import torch
+    from paper_1812_00282_b200._lib import check, lib, ptr
+    from paper_1812_00282_b200.estimator import log_zp
+    from paper_1812_00282_b200.parallel import split_range, union_sorted
+
+    cfg = vb.EstimatorConfig(256, 16, 8, seed=21)
+    single = vb.Pipeline(cfg.build_pool(), cfg, 8)
+    reps = [vb.Pipeline(cfg.build_pool(), cfg, 8) for _ in range(2)]
+    nwords = (1 << 16) // 32
+    bm = torch.zeros(2 * nwords, dtype=torch.int32, device="cuda")
+    rng = np.random.default_rng(0)
+    for t in range(24):
+        a = (0x0A000000 + rng.integers(0, 2000, 30_000)).astype(np.uint64)
+        b = rng.integers(1, 1 << 32, 30_000).astype(np.uint64)
+        want, _ = single.process_slice_soa(t, a, b)
+        for r, pipe in enumerate(reps):            # each replica scans its round-robin shard
+            pipe._t = t
+            pipe._scan(a[r::2], b[r::2])
+        torch.cuda.synchronize()
+        for r, pipe in enumerate(reps):
+            pipe.pool.synchronize()
+            check(lib.vate_dirty_bitmap(pipe.pool.handle, bm[r * nwords:].data_ptr()))
+            pipe.pool.synchronize()
+        for pipe in reps:
+            check(lib.vate_merge_dirty(pipe.pool.handle, bm.data_ptr(), 2))
+            pipe.pool.synchronize()
+        hosts = union_sorted([p.hosts.active(t, 8) for p in reps])
+        got_host, got_est = [], []
+        for r, pipe in enumerate(reps):
+            lo, hi = split_range(len(hosts), r, 2)
+            mine = np.ascontiguousarray(hosts[lo:hi])
+            p_in = C.c_uint64()
+            check(lib.vate_estimate_begin_hosts(pipe.pool.handle, ptr(mine), mine.size, 0, cfg.g,
+                                                cfg.cell_stream, 8, C.byref(p_in)))
+            assert p_in.value == single.last_pool_inactive, t
+            if mine.size:
+                out = (np.empty(mine.size, np.uint64), np.empty(mine.size, np.float64),
+                       np.empty(mine.size, np.float64), np.empty(mine.size, np.uint8))
+                kept = C.c_uint64()
+                check(lib.vate_estimate_finish(pipe.pool.handle, cfg.g, p_in.value,
+                                               log_zp(p_in.value, 1 << 16)[0], 0.0,
+                                               *(ptr(x) for x in out), mine.size, C.byref(kept)))
+                got_host.append(out[0][:kept.value])
+                got_est.append(out[1][:kept.value])
+        assert np.array_equal(np.concatenate(got_host), want.host), t
+        assert np.array_equal(np.concatenate(got_est), want.estimate), t
+        for pipe in reps:
+            pipe._maintain(t)
+            assert pipe.pool.snapshot_bytes() == single.pool.snapshot_bytes(), t
