@@ -51,6 +51,11 @@ WORKLOADS = {
     "cfg1": dict(name="cfg1-cpu-reference-shape", c=20, k=10, k_prime=10, g=1024,
                  hosts=10_000, packets=100_000, seed=0, partition="tail", floor=0.0,
                  base_aip=0x0A000000),
+    # configs[2]: Zipf(1.1) host popularity + 64 super-spreaders (10% of packets,
+    # random peers), pool 2^26
+    "cfg3": dict(name="cfg3-zipf-superspreaders", c=26, k=60, k_prime=60, g=1024,
+                 hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
+                 base_aip=0x0A000000, zipf=True),
     # configs[3]: long window, 512 MiB of u16 cells beyond L2
     "cfg4": dict(name="cfg4-long-window-k300", c=28, k=300, k_prime=300, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
@@ -162,8 +167,13 @@ def cpu_sample(w, seconds_budget=20.0, workers=None, sample_packets=1_000_000,
     pipe = vo.OraclePipeline(cfg, w["k_prime"], floor=w["floor"], workers=workers)
     per_step = []
     sample_packets = min(sample_packets, w["packets"])
+    tables = (vo.zipf_cdf(w["hosts"]), vo.spreader_cdf()) if w.get("zipf") else None
     for t in range(steps):
-        a, b = vo.synthetic_slice(t, sample_packets, w["hosts"], w["base_aip"])
+        if tables is not None:
+            a, b = vo.synthetic_zipf_slice(t, sample_packets, w["hosts"], *tables,
+                                           base_aip=w["base_aip"])
+        else:
+            a, b = vo.synthetic_slice(t, sample_packets, w["hosts"], w["base_aip"])
         t0 = time.perf_counter()
         pipe.scan(a, b)
         t1 = time.perf_counter()
@@ -257,17 +267,25 @@ def run_gpu(args, rank, world, local_rank):
     # regions (k_synth == oracle.synthetic_slice), 40 MB each, >> L2 in total.
     t_base = 1000 * rank
     prefill = 2 * w["k"]
+    zt = None
+    if w.get("zipf"):
+        from paper_1812_00282_b200.synth import ZipfTables
+        zt = ZipfTables(dev, w["hosts"])
+
+    def synth(t_, out_ptr):
+        if zt is not None:
+            zt.packets(pool, t_, n, w["base_aip"], w["seed"], out_ptr)
+        else:
+            check(lib.vate_synth_packets(h, t_, n, w["hosts"], w["base_aip"], w["seed"], out_ptr))
     n_dev = args.warmup + 2 * args.steps
     scratch = torch.empty((n, 2), dtype=torch.int32, device=f"cuda:{dev}")
     dslices = torch.empty((n_dev, n, 2), dtype=torch.int32, device=f"cuda:{dev}")
     for i in range(n_dev):
-        check(lib.vate_synth_packets(h, t_base + prefill + i, n, w["hosts"], w["base_aip"],
-                                     w["seed"], dslices[i].data_ptr()))
+        synth(t_base + prefill + i, dslices[i].data_ptr())
     n_host = args.warmup + args.steps
     hslices = torch.empty((n_host, n, 2), dtype=torch.int32, pin_memory=True)
     for i in range(n_host):
-        check(lib.vate_synth_packets(h, t_base + prefill + n_dev + i, n, w["hosts"], w["base_aip"],
-                                     w["seed"], scratch.data_ptr()))
+        synth(t_base + prefill + n_dev + i, scratch.data_ptr())
         pool.synchronize()
         hslices[i].copy_(scratch)
     pool.synchronize()
@@ -303,8 +321,7 @@ def run_gpu(args, rank, world, local_rank):
 
     t = 0
     for _ in range(prefill):             # fill the window: every block swept twice
-        check(lib.vate_synth_packets(h, t_base + t, n, w["hosts"], w["base_aip"], w["seed"],
-                                     scratch.data_ptr()))
+        synth(t_base + t, scratch.data_ptr())
         step(t, scratch.data_ptr(), True)
         t += 1
     di = 0

@@ -260,6 +260,13 @@ int vate_copy_device(vate_pool* p, void* dst, const void* src, uint64_t bytes);
 /* ---- synthetic traffic (bench / tests): oracle.synthetic_slice ---------- */
 int vate_synth_packets(vate_pool* p, int64_t t, uint64_t n, uint64_t hosts,
                        uint64_t base_aip, uint64_t trace_seed, uint32_t* pairs_dev);
+/* cfg 3 (oracle.synthetic_zipf_slice): Zipf host ranks from a fixed-point CDF
+ * table, plus spread_q16/65536 of packets from nspread super-spreaders with
+ * random peers (tables on the device, built by the caller). */
+int vate_synth_zipf(vate_pool* p, int64_t t, uint64_t n, uint64_t hosts, uint64_t base_aip,
+                    uint64_t trace_seed, const uint64_t* zipf_cdf_dev,
+                    const uint64_t* spread_cdf_dev, uint64_t nspread, uint32_t spread_q16,
+                    uint32_t* pairs_dev);
 
 #ifdef __cplusplus
 }

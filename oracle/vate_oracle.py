@@ -545,3 +545,58 @@ def synthetic_slice(t: int, n: int, hosts: int, base_aip: int = 0x0A000000,
 SYNTH_SALT = 0x51ED270B27C4DF1D
 SYNTH_HOST_SALT = 0xA5A5A5A5A5A5A5A5
 SYNTH_PEER_SALT = 0x3C6EF372FE94F82B
+
+
+# --- cfg 3: Zipf host popularity + super-spreaders (SURVEY.md §8(d) cfg 3) -----------
+
+ZIPF_Q = 40                            # CDF tables are fixed point with 40 fractional bits
+SPREAD_BASE = 0x0B000000
+SPREAD_BIP_SALT = 0x6A09E667F3BCC909
+SPREAD_PEER_SALT = 0xBB67AE8584CAA73B
+
+
+def zipf_cdf(hosts: int, s: float = 1.1) -> np.ndarray:
+    """Upper-bound table: rank i is drawn for u in [cdf[i-1], cdf[i])."""
+    w = 1.0 / np.arange(1, hosts + 1, dtype=np.float64) ** s
+    c = np.floor(np.cumsum(w) / w.sum() * float(1 << ZIPF_Q)).astype(np.uint64)
+    c[-1] = np.uint64(1 << ZIPF_Q)
+    return c
+
+
+def spreader_cdf(n: int = 64, seed: int = 0) -> np.ndarray:
+    """Traffic share per spreader proportional to a log-uniform cardinality in [1e4, 1e6]."""
+    u = (mix64(np.arange(n, dtype=U64) ^ U64(seed ^ 0x9E37)) >> U64(11)).astype(np.float64) / 2.0 ** 53
+    w = 10.0 ** (4.0 + 2.0 * u)
+    c = np.floor(np.cumsum(w) / w.sum() * float(1 << ZIPF_Q)).astype(np.uint64)
+    c[-1] = np.uint64(1 << ZIPF_Q)
+    return c
+
+
+def synthetic_zipf_slice(t: int, n: int, hosts: int, zcdf: np.ndarray, scdf: np.ndarray,
+                         spread_q16: int = 6554, base_aip: int = 0x0A000000, trace_seed: int = 0):
+    """Packets of slice t for cfg 3; integer-only, equal to csrc k_synth_zipf.
+
+    A packet is a spreader packet when the low 16 bits of its draw are below
+    spread_q16 (6554/65536 ~ 10%): spreader s ~ scdf, random 32-bit peer.  Else
+    a regular host rank ~ zcdf (Zipf s = 1.1) with the cfg-2 fixed peer sets.
+    """
+    stream = stream_of(trace_seed, SYNTH_SALT)
+    i = np.arange(n, dtype=U64) + U64((t & 0xFFFFFFFF) << 32)
+    with np.errstate(over="ignore"):
+        x = mix64(U64(stream) + i * U64(PHI))
+    u = x >> U64(24)
+    spread = (x & U64(0xFFFF)) < U64(spread_q16)
+    s_idx = np.searchsorted(scdf, u, side="right").astype(U64)
+    rank = np.searchsorted(zcdf, u, side="right").astype(U64)
+    r = mix64(rank ^ U64(SYNTH_HOST_SALT)) >> U64(40)
+    _, e = np.frexp(r.astype(np.float64))
+    lz = np.minimum(24 - e.astype(np.int64), 12)
+    npeers = U64(1) + (r & U64(7)) + (U64(1) << lz.astype(U64))
+    y = mix64(x ^ U64(SPREAD_PEER_SALT))
+    j = (y >> U64(32)) % npeers
+    with np.errstate(over="ignore"):
+        bip_reg = mix64((rank << U64(20)) ^ j ^ U64(SYNTH_PEER_SALT)) & U64(0xFFFFFFFF)
+    bip_spr = mix64(x ^ U64(SPREAD_BIP_SALT)) & U64(0xFFFFFFFF)
+    aip = np.where(spread, U64(SPREAD_BASE) + s_idx, (rank + U64(base_aip)) & U64(0xFFFFFFFF))
+    bip = np.where(spread, bip_spr, bip_reg)
+    return aip.astype(U64), bip.astype(U64)

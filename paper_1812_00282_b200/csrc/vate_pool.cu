@@ -658,6 +658,46 @@ __global__ void k_synth(long long t, uint64_t n, DivU64 dh, uint64_t base_aip, u
   }
 }
 
+// cfg 3 packets; must equal oracle/vate_oracle.py:synthetic_zipf_slice.
+constexpr uint64_t kSpreadBase = 0x0B000000ull;
+constexpr uint64_t kSpreadBipSalt = 0x6A09E667F3BCC909ull;
+constexpr uint64_t kSpreadPeerSalt = 0xBB67AE8584CAA73Bull;
+
+__device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__ v, uint64_t n,
+                                                    uint64_t key) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (v[mid] <= key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_synth_zipf(long long t, uint64_t n, uint64_t base_aip, uint64_t stream,
+                             const uint64_t* __restrict__ zcdf, uint64_t hosts,
+                             const uint64_t* __restrict__ scdf, uint64_t nspread,
+                             uint32_t spread_q16, uint2* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t hi = ((uint64_t)t & 0xFFFFFFFFull) << 32;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t x = mix64(stream + (hi + i) * kPhi);
+    const uint64_t u = x >> 24;
+    if ((x & 0xFFFFull) < spread_q16) {
+      const uint64_t s = upper_bound_u64(scdf, nspread, u);
+      out[i] = make_uint2((uint32_t)(kSpreadBase + s), (uint32_t)mix64(x ^ kSpreadBipSalt));
+    } else {
+      const uint64_t rank = upper_bound_u64(zcdf, hosts, u);
+      const uint32_t r = (uint32_t)(mix64(rank ^ kSynthHostSalt) >> 40);
+      const uint32_t lz = min(__clz(r) - 8, 12);
+      const uint32_t npeers = 1u + (r & 7u) + (1u << lz);
+      const uint32_t j = (uint32_t)((mix64(x ^ kSpreadPeerSalt) >> 32) % npeers);
+      const uint32_t bip = (uint32_t)mix64((rank << 20) ^ (uint64_t)j ^ kSynthPeerSalt);
+      out[i] = make_uint2((uint32_t)(rank + base_aip), bip);
+    }
+  }
+}
+
 }  // namespace vate
 
 using namespace vate;
@@ -1338,6 +1378,18 @@ int vate_merge_dirty(vate_pool* p, const uint32_t* bitmaps_dev, int nranks) {
 }
 
 // ---- synthetic traffic ------------------------------------------------------------
+
+int vate_synth_zipf(vate_pool* p, int64_t t, uint64_t n, uint64_t hosts, uint64_t base_aip,
+                    uint64_t trace_seed, const uint64_t* zipf_cdf_dev, const uint64_t* spread_cdf_dev,
+                    uint64_t nspread, uint32_t spread_q16, uint32_t* pairs_dev) {
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  if (hosts < 1 || nspread < 1) return set_error(VATE_EVALUE, "empty CDF table");
+  VATE_LAUNCH(p, VATE_K_OTHER, grid_for(n, kThreads), kThreads, 0, k_synth_zipf, (long long)t, n,
+              base_aip, mix64(trace_seed ^ kSynthSalt), zipf_cdf_dev, hosts, spread_cdf_dev, nspread,
+              spread_q16, (uint2*)pairs_dev);
+  return VATE_OK;
+}
 
 int vate_synth_packets(vate_pool* p, int64_t t, uint64_t n, uint64_t hosts, uint64_t base_aip,
                        uint64_t trace_seed, uint32_t* pairs_dev) {

@@ -764,3 +764,59 @@ def test_replica_merge_and_range_split_equal_one_pool():
         for pipe in reps:
             pipe._maintain(t)
             assert pipe.pool.snapshot_bytes() == single.pool.snapshot_bytes(), t
+
+
+# --- the synthetic generators: device == oracle ----------------------------------------
+
+def test_device_generators_equal_oracle():
+    import torch
+    from paper_1812_00282_b200._lib import check, lib
+    from paper_1812_00282_b200.synth import ZipfTables
+    pool = vb.AtPool(8, 2)
+    n = 1_000_000
+    out = torch.empty((n, 2), dtype=torch.int32, device="cuda")
+    for t in (0, 7, 123456):
+        check(lib.vate_synth_packets(pool.handle, t, n, 1_000_000, 0x0A000000, 0, out.data_ptr()))
+        pool.synchronize()
+        got = out.cpu().numpy().view(np.uint32)
+        a, b = vo.synthetic_slice(t, n, 1_000_000)
+        assert np.array_equal(got[:, 0], a) and np.array_equal(got[:, 1], b), t
+    zt = ZipfTables(0, 1_000_000)
+    assert np.array_equal(zt.z.cpu().numpy().view(np.uint64), vo.zipf_cdf(1_000_000))
+    assert np.array_equal(zt.s.cpu().numpy().view(np.uint64), vo.spreader_cdf())
+    for t in (0, 3):
+        zt.packets(pool, t, n, 0x0A000000, 0, out.data_ptr())
+        pool.synchronize()
+        got = out.cpu().numpy().view(np.uint32)
+        a, b = vo.synthetic_zipf_slice(t, n, 1_000_000, vo.zipf_cdf(1_000_000), vo.spreader_cdf())
+        assert np.array_equal(got[:, 0], a) and np.array_equal(got[:, 1], b), t
+
+
+def test_full_size_cfg3_zipf_superspreaders():
+    """BASELINE cfg 3: Zipf hosts + 64 super-spreaders with random peers (10 % of
+    5M packets), pool 2^26: P, maintenance, sampled g0 (spreaders included) and the
+    final ATP1 snapshot equal the oracle replaying the same packets."""
+    c, k = 26, 60
+    cfg = vb.EstimatorConfig(1024, c, k)
+    ocfg = vo.OracleConfig(1024, c, k)
+    pool = cfg.build_pool()
+    pipe = vb.Pipeline(pool, cfg, k)
+    opool = vo.OraclePool(c, k)
+    zc, sc = vo.zipf_cdf(1_000_000), vo.spreader_cdf()
+    for t in range(4):
+        a, b = vo.synthetic_zipf_slice(t, 5_000_000, 1_000_000, zc, sc)
+        got, _ = pipe.process_slice_soa(t, a, b)
+        opool.set_cells(ocfg.pair_cells(a, b))
+        assert pipe.last_pool_inactive == opool.count_inactive(k)
+        sample = np.unique(np.concatenate([
+            np.random.default_rng(t).choice(got.host, 2000, replace=False),
+            np.arange(vo.SPREAD_BASE, vo.SPREAD_BASE + 64, dtype=np.uint64)]))
+        idx = np.searchsorted(got.host, sample)
+        assert np.array_equal(got.host[idx], sample)
+        want = vo.reports_soa(ocfg, sample, vo.host_g0(opool, ocfg, sample, k),
+                              pipe.last_pool_inactive, t, k)
+        assert np.array_equal(got.estimate[idx], want.estimate), t
+        due, visited, cleared = opool.advance()
+        m = pipe.last_maintenance
+        assert (m.blocks, m.cells_maintained, m.cells_cleared) == (due, visited, cleared)
+    assert pool.snapshot_bytes() == opool.snapshot_bytes()
