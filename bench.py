@@ -258,6 +258,8 @@ def run_gpu(args, rank, world, local_rank):
     h = pool.handle
     check(lib.vate_pool_set_option(h, 0, ("auto", "gather", "smem").index(args.g0_kernel)))
     pool.set_option("incremental", 1 if args.incremental == "on" else 0)
+    if args.scan_check is not None:
+        pool.set_option("scan_check", args.scan_check)
     n = w["packets"]
     slice_bytes = n * 8
     torch.cuda.set_device(dev)
@@ -521,6 +523,8 @@ def main():
     ap.add_argument("--impl", choices=("vate", "reference"), default="vate")
     ap.add_argument("--g0-kernel", choices=("auto", "gather", "smem"), default="auto",
                     help="g0 gather variant (VATE_OPT_G0)")
+    ap.add_argument("--scan-check", type=int, choices=(0, 1), default=None,
+                    help="load-before-store scan (VATE_OPT_SCAN_CHECK)")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2",
                     help="workload shape (BASELINE.json configs); cfg2 is the headline")
     ap.add_argument("--incremental", choices=("on", "off"), default="on",

@@ -73,7 +73,8 @@ int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
  * 2 shared-memory / cluster-DSMEM kernel (c <= 24 only).  VATE_OPT_INCREMENTAL
  * = 1 (default) lets the fused estimate update g0 through an inverse index
  * (exact), 0 recomputes every g0 by a full gather. */
-enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 2 };
+enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 2,
+                   VATE_OPT_SCAN_CHECK = 3 };
 int vate_pool_set_option(vate_pool* p, int option, int64_t value);
 /* incremental-estimate counters: [rebuilds, delta slices, refresh slices, full
  * slices, last delta cells, last delta work, identity slices, hosts indexed,

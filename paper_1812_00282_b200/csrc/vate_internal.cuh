@@ -240,6 +240,7 @@ struct vate_pool {
   // options
   int opt_g0 = 0;
   int opt_inc = 1;            // incremental g0 through the inverse index
+  int opt_scan_check = 0;    // packed scan: load-before-store (heavy hitters)
   int opt_scan_v = 1;         // packed-scan unroll (uint4 loads per thread per iteration)
   const void* sorted_owner = nullptr;  // registry whose active set hosts_sorted holds
   uint64_t sorted_n = 0;

@@ -173,7 +173,7 @@ __global__ void k_fill(T* cells, uint64_t n, T value) {
 // read-modify-write.  The registry step issues all U first-probe loads (one
 // 16-byte sector each) before resolving any, so a thread keeps U independent
 // requests in flight; only misses take the probing insert.
-template <typename T, bool REG, int U>
+template <typename T, bool REG, int U, bool CHECK = false>
 __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint64_t (&bip)[U],
                                            int m, T* __restrict__ cells, const HashParams& H,
                                            const Layout& L, uint32_t bact0, const RegRef& R,
@@ -182,7 +182,10 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
   for (int q = 0; q < U; ++q) {
     if (q < m) {
       const uint64_t cell = cell_of(aip[q], slot_of(bip[q], H), H);
-      cells[cell] = (T)clock_of(bact0, block_of(cell, L), L.B);
+      const T act = (T)clock_of(bact0, block_of(cell, L), L.B);
+      // CHECK: skew-tolerant form for heavy hitters -- read first (L1 keeps hot
+      // lines) and store only if the cell does not already hold the clock
+      if (!CHECK || cells[cell] != act) cells[cell] = act;
     }
   }
   if (REG) {
@@ -206,7 +209,7 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
   }
 }
 
-template <typename T, bool REG, int V = 2>  // V uint4 loads (2 packets each) per iteration
+template <typename T, bool REG, int V = 2, bool CHECK = false>  // V uint4 loads per iteration
 __global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
     Layout L, uint32_t bact0, RegRef R, long long t) {
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
         a[2 * v] = b[2 * v] = a[2 * v + 1] = b[2 * v + 1] = 0;
       }
     }
-    scan_batch<T, REG, 2 * V>(a, b, m, cells, H, L, bact0, R, t);
+    scan_batch<T, REG, 2 * V, CHECK>(a, b, m, cells, H, L, bact0, R, t);
   }
 }
 
@@ -921,6 +924,10 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_g0 = (int)value;
     return VATE_OK;
   }
+  if (option == VATE_OPT_SCAN_CHECK && (value == 0 || value == 1)) {
+    p->opt_scan_check = (int)value;
+    return VATE_OK;
+  }
   if (option == VATE_OPT_SCAN_V && (value == 1 || value == 2 || value == 4)) {
     p->opt_scan_v = (int)value;
     return VATE_OK;
@@ -1023,7 +1030,11 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     return with_cell(p->cell_bytes, [&](auto tag) -> int {
       using T = decltype(tag);
       if (aligned16 && n >= 2) {
-        if (hosts && p->opt_scan_v == 1)
+        if (hosts && p->opt_scan_v == 1 && p->opt_scan_check)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 1, true>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
+                      (long long)t);
+        else if (hosts && p->opt_scan_v == 1)
           VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 1>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
                       (long long)t);
