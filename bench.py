@@ -244,6 +244,7 @@ def run_gpu(args, rank, world, local_rank):
     import paper_1812_00282_b200 as vb
     from paper_1812_00282_b200 import _lib
     from paper_1812_00282_b200._lib import lib, check
+    from paper_1812_00282_b200.parallel import ReplicaStep
 
     dist = None
     if world > 1:
@@ -301,24 +302,18 @@ def run_gpu(args, rank, world, local_rank):
     out_sets = (pinned_outs(), pinned_outs())   # reports double-buffered across slices
     outs = out_sets[0]
 
-    merger = _Merger(pool, world, dist, torch) if world > 1 else None
+    # N > 1: replica merge + host exchange + this rank's share of the estimate
+    replica = ReplicaStep(pipe, dist, torch) if world > 1 else None
+    run_slice = replica if replica is not None else pipe.step_fast
 
     def step(t, src, on_device):
-        """One slice; report rows of slice t land in out_sets[t % 2] asynchronously."""
-        if merger is not None:
-            pipe.scan_packed(t, src, n, on_device)
-            merger.merge()
-            rep = merger.estimate(pipe, t, out_sets[t % 2])
-            pipe._maintain(t)
-        else:
-            # device-resident in and out: the report rows stay in HBM (e2e moves them)
-            rep = pipe.step_fast(t, src, n, "device" if on_device else "host", None)
-            return 0 if rep is None else rep
-        return 0 if rep is None else len(rep)
+        """One slice; report rows stay in HBM (e2e moves them); returns the row count."""
+        rep = run_slice(t, src, n, "device" if on_device else "host", None)
+        return 0 if rep is None else rep
 
     def step_host(t, i):
         """e2e slice from pinned host packets; slice i+1's H2D overlaps slice i."""
-        rep = pipe.step_fast(t, staged[i % 2], n, "staged", out_sets[t % 2])
+        rep = run_slice(t, staged[i % 2], n, "staged", out_sets[t % 2])
         return 0 if rep is None else len(rep)
 
     t = 0
@@ -490,29 +485,6 @@ def _teardown(dist):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
-
-
-class _Merger:
-    """Per-slice replica merge + aip-range-split estimate for N > 1."""
-
-    def __init__(self, pool, world, dist, torch):
-        self.pool, self.world, self.dist, self.torch = pool, world, dist, torch
-        nwords = (pool.size + 31) // 32
-        dev = f"cuda:{pool.device}"
-        self.mine = torch.empty(nwords, dtype=torch.int32, device=dev)
-        self.all = torch.empty(world * nwords, dtype=torch.int32, device=dev)
-
-    def merge(self):
-        from paper_1812_00282_b200._lib import check, lib
-        check(lib.vate_dirty_bitmap(self.pool.handle, self.mine.data_ptr()))
-        self.pool.synchronize()
-        self.dist.all_gather_into_tensor(self.all, self.mine)
-        self.torch.cuda.synchronize(self.pool.device)
-        check(lib.vate_merge_dirty(self.pool.handle, self.all.data_ptr(), self.world))
-
-    def estimate(self, pipe, t, outs):
-        import paper_1812_00282_b200.parallel as par
-        return par.range_split_estimate(pipe, t, outs, self.dist, self.torch)
 
 
 def main():

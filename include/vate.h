@@ -178,6 +178,14 @@ int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t ce
 int vate_estimate_begin_hosts(vate_pool* p, const uint64_t* hosts, uint64_t n, int where,
                               uint64_t g, uint64_t cell_stream, int k_prime,
                               uint64_t* pool_inactive);
+/* vate_estimate_begin restricted to share `part` of `nparts` of the sorted
+ * active set (positions [n*part/nparts, n*(part+1)/nparts)): the multi-GPU
+ * split of Pipeline._estimate (pipeline.py:120-138) when every rank's
+ * registry holds the same hosts (vate_hosts_touched exchange). *nhosts is the
+ * share's size. */
+int vate_estimate_begin_part(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                             int64_t t, int k_prime, int part, int nparts, uint64_t* nhosts,
+                             uint64_t* pool_inactive);
 int vate_estimate_finish(vate_pool* p, uint64_t g, uint64_t pool_inactive, double log_zp,
                          double floor, uint64_t* out_host, double* out_est,
                          double* out_zv, uint8_t* out_sat, uint64_t cap, uint64_t* nkept);
@@ -232,6 +240,11 @@ int vate_hosts_active(vate_hosts* h, int64_t t, int k_prime, uint64_t* out, uint
 /* drop hosts last seen at or before t - k (SlidingHostSet.prune) */
 int vate_hosts_prune(vate_hosts* h, int64_t t);
 int vate_hosts_size(vate_hosts* h, uint64_t* n);
+/* keys last seen exactly in slice t (what this rank's scans registered in t),
+ * into device memory out_dev[cap]; *n = count (VATE_EVALUE if > cap). The
+ * multi-GPU exchange all-gathers these so every registry holds the union
+ * (SlidingHostSet.update, pipeline.py:50-52, over the sharded stream). */
+int vate_hosts_touched(vate_hosts* h, int64_t t, uint64_t* out_dev, uint64_t cap, uint64_t* n);
 
 /* ---- multi-GPU replica merge ---------------------------
  * Replicas share bact0 and hold identical cells at slice start, so a cell

@@ -78,6 +78,7 @@ _SIGS = {
     "vate_reports_from_counts": ([_p, _u64, _p, _u64, _u64, _dbl, _p, _p, _p], _int),
     "vate_estimate_begin": ([_p, _p, _u64, _u64, _i64, _int, _pu64, _pu64], _int),
     "vate_estimate_begin_hosts": ([_p, _p, _u64, _int, _u64, _u64, _int, _pu64], _int),
+    "vate_estimate_begin_part": ([_p, _p, _u64, _u64, _i64, _int, _int, _int, _pu64, _pu64], _int),
     "vate_estimate_finish": ([_p, _u64, _u64, _dbl, _dbl, _p, _p, _p, _p, _u64, _pu64], _int),
     "vate_estimate_finish_async": ([_p, _u64, _u64, _dbl, _dbl, _p, _p, _p, _p, _u64, _pu64], _int),
     "vate_estimate_wait": ([_p], _int),
@@ -93,6 +94,7 @@ _SIGS = {
     "vate_hosts_active": ([_p, _i64, _int, _p, _u64, _pu64], _int),
     "vate_hosts_prune": ([_p, _i64], _int),
     "vate_hosts_size": ([_p, _pu64], _int),
+    "vate_hosts_touched": ([_p, _i64, _p, _u64, _pu64], _int),
     "vate_dirty_bitmap": ([_p, _p], _int),
     "vate_merge_dirty": ([_p, _p, _int], _int),
     "vate_trace_bucket": ([_p, _p, _u64, _int, _u64, _i64, _u64, _int, _p, _u64, _u64, _p,

@@ -564,7 +564,8 @@ static int begin_enqueue(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t c
 // complete (after the caller's sync): the sorted active set, P, and g0 of
 // every active host (incremental or full); the g0 kernels are left running.
 static int begin_complete(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
-                          int64_t t, int k_prime, uint64_t* nhosts, uint64_t* pool_inactive) {
+                          int64_t t, int k_prime, uint64_t* nhosts, uint64_t* pool_inactive,
+                          int part = 0, int nparts = 1) {
   IncIndex& I = p->inc;
   if (I.lookup_pending) {  // misses of the previous lookup (landed before this sync)
     I.lookup_pending = false;
@@ -587,6 +588,11 @@ static int begin_complete(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t 
   uint64_t n = 0;
   int rc = hosts_active_finish(hosts, t, k_prime, &keys, &n);
   if (rc) return rc;
+  if (nparts > 1) {  // this rank's contiguous share of the sorted active set
+    const uint64_t lo = n * (uint64_t)part / nparts, hi = n * (uint64_t)(part + 1) / nparts;
+    keys += lo;
+    n = hi - lo;
+  }
   *nhosts = n;
   *pool_inactive = 0;
   if (n == 0) {  // no hosts: no report (pipeline.py:122-123); the index stays as it was
@@ -597,6 +603,7 @@ static int begin_complete(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t 
   rc = inc_compute_g0(p, keys, n, make_hash(g, p->c, cell_stream, 0), k_prime);
   if (rc) return rc;
   p->est_n = n;
+  p->est_keys = keys;
   p->est_kp = k_prime;
   p->est_g = g;
   return VATE_OK;
@@ -611,6 +618,19 @@ int vate_estimate_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t ce
   rc = sync_small(p);
   if (rc) return rc;
   return begin_complete(p, hosts, g, cell_stream, t, k_prime, nhosts, pool_inactive);
+}
+
+int vate_estimate_begin_part(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                             int64_t t, int k_prime, int part, int nparts, uint64_t* nhosts,
+                             uint64_t* pool_inactive) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (nparts < 1 || part < 0 || part >= nparts) return set_error(VATE_EVALUE, "bad part");
+  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime);
+  if (rc) return rc;
+  rc = sync_small(p);
+  if (rc) return rc;
+  return begin_complete(p, hosts, g, cell_stream, t, k_prime, nhosts, pool_inactive, part, nparts);
 }
 
 int vate_estimate_begin_hosts(vate_pool* p, const uint64_t* hosts, uint64_t n, int where,
@@ -647,6 +667,7 @@ int vate_estimate_begin_hosts(vate_pool* p, const uint64_t* hosts, uint64_t n, i
   VATE_CUDA(cudaEventSynchronize(p->ev_small));
   *pool_inactive = p->h_ctr[C_P];
   p->est_n = n;
+  p->est_keys = p->hosts_sorted.as<const uint64_t>();
   p->est_kp = k_prime;
   p->est_g = g;
   return VATE_OK;
@@ -668,7 +689,7 @@ static int estimate_finish_impl(vate_pool* p, uint64_t g, uint64_t pool_inactive
   uint64_t kept = 0;
   const int slot = p->out_slot;
   p->out_slot ^= 1;
-  rc = run_float_path(p, p->hosts_sorted.as<const uint64_t>(),
+  rc = run_float_path(p, p->est_keys,
                       p->g0_src ? p->g0_src : p->g0.as<const int32_t>(), n, F, slot, &kept);
   if (rc) return rc;
   *nkept = kept;

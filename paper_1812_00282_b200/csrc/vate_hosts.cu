@@ -225,6 +225,31 @@ __global__ void __launch_bounds__(256) k_keep(const RegEntry* __restrict__ table
   }
 }
 
+// Keys last seen exactly in slice t (the hosts this rank registered this slice).
+__global__ void k_touched(const RegEntry* __restrict__ table, uint64_t cap, long long t,
+                          const unsigned long long* special, uint64_t* __restrict__ out,
+                          uint64_t out_cap, unsigned long long* nout) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base <= cap; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    bool take = false;
+    unsigned long long key = 0;
+    if (i <= cap) {
+      const RegEntry e = table[i];
+      key = i < cap ? e.key : kEmptyKey;
+      take = (i < cap ? key != kEmptyKey : (*special & 0xFFFFFFFFull) != 0) && e.last == t;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (m) {
+      unsigned long long pos = 0;
+      if (lane == 0) pos = atomicAdd(nout, (unsigned long long)__popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << lane) - 1u));
+      if (take && pos < out_cap) out[pos] = key;
+    }
+  }
+}
+
 static int ensure_table(DevBuf& buf, uint64_t cap, cudaStream_t s) {
   int rc = buf.ensure((cap + 1) * sizeof(RegEntry));
   if (rc) return rc;
@@ -566,6 +591,25 @@ int vate_hosts_prune(vate_hosts* h, int64_t t) {
   h->member_valid = false;  // slots moved
   h->count_hint = c[H_NOUT] + (special ? 1 : 0);
   h->pending = 0;
+  return VATE_OK;
+}
+
+int vate_hosts_touched(vate_hosts* h, int64_t t, uint64_t* out_dev, uint64_t cap, uint64_t* n) {
+  if (!h) return set_error(VATE_EVALUE, "null registry handle");
+  vate_pool* p = h->pool;
+  int rc = enter(p);
+  if (rc) return rc;
+  rc = hosts_drain(h);  // parked inserts first
+  if (rc) return rc;
+  VATE_CUDA(cudaMemsetAsync(h->d_count + H_NOUT, 0, 8, p->stream));
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap + 1, kThreads, 148u * 16u), kThreads, 0, k_touched,
+              h->table.as<const RegEntry>(), h->cap, (long long)t, h->d_count + H_SPECIAL, out_dev,
+              cap, h->d_count + H_NOUT);
+  unsigned long long c[H_N];
+  rc = hosts_read_counters(h, c);
+  if (rc) return rc;
+  *n = c[H_NOUT];
+  if (*n > cap) return set_error(VATE_EVALUE, "touched-host buffer too small");
   return VATE_OK;
 }
 

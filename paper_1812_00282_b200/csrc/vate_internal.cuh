@@ -229,6 +229,7 @@ struct vate_pool {
 
   // fused-estimate state between begin/finish
   uint64_t est_n = 0;
+  const uint64_t* est_keys = nullptr;  // the hosts est_n counts (a share of hosts_sorted)
   int est_kp = 0;
   uint64_t est_g = 0;
 

@@ -9,14 +9,19 @@ every rank ORs them and writes its block clock into the dirty cells
 (vate_merge_dirty).  That is the reference's single-pool state exactly (the
 window-aware newest-timestamp max of SURVEY.md §8e).
 
-Host estimation then splits by aip range: the union of the ranks' active host
-sets is sorted, rank r estimates the r-th contiguous range, and concatenating
-the ranks' reports in rank order gives the reference's ascending host order
-(pipeline.py:57).
+Host estimation then splits by aip range without leaving the device: each
+rank compacts the hosts its scans registered this slice (vate_hosts_touched),
+those lists are all-gathered (the SURVEY's "ncclAllGather of newly seen aips")
+and inserted into every registry, so every rank holds the same sliding host
+set; rank r then estimates the r-th contiguous share of the sorted active set
+(vate_estimate_begin_part), and concatenating the ranks' reports in rank
+order gives the reference's ascending host order (pipeline.py:57).
 
 The pure functions here (``split_range``, ``union_sorted``) are shared with
 the CPU tests, which run the same protocol over gloo with the oracle as the
-per-rank pool (tests/test_multirank_cpu.py).
+per-rank pool (tests/test_multirank_cpu.py); the device phases
+(``dirty_bitmap`` … ``absorb_hosts``) are what ``ReplicaStep`` calls between
+collectives, and what the single-GPU replica test drives by hand.
 """
 
 from __future__ import annotations
@@ -25,8 +30,7 @@ import ctypes as C
 
 import numpy as np
 
-from ._lib import VATE_HOST, check, lib, ptr
-from .estimator import HostReports, log_zp
+from ._lib import VATE_DEVICE, check, lib
 
 
 def union_sorted(parts) -> np.ndarray:
@@ -42,45 +46,87 @@ def split_range(n: int, rank: int, world: int):
     return (n * rank) // world, (n * (rank + 1)) // world
 
 
-def all_gather_hosts(local: np.ndarray, dist, device) -> list:
-    """Variable-length all-gather of uint64 host arrays (sizes first, then padded)."""
-    import torch
-    world = dist.get_world_size()
-    n = torch.tensor([len(local)], dtype=torch.int64, device=device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n)
-    sizes = [int(s.item()) for s in sizes]
-    cap = max(sizes + [1])
-    buf = torch.zeros(cap, dtype=torch.int64, device=device)
-    if len(local):
-        buf[: len(local)] = torch.from_numpy(local.view(np.int64)).to(device)
-    bufs = [torch.zeros_like(buf) for _ in range(world)]
-    dist.all_gather(bufs, buf)
-    return [b[:s].cpu().numpy().view(np.uint64) for b, s in zip(bufs, sizes)]
+# --- device phases (one rank) ------------------------------------------------------------
+
+def dirty_bitmap(pipe, out_ptr: int) -> None:
+    """1 bit per cell: cells this replica set in the current slice."""
+    check(lib.vate_dirty_bitmap(pipe.pool.handle, int(out_ptr)))
 
 
-def range_split_estimate(pipe, t: int, outs, dist, torch) -> HostReports | None:
-    """Estimate this rank's aip range of the global active set (device pool merged)."""
-    rank, world = dist.get_rank(), dist.get_world_size()
-    device = f"cuda:{pipe.pool.device}"
-    local = pipe.hosts.active(t, pipe.k_prime)
-    hosts = union_sorted(all_gather_hosts(local, dist, device))
-    lo, hi = split_range(len(hosts), rank, world)
-    mine = np.ascontiguousarray(hosts[lo:hi])
-    p = C.c_uint64()
-    check(lib.vate_estimate_begin_hosts(pipe.pool.handle, ptr(mine), mine.size, VATE_HOST,
-                                        pipe.cfg.g, pipe.cfg.cell_stream, pipe.k_prime,
-                                        C.byref(p)))
-    if mine.size == 0:
-        return None
-    lzp, z_p = log_zp(p.value, pipe.pool.size)
-    host, est, zv, sat = outs
-    kept = C.c_uint64()
-    check(lib.vate_estimate_finish(pipe.pool.handle, pipe.cfg.g, p.value, lzp, float(pipe.floor),
-                                   ptr(host), ptr(est), ptr(zv), ptr(sat), len(host),
-                                   C.byref(kept)))
-    m = kept.value
-    pipe.last_pool_inactive = p.value
-    pipe.last_active = len(hosts)
-    return HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool), z_p,
-                       t - pipe.k_prime + 1, pipe.k_prime)
+def merge_dirty(pipe, all_ptr: int, world: int) -> None:
+    """OR the world's bitmaps and write each dirty cell's block clock."""
+    check(lib.vate_merge_dirty(pipe.pool.handle, int(all_ptr), world))
+
+
+def touched_hosts(pipe, t: int, out_ptr: int, cap: int) -> int:
+    """Hosts this replica's scans registered in slice t -> device u64[cap]; count."""
+    n = C.c_uint64()
+    check(lib.vate_hosts_touched(pipe.hosts.handle, t, int(out_ptr), int(cap), C.byref(n)))
+    return n.value
+
+
+def absorb_hosts(pipe, keys_ptr: int, n: int, t: int) -> None:
+    """Register another rank's touched hosts (device pointer) as seen in slice t."""
+    if n:
+        check(lib.vate_hosts_update(pipe.hosts.handle, int(keys_ptr), int(n), t, VATE_DEVICE))
+
+
+class ReplicaStep:
+    """One slice on one rank of a torch.distributed (NCCL) job.
+
+    scan own shard -> [dirty bitmap, touched hosts] -> all-gather both ->
+    merge cells, absorb hosts -> estimate own share -> advance (overlapped).
+    Collectives run on torch's stream; the pool's stream is synchronised
+    around them (the touched-host count is read on the host anyway).
+    """
+
+    def __init__(self, pipe, dist, torch):
+        self.pipe, self.dist, self.torch = pipe, dist, torch
+        self.world, self.rank = dist.get_world_size(), dist.get_rank()
+        self.dev = f"cuda:{pipe.pool.device}"
+        nwords = (pipe.pool.size + 31) // 32
+        self.mine = torch.empty(nwords, dtype=torch.int32, device=self.dev)
+        self.all = torch.empty(self.world * nwords, dtype=torch.int32, device=self.dev)
+        self.keys = torch.empty(1, dtype=torch.int64, device=self.dev)
+        self.keys_all = torch.empty(self.world, dtype=torch.int64, device=self.dev)
+        self.count = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.counts = torch.zeros(self.world, dtype=torch.int64, device=self.dev)
+
+    def exchange(self, t: int, n_packets: int) -> None:
+        torch, dist, pipe = self.torch, self.dist, self.pipe
+        if self.keys.numel() < max(n_packets, 1):      # touched <= packets scanned
+            self.keys = torch.empty(max(n_packets, 1), dtype=torch.int64, device=self.dev)
+        dirty_bitmap(pipe, self.mine.data_ptr())
+        nt = touched_hosts(pipe, t, self.keys.data_ptr(), self.keys.numel())  # syncs the pool
+        self.count.fill_(nt)
+        dist.all_gather_into_tensor(self.counts, self.count)
+        dist.all_gather_into_tensor(self.all, self.mine)
+        counts = self.counts.tolist()
+        cap = max(counts + [1])
+        if self.keys_all.numel() < self.world * cap:
+            self.keys_all = torch.empty(self.world * cap, dtype=torch.int64, device=self.dev)
+        dist.all_gather_into_tensor(self.keys_all[: self.world * cap], self.keys[:cap])
+        torch.cuda.current_stream(self.dev).synchronize()  # gathers visible to the pool stream
+        merge_dirty(pipe, self.all.data_ptr(), self.world)
+        base = self.keys_all.data_ptr()
+        for r, c in enumerate(counts):
+            if r != self.rank:
+                absorb_hosts(pipe, base + 8 * r * cap, c, t)
+
+    def __call__(self, t: int, pairs: int, n: int, where: str = "device", out=None):
+        """Rows of this rank's share (HostReports, or a count with out=None), streamed.
+
+        ``pairs``/``where`` as Pipeline.step_fast (device or host pointer, or a
+        staging slot from stage_packed)."""
+        pipe = self.pipe
+        if where == "staged":
+            check(lib.vate_scan_staged(pipe.pool.handle, pipe.cfg.g, pipe.cfg.cell_stream,
+                                       pipe.cfg.group_stream, int(pairs), int(n),
+                                       pipe.hosts.handle, t))
+        else:
+            pipe.scan_packed(t, pairs, n, where == "device")
+        self.exchange(t, n)
+        rep = pipe.estimate_soa(t, out, advance=True, wait=False, keep_on_device=out is None,
+                                part=self.rank, nparts=self.world)
+        pipe._deferred_t = t
+        return rep

@@ -143,7 +143,8 @@ class Pipeline:
                                    self.hosts.handle, t))
 
     def estimate_soa(self, t: int, out=None, advance: bool = False,
-                     wait: bool = True, keep_on_device: bool = False):
+                     wait: bool = True, keep_on_device: bool = False,
+                     part: int = 0, nparts: int = 1):
         """The estimate phase (pipeline.py:120-138) as arrays; None without hosts.
 
         ``out`` may supply preallocated (pinned) host arrays
@@ -154,11 +155,18 @@ class Pipeline:
         With ``wait=False`` the report rows are copied on the pool's D2H stream
         while the caller moves on (double-buffered): the arrays are complete
         after ``wait_reports()``; alternate two ``out`` sets between slices.
+        ``part``/``nparts`` estimate only that contiguous share of the sorted
+        active set (the multi-GPU split, parallel.ReplicaStep).
         """
         nh, p = C.c_uint64(), C.c_uint64()
-        check(lib.vate_estimate_begin(self.pool.handle, self.hosts.handle, self.cfg.g,
-                                      self.cfg.cell_stream, t, self.k_prime, C.byref(nh),
-                                      C.byref(p)))
+        if nparts > 1:
+            check(lib.vate_estimate_begin_part(self.pool.handle, self.hosts.handle, self.cfg.g,
+                                               self.cfg.cell_stream, t, self.k_prime, part,
+                                               nparts, C.byref(nh), C.byref(p)))
+        else:
+            check(lib.vate_estimate_begin(self.pool.handle, self.hosts.handle, self.cfg.g,
+                                          self.cfg.cell_stream, t, self.k_prime, C.byref(nh),
+                                          C.byref(p)))
         if self._deferred_t is not None:   # last slice's sweep finished before this sync
             self._collect(self._deferred_t)
             self._deferred_t = None

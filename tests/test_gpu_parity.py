@@ -766,6 +766,108 @@ def test_replica_merge_and_range_split_equal_one_pool():
             assert pipe.pool.snapshot_bytes() == single.pool.snapshot_bytes(), t
 
 
+def test_replica_step_protocol_device_resident():
+    """ReplicaStep's device phases with two replicas on one device (the NCCL
+    all-gathers replaced by device concatenation): dirty bitmaps merge the cells,
+    vate_hosts_touched + absorb make both registries hold the single pipeline's
+    host set, and vate_estimate_begin_part shares (incremental g0 on) concatenate
+    to the single pipeline's reports, slice after slice, with host churn."""
+    import torch
+    from paper_1812_00282_b200 import parallel as par
+
+    cfg = vb.EstimatorConfig(512, 16, 10, seed=5)
+    kp = 7
+    single = vb.Pipeline(cfg.build_pool(), cfg, kp)
+    reps = [vb.Pipeline(cfg.build_pool(), cfg, kp) for _ in range(2)]
+    nwords = (1 << 16) // 32
+    bm = torch.zeros(2 * nwords, dtype=torch.int32, device="cuda")
+    rng = np.random.default_rng(3)
+    for t in range(40):
+        n = int(rng.integers(0, 40_000)) if t % 9 != 4 else 0
+        lo_host = 200 * (t // 10)                 # the host population drifts
+        a = (0x0A000000 + lo_host + rng.integers(0, 3000, n)).astype(np.uint32)
+        b = rng.integers(1, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+        want, _ = single.process_slice_soa(t, a.astype(np.uint64), b.astype(np.uint64))
+        touched = []
+        for r, pipe in enumerate(reps):
+            pairs = np.ascontiguousarray(np.stack([a[r::2], b[r::2]], axis=1))
+            dev = torch.from_numpy(pairs.view(np.int32)).cuda()
+            pipe.scan_packed(t, dev.data_ptr(), len(pairs), True)
+            par.dirty_bitmap(pipe, bm[r * nwords:].data_ptr())
+            keys = torch.empty(max(len(pairs), 1), dtype=torch.int64, device="cuda")
+            m = par.touched_hosts(pipe, t, keys.data_ptr(), keys.numel())
+            assert m == len(np.unique(a[r::2])), t
+            touched.append((keys, m))
+        for r, pipe in enumerate(reps):
+            par.merge_dirty(pipe, bm.data_ptr(), 2)
+            keys, m = touched[1 - r]
+            par.absorb_hosts(pipe, keys.data_ptr(), m, t)
+        want_hosts = single.hosts.active(t, kp)
+        got_host, got_est, got_zv = [], [], []
+        for r, pipe in enumerate(reps):
+            assert np.array_equal(pipe.hosts.active(t, kp), want_hosts), t
+            rep = pipe.estimate_soa(t, advance=True, wait=True, part=r, nparts=2)
+            pipe._collect(t)
+            if rep is not None:
+                assert rep.z_p == want.z_p, t
+                got_host.append(rep.host.copy())
+                got_est.append(rep.estimate.copy())
+                got_zv.append(rep.z_v.copy())
+        if want is None:
+            assert not got_host, t
+        else:
+            assert np.array_equal(np.concatenate(got_host), want.host), t
+            assert np.array_equal(np.concatenate(got_est), want.estimate), t
+            assert np.array_equal(np.concatenate(got_zv), want.z_v), t
+        for pipe in reps:
+            assert pipe.pool.snapshot_bytes() == single.pool.snapshot_bytes(), t
+            assert len(pipe.hosts) == len(single.hosts), t
+
+
+def test_replica_step_over_nccl_world1():
+    """ReplicaStep itself (NCCL plumbing, stream hand-off, staged/host/device
+    inputs) on a world-size-1 NCCL group equals the single pipeline."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_1812_00282_b200.parallel import ReplicaStep
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = vb.EstimatorConfig(256, 15, 6, seed=8)
+        single = vb.Pipeline(cfg.build_pool(), cfg, 5)
+        pipe = vb.Pipeline(cfg.build_pool(), cfg, 5)
+        step = ReplicaStep(pipe, dist, torch)
+        rng = np.random.default_rng(4)
+        for t in range(16):
+            n = int(rng.integers(1, 20_000))
+            a = (0x0A000000 + rng.integers(0, 1500, n)).astype(np.uint32)
+            b = rng.integers(1, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+            pairs = np.ascontiguousarray(np.stack([a, b], axis=1))
+            want, _ = single.process_slice_soa(t, a.astype(np.uint64), b.astype(np.uint64))
+            out = (np.empty(n, np.uint64), np.empty(n, np.float64), np.empty(n, np.float64),
+                   np.empty(n, np.uint8))
+            mode = ("device", "host", "staged")[t % 3]
+            if mode == "device":
+                src = torch.from_numpy(pairs.view(np.int32)).cuda()
+                rep = step(t, src.data_ptr(), n, "device", out)
+            elif mode == "host":
+                rep = step(t, pairs.ctypes.data, n, "host", out)
+            else:
+                rep = step(t, pipe.stage_packed(pairs.ctypes.data, n), n, "staged", out)
+            pipe.wait_reports()
+            assert np.array_equal(rep.host, want.host), t
+            assert np.array_equal(rep.estimate, want.estimate), t
+            assert pipe.pool.snapshot_bytes() == single.pool.snapshot_bytes(), t
+    finally:
+        dist.destroy_process_group()
+
+
 # --- the synthetic generators: device == oracle ----------------------------------------
 
 def test_device_generators_equal_oracle():

@@ -2,11 +2,13 @@
 
 Each rank scans its round-robin shard of every slice into a private replica
 pool, replicas merge through an all-gather of dirty bitmaps (cells that hold
-their block clock), the union of the ranks' active hosts is range-split, and
-rank-ordered concatenation of the per-rank reports must equal a single pool
-fed every packet -- snapshots, host order and floats, slice by slice.  The
-device path (bench.py / paper_1812_00282_b200.parallel) runs the same
-protocol with vate_dirty_bitmap / vate_merge_dirty over NCCL.
+their block clock), the hosts each rank saw this slice are all-gathered and
+registered everywhere, every rank range-splits the (now identical) sorted
+active set, and rank-ordered concatenation of the per-rank reports must equal
+a single pool fed every packet -- snapshots, host sets, host order and floats,
+slice by slice.  The device path (paper_1812_00282_b200.parallel.ReplicaStep,
+bench.py --gpus N) runs the same protocol with vate_dirty_bitmap /
+vate_merge_dirty / vate_hosts_touched / vate_estimate_begin_part over NCCL.
 """
 
 import os
@@ -38,12 +40,27 @@ def _merge(pool, gathered):
     pool.cells[dirty] = pool.cell_clocks()[dirty].astype(np.uint32)
 
 
+def _gather_varlen(keys):
+    """Sizes first, then a padded all-gather (the shape ReplicaStep uses on NCCL)."""
+    world = dist.get_world_size()
+    n = torch.tensor([len(keys)], dtype=torch.int64)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    sizes = [int(x) for x in sizes]
+    cap = max(sizes + [1])
+    buf = torch.zeros(cap, dtype=torch.int64)
+    buf[: len(keys)] = torch.from_numpy(np.asarray(keys, dtype=np.uint64).view(np.int64))
+    bufs = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf)
+    return [b[:m].numpy().view(np.uint64) for b, m in zip(bufs, sizes)]
+
+
 def _worker(rank, world, port, result_q):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
     from oracle import vate_oracle as vo
-    from paper_1812_00282_b200.parallel import all_gather_hosts, split_range, union_sorted
+    from paper_1812_00282_b200.parallel import split_range, union_sorted
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -63,13 +80,21 @@ def _worker(rank, world, port, result_q):
         pool.set_cells(cfg.pair_cells(a[mine], b[mine]))
         if len(a[mine]):
             hosts.update(a[mine], t)
+        touched = np.unique(a[mine])     # what vate_hosts_touched returns here
         # replica merge
         bits = _dirty_bits(pool)
         gathered = [torch.zeros(len(bits), dtype=torch.uint8) for _ in range(world)]
         dist.all_gather(gathered, torch.from_numpy(bits))
         _merge(pool, [g.numpy() for g in gathered])
+        # every registry absorbs the others' touched hosts -> identical host sets
+        for r, keys in enumerate(_gather_varlen(touched)):
+            if r != rank and len(keys):
+                hosts.update(keys, t)
+        union = hosts.active(t, kp)
+        everyone = _gather_varlen(union)
+        ok &= all(np.array_equal(x, union) for x in everyone)
+        ok &= np.array_equal(union, union_sorted(everyone))
         # aip-range-split estimate
-        union = union_sorted(all_gather_hosts(hosts.active(t, kp), dist, "cpu"))
         lo, hi = split_range(len(union), rank, world)
         part = union[lo:hi]
         rep = None
