@@ -244,15 +244,19 @@ def run_gpu(args, rank, world, local_rank):
     import paper_1812_00282_b200 as vb
     from paper_1812_00282_b200 import _lib
     from paper_1812_00282_b200._lib import lib, check
-    from paper_1812_00282_b200.parallel import ReplicaStep
+    from paper_1812_00282_b200.parallel import PeerStep, ReplicaStep
 
     dist = None
+    # --share-device (functional check only): every rank on cuda:0, gloo plumbing
+    dev = 0 if args.share_device else local_rank
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        torch.cuda.set_device(dev)
+        if args.share_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     w = WORKLOAD
-    dev = local_rank
     cfg = vb.EstimatorConfig(w["g"], w["c"], w["k"], seed=w["seed"], partition=w["partition"])
     pool = cfg.build_pool(device=dev)
     pipe = vb.Pipeline(pool, cfg, w["k_prime"], floor=w["floor"])
@@ -303,7 +307,11 @@ def run_gpu(args, rank, world, local_rank):
     outs = out_sets[0]
 
     # N > 1: replica merge + host exchange + this rank's share of the estimate
-    replica = ReplicaStep(pipe, dist, torch) if world > 1 else None
+    replica = None
+    if world > 1 and args.exchange == "p2p":     # fused merge over peer memory (NVLink)
+        replica = PeerStep(pipe, dist, key_cap=n, mode=("auto", "one", "two").index(args.p2p_mode))
+    elif world > 1:                               # NCCL all-gathers + merge kernel
+        replica = ReplicaStep(pipe, dist, torch)
     run_slice = replica if replica is not None else pipe.step_fast
 
     def step(t, src, on_device):
@@ -396,7 +404,8 @@ def run_gpu(args, rank, world, local_rank):
     max_ms = dev_ms
     max_e2e = e2e_s
     if dist is not None:
-        v = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
+        v = torch.tensor([dev_ms, e2e_s], dtype=torch.float64,
+                         device="cpu" if args.share_device else f"cuda:{dev}")
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         max_ms, max_e2e = float(v[0]), float(v[1])
     total_packets = n * world * args.steps
@@ -470,6 +479,11 @@ def run_gpu(args, rank, world, local_rank):
                         "misses_since_rebuild": inc1["miss_accum"]},
         "clocks": clocks.summary(),
     }
+    if world > 1:
+        line["exchange"] = {"kind": args.exchange,
+                            **(replica.info() if args.exchange == "p2p" else {})}
+        if args.share_device:
+            line["config"]["parallelism"] += " (ranks share cuda:0: functional check, not scaling)"
     if cpu_mean is not None:
         line["cpu_baseline"] = {
             "value": w["packets"] / cpu_mean["slice_s"] / 1e6, "unit": UNIT, "cores": cores,
@@ -501,6 +515,14 @@ def main():
                     help="workload shape (BASELINE.json configs); cfg2 is the headline")
     ap.add_argument("--incremental", choices=("on", "off"), default="on",
                     help="exact incremental g0 through the inverse index (VATE_OPT_INCREMENTAL)")
+    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
+                    help="N > 1 slice exchange: fused peer-memory merge (default) or NCCL "
+                         "all-gathers + merge kernel")
+    ap.add_argument("--p2p-mode", choices=("auto", "one", "two"), default="auto",
+                    help="peer merge form: one-shot, two-shot, or auto (two-shot above 2 ranks)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="run every rank on cuda:0 over gloo (exercises the N > 1 path on "
+                         "one GPU; not a scaling measurement)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be at least 3")

@@ -255,6 +255,33 @@ int vate_hosts_touched(vate_hosts* h, int64_t t, uint64_t* out_dev, uint64_t cap
 int vate_dirty_bitmap(vate_pool* p, uint32_t* bitmap_dev);
 int vate_merge_dirty(vate_pool* p, const uint32_t* bitmaps_dev, int nranks);
 
+/* ---- multi-GPU exchange over peer memory (option P2P) -----
+ * Replaces the all-gather + vate_merge_dirty + touched-host all-gather of the
+ * NCCL path with one window per rank in its own HBM, mapped by every peer over
+ * NVLink (CUDA IPC), and kernels that OR the peers' dirty bitmaps straight
+ * into the cells.  Per slice: vate_peer_exchange after this rank's scans and
+ * before its estimate (vate_estimate_begin_part).  key_cap bounds the hosts one
+ * rank registers per slice (at most its packets per slice) and must be equal on
+ * every rank.
+ *   create: allocates the window; handle_out receives 64 bytes (cudaIpcMemHandle_t)
+ *           that the launcher all-gathers in rank order.
+ *   open:   maps the peers' windows (handles: world * 64 bytes); every rank must
+ *           have created its window before any rank exchanges (launcher barrier).
+ *   mode:   0 auto (one-shot for world <= 2, else two-shot), 1 one-shot (read every
+ *           peer's bitmap), 2 two-shot (reduce own segment, then gather the ORs).
+ *   exchange: dirty bitmap + touched keys published, arrival flags, fused OR-and-
+ *           apply, peers' keys into the registry; *touched_total = hosts registered
+ *           in slice t over all ranks (with repeats across ranks). */
+typedef struct vate_peer vate_peer;
+int vate_peer_create(vate_peer** out, vate_pool* p, vate_hosts* h, int rank, int world,
+                     uint64_t key_cap, uint8_t* handle_out);
+int vate_peer_open(vate_peer* x, const uint8_t* handles);
+int vate_peer_set_mode(vate_peer* x, int mode);
+int vate_peer_exchange(vate_peer* x, int64_t t, uint64_t* touched_total);
+int vate_peer_info(const vate_peer* x, uint64_t* window_bytes, uint64_t* nvlink_bytes,
+                   int* two_shot);
+int vate_peer_destroy(vate_peer* x);
+
 /* ---- trace ingest: traceio._read_binary + slice_stream (traceio.py:77-106,
  *      :188-230) -------------------------------------------------------
  * n 16-byte records {u64 ts_us, u32 aip, u32 bip} (host or device) are packed

@@ -97,6 +97,12 @@ _SIGS = {
     "vate_hosts_touched": ([_p, _i64, _p, _u64, _pu64], _int),
     "vate_dirty_bitmap": ([_p, _p], _int),
     "vate_merge_dirty": ([_p, _p, _int], _int),
+    "vate_peer_create": ([C.POINTER(_p), _p, _p, _int, _int, _u64, _p], _int),
+    "vate_peer_open": ([_p, _p], _int),
+    "vate_peer_set_mode": ([_p, _int], _int),
+    "vate_peer_exchange": ([_p, _i64, _pu64], _int),
+    "vate_peer_info": ([_p, _pu64, _pu64, C.POINTER(_int)], _int),
+    "vate_peer_destroy": ([_p], _int),
     "vate_trace_bucket": ([_p, _p, _u64, _int, _u64, _i64, _u64, _int, _p, _u64, _u64, _p,
                            C.POINTER(_i64)], _int),
     "vate_copy_device": ([_p, _p, _p, _u64], _int),
@@ -131,11 +137,14 @@ def shutting_down() -> bool:
 @_atexit.register
 def _close_all() -> None:
     objs = list(_LIVE.values())
+    for o in objs:                       # peer windows before the registries they feed
+        if getattr(o, "_is_peer", False):
+            o.close()
     for o in objs:                       # registries before the pools they live on
         if getattr(o, "_is_registry", False):
             o.close()
     for o in objs:
-        if not getattr(o, "_is_registry", False):
+        if not getattr(o, "_is_registry", False) and not getattr(o, "_is_peer", False):
             o.close()
     _SHUTDOWN[0] = True
 

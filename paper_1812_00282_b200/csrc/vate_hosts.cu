@@ -340,6 +340,40 @@ int hosts_drain(vate_hosts* h) {
   return VATE_OK;
 }
 
+// Stream-ordered touched-key compaction into caller memory (the multi-GPU peer
+// window): parked inserts are drained first (host sync); *nout_dev receives the
+// count, keys beyond cap are dropped (the caller checks the count).
+int hosts_touched_launch(vate_hosts* h, int64_t t, uint64_t* out_dev, uint64_t cap,
+                         unsigned long long* nout_dev) {
+  vate_pool* p = h->pool;
+  int rc = hosts_drain(h);
+  if (rc) return rc;
+  VATE_CUDA(cudaMemsetAsync(nout_dev, 0, 8, p->stream));
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap + 1, kThreads, 148u * 16u), kThreads, 0, k_touched,
+              h->table.as<const RegEntry>(), h->cap, (long long)t, h->d_count + H_SPECIAL, out_dev,
+              cap, nout_dev);
+  return VATE_OK;
+}
+
+// Parked-insert count and capacity (syncs the stream).
+int hosts_ovf_state(vate_hosts* h, uint64_t* novf, uint64_t* cap) {
+  unsigned long long c[H_N];
+  int rc = hosts_read_counters(h, c);
+  if (rc) return rc;
+  *novf = c[H_OVF];
+  *cap = h->ovf_cap;
+  return VATE_OK;
+}
+
+// Make room for n parked inserts and forget the parked ones (they are redone).
+int hosts_ovf_reset(vate_hosts* h, uint64_t n) {
+  int rc = h->ovf.ensure(n * sizeof(RegEntry));
+  if (rc) return rc;
+  h->ovf_cap = h->ovf.bytes / sizeof(RegEntry);
+  VATE_CUDA(cudaMemsetAsync(h->d_count + H_OVF, 0, 8, h->pool->stream));
+  return VATE_OK;
+}
+
 int hosts_prepare_insert(vate_hosts* h, uint64_t n) {
   if (h->pending + n > h->ovf_cap) {
     if (h->pending) {

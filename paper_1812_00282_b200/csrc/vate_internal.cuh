@@ -121,6 +121,29 @@ __host__ __device__ __forceinline__ uint64_t block_start(uint32_t b, const Layou
   return L.narrow * L.da.d + (uint64_t)(b - L.narrow) * L.da1.d;
 }
 
+// Calls f(j, act) for the cells i0+j, j < cnt, walking block boundaries.
+template <typename F>
+__device__ __forceinline__ void for_word_clocks(uint64_t i0, uint32_t cnt, const Layout& L,
+                                                uint32_t bact0, F f) {
+  uint32_t b = block_of(i0, L);
+  uint64_t next = block_start(b + 1, L);
+  uint32_t act = clock_of(bact0, b, L.B);
+  if (i0 + cnt <= next) {
+#pragma unroll
+    for (uint32_t j = 0; j < 32; ++j)
+      if (j < cnt) f(j, act);
+    return;
+  }
+  for (uint32_t j = 0; j < cnt; ++j) {
+    while (i0 + j >= next) {
+      ++b;
+      next = block_start(b + 1, L);
+      act = (act + 1 == L.B) ? 0 : act + 1;
+    }
+    f(j, act);
+  }
+}
+
 // Inactive for width k' (pools.py:187-193): sentinel, or (act + 2k - v) mod 2k
 // >= k'.  For stored values above 2k (only reachable through a hand-made
 // snapshot) the reference's uint64 wraparound is reproduced exactly.
@@ -318,6 +341,10 @@ void inc_release(vate_pool* p);
 // registry helpers (vate_hosts.cu)
 int hosts_drain(vate_hosts* h);
 int hosts_prepare_insert(vate_hosts* h, uint64_t n);
+int hosts_touched_launch(vate_hosts* h, int64_t t, uint64_t* out_dev, uint64_t cap,
+                         unsigned long long* nout_dev);
+int hosts_ovf_state(vate_hosts* h, uint64_t* novf, uint64_t* cap);
+int hosts_ovf_reset(vate_hosts* h, uint64_t n);
 int hosts_compact_active(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev,
                          uint64_t* n);
 // split form: launch (no sync; counters -> pinned), the caller syncs, finish sorts

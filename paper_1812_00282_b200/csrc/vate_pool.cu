@@ -334,29 +334,6 @@ __device__ __forceinline__ void load32(const T* __restrict__ p, uint32_t (&v)[32
   for (int j = 0; j < 32; ++j) v[j] = e[j];
 }
 
-// Calls f(j, act) for the cells i0+j, j < cnt, walking block boundaries.
-template <typename F>
-__device__ __forceinline__ void for_word_clocks(uint64_t i0, uint32_t cnt, const Layout& L,
-                                                uint32_t bact0, F f) {
-  uint32_t b = block_of(i0, L);
-  uint64_t next = block_start(b + 1, L);
-  uint32_t act = clock_of(bact0, b, L.B);
-  if (i0 + cnt <= next) {
-#pragma unroll
-    for (uint32_t j = 0; j < 32; ++j)
-      if (j < cnt) f(j, act);
-    return;
-  }
-  for (uint32_t j = 0; j < cnt; ++j) {
-    while (i0 + j >= next) {
-      ++b;
-      next = block_start(b + 1, L);
-      act = (act + 1 == L.B) ? 0 : act + 1;
-    }
-    f(j, act);
-  }
-}
-
 // Active bits of 32 cells that share one clock, SIMD-in-register for u8/u16
 // cells: a cell is active iff its value lies in the cyclic interval
 // [act-k'+1, act] (mod 2k) -- the predicate of pools.py:187-193 for values

@@ -71,7 +71,32 @@ def absorb_hosts(pipe, keys_ptr: int, n: int, t: int) -> None:
         check(lib.vate_hosts_update(pipe.hosts.handle, int(keys_ptr), int(n), t, VATE_DEVICE))
 
 
-class ReplicaStep:
+class _SliceStepBase:
+    """scan own shard -> exchange -> estimate own share (advance enqueued)."""
+
+    def exchange(self, t: int, n_packets: int) -> None:  # pragma: no cover - abstract
+        raise NotImplementedError
+
+    def __call__(self, t: int, pairs: int, n: int, where: str = "device", out=None):
+        """Rows of this rank's share (HostReports, or a count with out=None), streamed.
+
+        ``pairs``/``where`` as Pipeline.step_fast (device or host pointer, or a
+        staging slot from stage_packed)."""
+        pipe = self.pipe
+        if where == "staged":
+            check(lib.vate_scan_staged(pipe.pool.handle, pipe.cfg.g, pipe.cfg.cell_stream,
+                                       pipe.cfg.group_stream, int(pairs), int(n),
+                                       pipe.hosts.handle, t))
+        else:
+            pipe.scan_packed(t, pairs, n, where == "device")
+        self.exchange(t, n)
+        rep = pipe.estimate_soa(t, out, advance=True, wait=False, keep_on_device=out is None,
+                                part=self.rank, nparts=self.world)
+        pipe._deferred_t = t
+        return rep
+
+
+class ReplicaStep(_SliceStepBase):
     """One slice on one rank of a torch.distributed (NCCL) job.
 
     scan own shard -> [dirty bitmap, touched hosts] -> all-gather both ->
@@ -113,20 +138,62 @@ class ReplicaStep:
             if r != self.rank:
                 absorb_hosts(pipe, base + 8 * r * cap, c, t)
 
-    def __call__(self, t: int, pairs: int, n: int, where: str = "device", out=None):
-        """Rows of this rank's share (HostReports, or a count with out=None), streamed.
 
-        ``pairs``/``where`` as Pipeline.step_fast (device or host pointer, or a
-        staging slot from stage_packed)."""
-        pipe = self.pipe
-        if where == "staged":
-            check(lib.vate_scan_staged(pipe.pool.handle, pipe.cfg.g, pipe.cfg.cell_stream,
-                                       pipe.cfg.group_stream, int(pairs), int(n),
-                                       pipe.hosts.handle, t))
-        else:
-            pipe.scan_packed(t, pairs, n, where == "device")
-        self.exchange(t, n)
-        rep = pipe.estimate_soa(t, out, advance=True, wait=False, keep_on_device=out is None,
-                                part=self.rank, nparts=self.world)
-        pipe._deferred_t = t
-        return rep
+
+class PeerStep(_SliceStepBase):
+    """One slice on one rank, exchanging over peer memory instead of NCCL.
+
+    Every rank's exchange window lives in its own HBM and is mapped by every
+    peer (CUDA IPC over NVLink/NVSwitch); ``vate_peer_exchange`` publishes the
+    rank's dirty bitmap and touched hosts, raises its arrival flags and runs
+    the fused OR-and-apply merge and the host absorb as kernels that read the
+    peers' windows directly (csrc/vate_peer.cu).  ``dist`` carries only the
+    one-time 64-byte IPC handle exchange and a barrier (any backend: gloo on
+    one device for the tests, NCCL under torchrun).  ``key_cap`` bounds the
+    hosts one rank registers per slice (its packets per slice suffice) and must
+    be the same on every rank.  mode: 0 auto, 1 one-shot, 2 two-shot.
+    """
+
+    _is_peer = True
+
+    def __init__(self, pipe, dist, key_cap: int, mode: int = 0):
+        from ._lib import track
+        self.pipe, self.dist = pipe, dist
+        self.world, self.rank = dist.get_world_size(), dist.get_rank()
+        self.key_cap = int(key_cap)
+        h = C.c_void_p()
+        handle = (C.c_uint8 * 64)()
+        check(lib.vate_peer_create(C.byref(h), pipe.pool.handle, pipe.hosts.handle, self.rank,
+                                   self.world, self.key_cap, handle))
+        self.handle = h.value
+        track(self)
+        check(lib.vate_peer_set_mode(self.handle, int(mode)))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle))
+        buf = (C.c_uint8 * (64 * self.world)).from_buffer_copy(b"".join(handles))
+        check(lib.vate_peer_open(self.handle, buf))
+        dist.barrier()                   # every window mapped before anyone arrives
+        self.touched_total = 0
+
+    def exchange(self, t: int, n_packets: int) -> None:
+        if n_packets > self.key_cap:
+            raise ValueError(f"{n_packets} packets exceed the peer key_cap {self.key_cap}")
+        tot = C.c_uint64()
+        check(lib.vate_peer_exchange(self.handle, t, C.byref(tot)))
+        self.touched_total = tot.value
+
+    def info(self) -> dict:
+        wb, nb, ts = C.c_uint64(), C.c_uint64(), C.c_int()
+        check(lib.vate_peer_info(self.handle, C.byref(wb), C.byref(nb), C.byref(ts)))
+        return {"window_bytes": wb.value, "peer_read_bytes_per_slice": nb.value,
+                "two_shot": bool(ts.value)}
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            lib.vate_peer_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        from ._lib import shutting_down
+        if not shutting_down():
+            self.close()

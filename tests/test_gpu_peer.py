@@ -1,0 +1,127 @@
+"""The peer-memory exchange (csrc/vate_peer.cu, parallel.PeerStep) on one GPU.
+
+Only one B200 is available to this build, so the multi-GPU protocol runs as
+world_size 2 or 3 *processes on the same device*: each process owns a replica
+pool and registry, the exchange windows are CUDA-IPC mapped between the
+processes exactly as between GPUs, and the fused OR-and-apply merge and host
+absorb read the peers' windows directly (gloo carries only the one-time handle
+exchange).  Every slice, every rank's ATP1 snapshot must equal the oracle pool
+fed every packet, and the ranks' report shares concatenated in rank order must
+equal the oracle's reports (hosts, estimates, z_v, saturation) -- for the
+one-shot and the two-shot merge, ragged segment splits included (world 3).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, mode, c, k, result_q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+
+    import paper_1812_00282_b200 as vb
+    from oracle import vate_oracle as vo
+    from paper_1812_00282_b200.parallel import PeerStep, split_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    msgs = []
+    try:
+        kp, g = 5, 256
+        cfg = vb.EstimatorConfig(g, c, k, seed=9)
+        ocfg = vo.OracleConfig(g, c, k, seed=9)
+        pipe = vb.Pipeline(cfg.build_pool(device=0), cfg, kp)
+        ref = vo.OraclePipeline(ocfg, kp)
+        step = PeerStep(pipe, dist, key_cap=40_000, mode=mode)
+        rng = np.random.default_rng(11)
+        for t in range(18):
+            n = int(rng.integers(0, 30_000)) if t != 5 else 0
+            lo_host = 0 if t < 9 else 600        # host churn: half the hosts expire
+            a = (0x0A000000 + rng.integers(lo_host, lo_host + 1200, n)).astype(np.uint32)
+            b = rng.integers(1, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+            mine = np.ascontiguousarray(np.stack([a, b], axis=1)[rank::world])
+            cap = 4096
+            out = (np.empty(cap, np.uint64), np.empty(cap, np.float64), np.empty(cap, np.float64),
+                   np.empty(cap, np.uint8))
+            rep = step(t, mine.ctypes.data if len(mine) else 0, len(mine), "host", out)
+            pipe.wait_reports()
+            want = ref.process_slice(t, a.astype(np.uint64), b.astype(np.uint64))
+            if pipe.pool.snapshot_bytes() != ref.pool.snapshot_bytes():
+                msgs.append(f"rank {rank} t {t}: snapshot differs")
+            if want.reports is None:
+                if rep is not None and len(rep.host):
+                    msgs.append(f"rank {rank} t {t}: reports where the oracle has none")
+                continue
+            lo, hi = split_range(len(want.reports.host), rank, world)
+            got_host = np.zeros(0, np.uint64) if rep is None else rep.host
+            got_est = np.zeros(0, np.float64) if rep is None else rep.estimate
+            got_zv = np.zeros(0, np.float64) if rep is None else rep.z_v
+            if not np.array_equal(got_host, want.reports.host[lo:hi]):
+                msgs.append(f"rank {rank} t {t}: host share differs")
+            elif not (np.array_equal(got_est, want.reports.estimate[lo:hi])
+                      and np.array_equal(got_zv, want.reports.z_v[lo:hi])):
+                msgs.append(f"rank {rank} t {t}: estimates differ")
+            if pipe.last_pool_inactive != want.pool_inactive:
+                msgs.append(f"rank {rank} t {t}: pool_inactive differs")
+        info = step.info()
+        if info["two_shot"] != (mode == 2 or (mode == 0 and world > 2)):
+            msgs.append(f"rank {rank}: unexpected merge form {info}")
+        step.close()
+        pipe.close()
+        pipe.pool.close()
+    except Exception as e:  # report, do not hang the peers' barrier
+        msgs.append(f"rank {rank}: {type(e).__name__}: {e}")
+    result_q.put((rank, msgs))
+    dist.destroy_process_group()
+
+
+def _run(world, mode, c=15, k=6):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, c, k, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = {}
+    for _ in range(world):
+        r, msgs = q.get(timeout=400)
+        results[r] = msgs
+    for p in procs:
+        p.join(timeout=60)
+    problems = [m for r in sorted(results) for m in results[r]]
+    assert not problems, problems[:10]
+    assert all(p.exitcode == 0 for p in procs)
+
+
+@pytest.mark.timeout(500)
+def test_peer_exchange_two_ranks_one_shot():
+    _run(2, 1)
+
+
+@pytest.mark.timeout(500)
+def test_peer_exchange_two_ranks_two_shot():
+    _run(2, 2)
+
+
+@pytest.mark.timeout(500)
+def test_peer_exchange_three_ranks_auto_two_shot_u16():
+    """world 3 (auto picks two-shot): 2^13 cells = 256 words split into 128-B
+    segments of 96, 96 and 64 words; k = 130 makes the cells u16."""
+    _run(3, 0, c=13, k=130)
