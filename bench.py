@@ -211,7 +211,7 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean["slice_s"] * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype(w),
         "data": "synthetic (oracle.synthetic_slice)",
-        "config": _config(w, world),
+        "config": dict(_config(w, world), counter=args.counter),
         "estimate_ms_per_slice": mean["estimate_s"] * 1e3,
         "scan_mpps": w["packets"] / mean["scan_s"] / 1e6,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -257,7 +257,8 @@ def run_gpu(args, rank, world, local_rank):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     w = WORKLOAD
-    cfg = vb.EstimatorConfig(w["g"], w["c"], w["k"], seed=w["seed"], partition=w["partition"])
+    cfg = vb.EstimatorConfig(w["g"], w["c"], w["k"], seed=w["seed"], partition=w["partition"],
+                             counter_kind=args.counter)
     pool = cfg.build_pool(device=dev)
     pipe = vb.Pipeline(pool, cfg, w["k_prime"], floor=w["floor"])
     h = pool.handle
@@ -426,7 +427,8 @@ def run_gpu(args, rank, world, local_rank):
         "g0": (nh * (32 * w["g"] + 12) if args.incremental == "off" else None),
         "scan": n * 40,                                # 8 B pair + one 32 B sector write
         "bitmap": S * pool.cell_bytes + S // 8,        # pool read + bitmap write
-        "sweep": 2 * pool.cell_bytes * 2 * pool.max_block_size,
+        "sweep": (2 * pool.cell_bytes * 2 * pool.max_block_size if args.counter == "at" else
+                  2 * pool.cell_bytes * S if args.counter == "dr" else 0),
         "final": nh * (4 + 8 + 8 + 8 + 8 + 1),
         "registry": nh * 32,
         "sort": nh * 8 * 4 * 2,
@@ -456,6 +458,10 @@ def run_gpu(args, rank, world, local_rank):
         "scan_update_mpps": n / ((per_kind["scan"]["ms_total"] + per_kind["sweep"]["ms_total"])
                                  / args.steps / 1e3) / 1e6,
         "reports_per_slice": nh,
+        "maintain_ms_per_slice": per_kind["sweep"]["ms_total"] / args.steps,
+        "maintain_note": ("AT: the two due blocks (pools.py:221-249)" if args.counter == "at" else
+                          "DR: every cell slides (pools.py:339-349)" if args.counter == "dr" else
+                          "TS: no maintenance (pools.py:399-401)"),
         "kernels": per_kind,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
@@ -515,6 +521,9 @@ def main():
                     help="workload shape (BASELINE.json configs); cfg2 is the headline")
     ap.add_argument("--incremental", choices=("on", "off"), default="on",
                     help="exact incremental g0 through the inverse index (VATE_OPT_INCREMENTAL)")
+    ap.add_argument("--counter", choices=("at", "dr", "ts"), default="at",
+                    help="counter pool: AT (the product) or the DR / TS comparators "
+                         "(pools.py:301-410) for the paper's maintenance contrast")
     ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
                     help="N > 1 slice exchange: fused peer-memory merge (default) or NCCL "
                          "all-gathers + merge kernel")

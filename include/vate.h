@@ -42,6 +42,7 @@ enum vate_status {
 
 enum vate_where { VATE_HOST = 0, VATE_DEVICE = 1, VATE_STAGED = 2 };
 enum vate_partition { VATE_TAIL = 0, VATE_LOWDEV = 1 }; /* pools.py:27-29 */
+enum vate_kind { VATE_AT = 0, VATE_DR = 1, VATE_TS = 2 };  /* estimator.py COUNTER_KINDS */
 
 typedef struct vate_pool vate_pool;   /* AtPool on one device               */
 typedef struct vate_hosts vate_hosts; /* SlidingHostSet on the same device  */
@@ -54,6 +55,14 @@ int vate_device_count(int* n);
 /* ---- pool lifecycle: AtPool.__init__ (pools.py:72-100), make_pool
  *      (pools.py:413-421), _validate_pool_shape (pools.py:57-64) --------- */
 int vate_pool_create(vate_pool** out, int c, int k, int partition, int device);
+/* make_pool(kind, ...) (pools.py:413-421) for every counter kind: VATE_AT as
+ * above, or the comparators VATE_DR (DrPool, pools.py:301-353) and VATE_TS
+ * (TsPool, pools.py:356-410), which share the scan, registry, g0 and float
+ * path but not snapshots or the replica merge (VATE_ECONFIG).  partition is
+ * ignored for DR/TS, as make_pool ignores it. */
+int vate_pool_create_kind(vate_pool** out, int kind, int c, int k, int partition, int device);
+/* the pool's kind and, for TS, its own slice index (TsPool.t, pools.py:360) */
+int vate_pool_kind(const vate_pool* p, int* kind, uint64_t* slice_index);
 int vate_pool_destroy(vate_pool* p);
 /* bact0 (pools.py:96), cell storage bytes (1, 2 or 4), the stream (cudaStream_t) */
 int vate_pool_info(const vate_pool* p, int32_t* bact0, int32_t* cell_bytes, void** stream);
@@ -149,6 +158,9 @@ int vate_inactive_mask(vate_pool* p, const uint64_t* idx, uint64_t n, int k_prim
                        uint8_t* out, int where);
 /* PackedArray.get through AtPool.cells (bitpack.py:88-95). */
 int vate_get_cells(vate_pool* p, const uint64_t* idx, uint64_t n, uint32_t* out, int where);
+/* the same for every kind, 64-bit values (TS cells hold u64 slice indices,
+ * TS_UNSET = 2^64-1, counters.py:159) */
+int vate_get_cells64(vate_pool* p, const uint64_t* idx, uint64_t n, uint64_t* out, int where);
 /* inactive_virtual_counts (estimator.py:114-123): g0 per host. */
 int vate_host_g0(vate_pool* p, uint64_t g, uint64_t cell_stream, const uint64_t* aips,
                  uint64_t n, int k_prime, int32_t* g0, int where);

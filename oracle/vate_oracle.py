@@ -304,6 +304,104 @@ class OraclePool:
         return pool
 
 
+class OracleDrPool:
+    """2**c distance recorders (pools.py:301-353): fill k, set -> 0, every
+    recorder slides by one per slice saturating at k; inactive iff v >= k'."""
+
+    kind = "dr"
+
+    def __init__(self, c: int, k: int):
+        if not 1 <= k <= K_LIMIT or c > 32 or c < 1 or (1 << c) < 2 * k:
+            raise OracleConfigError("bad pool shape")          # pools.py:57-64
+        self.c, self.k, self.size = c, k, 1 << c
+        self.cells = np.full(self.size, k, dtype=np.int64)      # pools.py:311
+
+    def set_cells(self, idx) -> None:
+        i = np.asarray(idx).astype(np.int64)
+        if i.size and (i.min() < 0 or i.max() >= self.size):
+            raise ValueError("cell index out of range")
+        self.cells[i] = 0                                       # pools.py:314-315
+
+    def _check_width(self, k_prime: int) -> None:
+        if not 1 <= k_prime <= self.k:
+            raise ValueError(f"k'={k_prime} outside [1, {self.k}]")
+
+    def inactive_mask(self, idx, k_prime: int) -> np.ndarray:
+        self._check_width(k_prime)
+        return self.cells[np.asarray(idx).astype(np.int64)] >= k_prime   # pools.py:326-329
+
+    def inactive_bits(self, k_prime: int) -> np.ndarray:
+        self._check_width(k_prime)
+        return self.cells >= k_prime
+
+    def count_inactive(self, k_prime: int) -> int:
+        return int(self.inactive_bits(k_prime).sum())           # pools.py:331-337
+
+    def advance(self):
+        """pools.py:339-349: ((), every cell visited, cells reaching k)."""
+        slid = np.minimum(self.cells + 1, self.k)
+        cleared = int(((self.cells < self.k) & (slid == self.k)).sum())
+        self.cells = slid
+        return (), self.size, cleared
+
+
+class OracleTsPool:
+    """2**c last-seen slice indices (pools.py:356-410): u64, TS_UNSET when never
+    set, set -> the pool's slice index t, advance -> t += 1 with no maintenance;
+    inactive iff unset or t - last >= k' (u64 arithmetic)."""
+
+    kind = "ts"
+    UNSET = MASK64                                              # counters.py:159
+
+    def __init__(self, c: int, k: int):
+        if not 1 <= k <= K_LIMIT or c > 32 or c < 1 or (1 << c) < 2 * k:
+            raise OracleConfigError("bad pool shape")
+        self.c, self.k, self.size = c, k, 1 << c
+        self.cells = np.full(self.size, self.UNSET, dtype=U64)
+        self.t = 0
+
+    def set_cells(self, idx) -> None:
+        i = np.asarray(idx).astype(np.int64)
+        if i.size and (i.min() < 0 or i.max() >= self.size):
+            raise ValueError("cell index out of range")
+        self.cells[i] = U64(self.t)                             # pools.py:363-364
+
+    def _check_width(self, k_prime: int) -> None:
+        if not 1 <= k_prime <= self.k:
+            raise ValueError(f"k'={k_prime} outside [1, {self.k}]")
+
+    def _inactive(self, last, k_prime):
+        with np.errstate(over="ignore"):
+            age = U64(self.t) - last                            # wraps for UNSET
+        return (last == U64(self.UNSET)) | (age >= U64(k_prime))   # pools.py:375-380
+
+    def inactive_mask(self, idx, k_prime: int) -> np.ndarray:
+        self._check_width(k_prime)
+        return self._inactive(self.cells[np.asarray(idx).astype(np.int64)], k_prime)
+
+    def inactive_bits(self, k_prime: int) -> np.ndarray:
+        self._check_width(k_prime)
+        return self._inactive(self.cells, k_prime)
+
+    def count_inactive(self, k_prime: int) -> int:
+        return int(self.inactive_bits(k_prime).sum())
+
+    def advance(self):
+        self.t += 1                                             # pools.py:399-401
+        return (), 0, 0
+
+
+def make_oracle_pool(kind: str, c: int, k: int, partition: str = "tail"):
+    """make_pool (pools.py:413-421) for the oracle's pool kinds."""
+    if kind == "at":
+        return OraclePool(c, k, partition)
+    if kind == "dr":
+        return OracleDrPool(c, k)
+    if kind == "ts":
+        return OracleTsPool(c, k)
+    raise OracleConfigError(f"unknown counter kind {kind!r}")
+
+
 def pack_cells(cells: np.ndarray, width: int) -> bytes:
     """w-bit cells, LSB-first, into little-endian u64 words, zero pad (bitpack.py:26-78).
 
@@ -450,11 +548,11 @@ class OraclePipeline:
     SCAN_CHUNK = 1 << 15   # pipeline.py:26
 
     def __init__(self, cfg: OracleConfig, k_prime: int, floor: float = 0.0,
-                 workers: int = 1):
+                 workers: int = 1, kind: str = "at"):
         if not 1 <= k_prime <= cfg.k:
             raise ValueError(f"k'={k_prime} outside [1, {cfg.k}]")
         self.cfg = cfg
-        self.pool = OraclePool(cfg.c, cfg.k, cfg.partition)
+        self.pool = make_oracle_pool(kind, cfg.c, cfg.k, cfg.partition)
         self.hosts = OracleHosts(cfg.k)
         self.k_prime = k_prime
         self.floor = floor

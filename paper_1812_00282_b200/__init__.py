@@ -7,19 +7,19 @@ Importing this package fails loudly if the library has not been built.
 """
 
 from .errors import ConfigError, TraceError, TraceOrderError, TraceParseError
-from .pools import (LOW_DEVIATION, PARTITIONS, TAIL_REMAINDER, AtPool, MaintenanceReport,
-                    make_pool)
+from .pools import (LOW_DEVIATION, PARTITIONS, TAIL_REMAINDER, AtPool, DrPool, MaintenanceReport,
+                    TsPool, make_pool)
 from .estimator import (EstimateReport, EstimatorConfig, HostReports, estimate_host,
                         estimate_hosts, estimate_hosts_soa, estimate_linear, host_cells,
                         inactive_virtual_counts, pair_cells, record_packed, record_pairs,
                         reports_from_counts, reports_from_counts_soa)
 from .pipeline import Pipeline, SliceStats, SlidingHostSet
-from .counters import MAX_K, WindowConfig, ats_bits
+from .counters import MAX_K, TS_UNSET, WindowConfig, ats_bits, dr_bits
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "AtPool", "ConfigError", "EstimateReport", "EstimatorConfig", "HostReports",
+    "AtPool", "ConfigError", "DrPool", "TsPool", "TS_UNSET", "dr_bits", "EstimateReport", "EstimatorConfig", "HostReports",
     "LOW_DEVIATION", "MAX_K", "MaintenanceReport", "PARTITIONS", "Pipeline", "SliceStats",
     "SlidingHostSet", "TAIL_REMAINDER", "TraceError", "TraceOrderError", "TraceParseError",
     "WindowConfig", "ats_bits", "estimate_host", "estimate_hosts", "estimate_hosts_soa",

@@ -49,6 +49,9 @@ _SIGS = {
     "vate_abi_version": ([], _int),
     "vate_device_count": ([C.POINTER(_int)], _int),
     "vate_pool_create": ([C.POINTER(_p), _int, _int, _int, _int], _int),
+    "vate_pool_create_kind": ([C.POINTER(_p), _int, _int, _int, _int, _int], _int),
+    "vate_pool_kind": ([_p, C.POINTER(_int), _pu64], _int),
+    "vate_get_cells64": ([_p, _p, _u64, _p, _int], _int),
     "vate_pool_destroy": ([_p], _int),
     "vate_pool_info": ([_p, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_p)], _int),
     "vate_pool_sync": ([_p], _int),

@@ -8,6 +8,7 @@ csrc/vate_pool.cu (k_sweep, the comparison-only preserve).
 from dataclasses import dataclass
 
 MAX_K = 1 << 15
+TS_UNSET = (1 << 64) - 1   # counters.py:159: a TS cell never set
 
 
 @dataclass(frozen=True)
@@ -31,3 +32,8 @@ class WindowConfig:
 def ats_bits(k: int) -> int:
     """Bits per asynchronous timestamp: ceil(log2(2k+1)) (counters.py:52-54)."""
     return (2 * k).bit_length()
+
+
+def dr_bits(k: int) -> int:
+    """Bits per distance recorder: ceil(log2(k+1)) (counters.py:132-134)."""
+    return k.bit_length()

@@ -1,0 +1,254 @@
+// vate_compare.cu -- the comparator pools of the reference on the device
+// (pools.py:301-410): DrPool (VDRE distance recorders)
+// and TsPool (plain last-seen slice indices).  They exist to reproduce the
+// paper's VATE-vs-VDRE maintenance contrast and the
+// reference's AT == DR == TS estimate identity (test_estimator.py:233-255),
+// so they share the AT pool's handle, scan kernels (ConstRule store), host
+// registry, g0 gather and float path; only the cell predicate, the slice
+// advance and the cell type differ:
+//
+//   DR: dr_bits(k) = k.bit_length() bits (counters.py:132-134) -> u8 / u16
+//       cells, filled with k; set -> 0; advance -> v = min(v+1, k) for EVERY
+//       cell (the whole-pool sweep VATE avoids), cleared = cells reaching k;
+//       inactive(k') <=> v >= k'                           (pools.py:301-353)
+//   TS: u64 cells, filled with TS_UNSET = 2^64-1 (counters.py:159); set -> t
+//       (the pool's own slice index); advance -> t += 1, nothing maintained;
+//       inactive(k') <=> v == TS_UNSET or t - v >= k' (u64)  (pools.py:356-410)
+#include <string>
+
+#include "vate_internal.cuh"
+
+namespace vate {
+
+constexpr unsigned long long kTsUnset = ~0ull;  // counters.py:159
+
+struct CmpPred {
+  int kind;
+  uint32_t kp;
+  unsigned long long now;
+  template <typename T>
+  __device__ __forceinline__ bool inactive(T v) const {
+    if (kind == VATE_DR) return (uint64_t)v >= kp;
+    const unsigned long long x = (unsigned long long)v;
+    return x == kTsUnset || now - x >= (unsigned long long)kp;
+  }
+};
+
+template <typename T>
+__global__ void k_cmp_fill(T* __restrict__ cells, uint64_t n, T value) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    cells[i] = value;
+}
+
+// Inactive bitmap + P for the comparators: one 32-cell word per thread, 16-byte
+// loads (32 cells = 32 / 64 / 256 bytes for u8 / u16 / u64).
+template <typename T>
+__global__ void __launch_bounds__(256) k_cmp_bitmap(const T* __restrict__ cells, uint64_t size,
+                                                    CmpPred P, uint32_t* __restrict__ bitmap,
+                                                    uint64_t nwords,
+                                                    unsigned long long* pool_inactive) {
+  constexpr int NV = (int)sizeof(T) * 2;  // uint4 per 32 cells
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned local = 0;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
+    const uint64_t i0 = w * 32;
+    uint32_t bits = 0;
+    if (i0 + 32 <= size) {
+      uint4 r[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) r[v] = __ldcs(reinterpret_cast<const uint4*>(cells + i0) + v);
+      const T* e = reinterpret_cast<const T*>(r);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) bits |= (uint32_t)P.inactive(e[j]) << j;
+    } else {
+      for (uint64_t j = 0; i0 + j < size; ++j) bits |= (uint32_t)P.inactive(cells[i0 + j]) << j;
+    }
+    bitmap[w] = bits;
+    local += __popc(bits);
+  }
+  local = __reduce_add_sync(0xffffffffu, local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(pool_inactive, (unsigned long long)local);
+}
+
+template <typename T>
+__global__ void k_cmp_mask(const T* __restrict__ cells, uint64_t size,
+                           const uint64_t* __restrict__ idx, uint64_t n, CmpPred P,
+                           uint8_t* __restrict__ out, unsigned long long* err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t c = idx[i];
+    if (c >= size) {
+      *err = 1;
+      out[i] = 0;
+      continue;
+    }
+    out[i] = P.inactive(cells[c]);
+  }
+}
+
+template <typename T>
+__global__ void k_get64(const T* __restrict__ cells, uint64_t size, const uint64_t* __restrict__ idx,
+                        uint64_t n, unsigned long long* __restrict__ out, unsigned long long* err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t c = idx[i];
+    if (c >= size) {
+      *err = 1;
+      out[i] = 0;
+      continue;
+    }
+    out[i] = (unsigned long long)cells[c];
+  }
+}
+
+// DrPool.advance_slice (pools.py:339-349): every recorder slides by one,
+// saturating at k; a streaming read-modify-write of the whole pool, 16 bytes
+// per thread per step (HBM-bound: 2 * cell_bytes * 2^c per slice).
+template <typename T>
+__global__ void __launch_bounds__(256) k_dr_slide(T* __restrict__ cells, uint64_t size, uint32_t k,
+                                                  unsigned long long* cleared) {
+  constexpr int PER = 16 / (int)sizeof(T);
+  const uint64_t nvec = size / PER;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned local = 0;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nvec; q += stride) {
+    uint4 r = __ldcs(reinterpret_cast<const uint4*>(cells) + q);
+    T* e = reinterpret_cast<T*>(&r);
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const uint32_t v = e[j];
+      if (v < k) {
+        local += (v + 1 == k);
+        e[j] = (T)(v + 1);
+        any = true;
+      }
+    }
+    if (any) __stcs(reinterpret_cast<uint4*>(cells) + q, r);
+  }
+  // tail (size < PER only happens for tiny pools)
+  for (uint64_t i = nvec * PER + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < size;
+       i += stride) {
+    const uint32_t v = cells[i];
+    if (v < k) {
+      local += (v + 1 == k);
+      cells[i] = (T)(v + 1);
+    }
+  }
+  local = __reduce_add_sync(0xffffffffu, local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(cleared, (unsigned long long)local);
+}
+
+template <typename F>
+static int with_cmp_cell(const vate_pool* p, F f) {
+  if (p->kind == VATE_TS) return f(uint64_t{});
+  if (p->cell_bytes == 1) return f(uint8_t{});
+  return f(uint16_t{});
+}
+
+int cmp_fill(vate_pool* p) {
+  const uint64_t S = p->L.size;
+  return with_cmp_cell(p, [&](auto tag) -> int {
+    using T = decltype(tag);
+    const T init = p->kind == VATE_DR ? (T)p->k : (T)kTsUnset;
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(S, kThreads), kThreads, 0, k_cmp_fill<T>, (T*)p->cells,
+                S, init);
+    return VATE_OK;
+  });
+}
+
+int cmp_build_bitmap(vate_pool* p, int k_prime) {
+  const uint64_t nwords = (p->L.size + 31) / 32;
+  int rc = p->bitmap.ensure(nwords * 4 + 16);
+  if (rc) return rc;
+  VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_P, 0, 8, p->stream));
+  const CmpPred P{p->kind, (uint32_t)k_prime, p->ts_now};
+  rc = with_cmp_cell(p, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_BITMAP, grid_for(nwords, 256, 148u * 16u), 256, 0, k_cmp_bitmap<T>,
+                (const T*)p->cells, p->L.size, P, p->bitmap.as<uint32_t>(), nwords,
+                p->d_ctr + C_P);
+    return VATE_OK;
+  });
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_P, p->d_ctr + C_P, 8, cudaMemcpyDeviceToHost, p->stream));
+  return VATE_OK;
+}
+
+// Blocks are reported as (-1, -1): the reference's MaintenanceReport(()) for
+// DR / TS (pools.py:349, :401).
+int cmp_advance_async(vate_pool* p) {
+  p->adv_blocks[0] = p->adv_blocks[1] = -1;
+  VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_CLEARED, 0, 8, p->stream));
+  if (p->kind == VATE_DR) {
+    p->adv_maint = p->L.size;
+    int rc = with_cmp_cell(p, [&](auto tag) -> int {
+      using T = decltype(tag);
+      VATE_LAUNCH(p, VATE_K_SWEEP, grid_for(p->L.size / (16 / sizeof(T)) + 1, 256, 148u * 16u), 256,
+                  0, k_dr_slide<T>, (T*)p->cells, p->L.size, (uint32_t)p->k, p->d_ctr + C_CLEARED);
+      return VATE_OK;
+    });
+    if (rc) return rc;
+  } else {
+    p->adv_maint = 0;
+    p->ts_now += 1;  // TsPool.advance_slice (pools.py:399-401)
+  }
+  VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_CLEARED, p->d_ctr + C_CLEARED, 8, cudaMemcpyDeviceToHost,
+                            p->stream));
+  VATE_CUDA(cudaEventRecord(p->ev_adv, p->stream));
+  p->adv_pending = true;
+  return VATE_OK;
+}
+
+int cmp_inactive_mask(vate_pool* p, const uint64_t* d_idx, uint64_t n, int k_prime,
+                      uint8_t* out_dev) {
+  const CmpPred P{p->kind, (uint32_t)k_prime, p->ts_now};
+  return with_cmp_cell(p, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(n, kThreads), kThreads, 0, k_cmp_mask<T>,
+                (const T*)p->cells, p->L.size, d_idx, n, P, out_dev, p->d_ctr + C_ERR);
+    return VATE_OK;
+  });
+}
+
+}  // namespace vate
+
+using namespace vate;
+
+extern "C" {
+
+int vate_get_cells64(vate_pool* p, const uint64_t* idx, uint64_t n, uint64_t* out, int where) {
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  const void* d_idx;
+  rc = stage_in(p, p->in_a, idx, n * 8, where, &d_idx);
+  if (rc) return rc;
+  rc = p->out_buf.ensure(n * 8);
+  if (rc) return rc;
+  auto launch = [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(n, kThreads), kThreads, 0, k_get64<T>, (const T*)p->cells,
+                p->L.size, (const uint64_t*)d_idx, n, p->out_buf.as<unsigned long long>(),
+                p->d_ctr + C_ERR);
+    return VATE_OK;
+  };
+  if (p->kind == VATE_TS) rc = launch(uint64_t{});
+  else if (p->cell_bytes == 1) rc = launch(uint8_t{});
+  else if (p->cell_bytes == 2) rc = launch(uint16_t{});
+  else rc = launch(uint32_t{});
+  if (rc) return rc;
+  VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_ERR, p->d_ctr + C_ERR, 8, cudaMemcpyDeviceToHost, p->stream));
+  VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_ERR, 0, 8, p->stream));
+  VATE_CUDA(cudaMemcpyAsync(out, p->out_buf.ptr, n * 8, cudaMemcpyDeviceToHost, p->stream));
+  return sync_small(p);
+}
+
+int vate_pool_kind(const vate_pool* p, int* kind, uint64_t* slice_index) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  if (kind) *kind = p->kind;
+  if (slice_index) *slice_index = p->ts_now;
+  return VATE_OK;
+}
+
+}  // extern "C"

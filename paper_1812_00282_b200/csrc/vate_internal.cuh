@@ -144,6 +144,22 @@ __device__ __forceinline__ void for_word_clocks(uint64_t i0, uint32_t cnt, const
   }
 }
 
+// What a scan / set_many stores into a cell: the AT pool stores the clock of
+// the cell's block (pools.py:164-178); the comparators store a constant.
+struct AtRule {
+  Layout L;
+  uint32_t bact0;
+  template <typename T>
+  __device__ __forceinline__ T value(uint64_t cell) const {
+    return (T)clock_of(bact0, block_of(cell, L), L.B);
+  }
+};
+struct ConstRule {
+  unsigned long long v;  // DrPool: 0 (pools.py:314-315); TsPool: the slice index (:363-364)
+  template <typename T>
+  __device__ __forceinline__ T value(uint64_t) const { return (T)v; }
+};
+
 // Inactive for width k' (pools.py:187-193): sentinel, or (act + 2k - v) mod 2k
 // >= k'.  For stored values above 2k (only reachable through a hand-made
 // snapshot) the reference's uint64 wraparound is reproduced exactly.
@@ -223,6 +239,8 @@ struct IncIndex {
 
 struct vate_pool {
   int device = 0;
+  int kind = 0;            // VATE_AT, or a comparator: VATE_DR / VATE_TS (vate_compare.cu)
+  uint64_t ts_now = 0;     // TsPool.t: advances taken (pools.py:360)
   cudaStream_t stream = nullptr;
   int c = 0, k = 0, partition = 0;
   uint32_t width = 0;      // ats_bits(k) (counters.py:52-54)

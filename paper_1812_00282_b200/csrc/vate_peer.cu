@@ -239,6 +239,7 @@ int vate_peer_create(vate_peer** out, vate_pool* p, vate_hosts* h, int rank, int
   int rc = enter(p);
   if (rc) return rc;
   if (!h || h->pool != p) return set_error(VATE_EVALUE, "registry does not belong to the pool");
+  if (p->kind != VATE_AT) return set_error(VATE_ECONFIG, "the replica merge is defined for the AT pool only");
   if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
     return set_error(VATE_EVALUE, "rank/world out of range (world <= 64)");
   if (key_cap < 1) return set_error(VATE_EVALUE, "key_cap must be >= 1");

@@ -142,6 +142,18 @@ static int with_cell(int bytes, F f) {
   }
 }
 
+// Cell type and store rule of a pool: AT stores its block clock; the DR / TS
+// comparators store a constant per slice (0, or the slice index).
+template <typename F>
+static int with_store(vate_pool* p, F f) {
+  if (p->kind == VATE_AT)
+    return with_cell(p->cell_bytes, [&](auto tag) { return f(tag, AtRule{p->L, p->bact0}); });
+  const ConstRule r{p->kind == VATE_DR ? 0ull : p->ts_now};
+  if (p->kind == VATE_TS) return f(uint64_t{}, r);
+  if (p->cell_bytes == 1) return f(uint8_t{}, r);
+  return f(uint16_t{}, r);
+}
+
 __device__ __forceinline__ unsigned block_sum(unsigned v) {
   __shared__ unsigned warp_sums[32];
   v = __reduce_add_sync(0xffffffffu, v);
@@ -173,16 +185,15 @@ __global__ void k_fill(T* cells, uint64_t n, T value) {
 // read-modify-write.  The registry step issues all U first-probe loads (one
 // 16-byte sector each) before resolving any, so a thread keeps U independent
 // requests in flight; only misses take the probing insert.
-template <typename T, bool REG, int U, bool CHECK = false>
+template <typename T, bool REG, int U, bool CHECK = false, typename Rule>
 __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint64_t (&bip)[U],
                                            int m, T* __restrict__ cells, const HashParams& H,
-                                           const Layout& L, uint32_t bact0, const RegRef& R,
-                                           long long t) {
+                                           const Rule& rule, const RegRef& R, long long t) {
 #pragma unroll
   for (int q = 0; q < U; ++q) {
     if (q < m) {
       const uint64_t cell = cell_of(aip[q], slot_of(bip[q], H), H);
-      const T act = (T)clock_of(bact0, block_of(cell, L), L.B);
+      const T act = rule.template value<T>(cell);
       // CHECK: skew-tolerant form for heavy hitters -- read first (L1 keeps hot
       // lines) and store only if the cell does not already hold the clock
       if (!CHECK || cells[cell] != act) cells[cell] = act;
@@ -209,10 +220,10 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
   }
 }
 
-template <typename T, bool REG, int V = 2, bool CHECK = false>  // V uint4 loads per iteration
+template <typename T, bool REG, int V = 2, bool CHECK = false, typename Rule = AtRule>  // V uint4 loads per iteration
 __global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
-    Layout L, uint32_t bact0, RegRef R, long long t) {
+    Rule rule, RegRef R, long long t) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   for (; i < npairs2; i += V * stride) {
@@ -229,26 +240,26 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
         a[2 * v] = b[2 * v] = a[2 * v + 1] = b[2 * v + 1] = 0;
       }
     }
-    scan_batch<T, REG, 2 * V, CHECK>(a, b, m, cells, H, L, bact0, R, t);
+    scan_batch<T, REG, 2 * V, CHECK>(a, b, m, cells, H, rule, R, t);
   }
 }
 
-template <typename T, bool REG>
+template <typename T, bool REG, typename Rule = AtRule>
 __global__ void __launch_bounds__(kThreads) k_scan_packed8(
     const uint2* __restrict__ pairs, uint64_t n, T* __restrict__ cells, HashParams H,
-    Layout L, uint32_t bact0, RegRef R, long long t) {
+    Rule rule, RegRef R, long long t) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint2 q = pairs[i];
     const uint64_t a[1] = {q.x}, b[1] = {q.y};
-    scan_batch<T, REG, 1>(a, b, 1, cells, H, L, bact0, R, t);
+    scan_batch<T, REG, 1>(a, b, 1, cells, H, rule, R, t);
   }
 }
 
-template <typename T, bool REG>
+template <typename T, bool REG, typename Rule = AtRule>
 __global__ void __launch_bounds__(kThreads) k_scan_u64(
     const uint64_t* __restrict__ aips, const uint64_t* __restrict__ bips, uint64_t n,
-    T* __restrict__ cells, HashParams H, Layout L, uint32_t bact0, RegRef R, long long t) {
+    T* __restrict__ cells, HashParams H, Rule rule, RegRef R, long long t) {
   constexpr int U = 4;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += U * stride) {
@@ -264,7 +275,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_u64(
         m = q + 1;
       }
     }
-    scan_batch<T, REG, U>(a, b, m, cells, H, L, bact0, R, t);
+    scan_batch<T, REG, U>(a, b, m, cells, H, rule, R, t);
   }
 }
 
@@ -283,17 +294,17 @@ __global__ void k_host_cells(const uint64_t* __restrict__ aips, uint64_t n, uint
     out[i] = cell_of(aips[i / g], i % g, H);
 }
 
-template <typename T>
+template <typename T, typename Rule>
 __global__ void k_set_cells(const uint64_t* __restrict__ idx, uint64_t n, T* __restrict__ cells,
-                            Layout L, uint32_t bact0, unsigned long long* err) {
+                            uint64_t size, Rule rule, unsigned long long* err) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint64_t c = idx[i];
-    if (c >= L.size) {
+    if (c >= size) {
       *err = 1;
       continue;
     }
-    cells[c] = (T)clock_of(bact0, block_of(c, L), L.B);
+    cells[c] = rule.template value<T>(c);
   }
 }
 
@@ -687,8 +698,23 @@ using namespace vate;
 // ---------------------------------------------------------------------------
 
 namespace vate {
+// comparator pools (vate_compare.cu)
+int cmp_fill(vate_pool* p);
+int cmp_build_bitmap(vate_pool* p, int k_prime);
+int cmp_advance_async(vate_pool* p);
+int cmp_inactive_mask(vate_pool* p, const uint64_t* d_idx, uint64_t n, int k_prime,
+                      uint8_t* out_dev);
+
+static int require_at(const vate_pool* p, const char* what) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  if (p->kind != VATE_AT)
+    return set_error(VATE_ECONFIG, std::string(what) + " is defined for the AT pool only");
+  return VATE_OK;
+}
+
 // Build the k' inactive bitmap and enqueue P into h_ctr[C_P] (not synced).
 int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
+  if (p->kind != VATE_AT) return cmp_build_bitmap(p, k_prime);  // opt_inc is 0 there
   const uint64_t nwords = (p->L.size + 31) / 32;
   int rc = p->bitmap.ensure(nwords * 4 + 16);
   if (rc) return rc;
@@ -735,9 +761,11 @@ int vate_device_count(int* n) {
   return VATE_OK;
 }
 
-int vate_pool_create(vate_pool** out, int c, int k, int partition, int device) {
+static int pool_create(vate_pool** out, int kind, int c, int k, int partition, int device) {
   if (!out) return set_error(VATE_EVALUE, "null output pointer");
   *out = nullptr;
+  if (kind != VATE_AT && kind != VATE_DR && kind != VATE_TS)
+    return set_error(VATE_ECONFIG, "unknown counter kind " + std::to_string(kind));
   // _validate_pool_shape (pools.py:57-64) and AtPool.__init__ (pools.py:72-95)
   if (k < 1 || k > kMaxK)
     return set_error(VATE_ECONFIG, "k must be in [1, 32768], got " + std::to_string(k));
@@ -748,6 +776,7 @@ int vate_pool_create(vate_pool** out, int c, int k, int partition, int device) {
                                        " non-empty blocks");
   if (partition != VATE_TAIL && partition != VATE_LOWDEV)
     return set_error(VATE_ECONFIG, "unknown partition method");
+  if (kind != VATE_AT) partition = VATE_TAIL;  // make_pool passes it to AtPool only
   const uint64_t S = 1ull << c;
   const uint32_t B = 2u * (uint32_t)k;
   Layout L{};
@@ -755,7 +784,10 @@ int vate_pool_create(vate_pool** out, int c, int k, int partition, int device) {
   L.B = B;
   L.k = (uint32_t)k;
   L.part = partition;
-  if (partition == VATE_TAIL) {
+  if (kind != VATE_AT) {  // no blocks: only the size is used
+    L.da = make_div(1);
+    L.da1 = make_div(1);
+  } else if (partition == VATE_TAIL) {
     const uint64_t a = S / (B - 1), b = S % (B - 1);
     if (b == 0)
       return set_error(VATE_ECONFIG,
@@ -775,8 +807,12 @@ int vate_pool_create(vate_pool** out, int c, int k, int partition, int device) {
   p->c = c;
   p->k = k;
   p->partition = partition;
+  p->kind = kind;
   p->width = 32u - (uint32_t)__builtin_clz(B);  // (2k).bit_length()
-  p->cell_bytes = p->width <= 8 ? 1 : (p->width <= 16 ? 2 : 4);
+  if (kind == VATE_DR) p->width = 32u - (uint32_t)__builtin_clz((uint32_t)k);  // dr_bits
+  if (kind == VATE_TS) p->width = 64;
+  p->cell_bytes = p->width <= 8 ? 1 : (p->width <= 16 ? 2 : (p->width <= 32 ? 4 : 8));
+  if (kind != VATE_AT) p->opt_inc = 0;  // comparators: full g0 gather every estimate
   p->L = L;
   int rc = VATE_OK;
   cudaError_t e = cudaSetDevice(device);
@@ -798,12 +834,15 @@ int vate_pool_create(vate_pool** out, int c, int k, int partition, int device) {
   if (rc == VATE_OK) {
     memset(p->h_ctr, 0, C_N * sizeof(unsigned long long));
     // every cell starts at the sentinel 2k (ats_init, counters.py:57-59)
-    rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
-      using T = decltype(tag);
-      VATE_LAUNCH(p, VATE_K_OTHER, grid_for(S, kThreads), kThreads, 0, k_fill<T>, (T*)p->cells,
-                  S, (T)B);
-      return VATE_OK;
-    });
+    if (kind != VATE_AT)
+      rc = cmp_fill(p);
+    else
+      rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
+        using T = decltype(tag);
+        VATE_LAUNCH(p, VATE_K_OTHER, grid_for(S, kThreads), kThreads, 0, k_fill<T>, (T*)p->cells,
+                    S, (T)B);
+        return VATE_OK;
+      });
   }
   if (rc == VATE_OK) rc = sync_small(p);
   if (rc != VATE_OK) {
@@ -812,6 +851,14 @@ int vate_pool_create(vate_pool** out, int c, int k, int partition, int device) {
   }
   *out = p;
   return VATE_OK;
+}
+
+int vate_pool_create(vate_pool** out, int c, int k, int partition, int device) {
+  return pool_create(out, VATE_AT, c, k, partition, device);
+}
+
+int vate_pool_create_kind(vate_pool** out, int kind, int c, int k, int partition, int device) {
+  return pool_create(out, kind, c, k, partition, device);
 }
 
 int vate_pool_destroy(vate_pool* p) {
@@ -910,7 +957,7 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     return VATE_OK;
   }
   if (option == VATE_OPT_INCREMENTAL && (value == 0 || value == 1)) {
-    p->opt_inc = (int)value;
+    p->opt_inc = p->kind == VATE_AT ? (int)value : 0;
     if (!value) p->inc.valid = false;
     return VATE_OK;
   }
@@ -976,10 +1023,11 @@ int vate_set_cells(vate_pool* p, const uint64_t* idx, uint64_t n, int where) {
   const void* d_idx;
   rc = stage_in(p, p->in_a, idx, n * 8, where, &d_idx);
   if (rc) return rc;
-  return with_cell(p->cell_bytes, [&](auto tag) -> int {
+  return with_store(p, [&](auto tag, auto rule) -> int {
     using T = decltype(tag);
-    VATE_LAUNCH(p, VATE_K_SCAN, grid_for(n, kThreads), kThreads, 0, k_set_cells<T>,
-                (const uint64_t*)d_idx, n, (T*)p->cells, p->L, p->bact0, p->d_ctr + C_ERR);
+    VATE_LAUNCH(p, VATE_K_SCAN, grid_for(n, kThreads), kThreads, 0,
+                (k_set_cells<T, decltype(rule)>), (const uint64_t*)d_idx, n, (T*)p->cells,
+                p->L.size, rule, p->d_ctr + C_ERR);
     return VATE_OK;
   });
 }
@@ -1004,46 +1052,47 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     rc = stage_in(p, p->in_a, pairs, n * 8, where, &d_pairs);
     if (rc) return rc;
     const bool aligned16 = ((uintptr_t)d_pairs & 15u) == 0;
-    return with_cell(p->cell_bytes, [&](auto tag) -> int {
+    return with_store(p, [&](auto tag, auto rule) -> int {
       using T = decltype(tag);
+      using Rl = decltype(rule);
       if (aligned16 && n >= 2) {
         if (hosts && p->opt_scan_v == 1 && p->opt_scan_check)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 1, true>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 1, true, Rl>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else if (hosts && p->opt_scan_v == 1)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 1>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 1, false, Rl>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else if (hosts && p->opt_scan_v == 4)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 4>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 4, false, Rl>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else if (hosts)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 2, false, Rl>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, false>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, p->L, p->bact0, R,
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, false, 2, false, Rl>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         if (n & 1) {
           const uint2* last = (const uint2*)d_pairs + (n - 1);
           if (hosts)
-            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, true>), last, 1,
-                        (T*)p->cells, H, p->L, p->bact0, R, (long long)t);
+            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, true, Rl>), last, 1,
+                        (T*)p->cells, H, rule, R, (long long)t);
           else
-            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, false>), last, 1,
-                        (T*)p->cells, H, p->L, p->bact0, R, (long long)t);
+            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, false, Rl>), last, 1,
+                        (T*)p->cells, H, rule, R, (long long)t);
         }
       } else {
         if (hosts)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, true>),
-                      (const uint2*)d_pairs, n, (T*)p->cells, H, p->L, p->bact0, R,
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, true, Rl>),
+                      (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
                       (long long)t);
         else
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, false>),
-                      (const uint2*)d_pairs, n, (T*)p->cells, H, p->L, p->bact0, R,
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, false, Rl>),
+                      (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
                       (long long)t);
       }
       return VATE_OK;
@@ -1054,14 +1103,15 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
   if (rc) return rc;
   rc = stage_in(p, p->in_b, bips, n * 8, where, &d_b);
   if (rc) return rc;
-  return with_cell(p->cell_bytes, [&](auto tag) -> int {
+  return with_store(p, [&](auto tag, auto rule) -> int {
     using T = decltype(tag);
+    using Rl = decltype(rule);
     if (hosts)
-      VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_u64<T, true>), (const uint64_t*)d_a,
-                  (const uint64_t*)d_b, n, (T*)p->cells, H, p->L, p->bact0, R, (long long)t);
+      VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_u64<T, true, Rl>), (const uint64_t*)d_a,
+                  (const uint64_t*)d_b, n, (T*)p->cells, H, rule, R, (long long)t);
     else
-      VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_u64<T, false>), (const uint64_t*)d_a,
-                  (const uint64_t*)d_b, n, (T*)p->cells, H, p->L, p->bact0, R, (long long)t);
+      VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_u64<T, false, Rl>), (const uint64_t*)d_a,
+                  (const uint64_t*)d_b, n, (T*)p->cells, H, rule, R, (long long)t);
     return VATE_OK;
   });
 }
@@ -1157,6 +1207,7 @@ int vate_advance_async(vate_pool* p) {
   int rc = enter(p);
   if (rc) return rc;
   if (p->adv_pending) return set_error(VATE_EVALUE, "previous advance not collected");
+  if (p->kind != VATE_AT) return cmp_advance_async(p);
   const uint32_t B = p->L.B, k = p->L.k;
   p->bact0 = (p->bact0 + 1) % B;  // pools.py:228
   const uint32_t z = (B - p->bact0) % B, q = (k + B - p->bact0) % B;  // pools.py:231-232
@@ -1229,7 +1280,9 @@ int vate_inactive_mask(vate_pool* p, const uint64_t* idx, uint64_t n, int k_prim
   if (rc) return rc;
   rc = p->out_buf.ensure(n);
   if (rc) return rc;
-  rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
+  if (p->kind != VATE_AT)
+    rc = cmp_inactive_mask(p, (const uint64_t*)d_idx, n, k_prime, p->out_buf.as<uint8_t>());
+  else rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
     VATE_LAUNCH(p, VATE_K_OTHER, grid_for(n, kThreads), kThreads, 0, k_mask<T>, (const T*)p->cells,
                 (const uint64_t*)d_idx, n, p->L, p->bact0, (uint32_t)k_prime,
@@ -1246,6 +1299,7 @@ int vate_inactive_mask(vate_pool* p, const uint64_t* idx, uint64_t n, int k_prim
 int vate_get_cells(vate_pool* p, const uint64_t* idx, uint64_t n, uint32_t* out, int where) {
   int rc = enter(p);
   if (rc || n == 0) return rc;
+  if (p->kind == VATE_TS) return set_error(VATE_EVALUE, "TS cells are 64-bit: use vate_get_cells64");
   const void* d_idx;
   rc = stage_in(p, p->in_a, idx, n * 8, where, &d_idx);
   if (rc) return rc;
@@ -1271,13 +1325,16 @@ static uint64_t payload_words(const vate_pool* p) {
 }
 
 int vate_snapshot_size(const vate_pool* p, uint64_t* nbytes) {
-  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  int rc = require_at(p, "snapshot_bytes");
+  if (rc) return rc;
   *nbytes = 16 + 8 * payload_words(p);
   return VATE_OK;
 }
 
 int vate_snapshot(vate_pool* p, uint8_t* buf, uint64_t cap, uint64_t* len) {
-  int rc = enter(p);
+  int rc = require_at(p, "snapshot_bytes");
+  if (rc) return rc;
+  rc = enter(p);
   if (rc) return rc;
   const uint64_t nwords = payload_words(p), need = 16 + 8 * nwords;
   if (len) *len = need;
@@ -1305,7 +1362,9 @@ int vate_snapshot(vate_pool* p, uint8_t* buf, uint64_t cap, uint64_t* len) {
 }
 
 int vate_load(vate_pool* p, const uint8_t* buf, uint64_t len) {
-  int rc = enter(p);
+  int rc = require_at(p, "load");
+  if (rc) return rc;
+  rc = enter(p);
   if (rc) return rc;
   // pools.py:271-298
   if (len < 16) return set_error(VATE_ECONFIG, "pool snapshot is truncated");
@@ -1341,7 +1400,9 @@ int vate_load(vate_pool* p, const uint8_t* buf, uint64_t len) {
 // ---- replica merge --------------------------------------------------------------
 
 int vate_dirty_bitmap(vate_pool* p, uint32_t* bitmap_dev) {
-  int rc = enter(p);
+  int rc = require_at(p, "the replica merge");
+  if (rc) return rc;
+  rc = enter(p);
   if (rc) return rc;
   const uint64_t nwords = (p->L.size + 31) / 32;
   return with_cell(p->cell_bytes, [&](auto tag) -> int {
@@ -1353,7 +1414,9 @@ int vate_dirty_bitmap(vate_pool* p, uint32_t* bitmap_dev) {
 }
 
 int vate_merge_dirty(vate_pool* p, const uint32_t* bitmaps_dev, int nranks) {
-  int rc = enter(p);
+  int rc = require_at(p, "the replica merge");
+  if (rc) return rc;
+  rc = enter(p);
   if (rc) return rc;
   if (nranks < 1) return set_error(VATE_EVALUE, "nranks must be >= 1");
   const uint64_t nwords = (p->L.size + 31) / 32;

@@ -22,7 +22,7 @@ import numpy as np
 from . import hashing
 from ._lib import VATE_DEVICE, VATE_HOST, check, lib, ptr
 from .errors import ConfigError
-from .pools import TAIL_REMAINDER, AtPool, make_pool
+from .pools import TAIL_REMAINDER, AtPool, _DevicePool, make_pool
 
 COUNTER_KINDS = ("at", "dr", "ts")
 
@@ -171,8 +171,8 @@ def _u64(x) -> np.ndarray:
 
 
 def _check_pool_cfg(pool, cfg) -> None:
-    if not isinstance(pool, AtPool):
-        raise TypeError("pool must be a device AtPool")
+    if not isinstance(pool, _DevicePool):
+        raise TypeError("pool must be a device pool (AtPool, DrPool or TsPool)")
     if pool.c != cfg.c:
         raise ValueError(f"pool has c={pool.c} but the config has c={cfg.c}")
 

@@ -22,7 +22,7 @@ from . import _lib
 from ._lib import VATE_DEVICE, VATE_HOST, check, lib, ptr
 from .estimator import (EstimatorConfig, HostReports, _check_pool_cfg, _ensure_log_table,
                         _u64, context_pool, log_zp, log_zp_table)
-from .pools import AtPool, MaintenanceReport
+from .pools import AtPool, MaintenanceReport, maintenance_blocks
 
 SCAN_CHUNK = 1 << 15  # pipeline.py:26 (the device scan takes a whole slice at once)
 
@@ -202,7 +202,7 @@ class Pipeline:
         blocks = (C.c_int32 * 2)()
         maint, cleared = C.c_uint64(), C.c_uint64()
         check(lib.vate_advance_result(self.pool.handle, blocks, C.byref(maint), C.byref(cleared)))
-        rep = MaintenanceReport((blocks[0], blocks[1]), maint.value, cleared.value)
+        rep = MaintenanceReport(maintenance_blocks(blocks[0], blocks[1]), maint.value, cleared.value)
         return self._account(t, rep)
 
     def _account(self, t: int, rep: MaintenanceReport) -> MaintenanceReport:
@@ -281,7 +281,8 @@ class Pipeline:
                                   len(host) if host is not None else 0, C.byref(res)))
         if res.prev_collected:
             self._account(self._deferred_t, MaintenanceReport(
-                (res.prev_blocks[0], res.prev_blocks[1]), res.prev_maintained, res.prev_cleared))
+                maintenance_blocks(res.prev_blocks[0], res.prev_blocks[1]), res.prev_maintained,
+                res.prev_cleared))
         self._deferred_t = t
         self.last_active = res.nhosts
         if res.nhosts == 0:

@@ -8,9 +8,11 @@ AtPool extras (layout queries, bact0, snapshot_bytes / save / load), but the
 libvate_b200.so.  Layout queries (block_of, block_range, ...) are closed-form
 integer geometry answered on the host.
 
-Only the AT counter kind has a device implementation; the DR and TS
-comparator pools (pools.py:301-410) are outside this hot path
- and ``make_pool`` rejects them with ConfigError.
+The DR and TS comparator pools (pools.py:301-410) run on the device too
+(csrc/vate_compare.cu): ``DrPool`` (distance recorders, the VDRE baseline
+whose every cell slides every slice) and ``TsPool`` (64-bit last-seen slice
+indices).  They share the scan, host registry, g0 gather and float path with
+``AtPool``; snapshots and the replica merge are AT-only, as in the reference.
 """
 
 from __future__ import annotations
@@ -51,6 +53,11 @@ def _validate_pool_shape(c: int, k: int) -> None:
     if c < 1 or (1 << c) < 2 * k:
         raise ConfigError(
             f"pool of 2^{c} cells cannot hold 2k={2 * k} non-empty blocks")
+
+
+def maintenance_blocks(b0: int, b1: int) -> tuple:
+    """(b0, b1) for the AT pool; () for DR / TS (the library reports -1, -1)."""
+    return () if b0 < 0 else (b0, b1)
 
 
 def _as_u64(idx) -> np.ndarray:
@@ -123,16 +130,17 @@ class BlockLayout:
         return self._a2 + (1 if self._b2 else 0)
 
 
-class AtPool(BlockLayout):
-    """2**c asynchronous timestamps in 2k staggered-clock blocks, on the GPU."""
+class _DevicePool:
+    """Handle plumbing and the pool protocol shared by every device pool kind."""
 
     kind = "at"
+    _kind_code = 0
 
-    def __init__(self, c: int, k: int, partition: str = TAIL_REMAINDER, device: int = 0):
-        super().__init__(c, k, partition)
+    def _create(self, c: int, k: int, partition: str, device: int) -> None:
         self.device = device
         h = C.c_void_p()
-        check(lib.vate_pool_create(C.byref(h), c, k, PARTITIONS.index(partition), device))
+        check(lib.vate_pool_create_kind(C.byref(h), self._kind_code, c, k,
+                                        PARTITIONS.index(partition), device))
         self._h = h
         _lib.track(self)
 
@@ -159,13 +167,8 @@ class AtPool(BlockLayout):
         return bact0.value, cb.value, stream.value
 
     @property
-    def bact0(self) -> int:
-        """Clock of block 0 in the current slice (pools.py:96)."""
-        return self._info()[0]
-
-    @property
     def cell_bytes(self) -> int:
-        """Device bytes per cell: 1 (k <= 127), 2 (k <= 32767) or 4."""
+        """Device bytes per cell: AT 1 (k <= 127), 2 (k <= 32767) or 4; DR 1 or 2; TS 8."""
         return self._info()[1]
 
     @property
@@ -176,12 +179,6 @@ class AtPool(BlockLayout):
     def synchronize(self) -> None:
         check(lib.vate_pool_sync(self._h))
 
-    # --- layout: BlockLayout supplies block_of / block_range / block_sizes ---
-    def block_act(self, bi: int) -> int:
-        if not 0 <= bi < self.nblocks:
-            raise ValueError(f"block index {bi} outside [0, {self.nblocks})")
-        return (self.bact0 + bi) % self.nblocks
-
     # --- counter access (device) -------------------------------------------------
     def set_one(self, i: int) -> None:
         if not 0 <= i < self.size:
@@ -189,7 +186,7 @@ class AtPool(BlockLayout):
         self.set_many(np.array([i], dtype=np.uint64))
 
     def set_many(self, idx) -> None:
-        """Record activity on every cell in ``idx`` (pools.py:164-178)."""
+        """Record activity on every cell in ``idx`` (pools.py:164-178, :314, :363)."""
         idx = _as_u64(idx)
         check(lib.vate_set_cells(self._h, ptr(idx), idx.size, VATE_HOST))
 
@@ -207,7 +204,7 @@ class AtPool(BlockLayout):
         return not bool(self.inactive_mask(np.array([i], dtype=np.uint64), k_prime)[0])
 
     def inactive_mask(self, idx, k_prime: int) -> np.ndarray:
-        """True where the cell is inactive for width k' (pools.py:187-193)."""
+        """True where the cell is inactive for width k' (pools.py:187-193, :326, :375)."""
         self._validate_width(k_prime)
         idx = _as_u64(idx)
         out = np.empty(idx.shape, dtype=np.uint8)
@@ -225,22 +222,78 @@ class AtPool(BlockLayout):
     def inactive_fraction(self, k_prime: int) -> float:
         return self.count_inactive(k_prime) / self.size
 
-    # --- maintenance (pools.py:221-249) -------------------------------------------
+    # --- maintenance (pools.py:221-249, :339-349, :399-401) ---------------------------
     def advance_slice(self) -> MaintenanceReport:
         blocks = (C.c_int32 * 2)()
         maint, cleared = C.c_uint64(), C.c_uint64()
         check(lib.vate_advance(self._h, blocks, C.byref(maint), C.byref(cleared)))
-        return MaintenanceReport((blocks[0], blocks[1]), maint.value, cleared.value)
+        return MaintenanceReport(maintenance_blocks(blocks[0], blocks[1]), maint.value,
+                                 cleared.value)
+
+    @property
+    def memory_bytes(self) -> int:
+        """Device bytes of the cell array (unpacked cells)."""
+        return self.size * self.cell_bytes
+
+    @property
+    def cells(self) -> "DeviceCells":
+        return DeviceCells(self)
+
+    # --- instrumentation -----------------------------------------------------------
+    def launches(self) -> int:
+        n = C.c_uint64()
+        check(lib.vate_pool_launches(self._h, C.byref(n)))
+        return n.value
+
+    def set_option(self, option: str, value: int) -> None:
+        """Tuning switches: 'g0_kernel' (0 auto, 1 gather, 2 smem) and 'incremental' (0/1)."""
+        check(lib.vate_pool_set_option(self._h, ("g0_kernel", "incremental", "scan_v", "scan_check").index(option),
+                                       int(value)))
+
+    def inc_stats(self) -> dict:
+        """Counters of the incremental estimate (see DESIGN.md §4b)."""
+        out = (C.c_uint64 * 11)()
+        check(lib.vate_pool_inc_stats(self._h, out))
+        keys = ("rebuilds", "delta_slices", "refresh_slices", "full_slices",
+                "last_delta_cells", "last_delta_work", "identity_slices", "hosts_indexed",
+                "rebuild_us_total", "miss_accum", "extends")
+        return dict(zip(keys, list(out)))
+
+    def set_timing(self, on: bool) -> None:
+        check(lib.vate_pool_set_timing(self._h, int(on)))
+
+    def kernel_time(self, kind: str):
+        """(total ms, launches) recorded by CUDA events for one kernel kind."""
+        ms, n = C.c_double(), C.c_uint64()
+        check(lib.vate_pool_timing(self._h, _lib.KERNEL_KINDS.index(kind), C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+
+class AtPool(BlockLayout, _DevicePool):
+    """2**c asynchronous timestamps in 2k staggered-clock blocks, on the GPU."""
+
+    kind = "at"
+    _kind_code = 0
+
+    def __init__(self, c: int, k: int, partition: str = TAIL_REMAINDER, device: int = 0):
+        BlockLayout.__init__(self, c, k, partition)
+        self._create(c, k, partition, device)
+
+    @property
+    def bact0(self) -> int:
+        """Clock of block 0 in the current slice (pools.py:96)."""
+        return self._info()[0]
+
+    # --- layout: BlockLayout supplies block_of / block_range / block_sizes ---
+    def block_act(self, bi: int) -> int:
+        if not 0 <= bi < self.nblocks:
+            raise ValueError(f"block index {bi} outside [0, {self.nblocks})")
+        return (self.bact0 + bi) % self.nblocks
 
     # --- accounting and snapshots ---------------------------------------------------
     @property
     def bits_per_counter(self) -> int:
         return (2 * self.k).bit_length()   # counters.py:52-54
-
-    @property
-    def memory_bytes(self) -> int:
-        """Device bytes of the cell array (unpacked: 1, 2 or 4 bytes per cell)."""
-        return self.size * self.cell_bytes
 
     @property
     def packed_bytes(self) -> int:
@@ -288,58 +341,26 @@ class AtPool(BlockLayout):
             blob = fh.read()
         return cls.from_bytes(blob, device=device, where=str(path))
 
-    @property
-    def cells(self) -> "DeviceCells":
-        return DeviceCells(self)
-
-    # --- instrumentation -----------------------------------------------------------
-    def launches(self) -> int:
-        n = C.c_uint64()
-        check(lib.vate_pool_launches(self._h, C.byref(n)))
-        return n.value
-
-    def set_option(self, option: str, value: int) -> None:
-        """Tuning switches: 'g0_kernel' (0 auto, 1 gather, 2 smem) and 'incremental' (0/1)."""
-        check(lib.vate_pool_set_option(self._h, ("g0_kernel", "incremental", "scan_v", "scan_check").index(option),
-                                       int(value)))
-
-    def inc_stats(self) -> dict:
-        """Counters of the incremental estimate (see DESIGN.md §4b)."""
-        out = (C.c_uint64 * 11)()
-        check(lib.vate_pool_inc_stats(self._h, out))
-        keys = ("rebuilds", "delta_slices", "refresh_slices", "full_slices",
-                "last_delta_cells", "last_delta_work", "identity_slices", "hosts_indexed",
-                "rebuild_us_total", "miss_accum", "extends")
-        return dict(zip(keys, list(out)))
-
-    def set_timing(self, on: bool) -> None:
-        check(lib.vate_pool_set_timing(self._h, int(on)))
-
-    def kernel_time(self, kind: str):
-        """(total ms, launches) recorded by CUDA events for one kernel kind."""
-        ms, n = C.c_double(), C.c_uint64()
-        check(lib.vate_pool_timing(self._h, _lib.KERNEL_KINDS.index(kind), C.byref(ms), C.byref(n)))
-        return ms.value, n.value
 
 
 class DeviceCells:
     """Read view of the cells mirroring PackedArray's read API (bitpack.py:26-140)."""
 
-    def __init__(self, pool: AtPool):
+    def __init__(self, pool: _DevicePool):
         self._pool = pool
         self.size = pool.size
         self.width = pool.bits_per_counter
-        self.mask = np.uint64((1 << self.width) - 1)
+        self.mask = np.uint64((1 << self.width) - 1) if self.width < 64 else np.uint64(~0 & ((1 << 64) - 1))
 
     def __len__(self):
         return self.size
 
     def get(self, idx) -> np.ndarray:
         idx = _as_u64(idx)
-        out = np.empty(idx.shape, dtype=np.uint32)
+        out = np.empty(idx.shape, dtype=np.uint64)
         if idx.size:
-            check(lib.vate_get_cells(self._pool.handle, ptr(idx), idx.size, ptr(out), VATE_HOST))
-        return out.astype(np.uint64)
+            check(lib.vate_get_cells64(self._pool.handle, ptr(idx), idx.size, ptr(out), VATE_HOST))
+        return out
 
     def get_one(self, i: int) -> int:
         return int(self.get(np.array([i], dtype=np.uint64))[0])
@@ -358,12 +379,60 @@ class DeviceCells:
         return self._pool.memory_bytes
 
 
+class DrPool(_DevicePool):
+    """2**c distance recorders; every cell slides every slice (pools.py:301-353)."""
+
+    kind = "dr"
+    _kind_code = 1
+
+    def __init__(self, c: int, k: int, device: int = 0):
+        _validate_pool_shape(c, k)
+        self.c, self.k, self.size = c, k, 1 << c
+        self._create(c, k, TAIL_REMAINDER, device)
+
+    @property
+    def bits_per_counter(self) -> int:
+        return self.k.bit_length()          # dr_bits, counters.py:132-134
+
+    @property
+    def packed_bytes(self) -> int:
+        """The reference's PackedArray accounting (bitpack.py nbytes)."""
+        return (-(-self.size * self.bits_per_counter // 64) + 1) * 8
+
+
+class TsPool(_DevicePool):
+    """2**c plain last-seen slice indices; no maintenance (pools.py:356-410)."""
+
+    kind = "ts"
+    _kind_code = 2
+
+    def __init__(self, c: int, k: int, device: int = 0):
+        _validate_pool_shape(c, k)
+        self.c, self.k, self.size = c, k, 1 << c
+        self._create(c, k, TAIL_REMAINDER, device)
+
+    @property
+    def t(self) -> int:
+        """The pool's current slice index (advances taken, pools.py:360)."""
+        kind, t = C.c_int(), C.c_uint64()
+        check(lib.vate_pool_kind(self._h, C.byref(kind), C.byref(t)))
+        return t.value
+
+    @property
+    def bits_per_counter(self) -> int:
+        return 64
+
+    @property
+    def packed_bytes(self) -> int:
+        return self.size * 8
+
+
 def make_pool(kind: str, c: int, k: int, partition: str = TAIL_REMAINDER, device: int = 0):
-    """Build a counter pool by kind name (pools.py:413-421); 'at' only on the device."""
+    """Build a counter pool by kind name (pools.py:413-421)."""
     if kind == "at":
         return AtPool(c, k, partition, device=device)
-    if kind in ("dr", "ts"):
-        raise ConfigError(
-            f"counter kind {kind!r} has no device implementation "
-            "(comparator pools are outside the accelerated path)")
+    if kind == "dr":
+        return DrPool(c, k, device=device)
+    if kind == "ts":
+        return TsPool(c, k, device=device)
     raise ConfigError(f"unknown counter kind {kind!r}")

@@ -33,7 +33,7 @@ from slidecard.pipeline import Pipeline          # noqa: E402
 from slidecard.pools import AtPool               # noqa: E402
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from specs import PIPELINES, gen_slices as _slices  # noqa: E402
+from specs import COMPARATORS, PIPELINES, gen_slices as _slices  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 M64 = (1 << 64) - 1
@@ -189,6 +189,57 @@ def pipelines():
         print(name, n, "slices", os.path.getsize(os.path.join(OUT, f"pipe_{name}.npz")), "bytes")
 
 
+def comparators():
+    """DR and TS pools (pools.py:301-410) next to AT on the same slices."""
+    for name, spec in COMPARATORS.items():
+        rec = {}
+        reports = {}
+        for kind in ("at", "dr", "ts"):
+            cfg = est.EstimatorConfig(spec["g"], spec["c"], spec["k"], seed=spec["seed"],
+                                      counter_kind=kind, partition=spec["part"])
+            pool = cfg.build_pool()
+            pipe = Pipeline(pool, cfg, spec["kp"], floor=0.0)
+            rows = []
+            for t, aips, bips in _slices(spec):
+                pipe._scan(aips, bips)
+                if len(aips):
+                    pipe.hosts.update(aips, t)
+                live = pipe.hosts.active(t, spec["kp"])
+                if len(live):
+                    p = pool.count_inactive(spec["kp"])
+                    g0 = est.inactive_virtual_counts(pool, cfg, live, spec["kp"])
+                    reps = est.reports_from_counts(cfg, live, g0, p, t, spec["kp"])
+                else:
+                    p, g0, reps = -1, np.zeros(0, dtype=np.int64), []
+                cells = pool.cells.get_range(0, pool.size) if kind != "ts" else pool.cells
+                cells_sha = hashlib.sha256(np.asarray(cells, dtype=np.uint64).tobytes()).hexdigest()
+                mrep = pool.advance_slice()
+                if t % max(1, pool.k) == 0:
+                    pipe.hosts.prune(t)
+                rows.append(dict(p=p, g0=np.asarray(g0, dtype=np.int64),
+                                 est=np.array([r.estimate for r in reps], dtype=np.float64),
+                                 maintained=mrep.cells_maintained, cleared=mrep.cells_cleared,
+                                 nblocks=len(mrep.blocks), cells_sha=cells_sha))
+            pipe.close()
+            reports[kind] = [r["est"] for r in rows]
+            rec[f"{kind}_p"] = np.array([r["p"] for r in rows])
+            rec[f"{kind}_maintained"] = np.array([r["maintained"] for r in rows])
+            rec[f"{kind}_cleared"] = np.array([r["cleared"] for r in rows])
+            rec[f"{kind}_nblocks"] = np.array([r["nblocks"] for r in rows])
+            rec[f"{kind}_cells_sha"] = np.array([r["cells_sha"] for r in rows])
+            rec[f"{kind}_g0_cat"] = np.concatenate([r["g0"] for r in rows])
+            rec[f"{kind}_est_cat"] = np.concatenate([r["est"] for r in rows])
+            final = pool.cells.get_range(0, pool.size) if kind != "ts" else pool.cells
+            rec[f"{kind}_final_cells"] = np.asarray(final, dtype=np.uint64)
+            rec[f"{kind}_bits"] = np.array([pool.bits_per_counter])
+        for a, b in zip(reports["at"], reports["dr"]):
+            assert np.array_equal(a, b), name
+        for a, b in zip(reports["at"], reports["ts"]):
+            assert np.array_equal(a, b), name
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **rec)
+        print(name, os.path.getsize(os.path.join(OUT, f"{name}.npz")), "bytes")
+
+
 def appendix_b():
     """SURVEY.md Appendix B digest: c=20, k=10, g=1024, 25 slices x 100k pairs."""
     cfg = est.EstimatorConfig(g=1024, c=20, k=10, seed=0)
@@ -278,12 +329,39 @@ def cli_goldens():
     np.savez_compressed(os.path.join(OUT, "cli.npz"), **out)
 
 
+def cli_compare_goldens():
+    """`slidecard compare` (cli.py:167-204) and `estimate --counter dr|ts` on the
+    committed golden binary trace (cli.npz:trace_bin)."""
+    import tempfile
+
+    from slidecard import cli
+    d = tempfile.mkdtemp()
+    trace_bin = os.path.join(d, "t.bin")
+    with open(trace_bin, "wb") as fh:
+        fh.write(np.load(os.path.join(OUT, "cli.npz"))["trace_bin"].tobytes())
+    common = ["--trace", trace_bin, "--format", "binary", "--c", "14", "--g", "256", "--k", "6",
+              "--workers", "1"]
+    runs = {
+        "compare_floor0": ["compare"] + common + ["--floor", "0"],
+        "compare_default": ["compare"] + common + ["--k-prime", "4"],
+        "est_dr": ["estimate"] + common + ["--floor", "0", "--counter", "dr"],
+        "est_ts": ["estimate"] + common + ["--floor", "20", "--counter", "ts"],
+    }
+    out = {}
+    for name, argv in runs.items():
+        path = os.path.join(d, name + ".csv")
+        assert cli.main(argv + ["--out", path]) == 0
+        out[name] = np.frombuffer(open(path, "rb").read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "cli_compare.npz"), **out)
+
+
+ALL = (hash_kats, layouts, estimator_kats, snapshot_blob, appendix_b, pipelines, cli_goldens,
+       comparators, cli_compare_goldens)
+
 if __name__ == "__main__":
-    hash_kats()
-    layouts()
-    estimator_kats()
-    snapshot_blob()
-    appendix_b()
-    pipelines()
-    cli_goldens()
+    # no arguments: everything; else only the named generators (e.g. comparators)
+    wanted = sys.argv[1:]
+    for fn in ALL:
+        if not wanted or fn.__name__ in wanted:
+            fn()
     print("numpy", np.__version__)

@@ -47,3 +47,15 @@ PIPELINES = {
     "g_full_pool": dict(g=512, c=9, k=4, seed=9, part="tail", kp=3, floor=0.0,
                         slices=20, pairs=50, hosts=20, aip_base=1, data_seed=7),
 }
+
+
+# Comparator pools (DR / TS, pools.py:301-410) replayed next to AT on the same
+# slices: per-kind cells, P, g0, reports and maintenance; estimates must agree
+# across kinds (test_estimator.py:233-255).
+COMPARATORS = {
+    "cmp_k6": dict(g=256, c=14, k=6, seed=4, part="tail", kp=5, floor=0.0, slices=16,
+                   pairs=4_000, hosts=300, aip_base=0x0A000000, data_seed=8, empty=(5,)),
+    # k = 300: dr_bits = 9 -> 16-bit DR cells on the device
+    "cmp_k300_u16": dict(g=128, c=12, k=300, seed=2, part="low-dev", kp=200, floor=0.0,
+                         slices=40, pairs=300, hosts=40, aip_base=0x0A000000, data_seed=9),
+}

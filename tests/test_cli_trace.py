@@ -89,7 +89,7 @@ def test_golden_traces_read_back(tmp_path):
     (["--k", "4", "--k-prime", "9"], cli.EXIT_CONFIG),
     (["--floor", "-1"], cli.EXIT_CONFIG),
     (["--slice-us", "0"], cli.EXIT_CONFIG),
-    (["--counter", "dr"], cli.EXIT_CONFIG),
+    (["--counter", "dr", "--resume", "x.atp1"], cli.EXIT_CONFIG),
 ])
 def test_cli_config_errors_without_a_device(tmp_path, capsys, argv, code):
     trace = tmp_path / "t.csv"
@@ -192,3 +192,28 @@ def test_device_slices_equal_slice_stream(tmp_path, chunk):
         assert [g[0] for g in got] == [w[0] for w in want]
         for (t, a, b), (_, wa, wb) in zip(got, want):
             assert np.array_equal(a, wa) and np.array_equal(b, wb), t
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,argv", [
+    ("compare_floor0", ["compare", "--floor", "0"]),
+    ("compare_default", ["compare", "--k-prime", "4"]),
+    ("est_dr", ["estimate", "--floor", "0", "--counter", "dr"]),
+    ("est_ts", ["estimate", "--floor", "20", "--counter", "ts"]),
+])
+def test_cli_compare_and_comparator_counters_byte_identical(tmp_path, name, argv):
+    """`compare` (AT, DR, TS pools all on the device) and `estimate --counter dr|ts`
+    write the reference CLI's bytes (tests/golden/cli_compare.npz)."""
+    trace = _write_golden(tmp_path, "trace_bin", "t.bin")
+    out = tmp_path / "out.csv"
+    common = ["--trace", str(trace), "--format", "binary", "--c", "14", "--g", "256", "--k", "6"]
+    assert cli.main(argv[:1] + common + argv[1:] + ["--out", str(out)]) == 0
+    assert out.read_bytes() == load("cli_compare.npz")[name].tobytes()
+
+
+def test_cli_checkpoint_requires_the_at_pool(tmp_path, capsys):
+    trace = _write_golden(tmp_path, "trace_bin", "t.bin")
+    code = cli.main(["estimate", "--trace", str(trace), "--format", "binary", "--counter", "dr",
+                     "--checkpoint", str(tmp_path / "p.atp1")])
+    assert code == 2
+    assert "requires the 'at' counter pool" in capsys.readouterr().err

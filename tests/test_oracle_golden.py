@@ -185,3 +185,42 @@ def test_synthetic_generator_is_deterministic_and_bounded():
         a, b = vo.synthetic_slice(t, 10_000, 1000)
         pairs.update(zip(a.tolist(), b.tolist()))
     assert len(pairs) < 1000 * 40
+
+
+# --- comparator pools (DR / TS, pools.py:301-410) ------------------------------------
+
+from _golden import CMP_KINDS, CMP_NAMES, check_replay, replay_kind  # noqa: E402
+from specs import COMPARATORS  # noqa: E402
+
+
+@pytest.mark.parametrize("name", CMP_NAMES)
+@pytest.mark.parametrize("kind", CMP_KINDS)
+def test_oracle_comparator_pools_match_reference(name, kind):
+    """The oracle's AT / DR / TS pools replay the reference slice by slice: cells,
+    P, g0, estimates and maintenance reports."""
+    spec = COMPARATORS[name]
+    cfg = vo.OracleConfig(spec["g"], spec["c"], spec["k"], seed=spec["seed"],
+                          partition=spec["part"])
+    pipe = vo.OraclePipeline(cfg, spec["kp"], kind=kind)
+    kp = spec["kp"]
+
+    def scan(t, a, b):
+        pipe.scan(a, b)
+        if len(a):
+            pipe.hosts.update(a, t)
+
+    def advance(t):
+        r = pipe.pool.advance()
+        if t % max(1, cfg.k) == 0:
+            pipe.hosts.prune(t)
+        return r
+
+    got = replay_kind(
+        spec, kind, pipe.pool, scan, lambda t: pipe.hosts.active(t, kp),
+        lambda live: vo.host_g0(pipe.pool, cfg, live, kp), lambda: pipe.pool.count_inactive(kp),
+        lambda t, live, g0, p: vo.reports_soa(cfg, live, g0, p, t, kp).estimate, advance,
+        lambda: pipe.pool.cells)
+    check_replay(name, kind, got)
+    rec = load(f"{name}.npz")
+    assert np.array_equal(np.asarray(pipe.pool.cells, dtype=np.uint64),
+                          rec[f"{kind}_final_cells"])
