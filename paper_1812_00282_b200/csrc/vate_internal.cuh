@@ -284,6 +284,10 @@ struct vate_pool {
   int opt_inc = 1;            // incremental g0 through the inverse index
   int opt_scan_check = 0;    // packed scan: load-before-store (heavy hitters)
   int opt_scan_v = 1;         // packed-scan unroll (uint4 loads per thread per iteration)
+  int opt_l2 = 0;             // L2 persisting window: 0 off, 1 registry, 2 cells
+  int opt_bitmap_kw = 0;      // bitmap pass words per thread (0 auto)
+  void* l2_base = nullptr;    // window currently set on the stream
+  size_t l2_bytes = 0;
   const void* sorted_owner = nullptr;  // registry whose active set hosts_sorted holds
   uint64_t sorted_n = 0;
   uint64_t sorts_skipped = 0;

@@ -185,10 +185,33 @@ __global__ void k_fill(T* cells, uint64_t n, T value) {
 // read-modify-write.  The registry step issues all U first-probe loads (one
 // 16-byte sector each) before resolving any, so a thread keeps U independent
 // requests in flight; only misses take the probing insert.
+// Heavy-hitter form (CHECK, VATE_OPT_SCAN_CHECK): registry touches are
+// filtered per CTA by a small direct-mapped table of the slots this CTA already
+// stamped with t in shared memory.  Loads of `last`
+// come from L1 and are stale within a launch, so without it every packet of a
+// heavy hitter would store into the same 8 bytes -- hundreds of thousands of
+// same-address stores serialised at one L2 slice (cfg 3's Zipf head).
+constexpr int kTouchSlots = 1024;
+
+__device__ __forceinline__ void touch_filter_init(unsigned* filt) {
+  for (int i = threadIdx.x; i < kTouchSlots; i += blockDim.x) filt[i] = 0u;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void touch_last(const RegRef& R, unsigned* filt, uint64_t slot,
+                                           long long t) {
+  const unsigned tag = (unsigned)slot + 1u;
+  volatile unsigned* f = filt + (slot & (kTouchSlots - 1));
+  if (*f == tag) return;
+  *f = tag;
+  R.table[slot].last = t;
+}
+
 template <typename T, bool REG, int U, bool CHECK = false, typename Rule>
 __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint64_t (&bip)[U],
                                            int m, T* __restrict__ cells, const HashParams& H,
-                                           const Rule& rule, const RegRef& R, long long t) {
+                                           const Rule& rule, const RegRef& R, long long t,
+                                           unsigned* filt) {
 #pragma unroll
   for (int q = 0; q < U; ++q) {
     if (q < m) {
@@ -200,19 +223,28 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
     }
   }
   if (REG) {
-    // all U first probes in flight before any is resolved (one 16-B sector each)
+    // all U first probes in flight before any is resolved: each reads the home
+    // sector (two slots, one 256-bit load)
     uint64_t slot[U];
-    RegEntry e[U];
+    RegEntry e[U], f[U];
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      slot[q] = mix64(aip[q] ^ kRegSalt) & R.mask;
-      if (q < m) e[q] = R.table[slot[q]];
+      slot[q] = reg_home(aip[q], R.mask);
+      if (q < m) ld_pair(R.table + slot[q], e[q], f[q]);
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       if (q >= m) continue;
-      if (e[q].key == aip[q] && aip[q] != kEmptyKey) {
-        if (e[q].last != t) R.table[slot[q]].last = t;
+      if (aip[q] != kEmptyKey && e[q].key == aip[q]) {
+        if (e[q].last != t) {
+          if (CHECK) touch_last(R, filt, slot[q], t);
+          else R.table[slot[q]].last = t;
+        }
+      } else if (aip[q] != kEmptyKey && f[q].key == aip[q]) {
+        if (f[q].last != t) {
+          if (CHECK) touch_last(R, filt, slot[q] + 1, t);
+          else R.table[slot[q] + 1].last = t;
+        }
       } else {
         reg_insert(R, aip[q], t, false);
       }
@@ -224,6 +256,8 @@ template <typename T, bool REG, int V = 2, bool CHECK = false, typename Rule = A
 __global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
     Rule rule, RegRef R, long long t) {
+  __shared__ unsigned filt[REG && CHECK ? kTouchSlots : 1];
+  if (REG && CHECK) touch_filter_init(filt);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   for (; i < npairs2; i += V * stride) {
@@ -240,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
         a[2 * v] = b[2 * v] = a[2 * v + 1] = b[2 * v + 1] = 0;
       }
     }
-    scan_batch<T, REG, 2 * V, CHECK>(a, b, m, cells, H, rule, R, t);
+    scan_batch<T, REG, 2 * V, CHECK>(a, b, m, cells, H, rule, R, t, filt);
   }
 }
 
@@ -248,11 +282,12 @@ template <typename T, bool REG, typename Rule = AtRule>
 __global__ void __launch_bounds__(kThreads) k_scan_packed8(
     const uint2* __restrict__ pairs, uint64_t n, T* __restrict__ cells, HashParams H,
     Rule rule, RegRef R, long long t) {
+  unsigned* filt = nullptr;  // heavy-hitter filter only in the CHECK form of the packed16 scan
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint2 q = pairs[i];
     const uint64_t a[1] = {q.x}, b[1] = {q.y};
-    scan_batch<T, REG, 1>(a, b, 1, cells, H, rule, R, t);
+    scan_batch<T, REG, 1>(a, b, 1, cells, H, rule, R, t, filt);
   }
 }
 
@@ -261,6 +296,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_u64(
     const uint64_t* __restrict__ aips, const uint64_t* __restrict__ bips, uint64_t n,
     T* __restrict__ cells, HashParams H, Rule rule, RegRef R, long long t) {
   constexpr int U = 4;
+  unsigned* filt = nullptr;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += U * stride) {
     uint64_t a[U], b[U];
@@ -275,7 +311,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_u64(
         m = q + 1;
       }
     }
-    scan_batch<T, REG, U>(a, b, m, cells, H, rule, R, t);
+    scan_batch<T, REG, U>(a, b, m, cells, H, rule, R, t, filt);
   }
 }
 
@@ -448,14 +484,13 @@ __device__ __forceinline__ uint32_t word_inactive_bits(const T* __restrict__ cel
 
 // kW words per thread per iteration: all their 16-byte loads are issued before
 // any predicate, for memory-level parallelism.
-template <typename T>
+template <typename T, int kW>
 __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells, Layout L,
                                                      uint32_t bact0, uint32_t kp,
                                                      uint32_t* __restrict__ bitmap,
                                                      uint64_t nwords,
                                                      unsigned long long* pool_inactive,
                                                      DeltaOut D) {
-  constexpr int kW = sizeof(T) == 1 ? 4 : 2;
   constexpr int NV = (int)sizeof(T) * 2;
   constexpr unsigned kDeltaStage = 1024;
   __shared__ unsigned long long s_delta[kDeltaStage];
@@ -727,11 +762,21 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
                  I.dlist.as<unsigned long long>(), I.dlist_cap, p->d_ctr + C_DCNT,
                  p->d_ctr + C_DWORK};
   }
+  // words per thread per iteration (p->opt_bitmap_kw overrides: 1, 2 or 4)
+  int kw = p->opt_bitmap_kw;
+  if (kw == 0) kw = 1;  // measured best at c = 24, 26, 28 (scripts/micro_bitmap.py)
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
-    VATE_LAUNCH(p, VATE_K_BITMAP, grid_for((nwords + 3) / 4, kThreads, 148u * 32u), kThreads, 0,
-                k_bitmap<T>, (const T*)p->cells, p->L, p->bact0, (uint32_t)k_prime,
-                p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D);
+    const uint32_t grid = grid_for((nwords + kw - 1) / kw, kThreads, 148u * 32u);
+    if (kw == 4)
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 4>), (const T*)p->cells, p->L,
+                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D);
+    else if (kw == 2)
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 2>), (const T*)p->cells, p->L,
+                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D);
+    else
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1>), (const T*)p->cells, p->L,
+                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D);
     return VATE_OK;
   });
   if (rc) return rc;
@@ -948,6 +993,21 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_g0 = (int)value;
     return VATE_OK;
   }
+  if (option == VATE_OPT_L2_PERSIST && value >= 0 && value <= 2) {
+    p->opt_l2 = (int)value;
+    p->l2_base = nullptr;  // re-apply at the next scan
+    if (value == 0) {
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.num_bytes = 0;
+      VATE_CUDA(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+      VATE_CUDA(cudaCtxResetPersistingL2Cache());  // persisting lines would stay pinned
+    }
+    return VATE_OK;
+  }
+  if (option == VATE_OPT_BITMAP_KW && (value == 0 || value == 1 || value == 2 || value == 4)) {
+    p->opt_bitmap_kw = (int)value;
+    return VATE_OK;
+  }
   if (option == VATE_OPT_SCAN_CHECK && (value == 0 || value == 1)) {
     p->opt_scan_check = (int)value;
     return VATE_OK;
@@ -1032,6 +1092,48 @@ int vate_set_cells(vate_pool* p, const uint64_t* idx, uint64_t n, int where) {
   });
 }
 
+// L2 persistence for the scan's random-access target (VATE_OPT_L2_PERSIST):
+// 1 = the host registry (one random 16-B probe per packet), 2 = the cells.
+// Streamed packets are loaded evict-first, so the persisting lines survive the
+// 40 MB per slice of packet traffic.  The window is a stream attribute; it is
+// re-set only when the target moved (registry growth) or changed size.
+static int apply_l2_window(vate_pool* p, vate_hosts* hosts) {
+  if (p->opt_l2 == 0) return VATE_OK;
+  void* base = nullptr;
+  size_t bytes = 0;
+  if (p->opt_l2 == 1 && hosts) {
+    base = hosts->table.ptr;
+    bytes = (hosts->cap + 1) * sizeof(RegEntry);
+  } else if (p->opt_l2 == 2) {
+    base = p->cells;
+    bytes = p->L.size * (size_t)p->cell_bytes;
+  }
+  if (!base || (base == p->l2_base && bytes == p->l2_bytes)) return VATE_OK;
+  static int configured[64] = {0};
+  int maxp = 0, maxw = 0;
+  VATE_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, p->device));
+  VATE_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, p->device));
+  if (maxp <= 0 || maxw <= 0) {
+    p->opt_l2 = 0;  // no persistence on this device
+    return VATE_OK;
+  }
+  if (p->device >= 0 && p->device < 64 && !configured[p->device]) {
+    VATE_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
+    configured[p->device] = 1;
+  }
+  const size_t win = std::min(bytes, (size_t)maxw);
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = base;
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxp / (double)win);
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  VATE_CUDA(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+  p->l2_base = base;
+  p->l2_bytes = bytes;
+  return VATE_OK;
+}
+
 static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const uint64_t* bips,
                        const uint32_t* pairs, uint64_t n, int where, vate_hosts* hosts,
                        int64_t t) {
@@ -1045,6 +1147,8 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     if (rc) return rc;
     R = hosts->ref();
   }
+  rc = apply_l2_window(p, hosts);
+  if (rc) return rc;
   const uint32_t grid = p->opt_scan_v == 1 ? grid_for((n + 1) / 2, kThreads, 148u * 64u)
                                            : grid_for(n, kThreads, 148u * 16u);
   if (pairs) {

@@ -13,6 +13,25 @@ namespace vate {
 constexpr uint64_t kRegSalt = 0x2545F4914F6CDD1Dull;
 constexpr int kMaxProbe = 64;
 
+// Home slot of a key: linear probing starts at an EVEN slot, so the first two
+// probes share one 32-byte sector and one 256-bit load (ld_pair) answers both
+// -- at load factor <= 0.6 most lookups end inside that first sector.
+__device__ __forceinline__ uint64_t reg_home(uint64_t key, uint64_t mask) {
+  return (mix64(key ^ kRegSalt) & mask) & ~1ull;
+}
+
+// Slots s and s+1 (s even: one aligned 32-byte sector) in one load.
+__device__ __forceinline__ void ld_pair(const RegEntry* p, RegEntry& a, RegEntry& b) {
+  unsigned long long k0, l0, k1, l1;
+  asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(k0), "=l"(l0), "=l"(k1), "=l"(l1)
+               : "l"(p));
+  a.key = k0;
+  a.last = (long long)l0;
+  b.key = k1;
+  b.last = (long long)l1;
+}
+
 __device__ __forceinline__ void reg_touch(RegEntry* e, long long t, bool use_max) {
   if (use_max) {
     atomicMax(&e->last, t);
@@ -32,7 +51,7 @@ __device__ __forceinline__ void reg_insert(const RegRef& R, uint64_t key, long l
     reg_touch(e, t, use_max);
     return;
   }
-  uint64_t h = mix64(key ^ kRegSalt) & R.mask;
+  uint64_t h = reg_home(key, R.mask);
 #pragma unroll 1
   for (int probe = 0; probe < kMaxProbe; ++probe) {
     RegEntry* e = R.table + h;
