@@ -278,6 +278,7 @@ def run_gpu(args, rank, world, local_rank):
         pool.set_option("scan_check", scan_check)
     if args.l2_persist:
         pool.set_option("l2_persist", args.l2_persist)
+    pool.set_option("concurrent", args.concurrent)
     n = w["packets"]
     slice_bytes = n * 8
     torch.cuda.set_device(dev)
@@ -533,6 +534,9 @@ def main():
                     help="load-before-store scan (VATE_OPT_SCAN_CHECK)")
     ap.add_argument("--l2-persist", type=int, choices=(0, 1, 2), default=0,
                     help="L2 persisting window: 1 host registry, 2 cells (VATE_OPT_L2_PERSIST)")
+    ap.add_argument("--concurrent", type=int, choices=(0, 1), default=1,
+                    help="registry compaction beside the bitmap pass, advance beside g0 + float "
+                         "path, on a second stream (VATE_OPT_CONCURRENT)")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2",
                     help="workload shape (BASELINE.json configs); cfg2 is the headline")
     ap.add_argument("--incremental", choices=("on", "off"), default="on",

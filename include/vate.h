@@ -83,7 +83,11 @@ int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
  * = 1 (default) lets the fused estimate update g0 through an inverse index
  * (exact), 0 recomputes every g0 by a full gather. */
 enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 2,
-                   VATE_OPT_SCAN_CHECK = 3, VATE_OPT_L2_PERSIST = 4, VATE_OPT_BITMAP_KW = 5 };
+                   VATE_OPT_SCAN_CHECK = 3, VATE_OPT_L2_PERSIST = 4, VATE_OPT_BITMAP_KW = 5,
+                   VATE_OPT_CONCURRENT = 6 };
+/* VATE_OPT_CONCURRENT (default 1): the estimate's registry compaction runs
+ * beside the bitmap pass, and the slice advance beside g0 + float path, on a
+ * second stream of the pool (fork/join by events; results unchanged). */
 /* VATE_OPT_L2_PERSIST: 0 off (default), 1 an L2 persisting access-policy window
  * over the host registry (the scan's random probe target), 2 over the cells. */
 int vate_pool_set_option(vate_pool* p, int option, int64_t value);

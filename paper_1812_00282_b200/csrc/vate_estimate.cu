@@ -9,6 +9,8 @@
 #include <cstring>
 #include <string>
 
+#include <utility>
+
 #include "vate_internal.cuh"
 
 namespace vate {
@@ -556,9 +558,24 @@ static int begin_enqueue(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t c
   if (rc) return rc;
   if (g < 1 || g > p->L.size) return set_error(VATE_ECONFIG, "g must be in [1, 2^c]");
   p->est_n = 0;
+  if (!p->opt_concurrent) {
+    rc = build_bitmap(p, k_prime, inc_delta_ready(p, g, cell_stream, k_prime));
+    if (rc) return rc;
+    return hosts_active_launch(hosts, t, k_prime);  // pipeline.py:121
+  }
+  // fork: the registry compaction (reads the registry) runs on the aux stream
+  // beside the bitmap pass (reads the cells); joined before the round trip
+  VATE_CUDA(cudaEventRecord(p->ev_fork, p->stream));
+  VATE_CUDA(cudaStreamWaitEvent(p->aux_stream, p->ev_fork, 0));
+  std::swap(p->stream, p->aux_stream);
+  rc = hosts_active_launch(hosts, t, k_prime);  // pipeline.py:121
+  std::swap(p->stream, p->aux_stream);
+  if (rc) return rc;
+  VATE_CUDA(cudaEventRecord(p->ev_join, p->aux_stream));
   rc = build_bitmap(p, k_prime, inc_delta_ready(p, g, cell_stream, k_prime));
   if (rc) return rc;
-  return hosts_active_launch(hosts, t, k_prime);  // pipeline.py:121
+  VATE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_join, 0));
+  return VATE_OK;
 }
 
 // complete (after the caller's sync): the sorted active set, P, and g0 of
@@ -744,14 +761,31 @@ int vate_slice_step(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_s
   if (rc) return rc;
   res->nhosts = nh;
   res->pool_inactive = pin;
-  // maintenance may run before the float path: it touches cells, not g0
+  // maintenance may run before the float path: it touches cells, not g0 --
+  // with opt_concurrent on the aux stream, beside g0 and the float path, and
+  // joined back so the next scan follows it
+  const bool fork = p->opt_concurrent != 0;
+  if (fork) {
+    VATE_CUDA(cudaEventRecord(p->ev_fork, p->stream));
+    VATE_CUDA(cudaStreamWaitEvent(p->aux_stream, p->ev_fork, 0));
+    std::swap(p->stream, p->aux_stream);
+  }
   rc = vate_advance_async(p);
+  if (fork) {
+    std::swap(p->stream, p->aux_stream);
+    if (rc == VATE_OK) {
+      cudaError_t e = cudaEventRecord(p->ev_join, p->aux_stream);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    }
+  }
   if (rc) return rc;
-  if (nh == 0) return VATE_OK;
   uint64_t kept = 0;
-  rc = vate_estimate_finish_async(p, g, pin, log_zp_table[pin], floor, out_host, out_est, out_zv,
-                                  out_sat, cap, &kept);
-  res->nkept = kept;
+  if (nh) {
+    rc = vate_estimate_finish_async(p, g, pin, log_zp_table[pin], floor, out_host, out_est,
+                                    out_zv, out_sat, cap, &kept);
+    res->nkept = kept;
+  }
+  if (fork) VATE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_join, 0));
   return rc;
 }
 

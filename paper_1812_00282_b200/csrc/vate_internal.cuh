@@ -286,6 +286,9 @@ struct vate_pool {
   int opt_scan_v = 1;         // packed-scan unroll (uint4 loads per thread per iteration)
   int opt_l2 = 0;             // L2 persisting window: 0 off, 1 registry, 2 cells
   int opt_bitmap_kw = 0;      // bitmap pass words per thread (0 auto)
+  int opt_concurrent = 1;     // fork independent estimate phases onto aux_stream
+  cudaStream_t aux_stream = nullptr;   // second compute stream (fork/join with events)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* l2_base = nullptr;    // window currently set on the stream
   size_t l2_bytes = 0;
   const void* sorted_owner = nullptr;  // registry whose active set hosts_sorted holds

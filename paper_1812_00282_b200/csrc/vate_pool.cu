@@ -868,6 +868,9 @@ static int pool_create(vate_pool** out, int kind, int c, int k, int partition, i
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_small, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_adv, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->aux_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
     for (cudaEvent_t* ev : {&p->ev_fin[i], &p->ev_d2h[i], &p->ev_h2d[i], &p->ev_used[i]})
@@ -912,6 +915,7 @@ int vate_pool_destroy(vate_pool* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   if (p->d2h_stream) cudaStreamSynchronize(p->d2h_stream);
   if (p->h2d_stream) cudaStreamSynchronize(p->h2d_stream);
+  if (p->aux_stream) cudaStreamSynchronize(p->aux_stream);
   for (DevBuf* b : {&p->bitmap, &p->in_a, &p->in_b, &p->out_buf, &p->hosts_sorted, &p->hosts_tmp,
                     &p->g0, &p->flags, &p->sel_idx, &p->cub_tmp, &p->lzv})
     b->release();
@@ -923,6 +927,9 @@ int vate_pool_destroy(vate_pool* p) {
   }
   if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
   if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
+  if (p->aux_stream) cudaStreamDestroy(p->aux_stream);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   inc_release(p);
   if (p->cells) cudaFree(p->cells);
   if (p->d_ctr) cudaFree(p->d_ctr);
@@ -1002,6 +1009,10 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
       VATE_CUDA(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
       VATE_CUDA(cudaCtxResetPersistingL2Cache());  // persisting lines would stay pinned
     }
+    return VATE_OK;
+  }
+  if (option == VATE_OPT_CONCURRENT && (value == 0 || value == 1)) {
+    p->opt_concurrent = (int)value;
     return VATE_OK;
   }
   if (option == VATE_OPT_BITMAP_KW && (value == 0 || value == 1 || value == 2 || value == 4)) {

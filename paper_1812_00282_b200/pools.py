@@ -248,7 +248,7 @@ class _DevicePool:
     def set_option(self, option: str, value: int) -> None:
         """Tuning switches: 'g0_kernel' (0 auto, 1 gather, 2 smem) and 'incremental' (0/1)."""
         check(lib.vate_pool_set_option(self._h, ("g0_kernel", "incremental", "scan_v", "scan_check",
-                                                     "l2_persist", "bitmap_kw").index(option),
+                                                     "l2_persist", "bitmap_kw", "concurrent").index(option),
                                        int(value)))
 
     def inc_stats(self) -> dict:
