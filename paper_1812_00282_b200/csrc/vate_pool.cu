@@ -207,11 +207,30 @@ __device__ __forceinline__ void touch_last(const RegRef& R, unsigned* filt, uint
   R.table[slot].last = t;
 }
 
+// Registry misses of the home sector are deferred to a per-CTA shared-memory
+// queue and inserted after the CTA's packets, by dense threads: in-line, a
+// warp would run the probe loop as long as its slowest of 64 packets.
+constexpr int kDeferCap = 1024;
+struct DeferQ {
+  unsigned long long keys[kDeferCap];
+  unsigned n;
+};
+
+__device__ __forceinline__ void defer_init(DeferQ* dq) {
+  if (threadIdx.x == 0) dq->n = 0;
+}
+
+__device__ __forceinline__ void defer_drain(DeferQ* dq, const RegRef& R, long long t) {
+  __syncthreads();
+  const unsigned n = min(dq->n, (unsigned)kDeferCap);
+  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) reg_insert(R, dq->keys[i], t, false);
+}
+
 template <typename T, bool REG, int U, bool CHECK = false, typename Rule>
 __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint64_t (&bip)[U],
                                            int m, T* __restrict__ cells, const HashParams& H,
                                            const Rule& rule, const RegRef& R, long long t,
-                                           unsigned* filt) {
+                                           unsigned* filt, DeferQ* dq = nullptr) {
 #pragma unroll
   for (int q = 0; q < U; ++q) {
     if (q < m) {
@@ -246,6 +265,13 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
           else R.table[slot[q] + 1].last = t;
         }
       } else {
+        if (dq) {
+          const unsigned pos = atomicAdd(&dq->n, 1u);
+          if (pos < (unsigned)kDeferCap) {
+            dq->keys[pos] = aip[q];
+            continue;
+          }
+        }
         reg_insert(R, aip[q], t, false);
       }
     }
@@ -257,7 +283,11 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
     Rule rule, RegRef R, long long t) {
   __shared__ unsigned filt[REG && CHECK ? kTouchSlots : 1];
-  if (REG && CHECK) touch_filter_init(filt);
+  __shared__ __align__(16) unsigned char dq_raw[REG ? sizeof(DeferQ) : 16];
+  DeferQ* dq = REG ? reinterpret_cast<DeferQ*>(dq_raw) : nullptr;
+  if (REG) defer_init(dq);
+  if (REG && CHECK) touch_filter_init(filt);  // (its barrier also publishes dq->n = 0)
+  else if (REG) __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   for (; i < npairs2; i += V * stride) {
@@ -274,8 +304,9 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
         a[2 * v] = b[2 * v] = a[2 * v + 1] = b[2 * v + 1] = 0;
       }
     }
-    scan_batch<T, REG, 2 * V, CHECK>(a, b, m, cells, H, rule, R, t, filt);
+    scan_batch<T, REG, 2 * V, CHECK>(a, b, m, cells, H, rule, R, t, filt, dq);
   }
+  if (REG) defer_drain(dq, R, t);
 }
 
 template <typename T, bool REG, typename Rule = AtRule>

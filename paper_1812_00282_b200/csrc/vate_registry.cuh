@@ -40,9 +40,30 @@ __device__ __forceinline__ void reg_touch(RegEntry* e, long long t, bool use_max
   }
 }
 
-// Insert-or-touch.  use_max is only used when draining the overflow list,
-// where entries of several calls meet (identical to overwrite whenever slice
-// indices are non-decreasing, as Pipeline.run feeds them).
+// Claim or find `key` at slot e (seen empty by a weak load): the CAS settles
+// races; returns true when the key is (now) stored there.
+__device__ __forceinline__ bool reg_claim(const RegRef& R, RegEntry* e, uint64_t key, long long t,
+                                          bool use_max) {
+  const unsigned long long prev = atomicCAS(&e->key, kEmptyKey, key);
+  if (prev == kEmptyKey) {
+    atomicAdd(R.count, 1ull);
+    reg_touch(e, t, use_max);
+    return true;
+  }
+  if (prev == key) {
+    reg_touch(e, t, use_max);
+    return true;
+  }
+  return false;  // another key took the slot first
+}
+
+// Insert-or-touch, one 32-byte sector (two slots, one 256-bit load) per probe
+// step.  Weak loads are safe here: a slot's key changes only once (empty ->
+// key) within a launch and there are no deletions, so a stale "empty" only
+// sends us to the CAS, which reports the truth.  use_max is only used when
+// draining the overflow list, where entries of several calls meet (identical
+// to overwrite whenever slice indices are non-decreasing, as Pipeline.run
+// feeds them).
 __device__ __forceinline__ void reg_insert(const RegRef& R, uint64_t key, long long t,
                                            bool use_max) {
   if (key == kEmptyKey) {  // the one key that collides with the empty marker
@@ -53,26 +74,21 @@ __device__ __forceinline__ void reg_insert(const RegRef& R, uint64_t key, long l
   }
   uint64_t h = reg_home(key, R.mask);
 #pragma unroll 1
-  for (int probe = 0; probe < kMaxProbe; ++probe) {
-    RegEntry* e = R.table + h;
-    unsigned long long k = *((volatile unsigned long long*)&e->key);
-    if (k == key) {
-      reg_touch(e, t, use_max);
+  for (int step = 0; step < kMaxProbe / 2; ++step) {
+    RegEntry a, b;
+    ld_pair(R.table + h, a, b);
+    if (a.key == key) {
+      reg_touch(R.table + h, t, use_max);
       return;
     }
-    if (k == kEmptyKey) {
-      unsigned long long prev = atomicCAS(&e->key, kEmptyKey, key);
-      if (prev == kEmptyKey) {
-        atomicAdd(R.count, 1ull);
-        reg_touch(e, t, use_max);
-        return;
-      }
-      if (prev == key) {
-        reg_touch(e, t, use_max);
-        return;
-      }
+    if (a.key == kEmptyKey && reg_claim(R, R.table + h, key, t, use_max)) return;
+    // slot h is (now) some other key: b is next in the probe sequence
+    if (b.key == key) {
+      reg_touch(R.table + h + 1, t, use_max);
+      return;
     }
-    h = (h + 1) & R.mask;
+    if (b.key == kEmptyKey && reg_claim(R, R.table + h + 1, key, t, use_max)) return;
+    h = (h + 2) & R.mask;  // both slots hold other keys (non-empty keys never change)
   }
   // probe limit: park it; the host drains (grows + reinserts) before any read
   unsigned long long slot = atomicAdd(R.ovf_n, 1ull);
