@@ -309,17 +309,26 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
   if (REG) defer_drain(dq, R, t);
 }
 
-template <typename T, bool REG, typename Rule = AtRule>
+// One 8-byte packet per thread (the default form, VATE_OPT_SCAN_V = 0): the
+// most threads, the shortest per-thread dependency chain; registry misses go
+// through the same per-CTA deferred queue, CHECK adds the heavy-hitter forms.
+template <typename T, bool REG, bool CHECK = false, typename Rule = AtRule>
 __global__ void __launch_bounds__(kThreads) k_scan_packed8(
     const uint2* __restrict__ pairs, uint64_t n, T* __restrict__ cells, HashParams H,
     Rule rule, RegRef R, long long t) {
-  unsigned* filt = nullptr;  // heavy-hitter filter only in the CHECK form of the packed16 scan
+  __shared__ unsigned filt[REG && CHECK ? kTouchSlots : 1];
+  __shared__ __align__(16) unsigned char dq_raw[REG ? sizeof(DeferQ) : 16];
+  DeferQ* dq = REG ? reinterpret_cast<DeferQ*>(dq_raw) : nullptr;
+  if (REG) defer_init(dq);
+  if (REG && CHECK) touch_filter_init(filt);
+  else if (REG) __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint2 q = pairs[i];
+    const uint2 q = __ldcs(pairs + i);  // streamed once: evict-first
     const uint64_t a[1] = {q.x}, b[1] = {q.y};
-    scan_batch<T, REG, 1>(a, b, 1, cells, H, rule, R, t, filt);
+    scan_batch<T, REG, 1, CHECK>(a, b, 1, cells, H, rule, R, t, filt, dq);
   }
+  if (REG) defer_drain(dq, R, t);
 }
 
 template <typename T, bool REG, typename Rule = AtRule>
@@ -1054,7 +1063,7 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_scan_check = (int)value;
     return VATE_OK;
   }
-  if (option == VATE_OPT_SCAN_V && (value == 1 || value == 2 || value == 4)) {
+  if (option == VATE_OPT_SCAN_V && (value == 0 || value == 1 || value == 2 || value == 4)) {
     p->opt_scan_v = (int)value;
     return VATE_OK;
   }
@@ -1191,8 +1200,10 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
   }
   rc = apply_l2_window(p, hosts);
   if (rc) return rc;
-  const uint32_t grid = p->opt_scan_v == 1 ? grid_for((n + 1) / 2, kThreads, 148u * 64u)
-                                           : grid_for(n, kThreads, 148u * 16u);
+  // packed16: one iteration of V uint4 (2V packets) per thread; others: grid-stride
+  const uint64_t per_thread = 2ull * (uint64_t)(p->opt_scan_v > 0 ? p->opt_scan_v : 1);
+  const uint32_t grid16 = grid_for((n + per_thread - 1) / per_thread, kThreads, 148u * 64u);
+  const uint32_t grid = grid_for(n, kThreads, 148u * 16u);
   if (pairs) {
     const void* d_pairs;
     rc = stage_in(p, p->in_a, pairs, n * 8, where, &d_pairs);
@@ -1201,43 +1212,48 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     return with_store(p, [&](auto tag, auto rule) -> int {
       using T = decltype(tag);
       using Rl = decltype(rule);
-      if (aligned16 && n >= 2) {
+      if (aligned16 && n >= 2 && p->opt_scan_v > 0) {
         if (hosts && p->opt_scan_v == 1 && p->opt_scan_check)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 1, true, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, true, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else if (hosts && p->opt_scan_v == 1)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 1, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, false, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else if (hosts && p->opt_scan_v == 4)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 4, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 4, false, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else if (hosts)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, 2, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 2, false, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, false, 2, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, false, 2, false, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         if (n & 1) {
           const uint2* last = (const uint2*)d_pairs + (n - 1);
           if (hosts)
-            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, true, Rl>), last, 1,
+            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, true, false, Rl>), last, 1,
                         (T*)p->cells, H, rule, R, (long long)t);
           else
-            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, false, Rl>), last, 1,
+            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, false, false, Rl>), last, 1,
                         (T*)p->cells, H, rule, R, (long long)t);
         }
-      } else {
-        if (hosts)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, true, Rl>),
+      } else {  // unaligned input, or scan_v == 0: one 8-byte packet per thread
+        const uint32_t grid8 = grid_for(n, kThreads, 148u * 64u);
+        if (hosts && p->opt_scan_check)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, true, true, Rl>),
+                      (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
+                      (long long)t);
+        else if (hosts)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, true, false, Rl>),
                       (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
                       (long long)t);
         else
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, false, false, Rl>),
                       (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
                       (long long)t);
       }

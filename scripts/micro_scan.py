@@ -49,7 +49,7 @@ for l2 in [int(x) for x in os.environ.get("MICRO_L2", "0").split(",")]:
     pool.set_option("l2_persist", l2)
     for chk in (0, 1):
         pool.set_option("scan_check", chk)
-        for v in (1, 2):
+        for v in (1, 0):
             pool.set_option("scan_v", v)
             ms = run(pipe.hosts.handle, 100)
             print(f"{tag} l2={l2} check={chk} V={v} scan+registry ms/launch {ms:.4f}  "
