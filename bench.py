@@ -487,6 +487,7 @@ def run_gpu(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(e2e_rows / args.steps * 25),
                 "host_ms_per_step": {k: v / args.steps for k, v in host_ms.items()}},
         "gpu_launches": int(launches),
+        "active_set_ordering": pool.sort_stats(),
         "g0_kernel": args.g0_kernel,
         "incremental": {"enabled": args.incremental == "on",
                         **{k: inc1[k] - inc0[k] for k in ("rebuilds", "delta_slices",

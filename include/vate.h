@@ -84,7 +84,11 @@ int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
  * (exact), 0 recomputes every g0 by a full gather. */
 enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 2,
                    VATE_OPT_SCAN_CHECK = 3, VATE_OPT_L2_PERSIST = 4, VATE_OPT_BITMAP_KW = 5,
-                   VATE_OPT_CONCURRENT = 6 };
+                   VATE_OPT_CONCURRENT = 6, VATE_OPT_INC_SORT = 7 };
+/* VATE_OPT_INC_SORT (default 1): when few hosts join or leave the window, the
+ * sorted active set (SlidingHostSet.active, pipeline.py:54-58) is updated by
+ * merging the sorted arrivals and removing the departures instead of a full
+ * radix sort. */
 /* VATE_OPT_CONCURRENT (default 1): the estimate's registry compaction runs
  * beside the bitmap pass, and the slice advance beside g0 + float path, on a
  * second stream of the pool (fork/join by events; results unchanged). */
@@ -96,6 +100,8 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value);
  * total index-rebuild time in microseconds, misses gathered since the rebuild,
  * extensions (previous misses merged into the index)] */
 int vate_pool_inc_stats(vate_pool* p, uint64_t out[11]);
+/* active-set ordering work: [full radix sorts, incremental merges, reuses] */
+int vate_pool_sort_stats(const vate_pool* p, uint64_t out[3]);
 
 /* cudaProfilerStart/Stop, so `ncu --profile-from-start off` captures exactly a
  * timed region (bench.py with VATE_PROFILE_REGION=1). */

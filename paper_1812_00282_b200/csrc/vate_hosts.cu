@@ -10,13 +10,25 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <string>
+#include <utility>
 
 #include "vate_internal.cuh"
 #include "vate_registry.cuh"
 
 namespace vate {
 
-enum HCtr { H_COUNT = 0, H_OVF = 1, H_SPECIAL = 2, H_MAXKEY = 3, H_NOUT = 4, H_CHANGES = 5, H_NOUT2 = 6, H_N = 8 };
+enum HCtr { H_COUNT = 0, H_OVF = 1, H_SPECIAL = 2, H_MAXKEY = 3, H_NOUT = 4, H_CHANGES = 5, H_NOUT2 = 6,
+            H_ARR = 7, H_DEP = 8, H_N = 10 };
+
+// Membership flips of one compaction, for the incremental sorted-set update:
+// keys that joined (arrivals) and left (departures) the window's active set.
+struct FlipLists {
+  unsigned long long* arr;
+  unsigned long long* dep;
+  uint64_t cap;            // entries per list; a list that overflows forces a full sort
+  unsigned long long* n_arr;
+  unsigned long long* n_dep;
+};
 
 RegRef make_ref(const vate_hosts* h, const DevBuf& table, uint64_t cap) {
   RegRef R{};
@@ -65,7 +77,7 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
                                                 uint8_t* __restrict__ member,
                                                 unsigned long long* nout,
                                                 unsigned long long* maxkey,
-                                                unsigned long long* changes) {
+                                                unsigned long long* changes, FlipLists F) {
   __shared__ unsigned s_n, s_flips;
   __shared__ unsigned long long s_max;
   if (threadIdx.x == 0) {
@@ -90,6 +102,10 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
       if ((member[i] != 0) != tk) {
         member[i] = tk;
         ++flips;
+        if (F.arr) {  // rare in steady traffic: one atomic per flip
+          const unsigned long long pos = atomicAdd(tk ? F.n_arr : F.n_dep, 1ull);
+          if (pos < F.cap) (tk ? F.arr : F.dep)[pos] = e.key;
+        }
       }
       if (tk) {
         ++mine;
@@ -390,6 +406,45 @@ int hosts_prepare_insert(vate_hosts* h, uint64_t n) {
   return VATE_OK;
 }
 
+// lower_bound in a sorted device array
+__device__ __forceinline__ uint64_t lower_bound_u64(const unsigned long long* a, uint64_t n,
+                                                    unsigned long long x) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Incremental sorted-set update: new = (old \ dep) U arr, all sorted, arr and
+// old disjoint, dep a subset of old.  Every element's final rank is found by
+// binary search, so the merge is one scatter pass.
+__global__ void k_merge_old(const unsigned long long* __restrict__ old, uint64_t n_old,
+                            const unsigned long long* __restrict__ dep, uint64_t n_dep,
+                            const unsigned long long* __restrict__ arr, uint64_t n_arr,
+                            unsigned long long* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_old; i += stride) {
+    const unsigned long long x = old[i];
+    const uint64_t d = lower_bound_u64(dep, n_dep, x);
+    if (d < n_dep && dep[d] == x) continue;  // departed
+    out[i - d + lower_bound_u64(arr, n_arr, x)] = x;
+  }
+}
+
+__global__ void k_merge_new(const unsigned long long* __restrict__ old, uint64_t n_old,
+                            const unsigned long long* __restrict__ dep, uint64_t n_dep,
+                            const unsigned long long* __restrict__ arr, uint64_t n_arr,
+                            unsigned long long* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_arr; j += stride) {
+    const unsigned long long y = arr[j];
+    out[j + lower_bound_u64(old, n_old, y) - lower_bound_u64(dep, n_dep, y)] = y;
+  }
+}
+
 static int sort_keys(vate_pool* p, uint64_t* in, uint64_t* out, uint64_t n, int end_bit) {
   size_t bytes = 0;
   VATE_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const unsigned long long*)in,
@@ -427,11 +482,20 @@ int hosts_active_launch(vate_hosts* h, int64_t t, int k_prime) {
     VATE_CUDA(cudaMemsetAsync(h->member.ptr, 0, h->cap + 1, p->stream));
     h->member_valid = false;  // first compaction after a (re)layout always sorts
   }
-  VATE_CUDA(cudaMemsetAsync(h->d_count + H_MAXKEY, 0, 32, p->stream));
+  VATE_CUDA(cudaMemsetAsync(h->d_count + H_MAXKEY, 0, 8 * (H_N - H_MAXKEY), p->stream));
+  FlipLists F{};
+  h->flip_cap = std::max<uint64_t>(4096, h->cap / 16);
+  rc = h->flips.ensure(4 * h->flip_cap * 8);
+  if (rc) return rc;
+  F.arr = h->flips.as<unsigned long long>();
+  F.dep = F.arr + h->flip_cap;
+  F.cap = h->flip_cap;
+  F.n_arr = h->d_count + H_ARR;
+  F.n_dep = h->d_count + H_DEP;
   VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for((h->cap + 4) / 4, 256, 148u * 8u), 256, 0, k_active,
               h->table.as<const RegEntry>(), h->cap, h->d_count + H_SPECIAL,
               (long long)(t - k_prime), h->member.as<uint8_t>(), h->d_count + H_NOUT,
-              h->d_count + H_MAXKEY, h->d_count + H_CHANGES);
+              h->d_count + H_MAXKEY, h->d_count + H_CHANGES, F);
   VATE_CUDA(cudaMemcpyAsync(h->h_count, h->d_count, H_N * 8, cudaMemcpyDeviceToHost, p->stream));
   return VATE_OK;
 }
@@ -454,11 +518,49 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
   *n = h->h_count[H_NOUT];
   *keys_dev = p->hosts_sorted.as<uint64_t>();
   // same membership as the last compaction, whose sorted list is still in place
+  const bool was_valid = h->member_valid;  // member[] held the previous compaction's set
   const bool reuse = h->member_valid && h->h_count[H_CHANGES] == 0 && p->sorted_owner == h &&
                      p->sorted_n == *n;
   h->member_valid = true;
   if (reuse) {
     p->sorts_skipped++;
+    return VATE_OK;
+  }
+  // membership changed by a few keys: merge them into the previous sorted list
+  const uint64_t na = h->h_count[H_ARR], nd = h->h_count[H_DEP];
+  const bool incremental = p->opt_inc_sort && was_valid &&
+                           p->sorted_owner == h && na <= h->flip_cap && nd <= h->flip_cap &&
+                           p->sorted_n + na - nd == *n && (na + nd) * 8 <= *n;
+  if (incremental) {
+    unsigned long long* arr = h->flips.as<unsigned long long>();
+    unsigned long long* dep = arr + h->flip_cap;
+    unsigned long long* arr_s = dep + h->flip_cap;
+    unsigned long long* dep_s = arr_s + h->flip_cap;
+    if (na > 1) {
+      rc = sort_keys(p, (uint64_t*)arr, (uint64_t*)arr_s, na, 64);
+      if (rc) return rc;
+    } else if (na == 1) {
+      VATE_CUDA(cudaMemcpyAsync(arr_s, arr, 8, cudaMemcpyDeviceToDevice, p->stream));
+    }
+    if (nd > 1) {
+      rc = sort_keys(p, (uint64_t*)dep, (uint64_t*)dep_s, nd, 64);
+      if (rc) return rc;
+    } else if (nd == 1) {
+      VATE_CUDA(cudaMemcpyAsync(dep_s, dep, 8, cudaMemcpyDeviceToDevice, p->stream));
+    }
+    const auto* old = p->hosts_sorted.as<const unsigned long long>();
+    auto* out = p->hosts_tmp.as<unsigned long long>();
+    VATE_LAUNCH(p, VATE_K_SORT, grid_for(p->sorted_n, 256, 148u * 16u), 256, 0, k_merge_old, old,
+                p->sorted_n, dep_s, nd, arr_s, na, out);
+    if (na)
+      VATE_LAUNCH(p, VATE_K_SORT, grid_for(na, 256, 148u * 16u), 256, 0, k_merge_new, old,
+                  p->sorted_n, dep_s, nd, arr_s, na, out);
+    std::swap(p->hosts_sorted.ptr, p->hosts_tmp.ptr);
+    std::swap(p->hosts_sorted.bytes, p->hosts_tmp.bytes);
+    *keys_dev = p->hosts_sorted.as<uint64_t>();
+    p->sorted_n = *n;
+    p->sorted_version++;
+    p->sorts_incremental++;
     return VATE_OK;
   }
   // membership changed: write the member keys (same predicate, from member[])
@@ -481,6 +583,7 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
   p->sorted_owner = h;
   p->sorted_n = *n;
   p->sorted_version++;
+  p->sorts_full++;
   return VATE_OK;
 }
 

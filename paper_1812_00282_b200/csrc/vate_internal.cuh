@@ -294,6 +294,8 @@ struct vate_pool {
   const void* sorted_owner = nullptr;  // registry whose active set hosts_sorted holds
   uint64_t sorted_n = 0;
   uint64_t sorts_skipped = 0;
+  uint64_t sorts_full = 0, sorts_incremental = 0;
+  int opt_inc_sort = 1;       // merge membership flips into the sorted active set
   uint64_t sorted_version = 1;         // bumps whenever hosts_sorted changes content
   const int32_t* g0_src = nullptr;     // g0 array the float path reads (p->g0 or inc.g0x)
   cudaEvent_t ev_adv = nullptr;        // advance counters landed in h_ctr
@@ -326,6 +328,9 @@ struct vate_hosts {
   bool needs_grow = false; // load factor passed 1/2: grow at the next drain point
   vate::DevBuf member;     // u8 per slot: in the active set of the last compaction
   bool member_valid = false;
+  vate::DevBuf flips;      // arrivals, departures and their sorted copies (4 x flip_cap)
+  uint64_t flip_cap = 0;
+
   vate::RegRef ref() const;
 };
 

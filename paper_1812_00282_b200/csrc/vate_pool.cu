@@ -1051,6 +1051,10 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     }
     return VATE_OK;
   }
+  if (option == VATE_OPT_INC_SORT && (value == 0 || value == 1)) {
+    p->opt_inc_sort = (int)value;
+    return VATE_OK;
+  }
   if (option == VATE_OPT_CONCURRENT && (value == 0 || value == 1)) {
     p->opt_concurrent = (int)value;
     return VATE_OK;
@@ -1073,6 +1077,14 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     return VATE_OK;
   }
   return set_error(VATE_EVALUE, "unknown option or value");
+}
+
+int vate_pool_sort_stats(const vate_pool* p, uint64_t out[3]) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  out[0] = p->sorts_full;
+  out[1] = p->sorts_incremental;
+  out[2] = p->sorts_skipped;
+  return VATE_OK;
 }
 
 int vate_pool_inc_stats(vate_pool* p, uint64_t out[11]) {

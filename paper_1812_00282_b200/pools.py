@@ -248,7 +248,8 @@ class _DevicePool:
     def set_option(self, option: str, value: int) -> None:
         """Tuning switches: 'g0_kernel' (0 auto, 1 gather, 2 smem) and 'incremental' (0/1)."""
         check(lib.vate_pool_set_option(self._h, ("g0_kernel", "incremental", "scan_v", "scan_check",
-                                                     "l2_persist", "bitmap_kw", "concurrent").index(option),
+                                                     "l2_persist", "bitmap_kw", "concurrent",
+                                                     "inc_sort").index(option),
                                        int(value)))
 
     def inc_stats(self) -> dict:
@@ -259,6 +260,12 @@ class _DevicePool:
                 "last_delta_cells", "last_delta_work", "identity_slices", "hosts_indexed",
                 "rebuild_us_total", "miss_accum", "extends")
         return dict(zip(keys, list(out)))
+
+    def sort_stats(self) -> dict:
+        """How the sorted active set was produced: full sorts, merges, reuses."""
+        out = (C.c_uint64 * 3)()
+        check(lib.vate_pool_sort_stats(self._h, out))
+        return dict(zip(("full", "incremental", "reused"), list(out)))
 
     def set_timing(self, on: bool) -> None:
         check(lib.vate_pool_set_timing(self._h, int(on)))

@@ -921,3 +921,34 @@ def test_full_size_cfg3_zipf_superspreaders():
         m = pipe.last_maintenance
         assert (m.blocks, m.cells_maintained, m.cells_cleared) == (due, visited, cleared)
     assert pool.snapshot_bytes() == opool.snapshot_bytes()
+
+
+@pytest.mark.parametrize("inc_sort", [1, 0])
+def test_active_set_merge_under_small_churn(inc_sort):
+    """SlidingHostSet.active (pipeline.py:54-58) when a few hosts join and leave
+    each slice: the sorted active set is updated by merging the sorted arrivals
+    and dropping the departures (VATE_OPT_INC_SORT) -- equal to the oracle's set,
+    reports and all, slice by slice, with the special key 2^64-1 among them."""
+    cfg = vb.EstimatorConfig(128, 14, 8, seed=6)
+    ocfg = vo.OracleConfig(128, 14, 8, seed=6)
+    pool = cfg.build_pool()
+    pool.set_option("inc_sort", inc_sort)
+    pipe = vb.Pipeline(pool, cfg, 5)
+    opipe = vo.OraclePipeline(ocfg, 5)
+    rng = np.random.default_rng(12)
+    base = rng.choice(1 << 40, 3000, replace=False).astype(np.uint64)
+    for t in range(30):
+        churn = rng.choice(1 << 40, 20, replace=False).astype(np.uint64) + np.uint64(1 << 41)
+        a = np.concatenate([base[rng.integers(0, len(base), 6000)], churn])
+        if t % 7 == 3:
+            a = np.concatenate([a, np.array([2**64 - 1], dtype=np.uint64)])
+        b = rng.integers(1, 1 << 40, len(a)).astype(np.uint64)
+        got, _ = pipe.process_slice_soa(t, a, b)
+        want = opipe.process_slice(t, a, b)
+        assert np.array_equal(got.host, want.reports.host), t
+        assert np.array_equal(got.estimate, want.reports.estimate), t
+    st = pool.sort_stats()
+    if inc_sort:
+        assert st["incremental"] > 10, st
+    else:
+        assert st["incremental"] == 0, st
