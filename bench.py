@@ -279,6 +279,9 @@ def run_gpu(args, rank, world, local_rank):
     if args.l2_persist:
         pool.set_option("l2_persist", args.l2_persist)
     pool.set_option("concurrent", args.concurrent)
+    for kv in args.opt:                       # experiments: --opt spin_wait=0 ...
+        name, val = kv.split("=")
+        pool.set_option(name, int(val))
     n = w["packets"]
     slice_bytes = n * 8
     torch.cuda.set_device(dev)
@@ -535,6 +538,8 @@ def main():
                     help="load-before-store scan (VATE_OPT_SCAN_CHECK)")
     ap.add_argument("--l2-persist", type=int, choices=(0, 1, 2), default=0,
                     help="L2 persisting window: 1 host registry, 2 cells (VATE_OPT_L2_PERSIST)")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="extra pool option name=value (AtPool.set_option), for A/B runs")
     ap.add_argument("--concurrent", type=int, choices=(0, 1), default=1,
                     help="registry compaction beside the bitmap pass, advance beside g0 + float "
                          "path, on a second stream (VATE_OPT_CONCURRENT)")

@@ -72,6 +72,10 @@ int vate_pool_launches(const vate_pool* p, uint64_t* n);
 /* per-kernel CUDA-event timing (bench only): kind ids in vate_kernel_kind */
 int vate_pool_set_timing(vate_pool* p, int on);
 int vate_pool_timing(vate_pool* p, int kind, double* total_ms, uint64_t* launches);
+/* the timed launches since timing was switched on: out[3i..3i+2] = (kind, start
+ * ms, end ms) relative to the switch-on; *n = count (may exceed cap).  Gaps
+ * between consecutive launches are device idle time (bench diagnostics). */
+int vate_pool_timeline(vate_pool* p, double* out, uint64_t cap, uint64_t* n);
 
 /* stream-ordered timestamps for benchmarking: mark(id) records CUDA event id
  * (0..15) on the pool's stream; elapsed waits for both and returns ms. */
@@ -84,7 +88,11 @@ int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
  * (exact), 0 recomputes every g0 by a full gather. */
 enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 2,
                    VATE_OPT_SCAN_CHECK = 3, VATE_OPT_L2_PERSIST = 4, VATE_OPT_BITMAP_KW = 5,
-                   VATE_OPT_CONCURRENT = 6, VATE_OPT_INC_SORT = 7 };
+                   VATE_OPT_CONCURRENT = 6, VATE_OPT_INC_SORT = 7, VATE_OPT_SPIN_WAIT = 8 };
+/* VATE_OPT_SPIN_WAIT (default 0): the slice's host round trip spins on a flag
+ * a one-thread kernel writes to mapped pinned memory (bounded; falls back to
+ * cudaStreamSynchronize).  Measured slower than the driver's wait on B200
+ * (scripts/timeline.py), kept for the record. */
 /* VATE_OPT_INC_SORT (default 1): when few hosts join or leave the window, the
  * sorted active set (SlidingHostSet.active, pipeline.py:54-58) is updated by
  * merging the sorted arrivals and removing the departures instead of a full

@@ -296,6 +296,10 @@ struct vate_pool {
   uint64_t sorts_skipped = 0;
   uint64_t sorts_full = 0, sorts_incremental = 0;
   int opt_inc_sort = 1;       // merge membership flips into the sorted active set
+  int opt_spin = 0;           // host round trip: spin on a mapped flag (measured slower: off)
+  volatile unsigned long long* h_flag = nullptr;  // mapped pinned sequence flag
+  unsigned long long* d_flag = nullptr;
+  unsigned long long flag_seq = 0;
   uint64_t sorted_version = 1;         // bumps whenever hosts_sorted changes content
   const int32_t* g0_src = nullptr;     // g0 array the float path reads (p->g0 or inc.g0x)
   cudaEvent_t ev_adv = nullptr;        // advance counters landed in h_ctr
@@ -311,6 +315,8 @@ struct vate_pool {
   };
   std::vector<Timed> timed_pending;
   std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t timeline_ref = nullptr;  // recorded when timing is switched on
+  std::vector<double> timeline;        // (kind, start ms, end ms) per timed launch
   double timed_ms[VATE_K_COUNT] = {0};
   uint64_t timed_n[VATE_K_COUNT] = {0};
 };

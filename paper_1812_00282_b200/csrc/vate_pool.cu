@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -77,8 +78,38 @@ int stage_in(vate_pool* p, DevBuf& buf, const void* src, size_t bytes, int where
   return VATE_OK;
 }
 
-int sync_small(vate_pool* p) {
+// The host round trip of a slice: a one-thread kernel stores a sequence number
+// into mapped pinned memory after everything enqueued so far, and the host
+// spins on it (a few hundred ns after the GPU gets there, instead of the
+// driver's wait); after 2 ms of spinning, or without a flag, it falls back to
+// cudaStreamSynchronize (which also surfaces any sticky error).
+__global__ void k_signal(unsigned long long* flag, unsigned long long seq) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(seq) : "memory");
+}
+
+static int wait_stream(vate_pool* p) {
+  if (p->opt_spin && p->h_flag) {
+    const unsigned long long seq = ++p->flag_seq;
+    k_signal<<<1, 1, 0, p->stream>>>(p->d_flag, seq);
+    p->launches++;
+    if (cudaGetLastError() == cudaSuccess) {
+      const auto t0 = std::chrono::steady_clock::now();
+      unsigned spins = 0;
+      while (*p->h_flag < seq) {
+        if ((++spins & 1023u) == 0 &&
+            std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2))
+          break;
+      }
+      if (*p->h_flag >= seq) return VATE_OK;
+    }
+  }
   VATE_CUDA(cudaStreamSynchronize(p->stream));
+  return VATE_OK;
+}
+
+int sync_small(vate_pool* p) {
+  int wrc = wait_stream(p);
+  if (wrc) return wrc;
   if (p->h_ctr && p->h_ctr[C_ERR]) {
     p->h_ctr[C_ERR] = 0;
     return set_error(VATE_EVALUE, "cell index outside the pool");
@@ -114,11 +145,20 @@ void timing_end(vate_pool* p, int kind, cudaEvent_t a) {
 int collect_timing(vate_pool* p) {
   if (p->timed_pending.empty()) return VATE_OK;
   VATE_CUDA(cudaStreamSynchronize(p->stream));
+  if (p->aux_stream) VATE_CUDA(cudaStreamSynchronize(p->aux_stream));
   for (auto& t : p->timed_pending) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, t.a, t.b);
     p->timed_ms[t.kind] += ms;
     p->timed_n[t.kind] += 1;
+    if (p->timeline_ref && p->timeline.size() < 3 * 65536) {  // (kind, start, end) in ms
+      float s0 = 0.f, s1 = 0.f;
+      cudaEventElapsedTime(&s0, p->timeline_ref, t.a);
+      cudaEventElapsedTime(&s1, p->timeline_ref, t.b);
+      p->timeline.push_back((double)t.kind);
+      p->timeline.push_back(s0);
+      p->timeline.push_back(s1);
+    }
     p->event_pool.push_back(t.a);
     p->event_pool.push_back(t.b);
   }
@@ -911,6 +951,11 @@ static int pool_create(vate_pool** out, int kind, int c, int k, int partition, i
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->aux_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&p->h_flag, 64, cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    *p->h_flag = 0;
+    e = cudaHostGetDevicePointer((void**)&p->d_flag, (void*)p->h_flag, 0);
+  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
     for (cudaEvent_t* ev : {&p->ev_fin[i], &p->ev_d2h[i], &p->ev_h2d[i], &p->ev_used[i]})
@@ -969,6 +1014,8 @@ int vate_pool_destroy(vate_pool* p) {
   if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
   if (p->aux_stream) cudaStreamDestroy(p->aux_stream);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->timeline_ref) cudaEventDestroy(p->timeline_ref);
+  if (p->h_flag) cudaFreeHost((void*)p->h_flag);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   inc_release(p);
   if (p->cells) cudaFree(p->cells);
@@ -1016,6 +1063,11 @@ int vate_pool_set_timing(vate_pool* p, int on) {
   rc = collect_timing(p);
   if (rc) return rc;
   p->timing = on != 0;
+  p->timeline.clear();
+  if (p->timing) {
+    if (!p->timeline_ref) VATE_CUDA(cudaEventCreate(&p->timeline_ref));
+    VATE_CUDA(cudaEventRecord(p->timeline_ref, p->stream));
+  }
   for (int i = 0; i < VATE_K_COUNT; ++i) {
     p->timed_ms[i] = 0;
     p->timed_n[i] = 0;
@@ -1051,6 +1103,10 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     }
     return VATE_OK;
   }
+  if (option == VATE_OPT_SPIN_WAIT && (value == 0 || value == 1)) {
+    p->opt_spin = (int)value;
+    return VATE_OK;
+  }
   if (option == VATE_OPT_INC_SORT && (value == 0 || value == 1)) {
     p->opt_inc_sort = (int)value;
     return VATE_OK;
@@ -1077,6 +1133,17 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     return VATE_OK;
   }
   return set_error(VATE_EVALUE, "unknown option or value");
+}
+
+int vate_pool_timeline(vate_pool* p, double* out, uint64_t cap, uint64_t* n) {
+  int rc = enter(p);
+  if (rc) return rc;
+  rc = collect_timing(p);
+  if (rc) return rc;
+  const uint64_t m = p->timeline.size() / 3;
+  *n = m;
+  for (uint64_t i = 0; i < 3 * std::min<uint64_t>(m, cap); ++i) out[i] = p->timeline[i];
+  return VATE_OK;
 }
 
 int vate_pool_sort_stats(const vate_pool* p, uint64_t out[3]) {

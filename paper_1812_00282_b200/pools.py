@@ -249,7 +249,7 @@ class _DevicePool:
         """Tuning switches: 'g0_kernel' (0 auto, 1 gather, 2 smem) and 'incremental' (0/1)."""
         check(lib.vate_pool_set_option(self._h, ("g0_kernel", "incremental", "scan_v", "scan_check",
                                                      "l2_persist", "bitmap_kw", "concurrent",
-                                                     "inc_sort").index(option),
+                                                     "inc_sort", "spin_wait").index(option),
                                        int(value)))
 
     def inc_stats(self) -> dict:
@@ -266,6 +266,16 @@ class _DevicePool:
         out = (C.c_uint64 * 3)()
         check(lib.vate_pool_sort_stats(self._h, out))
         return dict(zip(("full", "incremental", "reused"), list(out)))
+
+    def timeline(self):
+        """(kind, start ms, end ms) of every timed launch since set_timing(True)."""
+        n = C.c_uint64()
+        check(lib.vate_pool_timeline(self._h, None, 0, C.byref(n)))
+        out = np.zeros(3 * n.value, dtype=np.float64)
+        if n.value:
+            check(lib.vate_pool_timeline(self._h, ptr(out), n.value, C.byref(n)))
+        return [(_lib.KERNEL_KINDS[int(out[3 * i])], out[3 * i + 1], out[3 * i + 2])
+                for i in range(len(out) // 3)]
 
     def set_timing(self, on: bool) -> None:
         check(lib.vate_pool_set_timing(self._h, int(on)))

@@ -1,0 +1,38 @@
+"""Device timeline of the cfg 2 slice step: every launch (CUDA events around
+each kernel) and the idle gaps between them, for a few steady-state slices."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_1812_00282_b200 as vb
+from paper_1812_00282_b200._lib import lib, check
+
+cfg = vb.EstimatorConfig(1024, 24, 60)
+pool = cfg.build_pool()
+for kv in os.environ.get("TL_OPTS", "").split():
+    k_, v_ = kv.split("=")
+    pool.set_option(k_, int(v_))
+pipe = vb.Pipeline(pool, cfg, 60)
+n = 5_000_000
+NB = 140
+bufs = torch.empty((NB, n, 2), dtype=torch.int32, device="cuda:0")
+for i in range(NB):
+    check(lib.vate_synth_packets(pool.handle, i, n, 1_000_000, 0x0A000000, 0, bufs[i].data_ptr()))
+for t in range(130):
+    pipe.step_fast(t, bufs[t].data_ptr(), n, "device", None)
+pipe.wait_reports()
+pool.synchronize()
+pool.set_timing(True)
+for t in range(130, 136):
+    pipe.step_fast(t, bufs[t].data_ptr(), n, "device", None)
+pipe.wait_reports()
+pool.synchronize()
+tl = pool.timeline()
+tl.sort(key=lambda x: x[1])
+prev_end = None
+for kind, s, e in tl:
+    gap = (s - prev_end) * 1e3 if prev_end is not None else 0.0
+    print(f"{kind:9s} start {s*1e3:9.1f} us  dur {(e-s)*1e3:7.1f} us  gap-before {gap:7.1f} us")
+    prev_end = e if prev_end is None else max(prev_end, e)
+scans = [s for k, s, e in tl if k == "scan"]
+print("slice period us:", np.diff(scans) * 1e3)
