@@ -432,6 +432,20 @@ def run_gpu(args, rank, world, local_rank):
         _teardown(dist)
         return
 
+    # speed of light of the scan's memory pattern on this pool shape: one random
+    # 32-B registry-sized load + one random cell store per packet, no hashing,
+    # no input stream (scratch pool; csrc vate_bench_sol_scatter)
+    sol = None
+    if rank == 0:
+        scratch_pool = vb.AtPool(w["c"], w["k"], w["partition"], device=dev)
+        table_bytes = 16 * (1 << max(12, (2 * w["hosts"] - 1).bit_length()))
+        sol_ms = C.c_double()
+        check(lib.vate_bench_sol_scatter(scratch_pool.handle, n, table_bytes, 10,
+                                         C.byref(sol_ms)))
+        scratch_pool.close()
+        sol = {"ms_per_slice_of_packets": sol_ms.value, "registry_table_bytes": table_bytes,
+               "pool_bytes": (1 << w["c"]) * (1 if 2 * w["k"] <= 254 else 2)}
+
     peaks, peak_src = _peaks()
     hbm = float(peaks["hbm_gbs"])
     # dominant kernel by event time; algorithmic bytes per launch
@@ -491,6 +505,12 @@ def run_gpu(args, rank, world, local_rank):
                 "host_ms_per_step": {k: v / args.steps for k, v in host_ms.items()}},
         "gpu_launches": int(launches),
         "active_set_ordering": pool.sort_stats(),
+        "scan_speed_of_light": dict(sol, scan_ms_per_launch=per_kind["scan"]["ms_per_launch"],
+                                    scan_over_sol=per_kind["scan"]["ms_per_launch"]
+                                    / sol["ms_per_slice_of_packets"],
+                                    note="random 32-B load (registry-sized table) + random "
+                                         "cell store per packet, no hashing or packet "
+                                         "stream: the L2/HBM random-access ceiling") if sol else None,
         "g0_kernel": args.g0_kernel,
         "incremental": {"enabled": args.incremental == "on",
                         **{k: inc1[k] - inc0[k] for k in ("rebuilds", "delta_slices",

@@ -330,6 +330,14 @@ int vate_trace_bucket(vate_pool* p, const uint8_t* records, uint64_t n, int wher
 /* stream-ordered device-to-device copy on the pool's stream (ingest carry) */
 int vate_copy_device(vate_pool* p, void* dst, const void* src, uint64_t bytes);
 
+/* ---- speed-of-light probe (bench only) -----------------------------------
+ * n "packets" of the scan's memory pattern without its arithmetic or input
+ * stream: one random 32-B load from a table_bytes table and one random byte
+ * store into the pool's cells (power-of-two spans; clobbers the cells -- use a
+ * scratch pool).  Mean ms per launch over reps. */
+int vate_bench_sol_scatter(vate_pool* p, uint64_t n, uint64_t table_bytes, int reps,
+                           double* ms_per_rep);
+
 /* ---- synthetic traffic (bench / tests): oracle.synthetic_slice ---------- */
 int vate_synth_packets(vate_pool* p, int64_t t, uint64_t n, uint64_t hosts,
                        uint64_t base_aip, uint64_t trace_seed, uint32_t* pairs_dev);

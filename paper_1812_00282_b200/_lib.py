@@ -112,6 +112,7 @@ _SIGS = {
                            C.POINTER(_i64)], _int),
     "vate_copy_device": ([_p, _p, _p, _u64], _int),
     "vate_synth_zipf": ([_p, _i64, _u64, _u64, _u64, _u64, _p, _p, _u64, C.c_uint32, _p], _int),
+    "vate_bench_sol_scatter": ([_p, _u64, _u64, _int, _pdbl], _int),
     "vate_synth_packets": ([_p, _i64, _u64, _u64, _u64, _u64, _p], _int),
 }
 

@@ -252,3 +252,61 @@ int vate_pool_kind(const vate_pool* p, int* kind, uint64_t* slice_index) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Speed-of-light probe for the scan's memory pattern (bench only): per
+// "packet", one random 32-byte sector load from a table of table_bytes and one
+// random 1-byte store into a buffer of cell_bytes, addresses from a counter
+// hash (no input stream, no dependency between them).  Both buffers sized as
+// the scan's registry and pool, so this is the L2 (or HBM) random-access
+// ceiling the scan kernel is measured against.
+// ---------------------------------------------------------------------------
+namespace vate {
+__global__ void __launch_bounds__(256) k_sol_scatter(const uint4* __restrict__ table,
+                                                     uint64_t table_mask,
+                                                     uint8_t* __restrict__ cells,
+                                                     uint64_t cell_mask, uint64_t n,
+                                                     unsigned long long* sink) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long acc = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t h = mix64(i * kPhi + 12345);
+    cells[h & cell_mask] = (uint8_t)i;
+    const uint4 v = table[(h >> 32) & table_mask];
+    acc += v.x ^ v.w;
+  }
+  if (acc == 0x9E3779B97F4A7C15ull) *sink = acc;  // keeps the loads alive
+}
+}  // namespace vate
+
+extern "C" int vate_bench_sol_scatter(vate_pool* p, uint64_t n, uint64_t table_bytes,
+                                      int reps, double* ms_per_rep) {
+  int rc = enter(p);
+  if (rc) return rc;
+  const uint64_t cell_bytes = p->L.size * (uint64_t)p->cell_bytes;
+  DevBuf table;
+  rc = table.ensure(table_bytes);
+  if (rc) return rc;
+  VATE_CUDA(cudaMemsetAsync(table.ptr, 0, table_bytes, p->stream));
+  cudaEvent_t a, b;
+  VATE_CUDA(cudaEventCreate(&a));
+  VATE_CUDA(cudaEventCreate(&b));
+  const uint32_t grid = grid_for(n, 256, 148u * 64u);
+  uint64_t tmask = 1;
+  while (tmask * 2 * 16 <= table_bytes) tmask *= 2;
+  VATE_LAUNCH(p, VATE_K_OTHER, grid, 256, 0, k_sol_scatter, table.as<const uint4>(), tmask - 1,
+              (uint8_t*)p->cells, cell_bytes - 1, n, p->d_ctr + C_TRACE);  // warm-up
+  VATE_CUDA(cudaEventRecord(a, p->stream));
+  for (int r = 0; r < reps; ++r)
+    VATE_LAUNCH(p, VATE_K_OTHER, grid, 256, 0, k_sol_scatter, table.as<const uint4>(), tmask - 1,
+                (uint8_t*)p->cells, cell_bytes - 1, n, p->d_ctr + C_TRACE);
+  VATE_CUDA(cudaEventRecord(b, p->stream));
+  VATE_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  VATE_CUDA(cudaEventElapsedTime(&ms, a, b));
+  *ms_per_rep = ms / reps;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  table.release();
+  return VATE_OK;
+}
