@@ -71,19 +71,26 @@ KERNEL_SYMBOL = {"scan": "k_scan_packed16", "bitmap": "k_bitmap", "g0": "k_g0", 
                  "registry": "k_active", "sweep": "k_sweep"}
 
 
-def _ncu_traffic(kind):
-    """dram read+write bytes per launch of the kernel behind `kind`, from the committed
-    ncu --set full summaries (profiles/*ncu_kernels.txt); None if not captured."""
+def _ncu_traffic(kind, cfg="cfg2"):
+    """dram read+write bytes per launch of the kernel behind `kind` for this workload,
+    from the committed ncu --set full summaries (profiles/*ncu_kernels.txt; captures of
+    other configs are named *_<cfg>_*, cfg 2's carry no config tag); None if not captured."""
     import glob
     sym = KERNEL_SYMBOL.get(kind)
     if sym is None:
         return None
+
+    def mine(header):
+        if "_full" in header or sym not in header:
+            return False
+        return f"_{cfg}_" in header if cfg != "cfg2" else "_cfg" not in header
+
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_kernels.txt")), reverse=True):
         cur, vals = None, {}
         for line in open(path):
             if line.startswith("## "):
                 cur = line
-            elif cur and sym in cur and "_full" not in cur and "dram__bytes" in line:
+            elif cur and mine(cur) and "dram__bytes" in line:
                 parts = line.split()
                 v, unit = float(parts[1]), parts[2] if len(parts) > 2 else "byte"
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
@@ -497,7 +504,7 @@ def run_gpu(args, rank, world, local_rank):
         "kernels": per_kind,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": _ncu_traffic(dom),
+                     "traffic": _ncu_traffic(dom, args.config),
                      "traffic_source": "profiles/*ncu_kernels.txt (ncu --set full, one launch)",
                      "algorithmic_bytes_per_launch": alg_bytes[dom]},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": slice_bytes,
