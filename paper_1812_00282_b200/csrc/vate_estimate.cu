@@ -552,7 +552,7 @@ int vate_reports_from_counts(vate_pool* p, uint64_t g, const int32_t* g0, uint64
 // enqueue: the bitmap pass (P, and the flipped cells when the index is live)
 // and the active-set compaction; their counters are copied to pinned memory.
 static int begin_enqueue(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
-                         int64_t t, int k_prime) {
+                         int64_t t, int k_prime, bool whole_set = true) {
   if (!hosts || hosts->pool != p) return set_error(VATE_EVALUE, "registry does not belong to pool");
   int rc = check_width(p, k_prime);
   if (rc) return rc;
@@ -574,6 +574,10 @@ static int begin_enqueue(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t c
   VATE_CUDA(cudaEventRecord(p->ev_join, p->aux_stream));
   rc = build_bitmap(p, k_prime, inc_delta_ready(p, g, cell_stream, k_prime));
   if (rc) return rc;
+  if (whole_set) {  // the delta apply overlaps the round trip (behind active on aux)
+    rc = inc_apply_early(p, hosts_nactive_dev(hosts), g);
+    if (rc) return rc;
+  }
   VATE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_join, 0));
   return VATE_OK;
 }
@@ -600,6 +604,13 @@ static int begin_complete(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t 
       I.identity_ok = true;
       I.identity_version = I.lookup_version;
     }
+  }
+  if (I.early_apply) {
+    // the guard of the early delta apply read the registry's first active count
+    // (now in the pinned counters); a relaunch below may reset it on the device,
+    // so this stream waits for the apply first
+    I.early_nhosts = hosts_nactive_host(hosts);
+    VATE_CUDA(cudaStreamWaitEvent(p->stream, I.ev_apply, 0));
   }
   uint64_t* keys = nullptr;
   uint64_t n = 0;
@@ -643,7 +654,7 @@ int vate_estimate_begin_part(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64
   int rc = enter(p);
   if (rc) return rc;
   if (nparts < 1 || part < 0 || part >= nparts) return set_error(VATE_EVALUE, "bad part");
-  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime);
+  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime, nparts == 1);
   if (rc) return rc;
   rc = sync_small(p);
   if (rc) return rc;

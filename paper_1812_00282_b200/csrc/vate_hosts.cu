@@ -500,6 +500,9 @@ int hosts_active_launch(vate_hosts* h, int64_t t, int k_prime) {
   return VATE_OK;
 }
 
+const unsigned long long* hosts_nactive_dev(const vate_hosts* h) { return h->d_count + H_NOUT; }
+uint64_t hosts_nactive_host(const vate_hosts* h) { return h->h_count[H_NOUT]; }
+
 // After the caller's sync: handle parked inserts, then sort the active keys.
 int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev, uint64_t* n) {
   vate_pool* p = h->pool;

@@ -23,6 +23,8 @@
 
 #include <string>
 
+#include <utility>
+
 #include "vate_internal.cuh"
 
 namespace vate {
@@ -55,10 +57,26 @@ __global__ void k_inc_fill(const uint64_t* __restrict__ X, uint64_t total, DivU6
 }
 
 // One warp per flipped cell: +1 to every pair that became inactive, -1 otherwise.
+// Early form (guard != nullptr, launched before the slice's host round trip):
+// the kernel itself takes the host's delta-vs-refresh decision from the same
+// counters -- the delta list is complete (count <= cap) and its work is at most
+// a quarter of a full recompute (work <= nhosts * g / 4) -- and does nothing
+// otherwise; the host repeats the decision after the round trip.
+struct ApplyGuard {
+  const unsigned long long* work;
+  const unsigned long long* nhosts;
+  uint64_t g;
+};
+__device__ __forceinline__ bool apply_allowed(const unsigned long long* count, uint64_t cap,
+                                              const ApplyGuard& G) {
+  return *count <= cap && *G.work <= (*G.nhosts * G.g) / 4;
+}
+
 __global__ void k_inc_apply(const unsigned long long* __restrict__ list,
                             const unsigned long long* count, uint64_t cap,
                             const uint32_t* __restrict__ off, const uint32_t* __restrict__ ent,
-                            int32_t* __restrict__ g0x) {
+                            int32_t* __restrict__ g0x, ApplyGuard G) {
+  if (G.work && !apply_allowed(count, cap, G)) return;
   const uint64_t n = umin64(*count, cap);
   const int lane = threadIdx.x & 31;
   const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -366,11 +384,19 @@ int inc_compute_g0(vate_pool* p, const uint64_t* hosts, uint64_t n, HashParams H
     const uint64_t dcells = p->h_ctr[C_DCNT], dwork = p->h_ctr[C_DWORK];
     I.last_delta_cells = dcells;
     I.last_delta_work = dwork;
+    // the early kernel (if launched) decided on the same counters and on the
+    // active count of the first compaction (begin_complete made the stream wait
+    // for it before anything could reset that count)
+    const bool applied = I.early_apply && dcells <= I.dlist_cap &&
+                         dwork <= I.early_nhosts * H.g / 4;
+    I.early_apply = false;
     if (dcells <= I.dlist_cap && dwork <= n * H.g / 4) {
-      VATE_LAUNCH(p, VATE_K_G0, grid_for(umin64(dcells, 1u << 20) * 32 + 32, kThreads, 148u * 16u),
-                  kThreads, 0, k_inc_apply, I.dlist.as<const unsigned long long>(),
-                  p->d_ctr + C_DCNT, I.dlist_cap, I.off.as<const uint32_t>(),
-                  I.ent.as<const uint32_t>(), I.g0x.as<int32_t>());
+      if (!applied)
+        VATE_LAUNCH(p, VATE_K_G0, grid_for(umin64(dcells, 1u << 20) * 32 + 32, kThreads,
+                                           148u * 16u),
+                    kThreads, 0, k_inc_apply, I.dlist.as<const unsigned long long>(),
+                    p->d_ctr + C_DCNT, I.dlist_cap, I.off.as<const uint32_t>(),
+                    I.ent.as<const uint32_t>(), I.g0x.as<int32_t>(), ApplyGuard{});
       I.delta_slices++;
     } else {  // too much churn for the delta: refresh every host of X in one gather
       if ((rc = launch_g0(p, I.X.as<const uint64_t>(), I.m, H, I.g0x.as<int32_t>()))) return rc;
@@ -416,4 +442,34 @@ int inc_compute_g0(vate_pool* p, const uint64_t* hosts, uint64_t n, HashParams H
   return VATE_OK;
 }
 
+}  // namespace vate
+
+namespace vate {
+// Launch the delta apply right behind the bitmap pass, on the aux stream, so it
+// overlaps the slice's host round trip (see k_inc_apply).  Only in steady
+// state: the index is live, no previous lookup is pending (its misses could
+// extend X, which must precede the delta) and the whole active set is this
+// pool's (no multi-GPU share).  nhosts_dev is the registry's active count.
+int inc_apply_early(vate_pool* p, const unsigned long long* nhosts_dev, uint64_t g) {
+  IncIndex& I = p->inc;
+  if (!I.delta_launched || I.lookup_pending || I.want_extend || !p->opt_concurrent) return VATE_OK;
+  if (!I.ev_apply) VATE_CUDA(cudaEventCreateWithFlags(&I.ev_apply, cudaEventDisableTiming));
+  VATE_CUDA(cudaEventRecord(I.ev_apply, p->stream));           // bitmap + delta list done
+  VATE_CUDA(cudaStreamWaitEvent(p->aux_stream, I.ev_apply, 0));
+  std::swap(p->stream, p->aux_stream);
+  cudaEvent_t ta = nullptr;
+  timing_begin(p, VATE_K_G0, &ta);
+  k_inc_apply<<<148u * 16u, kThreads, 0, p->stream>>>(
+      I.dlist.as<const unsigned long long>(), p->d_ctr + C_DCNT, I.dlist_cap,
+      I.off.as<const uint32_t>(), I.ent.as<const uint32_t>(), I.g0x.as<int32_t>(),
+      ApplyGuard{p->d_ctr + C_DWORK, nhosts_dev, g});
+  p->launches++;
+  timing_end(p, VATE_K_G0, ta);
+  const cudaError_t le = cudaGetLastError();
+  std::swap(p->stream, p->aux_stream);
+  if (le != cudaSuccess) return cuda_fail(le, "k_inc_apply (early)");
+  VATE_CUDA(cudaEventRecord(I.ev_apply, p->aux_stream));
+  I.early_apply = true;
+  return VATE_OK;
+}
 }  // namespace vate

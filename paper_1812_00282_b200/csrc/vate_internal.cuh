@@ -208,6 +208,9 @@ namespace vate {
 // bitmap, and that bitmap.  Invariant: g0x[i] == #inactive slots of X[i] in bprev.
 struct IncIndex {
   bool valid = false;
+  bool early_apply = false;               // this slice's delta was launched before the round trip
+  uint64_t early_nhosts = 0;              // the active count that launch's guard read
+  cudaEvent_t ev_apply = nullptr;
   uint64_t g = 0, cs = 0;
   int kp = 0;
   uint64_t m = 0;                         // hosts in X
@@ -372,6 +375,7 @@ int launch_g0_list(vate_pool* p, const uint64_t* hosts_dev, const uint32_t* idx_
                    const unsigned long long* count_dev, uint64_t cap, HashParams H, int32_t* g0_dev);
 bool inc_delta_ready(vate_pool* p, uint64_t g, uint64_t cs, int kp);
 int inc_compute_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H, int kp);
+int inc_apply_early(vate_pool* p, const unsigned long long* nhosts_dev, uint64_t g);
 void inc_release(vate_pool* p);
 
 // registry helpers (vate_hosts.cu)
@@ -385,6 +389,8 @@ int hosts_compact_active(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_
                          uint64_t* n);
 // split form: launch (no sync; counters -> pinned), the caller syncs, finish sorts
 int hosts_active_launch(vate_hosts* h, int64_t t, int k_prime);
+const unsigned long long* hosts_nactive_dev(const vate_hosts* h);  // k_active's count
+uint64_t hosts_nactive_host(const vate_hosts* h);                  // its pinned copy
 int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev, uint64_t* n);
 
 }  // namespace vate

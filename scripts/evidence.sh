@@ -24,3 +24,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_d
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_g0" -s 130 -c 1 \
    -o gpurun_out/ev_prof_k_g0_full python bench.py --steps 20 --warmup 3 --incremental off > /dev/null 2>&1
 tail -2 gpurun_out/ev_smoke.log; tail -3 gpurun_out/ev_pytest_gpu.log; ls gpurun_out | head -50
+# summaries on the box (gpurun brings back <= 64 MiB): text summaries, then drop
+# every report but the cfg 2 scan's
+python scripts/ncu_summary.py "gpurun_out/ev_prof_*.ncu-rep" > gpurun_out/ev_ncu_kernels.txt 2>&1
+python scripts/launch_summary.py gpurun_out/ev_launches.csv 10 > gpurun_out/ev_launches_summary.txt 2>&1
+for f in gpurun_out/ev_prof_*.ncu-rep; do
+  case "$f" in *k_scan_packed16*) ;; *) rm -f "$f" ;; esac
+done
+rm -f gpurun_out/prof_*.ncu-rep
+du -sh gpurun_out
