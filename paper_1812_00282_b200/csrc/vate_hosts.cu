@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
                                                 uint8_t* __restrict__ member,
                                                 unsigned long long* nout,
                                                 unsigned long long* maxkey,
-                                                unsigned long long* changes, FlipLists F) {
+                                                unsigned long long* changes, FlipLists F,
+                                                Publish pub) {
   __shared__ unsigned s_n, s_flips;
   __shared__ unsigned long long s_max;
   if (threadIdx.x == 0) {
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
     if (s_flips) atomicAdd(changes, (unsigned long long)s_flips);
     if (s_max) atomicMax(maxkey, s_max);
   }
+  publish_last_block(pub);  // every registry counter straight into pinned memory
 }
 
 // Pass 2 (only when membership changed): the member keys, appended in arbitrary
@@ -495,8 +497,8 @@ int hosts_active_launch(vate_hosts* h, int64_t t, int k_prime) {
   VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for((h->cap + 4) / 4, 256, 148u * 8u), 256, 0, k_active,
               h->table.as<const RegEntry>(), h->cap, h->d_count + H_SPECIAL,
               (long long)(t - k_prime), h->member.as<uint8_t>(), h->d_count + H_NOUT,
-              h->d_count + H_MAXKEY, h->d_count + H_CHANGES, F);
-  VATE_CUDA(cudaMemcpyAsync(h->h_count, h->d_count, H_N * 8, cudaMemcpyDeviceToHost, p->stream));
+              h->d_count + H_MAXKEY, h->d_count + H_CHANGES, F,
+              Publish{p->d_done + 1, h->d_count, h->h_count_dev, (1u << H_N) - 1u});
   return VATE_OK;
 }
 
@@ -618,6 +620,7 @@ int vate_hosts_create(vate_hosts** out, vate_pool* p, int k) {
   h->cap = 1 << 12;
   cudaError_t e = cudaMalloc(&h->d_count, H_N * 8);
   if (e == cudaSuccess) e = cudaMallocHost(&h->h_count, H_N * 8);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&h->h_count_dev, h->h_count, 0);
   if (e != cudaSuccess) {
     delete h;
     return cuda_fail(e, "cudaMalloc");

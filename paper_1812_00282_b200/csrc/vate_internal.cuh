@@ -160,6 +160,33 @@ struct ConstRule {
   __device__ __forceinline__ T value(uint64_t) const { return (T)v; }
 };
 
+// Zero-copy publication of a kernel's counters for the slice's host round
+// trip: the last CTA to finish copies n device counters into pinned host
+// memory (mapped; UVA), replacing a small D2H memcpy whose copy-engine latency
+// sat on the round trip.  Called by every thread at the very end of a kernel,
+// after the CTA's atomics on src; done[0] must be 0 at launch and is reset.
+struct Publish {
+  unsigned int* done;
+  const unsigned long long* src;
+  unsigned long long* dst;  // device alias of pinned host memory (nullptr: off)
+  unsigned mask;            // counters i with bit i set are copied
+};
+__device__ __forceinline__ void publish_last_block(const Publish& P) {
+  if (!P.dst) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned ticket = atomicAdd(P.done, 1u);
+    if (ticket == gridDim.x - 1) {
+      __threadfence();
+      for (int i = 0; i < 32; ++i)
+        if ((P.mask >> i) & 1u) P.dst[i] = *((volatile const unsigned long long*)P.src + i);
+      __threadfence_system();
+      *P.done = 0u;
+    }
+  }
+}
+
 // Inactive for width k' (pools.py:187-193): sentinel, or (act + 2k - v) mod 2k
 // >= k'.  For stored values above 2k (only reachable through a hand-made
 // snapshot) the reference's uint64 wraparound is reproduced exactly.
@@ -268,6 +295,8 @@ struct vate_pool {
 
   unsigned long long* d_ctr = nullptr;  // device counters (see enum in .cu)
   unsigned long long* h_ctr = nullptr;  // pinned mirror
+  unsigned long long* h_ctr_dev = nullptr;  // its device alias (zero-copy publication)
+  unsigned int* d_done = nullptr;       // last-block tickets: [0] bitmap, [1] registry
   cudaEvent_t ev_small = nullptr;
   cudaEvent_t marks[16] = {nullptr};
 
@@ -331,6 +360,7 @@ struct vate_hosts {
   vate::DevBuf table, ovf, scratch;
   unsigned long long* d_count = nullptr;  // [0] count, [1] ovf_n, [2] special flag, [3] maxkey, [4] nout
   unsigned long long* h_count = nullptr;  // pinned mirror of d_count
+  unsigned long long* h_count_dev = nullptr;  // its device alias (k_active publishes)
   uint64_t ovf_cap = 0;
   uint64_t pending = 0;    // registry inserts enqueued since the last drain
   uint64_t count_hint = 0; // last count read back

@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
                                                      uint32_t* __restrict__ bitmap,
                                                      uint64_t nwords,
                                                      unsigned long long* pool_inactive,
-                                                     DeltaOut D) {
+                                                     DeltaOut D, Publish pub) {
   constexpr int NV = (int)sizeof(T) * 2;
   constexpr unsigned kDeltaStage = 1024;
   __shared__ unsigned long long s_delta[kDeltaStage];
@@ -638,6 +638,7 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
   }
   const unsigned s = block_sum(local);
   if (threadIdx.x == 0 && s) atomicAdd(pool_inactive, (unsigned long long)s);
+  publish_last_block(pub);  // P (and the delta counts) straight into pinned memory
 }
 
 template <typename T>
@@ -843,6 +844,9 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
                  p->d_ctr + C_DWORK};
   }
   // words per thread per iteration (p->opt_bitmap_kw overrides: 1, 2 or 4)
+  // counters [C_P .. C_DWORK] published by the last CTA (zero-copy)
+  const Publish pub{p->d_done, p->d_ctr, p->h_ctr_dev,
+                    (1u << C_P) | (with_delta ? (1u << C_DCNT) | (1u << C_DWORK) : 0u)};
   int kw = p->opt_bitmap_kw;
   if (kw == 0) kw = 1;  // measured best at c = 24, 26, 28 (scripts/micro_bitmap.py)
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
@@ -850,21 +854,18 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
     const uint32_t grid = grid_for((nwords + kw - 1) / kw, kThreads, 148u * 32u);
     if (kw == 4)
       VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 4>), (const T*)p->cells, p->L,
-                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D);
+                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub);
     else if (kw == 2)
       VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 2>), (const T*)p->cells, p->L,
-                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D);
+                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub);
     else
       VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1>), (const T*)p->cells, p->L,
-                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D);
+                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub);
     return VATE_OK;
   });
   if (rc) return rc;
-  // P (and the delta counts) reach the host with the estimate's one round trip
-  VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_P, p->d_ctr + C_P, 8, cudaMemcpyDeviceToHost, p->stream));
-  if (with_delta)
-    VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_DCNT, p->d_ctr + C_DCNT, 16, cudaMemcpyDeviceToHost,
-                              p->stream));
+  // P (and the delta counts) reach the host with the estimate's one round trip,
+  // written into pinned memory by the kernel's last CTA
   return VATE_OK;
 }
 
@@ -945,6 +946,9 @@ static int pool_create(vate_pool** out, int kind, int c, int k, int partition, i
   if (e == cudaSuccess) e = cudaMalloc(&p->cells, S * (uint64_t)p->cell_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_ctr, C_N * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMallocHost(&p->h_ctr, C_N * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&p->h_ctr_dev, p->h_ctr, 0);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_done, 64);
+  if (e == cudaSuccess) e = cudaMemset(p->d_done, 0, 64);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_small, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_adv, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking);
@@ -1016,6 +1020,7 @@ int vate_pool_destroy(vate_pool* p) {
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->timeline_ref) cudaEventDestroy(p->timeline_ref);
   if (p->h_flag) cudaFreeHost((void*)p->h_flag);
+  if (p->d_done) cudaFree(p->d_done);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   inc_release(p);
   if (p->cells) cudaFree(p->cells);
