@@ -315,7 +315,7 @@ struct vate_pool {
   int opt_g0 = 0;
   int opt_inc = 1;            // incremental g0 through the inverse index
   int opt_scan_check = 0;    // packed scan: load-before-store (heavy hitters)
-  int opt_scan_v = 1;         // packed-scan unroll (uint4 loads per thread per iteration)
+  int opt_scan_v = 1;         // packed scan form: 1 (default), 0, 2, 4 per-thread unroll; 8 TMA-fed persistent
   int opt_l2 = 0;             // L2 persisting window: 0 off, 1 registry, 2 cells
   int opt_bitmap_kw = 0;      // bitmap pass words per thread (0 auto)
   int opt_concurrent = 1;     // fork independent estimate phases onto aux_stream

@@ -371,6 +371,100 @@ __global__ void __launch_bounds__(kThreads) k_scan_packed8(
   if (REG) defer_drain(dq, R, t);
 }
 
+// ---------------------------------------------------------------------------
+// Persistent scan with the packet stream moved by TMA (VATE_OPT_SCAN_V = 8, for
+// 16-byte-aligned input; measured no faster than the default one-uint4-per-
+// thread form on cfg 2/3/4 -- the stream is not what bounds the scan, the
+// random cell stores and registry probes are): each CTA pulls 8 KB tiles (1024
+// packets) into a two-stage shared-memory ring with cp.async.bulk, signalled on
+// an mbarrier, while its threads hash, store and probe the previous tile -- the
+// stream never sits on the per-packet dependency chain.  Tiles are handed out
+// by an atomic counter (balanced tails); each thread takes 4 packets at a time
+// so 4 registry home-sector loads are in flight together.
+// ---------------------------------------------------------------------------
+constexpr int kTmaTile = 1024;                       // packets per tile (8 KB)
+constexpr int kTmaPerThread = kTmaTile / kThreads;   // 4
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+template <typename T, bool CHECK, typename Rule>
+__global__ void __launch_bounds__(kThreads, 4) k_scan_tma(
+    const uint2* __restrict__ pairs, uint64_t ntiles, T* __restrict__ cells, HashParams H,
+    Rule rule, RegRef R, long long t, unsigned* __restrict__ tile_counter) {
+  __shared__ __align__(128) uint2 buf[2][kTmaTile];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ unsigned next_tile[2];
+  __shared__ unsigned filt[CHECK ? kTouchSlots : 1];
+  __shared__ __align__(16) unsigned char dq_raw[sizeof(DeferQ)];
+  DeferQ* dq = reinterpret_cast<DeferQ*>(dq_raw);
+  defer_init(dq);
+  if (CHECK) touch_filter_init(filt);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const unsigned first = atomicAdd(tile_counter, 1u);
+    next_tile[0] = first;
+    if (first < ntiles) {
+      mbar_expect_tx(&bar[0], kTmaTile * 8);
+      bulk_g2s(buf[0], pairs + (uint64_t)first * kTmaTile, kTmaTile * 8, &bar[0]);
+    }
+  }
+  __syncthreads();
+  for (unsigned k = 0;; ++k) {
+    const int s = k & 1;
+    const unsigned tile = next_tile[s];
+    if (tile >= ntiles) break;
+    if (threadIdx.x == 0) {  // claim and prefetch the next tile into the other stage
+      const unsigned nt = atomicAdd(tile_counter, 1u);
+      next_tile[s ^ 1] = nt;
+      if (nt < ntiles) {
+        // the stage was read through the generic proxy before the last barrier
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[s ^ 1], kTmaTile * 8);
+        bulk_g2s(buf[s ^ 1], pairs + (uint64_t)nt * kTmaTile, kTmaTile * 8, &bar[s ^ 1]);
+      }
+    }
+    mbar_wait(&bar[s], (k >> 1) & 1);
+    uint64_t a[kTmaPerThread], b[kTmaPerThread];
+#pragma unroll
+    for (int q = 0; q < kTmaPerThread; ++q) {
+      const uint2 v = buf[s][threadIdx.x + q * kThreads];
+      a[q] = v.x;
+      b[q] = v.y;
+    }
+    scan_batch<T, true, kTmaPerThread, CHECK>(a, b, kTmaPerThread, cells, H, rule, R, t, filt, dq);
+    __syncthreads();  // stage s is read; next_tile[s ^ 1] is visible
+  }
+  defer_drain(dq, R, t);
+}
+
 template <typename T, bool REG, typename Rule = AtRule>
 __global__ void __launch_bounds__(kThreads) k_scan_u64(
     const uint64_t* __restrict__ aips, const uint64_t* __restrict__ bips, uint64_t n,
@@ -1128,7 +1222,8 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_scan_check = (int)value;
     return VATE_OK;
   }
-  if (option == VATE_OPT_SCAN_V && (value == 0 || value == 1 || value == 2 || value == 4)) {
+  if (option == VATE_OPT_SCAN_V &&
+      (value == 0 || value == 1 || value == 2 || value == 4 || value == 8)) {
     p->opt_scan_v = (int)value;
     return VATE_OK;
   }
@@ -1296,7 +1391,25 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     return with_store(p, [&](auto tag, auto rule) -> int {
       using T = decltype(tag);
       using Rl = decltype(rule);
-      if (aligned16 && n >= 2 && p->opt_scan_v > 0) {
+      if (aligned16 && hosts && p->opt_scan_v == 8 && n >= (uint64_t)kTmaTile) {
+        // TMA-fed persistent scan over the full tiles; the remainder below
+        const uint64_t ntiles = n / kTmaTile, rest = n - ntiles * kTmaTile;
+        VATE_CUDA(cudaMemsetAsync(p->d_done + 2, 0, 4, p->stream));
+        const uint32_t gt = (uint32_t)umin64(ntiles, 148u * 4u);
+        if (p->opt_scan_check)
+          VATE_LAUNCH(p, VATE_K_SCAN, gt, kThreads, 0, (k_scan_tma<T, true, Rl>),
+                      (const uint2*)d_pairs, ntiles, (T*)p->cells, H, rule, R, (long long)t,
+                      p->d_done + 2);
+        else
+          VATE_LAUNCH(p, VATE_K_SCAN, gt, kThreads, 0, (k_scan_tma<T, false, Rl>),
+                      (const uint2*)d_pairs, ntiles, (T*)p->cells, H, rule, R, (long long)t,
+                      p->d_done + 2);
+        if (rest)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid_for(rest, kThreads, 148u * 64u), kThreads, 0,
+                      (k_scan_packed8<T, true, false, Rl>),
+                      (const uint2*)d_pairs + ntiles * kTmaTile, rest, (T*)p->cells, H, rule, R,
+                      (long long)t);
+      } else if (aligned16 && n >= 2 && p->opt_scan_v > 0 && p->opt_scan_v <= 4) {
         if (hosts && p->opt_scan_v == 1 && p->opt_scan_check)
           VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, true, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,

@@ -41,7 +41,7 @@ def run(hosts, t0):
                                        bufs[t].data_ptr(), n, 1, hosts, T[0]))
             pool.advance_slice()
     ms, kk = pool.kernel_time("scan")
-    return ms / kk
+    return ms / (3 * NB)   # per scan call (a call may launch more than one kernel)
 
 
 tag = f"c={c}{' zipf' if zipf else ''}"
@@ -49,7 +49,7 @@ for l2 in [int(x) for x in os.environ.get("MICRO_L2", "0").split(",")]:
     pool.set_option("l2_persist", l2)
     for chk in (0, 1):
         pool.set_option("scan_check", chk)
-        for v in (1, 0):
+        for v in (1, 8):
             pool.set_option("scan_v", v)
             ms = run(pipe.hosts.handle, 100)
             print(f"{tag} l2={l2} check={chk} V={v} scan+registry ms/launch {ms:.4f}  "
