@@ -658,7 +658,7 @@ __device__ __forceinline__ uint32_t word_inactive_bits(const T* __restrict__ cel
 
 // kW words per thread per iteration: all their 16-byte loads are issued before
 // any predicate, for memory-level parallelism.
-template <typename T, int kW>
+template <typename T, int kW, bool STREAM = true>
 __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells, Layout L,
                                                      uint32_t bact0, uint32_t kp,
                                                      uint32_t* __restrict__ bitmap,
@@ -685,7 +685,12 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
       const uint64_t w = w0 + q * stride;
       if (w < nwords && (w + 1) * 32 <= L.size) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) r[q][v] = __ldcs(reinterpret_cast<const uint4*>(cells + w * 32) + v);
+        for (int v = 0; v < NV; ++v) {
+          const uint4* src = reinterpret_cast<const uint4*>(cells + w * 32) + v;
+          // an L2-resident pool must stay resident for the next scan: normal
+          // priority; a pool beyond L2 is streamed evict-first
+          r[q][v] = STREAM ? __ldcs(src) : __ldcg(src);
+        }
       }
     }
 #pragma unroll
@@ -946,15 +951,21 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
     const uint32_t grid = grid_for((nwords + kw - 1) / kw, kThreads, 148u * 32u);
+    const bool stream = p->L.size * (uint64_t)p->cell_bytes > (64ull << 20);
     if (kw == 4)
       VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 4>), (const T*)p->cells, p->L,
                   p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub);
     else if (kw == 2)
       VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 2>), (const T*)p->cells, p->L,
                   p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub);
+    else if (stream)
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1, true>), (const T*)p->cells,
+                  p->L, p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords,
+                  p->d_ctr + C_P, D, pub);
     else
-      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1>), (const T*)p->cells, p->L,
-                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub);
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1, false>), (const T*)p->cells,
+                  p->L, p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords,
+                  p->d_ctr + C_P, D, pub);
     return VATE_OK;
   });
   if (rc) return rc;

@@ -952,3 +952,36 @@ def test_active_set_merge_under_small_churn(inc_sort):
         assert st["incremental"] > 10, st
     else:
         assert st["incremental"] == 0, st
+
+
+@pytest.mark.parametrize("form", [(1, 0), (1, 1), (0, 0), (0, 1), (2, 0), (4, 0), (8, 0), (8, 1)])
+def test_scan_forms_are_equivalent(form):
+    """Every packed-scan form (VATE_OPT_SCAN_V: 0 one packet per thread, 1/2/4
+    uint4 per thread, 8 TMA-fed persistent; VATE_OPT_SCAN_CHECK heavy-hitter
+    form) leaves the reference's cells and host set: ATP1 bytes, reports and
+    the registry after skewed traffic (a heavy host, odd packet counts, tiles
+    plus remainders) equal the oracle's, slice by slice."""
+    import torch
+    v, chk = form
+    cfg = vb.EstimatorConfig(256, 16, 6, seed=5)
+    ocfg = vo.OracleConfig(256, 16, 6, seed=5)
+    pool = cfg.build_pool()
+    pool.set_option("scan_v", v)
+    pool.set_option("scan_check", chk)
+    pipe = vb.Pipeline(pool, cfg, 5)
+    opipe = vo.OraclePipeline(ocfg, 5)
+    rng = np.random.default_rng(31)
+    for t in range(10):
+        n = int(rng.integers(1, 9000)) | 1 if t % 3 else 4096 + 3
+        a = (0x0A000000 + rng.integers(0, 900, n)).astype(np.uint32)
+        a[rng.random(n) < 0.3] = 0x0A0000FF                      # a heavy hitter
+        b = rng.integers(1, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+        pairs = torch.from_numpy(np.ascontiguousarray(np.stack([a, b], axis=1)).view(np.int32)).cuda()
+        got = pipe.step_fast(t, pairs.data_ptr(), n, "device",
+                             (np.empty(2048, np.uint64), np.empty(2048), np.empty(2048),
+                              np.empty(2048, np.uint8)))
+        pipe.wait_reports()
+        want = opipe.process_slice(t, a.astype(np.uint64), b.astype(np.uint64))
+        assert np.array_equal(got.host, want.reports.host), (form, t)
+        assert np.array_equal(got.estimate, want.reports.estimate), (form, t)
+        assert pool.snapshot_bytes() == opipe.pool.snapshot_bytes(), (form, t)
