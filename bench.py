@@ -337,6 +337,21 @@ def run_gpu(args, rank, world, local_rank):
     elif world > 1:                               # NCCL all-gathers + merge kernel
         replica = ReplicaStep(pipe, dist, torch)
     run_slice = replica if replica is not None else pipe.step_fast
+    lagged = bool(args.lagged) and replica is None
+
+    def _lagged_rows(res):
+        return None if res is None else res[1]
+
+    if lagged:   # software-pipelined step: slice t-1 completes beside slice t's scan
+        def run_slice(t_, src_, n_, where_, out_):
+            return _lagged_rows(pipe.step_lagged(t_, src_, n_, where_, out_))
+
+    def flush(out=None):
+        """Complete the pending slice of a lagged run (no-op otherwise)."""
+        if lagged:
+            rep = _lagged_rows(pipe.flush_lagged(out))
+            return 0 if rep is None else (rep if out is None else len(rep))
+        return 0
 
     def step(t, src, on_device):
         """One slice; report rows stay in HBM (e2e moves them); returns the row count."""
@@ -358,6 +373,8 @@ def run_gpu(args, rank, world, local_rank):
         step(t, dslices[di].data_ptr(), True)
         t += 1
         di += 1
+
+    flush()
 
     def barrier():
         pipe.wait_reports()
@@ -381,6 +398,7 @@ def run_gpu(args, rank, world, local_rank):
             rows += step(t, dslices[di].data_ptr(), True)
             t += 1
             di += 1
+        rows += flush()                  # the last slice's reports are part of the work
         check(lib.vate_mark(h, 1))
         barrier()
         if profile_region:
@@ -397,6 +415,7 @@ def run_gpu(args, rank, world, local_rank):
             step(t, dslices[di].data_ptr(), True)
             t += 1
             di += 1
+        flush()
         barrier()
         kt = {kind: pool.kernel_time(kind) for kind in _lib.KERNEL_KINDS}
         pool.set_timing(False)
@@ -409,6 +428,7 @@ def run_gpu(args, rank, world, local_rank):
             staged[(i + 1) % 2] = pipe.stage_packed(hslices[i + 1].data_ptr(), n)
             step_host(t, i)
             t += 1
+        flush(out_sets[t % 2])
         barrier()
         e0 = time.perf_counter()
         e2e_rows = 0
@@ -422,6 +442,7 @@ def run_gpu(args, rank, world, local_rank):
             host_ms["stage"] += (b - a) * 1e3
             host_ms["step"] += (time.perf_counter() - b) * 1e3
             t += 1
+        e2e_rows += flush(out_sets[t % 2])
         barrier()
         e2e_s = time.perf_counter() - e0
 
@@ -511,6 +532,7 @@ def run_gpu(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(e2e_rows / args.steps * 25),
                 "host_ms_per_step": {k: v / args.steps for k, v in host_ms.items()}},
         "gpu_launches": int(launches),
+        "slice_step": "lagged (Pipeline.step_lagged)" if lagged else "Pipeline.step_fast",
         "active_set_ordering": pool.sort_stats(),
         "scan_speed_of_light": dict(sol, scan_ms_per_launch=per_kind["scan"]["ms_per_launch"],
                                     scan_over_sol=per_kind["scan"]["ms_per_launch"]
@@ -567,6 +589,9 @@ def main():
                     help="L2 persisting window: 1 host registry, 2 cells (VATE_OPT_L2_PERSIST)")
     ap.add_argument("--opt", action="append", default=[],
                     help="extra pool option name=value (AtPool.set_option), for A/B runs")
+    ap.add_argument("--lagged", type=int, choices=(0, 1), default=1,
+                    help="software-pipelined slice step (Pipeline.step_lagged): slice t's "
+                         "reports complete beside slice t+1's scan")
     ap.add_argument("--concurrent", type=int, choices=(0, 1), default=1,
                     help="registry compaction beside the bitmap pass, advance beside g0 + float "
                          "path, on a second stream (VATE_OPT_CONCURRENT)")

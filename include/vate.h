@@ -249,12 +249,46 @@ typedef struct vate_step_result {
   int32_t prev_collected;
   int32_t prev_blocks[2];
   uint64_t prev_maintained, prev_cleared;
+  int64_t prev_t;      /* lagged step: the slice these results belong to */
+  int32_t prev_valid;  /* lagged step: 1 if a slice was completed by this call */
 } vate_step_result;
 int vate_slice_step(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
                     uint64_t group_stream, const uint32_t* pairs, uint64_t n, int where,
                     int64_t t, int k_prime, double floor, const double* log_zp_table,
                     uint64_t* out_host, double* out_est, double* out_zv, uint8_t* out_sat,
                     uint64_t cap, vate_step_result* res);
+
+/* Software-pipelined form of vate_slice_step: enqueues slice t's scan, then
+ * completes the PREVIOUS slice (reports into the out arrays, its counts and
+ * maintenance in res, res->prev_t / prev_valid say which slice; its g0 lookups,
+ * float path and copies run on a second stream beside slice t's scan), then
+ * enqueues slice t's bitmap pass, registry compaction, delta apply and sweep.
+ * Results are those of vate_slice_step, one call later; vate_slice_flush
+ * completes the last slice.  Use one or the other per pool, not both. */
+int vate_slice_step_lagged(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                           uint64_t group_stream, const uint32_t* pairs, uint64_t n, int where,
+                           int64_t t, int k_prime, double floor, const double* log_zp_table,
+                           uint64_t* out_host, double* out_est, double* out_zv,
+                           uint8_t* out_sat, uint64_t cap, vate_step_result* res);
+int vate_slice_flush(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                     double floor, const double* log_zp_table, uint64_t* out_host,
+                     double* out_est, double* out_zv, uint8_t* out_sat, uint64_t cap,
+                     vate_step_result* res);
+/* The same in two halves, for pools too large for a log table: begin enqueues
+ * slice t's scan and completes the previous slice up to g0 (res->nhosts,
+ * res->pool_inactive); the caller takes log_zp = np.log of the clamped pool
+ * fraction (estimator.py:148-151) and end runs the previous slice's float path
+ * and enqueues slice t's estimate front and sweep.  flush_begin + end (with any
+ * group_stream) complete the last slice. */
+int vate_slice_lagged_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                            uint64_t group_stream, const uint32_t* pairs, uint64_t n, int where,
+                            int64_t t, int k_prime, vate_step_result* res);
+int vate_slice_lagged_end(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                          uint64_t group_stream, double floor, double log_zp, uint64_t* out_host,
+                          double* out_est, double* out_zv, uint8_t* out_sat, uint64_t cap,
+                          vate_step_result* res);
+int vate_slice_lagged_flush_begin(vate_pool* p, vate_hosts* hosts, uint64_t g,
+                                  uint64_t cell_stream, vate_step_result* res);
 
 /* ---- snapshots: AtPool.snapshot_bytes / load (pools.py:261-298) -------- */
 int vate_snapshot_size(const vate_pool* p, uint64_t* nbytes);

@@ -31,7 +31,8 @@ class StepResult(C.Structure):
     """vate_step_result (include/vate.h)."""
     _fields_ = [("nhosts", C.c_uint64), ("nkept", C.c_uint64), ("pool_inactive", C.c_uint64),
                 ("prev_collected", C.c_int32), ("prev_blocks", C.c_int32 * 2),
-                ("prev_maintained", C.c_uint64), ("prev_cleared", C.c_uint64)]
+                ("prev_maintained", C.c_uint64), ("prev_cleared", C.c_uint64),
+                ("prev_t", C.c_int64), ("prev_valid", C.c_int32)]
 
 
 _p = C.c_void_p
@@ -90,6 +91,13 @@ _SIGS = {
     "vate_reports_device": ([_p, _p, _p, _p, _p], _int),
     "vate_slice_step": ([_p, _p, _u64, _u64, _u64, _p, _u64, _int, _i64, _int, _dbl, _p,
                          _p, _p, _p, _p, _u64, C.POINTER(StepResult)], _int),
+    "vate_slice_step_lagged": ([_p, _p, _u64, _u64, _u64, _p, _u64, _int, _i64, _int, _dbl, _p,
+                                _p, _p, _p, _p, _u64, _p], _int),
+    "vate_slice_flush": ([_p, _p, _u64, _u64, _dbl, _p, _p, _p, _p, _p, _u64, _p], _int),
+    "vate_slice_lagged_begin": ([_p, _p, _u64, _u64, _u64, _p, _u64, _int, _i64, _int, _p], _int),
+    "vate_slice_lagged_end": ([_p, _p, _u64, _u64, _u64, _dbl, _dbl, _p, _p, _p, _p, _u64, _p],
+                              _int),
+    "vate_slice_lagged_flush_begin": ([_p, _p, _u64, _u64, _p], _int),
     "vate_snapshot_size": ([_p, _pu64], _int),
     "vate_snapshot": ([_p, _p, _u64, _pu64], _int),
     "vate_load": ([_p, _p, _u64], _int),

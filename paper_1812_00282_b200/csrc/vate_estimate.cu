@@ -800,6 +800,198 @@ int vate_slice_step(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_s
   return rc;
 }
 
+// ---- lagged (software-pipelined) slice step ----------------------------------
+// The step for slice t enqueues slice t's scan first, then completes the
+// PREVIOUS slice (its round trip has long landed; its g0 lookups, float path
+// and report copies run on the aux stream beside this scan), then enqueues
+// slice t's bitmap pass, registry compaction, early delta apply and sweep.  The
+// GPU goes from one slice's sweep straight into the next slice's scan; the
+// results of slice t arrive with the call for slice t+1 (or the flush).
+// Two halves around the previous slice's P (the float path needs np.log of the
+// pool fraction, taken on the host when no table is given): begin (scan t,
+// previous slice up to g0) and end (previous slice's float path, prune; slice
+// t up to its sweep).  Falls back to completing the previous slice before the
+// scan when the registry's parked-insert list could fill (a drain must not
+// rehash the table under a running scan).
+static int lagged_begin_prev(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                             vate_step_result* res) {
+  if (!p->lag_pending) return VATE_OK;
+  p->lag_pending = false;
+  p->lag_completing = true;
+  const int64_t t = p->lag_t;
+  const int kp = p->lag_kp;
+  res->prev_t = t;
+  res->prev_valid = 1;
+  VATE_CUDA(cudaEventSynchronize(p->ev_counts));  // its bitmap + compaction counters landed
+  if (p->adv_pending) {  // its sweep (right behind its bitmap pass)
+    res->prev_collected = 1;
+    int rc = vate_advance_result(p, res->prev_blocks, &res->prev_maintained, &res->prev_cleared);
+    if (rc) return rc;
+  }
+  // post-round-trip work of slice t on the aux stream, beside the next scan
+  std::swap(p->stream, p->aux_stream);
+  hosts->lagged = true;
+  uint64_t nh = 0, pin = 0;
+  int rc = begin_complete(p, hosts, g, cell_stream, t, kp, &nh, &pin);
+  hosts->lagged = false;
+  std::swap(p->stream, p->aux_stream);
+  res->nhosts = nh;
+  res->pool_inactive = pin;
+  return rc;
+}
+
+static int lagged_end_prev(vate_pool* p, vate_hosts* hosts, uint64_t g, double floor,
+                           double log_zp, uint64_t* out_host, double* out_est, double* out_zv,
+                           uint8_t* out_sat, uint64_t cap, vate_step_result* res) {
+  if (!p->lag_completing) return VATE_OK;
+  p->lag_completing = false;
+  const int64_t t = p->lag_t;
+  std::swap(p->stream, p->aux_stream);
+  int rc = VATE_OK;
+  if (res->nhosts) {
+    uint64_t kept = 0;
+    rc = vate_estimate_finish_async(p, g, res->pool_inactive, log_zp, floor, out_host, out_est,
+                                    out_zv, out_sat, cap, &kept);
+    res->nkept = kept;
+  }
+  // everything above (g0 delta / lookups read the delta list and bitmap buffers
+  // the next bitmap pass rewrites) must finish before slice t+1's bitmap pass
+  if (rc == VATE_OK) {
+    const cudaError_t e = cudaEventRecord(p->ev_post, p->stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaEventRecord (post)");
+    else p->post_recorded = true;
+  }
+  std::swap(p->stream, p->aux_stream);
+  // SlidingHostSet.prune (pipeline.py:59-64, at t % k == 0) after slice t's
+  // reports: the next slice's scan may have stamped hosts already, which the
+  // prune keeps (last > t - k), exactly as if it had run first.  The post work
+  // above reads registry slots the prune's rebuild moves: wait for it first.
+  if (rc == VATE_OK && t % (int64_t)(hosts->k > 0 ? hosts->k : 1) == 0) {
+    const cudaError_t e = cudaStreamSynchronize(p->aux_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize (prune)");
+    rc = vate_hosts_prune(hosts, t);
+  }
+  return rc;
+}
+
+int vate_slice_lagged_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                            uint64_t group_stream, const uint32_t* pairs, uint64_t n, int where,
+                            int64_t t, int k_prime, vate_step_result* res) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (!res || !hosts) return set_error(VATE_EVALUE, "null argument");
+  if (p->lag_completing) return set_error(VATE_EVALUE, "lagged step: end of the previous call missing");
+  memset(res, 0, sizeof(*res));
+  rc = check_width(p, k_prime);
+  if (rc) return rc;
+  if (!p->ev_counts) VATE_CUDA(cudaEventCreateWithFlags(&p->ev_counts, cudaEventDisableTiming));
+  if (!p->ev_post) VATE_CUDA(cudaEventCreateWithFlags(&p->ev_post, cudaEventDisableTiming));
+  p->lag_next_t = t;
+  p->lag_next_kp = k_prime;
+  p->lag_has_next = true;
+  // a scan that might have to drain the registry waits for the previous slice
+  p->lag_deferred_scan = hosts->pending + n > hosts->ovf_cap;
+  if (p->lag_deferred_scan) {
+    p->lag_scan_pairs = pairs;
+    p->lag_scan_n = n;
+    p->lag_scan_where = where;
+    return lagged_begin_prev(p, hosts, g, cell_stream, res);  // scan after the end
+  }
+  if (where == VATE_STAGED) {
+    rc = vate_scan_staged(p, g, cell_stream, group_stream, (int)(uintptr_t)pairs, n, hosts, t);
+  } else if (n) {
+    rc = vate_scan_packed(p, g, cell_stream, group_stream, pairs, n, where, hosts, t);
+  }
+  if (rc) return rc;
+  return lagged_begin_prev(p, hosts, g, cell_stream, res);
+}
+
+int vate_slice_lagged_end(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                          uint64_t group_stream, double floor, double log_zp, uint64_t* out_host,
+                          double* out_est, double* out_zv, uint8_t* out_sat, uint64_t cap,
+                          vate_step_result* res) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (!res || !hosts) return set_error(VATE_EVALUE, "null argument");
+  rc = lagged_end_prev(p, hosts, g, floor, log_zp, out_host, out_est, out_zv, out_sat, cap, res);
+  if (rc) return rc;
+  if (!p->lag_has_next) {  // a flush: nothing follows
+    VATE_CUDA(cudaStreamSynchronize(p->aux_stream));
+    return VATE_OK;
+  }
+  p->lag_has_next = false;
+  const int64_t t = p->lag_next_t;
+  const int k_prime = p->lag_next_kp;
+  if (p->lag_deferred_scan) {  // the previous slice is complete: drain, grow, scan
+    p->lag_deferred_scan = false;
+    VATE_CUDA(cudaStreamSynchronize(p->aux_stream));
+    rc = hosts_drain(hosts);
+    if (rc) return rc;
+    rc = hosts->ovf.ensure(2 * (p->lag_scan_n + 1) * sizeof(RegEntry));  // two slices' parks
+    if (rc) return rc;
+    hosts->ovf_cap = hosts->ovf.bytes / sizeof(RegEntry);
+    if (p->lag_scan_where == VATE_STAGED) {
+      rc = vate_scan_staged(p, g, cell_stream, group_stream, (int)(uintptr_t)p->lag_scan_pairs,
+                            p->lag_scan_n, hosts, t);
+    } else if (p->lag_scan_n) {
+      rc = vate_scan_packed(p, g, cell_stream, group_stream, p->lag_scan_pairs, p->lag_scan_n,
+                            p->lag_scan_where, hosts, t);
+    }
+    if (rc) return rc;
+  }
+  // slice t up to its counters; then its sweep (it reads no g0, only cells already counted)
+  if (p->post_recorded) {
+    VATE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_post, 0));
+    p->post_recorded = false;
+  }
+  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime);
+  if (rc) return rc;
+  VATE_CUDA(cudaEventRecord(p->ev_counts, p->stream));
+  rc = vate_advance_async(p);
+  if (rc) return rc;
+  p->lag_pending = true;
+  p->lag_t = t;
+  p->lag_kp = k_prime;
+  return VATE_OK;
+}
+
+int vate_slice_lagged_flush_begin(vate_pool* p, vate_hosts* hosts, uint64_t g,
+                                  uint64_t cell_stream, vate_step_result* res) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (!res || !hosts) return set_error(VATE_EVALUE, "null argument");
+  memset(res, 0, sizeof(*res));
+  p->lag_has_next = false;
+  p->lag_deferred_scan = false;
+  return lagged_begin_prev(p, hosts, g, cell_stream, res);
+}
+
+int vate_slice_step_lagged(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                           uint64_t group_stream, const uint32_t* pairs, uint64_t n, int where,
+                           int64_t t, int k_prime, double floor, const double* log_zp_table,
+                           uint64_t* out_host, double* out_est, double* out_zv,
+                           uint8_t* out_sat, uint64_t cap, vate_step_result* res) {
+  if (!log_zp_table) return set_error(VATE_EVALUE, "null log table");
+  int rc = vate_slice_lagged_begin(p, hosts, g, cell_stream, group_stream, pairs, n, where, t,
+                                   k_prime, res);
+  if (rc) return rc;
+  return vate_slice_lagged_end(p, hosts, g, cell_stream, group_stream, floor,
+                               log_zp_table[res->pool_inactive], out_host, out_est, out_zv,
+                               out_sat, cap, res);
+}
+
+int vate_slice_flush(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
+                     double floor, const double* log_zp_table, uint64_t* out_host,
+                     double* out_est, double* out_zv, uint8_t* out_sat, uint64_t cap,
+                     vate_step_result* res) {
+  if (!log_zp_table) return set_error(VATE_EVALUE, "null log table");
+  int rc = vate_slice_lagged_flush_begin(p, hosts, g, cell_stream, res);
+  if (rc) return rc;
+  return vate_slice_lagged_end(p, hosts, g, cell_stream, 0, floor,
+                               log_zp_table[res->pool_inactive], out_host, out_est, out_zv,
+                               out_sat, cap, res);
+}
+
 int vate_reports_device(vate_pool* p, uint64_t** host, double** est, double** zv,
                         uint8_t** sat) {
   if (!p) return set_error(VATE_EVALUE, "null pool handle");

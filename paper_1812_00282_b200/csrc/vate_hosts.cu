@@ -8,6 +8,7 @@
 // overflow list and re-inserted at the next drain, which every read of the
 // registry performs first, so no update is ever lost.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 
 #include <string>
 #include <utility>
@@ -506,9 +507,70 @@ const unsigned long long* hosts_nactive_dev(const vate_hosts* h) { return h->d_c
 uint64_t hosts_nactive_host(const vate_hosts* h) { return h->h_count[H_NOUT]; }
 
 // After the caller's sync: handle parked inserts, then sort the active keys.
+// Lagged slice step (vate_slice_step_lagged): the next slice's scan may already
+// be running, so the table must not be rehashed and membership cannot be
+// recomputed.  Inserts parked by this slice's scans are the first novf entries
+// of the overflow list (the compaction's counter snapshot) and all were seen in
+// this slice: the active set is the compaction's members plus those keys,
+// sorted and deduplicated.  The table grows at the next compaction launch.
+__global__ void k_ovf_keys(const RegEntry* __restrict__ ovf, uint64_t n,
+                           unsigned long long* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = ovf[i].key;
+}
+
+static int active_with_parked(vate_hosts* h, uint64_t novf, uint64_t** keys_dev, uint64_t* n) {
+  vate_pool* p = h->pool;
+  const uint64_t members = h->h_count[H_NOUT];
+  int rc = p->hosts_tmp.ensure((members + novf + 2) * 8);
+  if (rc) return rc;
+  rc = p->hosts_sorted.ensure((members + novf + 2) * 8);
+  if (rc) return rc;
+  if (members)
+    VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(h->cap + 1, kActTile, 148u * 8u), 256, 0,
+                k_active_keys, h->table.as<const RegEntry>(), h->cap,
+                h->member.as<const uint8_t>(), p->hosts_tmp.as<uint64_t>(),
+                h->d_count + H_NOUT2);
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for(novf, kThreads, 148u * 8u), kThreads, 0, k_ovf_keys,
+              h->ovf.as<const RegEntry>(), novf, p->hosts_tmp.as<unsigned long long>() + members);
+  const uint64_t total = members + novf;
+  rc = sort_keys(p, p->hosts_tmp.as<uint64_t>(), p->hosts_sorted.as<uint64_t>(), total, 64);
+  if (rc) return rc;
+  size_t bytes = 0;
+  VATE_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, p->hosts_sorted.as<unsigned long long>(),
+                                      p->hosts_tmp.as<unsigned long long>(),
+                                      h->d_count + H_NOUT2, (int64_t)total, p->stream));
+  rc = p->cub_tmp.ensure(bytes + 256);
+  if (rc) return rc;
+  VATE_CUDA(cub::DeviceSelect::Unique(p->cub_tmp.ptr, bytes,
+                                      p->hosts_sorted.as<unsigned long long>(),
+                                      p->hosts_tmp.as<unsigned long long>(),
+                                      h->d_count + H_NOUT2, (int64_t)total, p->stream));
+  p->launches += 2;
+  unsigned long long uniq = 0;
+  VATE_CUDA(cudaMemcpyAsync(&uniq, h->d_count + H_NOUT2, 8, cudaMemcpyDeviceToHost, p->stream));
+  VATE_CUDA(cudaStreamSynchronize(p->stream));
+  std::swap(p->hosts_sorted.ptr, p->hosts_tmp.ptr);
+  std::swap(p->hosts_sorted.bytes, p->hosts_tmp.bytes);
+  *keys_dev = p->hosts_sorted.as<uint64_t>();
+  *n = uniq;
+  h->member_valid = false;  // the list is not member[]'s set: the next compaction sorts
+  h->needs_grow = true;     // drain (grow + re-insert) before the next compaction
+  p->sorted_owner = h;
+  p->sorted_n = uniq;
+  p->sorted_version++;
+  p->sorts_full++;
+  return VATE_OK;
+}
+
 int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_dev, uint64_t* n) {
   vate_pool* p = h->pool;
   int rc;
+  if (h->h_count[H_OVF] && h->lagged) {
+    h->count_hint = h->h_count[H_COUNT];
+    return active_with_parked(h, h->h_count[H_OVF], keys_dev, n);
+  }
   if (h->h_count[H_OVF]) {  // inserts hit the probe limit: grow, re-insert, recompute
     rc = hosts_drain(h);
     if (rc) return rc;

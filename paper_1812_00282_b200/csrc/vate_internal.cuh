@@ -321,6 +321,21 @@ struct vate_pool {
   int opt_concurrent = 1;     // fork independent estimate phases onto aux_stream
   cudaStream_t aux_stream = nullptr;   // second compute stream (fork/join with events)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // lagged slice step: the slice whose results the next call completes
+  bool lag_pending = false;      // a slice awaits completion (lag_t, lag_kp)
+  bool lag_completing = false;   // begin ran for it; end must follow
+  int64_t lag_t = 0;
+  int lag_kp = 0;
+  bool lag_has_next = false;     // the slice begin announced (lag_next_*)
+  int64_t lag_next_t = 0;
+  int lag_next_kp = 0;
+  bool lag_deferred_scan = false;  // its scan waits for the previous slice's end
+  const uint32_t* lag_scan_pairs = nullptr;
+  uint64_t lag_scan_n = 0;
+  int lag_scan_where = 0;
+  cudaEvent_t ev_counts = nullptr;
+  cudaEvent_t ev_post = nullptr;       // the completed slice's post-round-trip work
+  bool post_recorded = false;
   void* l2_base = nullptr;    // window currently set on the stream
   size_t l2_bytes = 0;
   const void* sorted_owner = nullptr;  // registry whose active set hosts_sorted holds
@@ -365,6 +380,7 @@ struct vate_hosts {
   uint64_t pending = 0;    // registry inserts enqueued since the last drain
   uint64_t count_hint = 0; // last count read back
   bool needs_grow = false; // load factor passed 1/2: grow at the next drain point
+  bool lagged = false;     // completing a slice while the next one's scan may run
   vate::DevBuf member;     // u8 per slot: in the active set of the last compaction
   bool member_valid = false;
   vate::DevBuf flips;      // arrivals, departures and their sorted copies (4 x flip_cap)

@@ -1123,6 +1123,8 @@ int vate_pool_destroy(vate_pool* p) {
   if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
   if (p->aux_stream) cudaStreamDestroy(p->aux_stream);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_counts) cudaEventDestroy(p->ev_counts);
+  if (p->ev_post) cudaEventDestroy(p->ev_post);
   if (p->timeline_ref) cudaEventDestroy(p->timeline_ref);
   if (p->h_flag) cudaFreeHost((void*)p->h_flag);
   if (p->d_done) cudaFree(p->d_done);

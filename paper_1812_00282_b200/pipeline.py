@@ -205,10 +205,10 @@ class Pipeline:
         rep = MaintenanceReport(maintenance_blocks(blocks[0], blocks[1]), maint.value, cleared.value)
         return self._account(t, rep)
 
-    def _account(self, t: int, rep: MaintenanceReport) -> MaintenanceReport:
+    def _account(self, t: int, rep: MaintenanceReport, prune: bool = True) -> MaintenanceReport:
         self.total_maintained += rep.cells_maintained
         self.total_cleared += rep.cells_cleared
-        if t % max(1, self.pool.k) == 0:
+        if prune and t % max(1, self.pool.k) == 0:   # (the lagged step prunes in the library)
             self.hosts.prune(t)
         self.last_maintenance = rep
         return rep
@@ -294,6 +294,68 @@ class Pipeline:
         return HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool),
                            res.pool_inactive / float(self.pool.size), t - self.k_prime + 1,
                            self.k_prime)
+
+    def step_lagged(self, t: int, pairs: int, n: int, where: str, out):
+        # (pools too large for the log table take two library calls per slice)
+        """Software-pipelined step_fast (vate_slice_step_lagged): enqueue slice t
+        and complete the previous slice, whose rows this returns as
+        ``(t_prev, rows)`` -- ``rows`` as step_fast returns them -- or None on the
+        first call.  The previous slice's g0 lookups and float path run beside
+        slice t's scan, so the GPU never waits on the host round trip.  ``out``
+        receives the previous slice's rows; call ``flush_lagged`` after the last
+        slice.  Results are identical to step_fast's, one call later."""
+        return self._lagged(None, out, t, pairs, n, where)
+
+    def flush_lagged(self, out):
+        """Complete the last slice of a step_lagged run: ``(t, rows)`` or None."""
+        return self._lagged(None, out)
+
+    def _lagged(self, fn, out, t=None, pairs=0, n=0, where="device"):
+        tab = getattr(self, "_lzp_tab", None)
+        if tab is None:
+            tab = self._lzp_tab = log_zp_table(self.pool.c)
+        host, est, zv, sat = out if out is not None else (None, None, None, None)
+        res = _lib.StepResult()
+        outs = (*(ptr(a) if a is not None else None for a in (host, est, zv, sat)),
+                len(host) if host is not None else 0, C.byref(res))
+        h, hs, cfg = self.pool.handle, self.hosts.handle, self.cfg
+        where_code = {"host": VATE_HOST, "device": VATE_DEVICE, "staged": _lib.VATE_STAGED}[where]
+        if tab is not None:      # one call; np.log of P from the table
+            if t is None:
+                check(lib.vate_slice_flush(h, hs, cfg.g, cfg.cell_stream, float(self.floor),
+                                           ptr(tab), *outs))
+            else:
+                check(lib.vate_slice_step_lagged(h, hs, cfg.g, cfg.cell_stream, cfg.group_stream,
+                                                 int(pairs), int(n), where_code, t, self.k_prime,
+                                                 float(self.floor), ptr(tab), *outs))
+        else:                    # two halves around np.log of the previous slice's P
+            if t is None:
+                check(lib.vate_slice_lagged_flush_begin(h, hs, cfg.g, cfg.cell_stream,
+                                                        C.byref(res)))
+            else:
+                check(lib.vate_slice_lagged_begin(h, hs, cfg.g, cfg.cell_stream, cfg.group_stream,
+                                                  int(pairs), int(n), where_code, t,
+                                                  self.k_prime, C.byref(res)))
+            lzp = log_zp(res.pool_inactive, self.pool.size)[0] if res.nhosts else 0.0
+            check(lib.vate_slice_lagged_end(h, hs, cfg.g, cfg.cell_stream, cfg.group_stream,
+                                            float(self.floor), lzp, *outs))
+        if not res.prev_valid:
+            return None
+        tp = res.prev_t
+        if res.prev_collected:
+            self._account(tp, MaintenanceReport(
+                maintenance_blocks(res.prev_blocks[0], res.prev_blocks[1]), res.prev_maintained,
+                res.prev_cleared), prune=False)
+        self.last_active = res.nhosts
+        if res.nhosts == 0:
+            return tp, None
+        self.last_pool_inactive = res.pool_inactive
+        m = res.nkept
+        if out is None:
+            return tp, m
+        return tp, HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool),
+                               res.pool_inactive / float(self.pool.size), tp - self.k_prime + 1,
+                               self.k_prime)
 
     def reports_device(self):
         """(host, estimate, z_v, saturated) device addresses of the last report rows."""

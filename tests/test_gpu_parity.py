@@ -985,3 +985,61 @@ def test_scan_forms_are_equivalent(form):
         assert np.array_equal(got.host, want.reports.host), (form, t)
         assert np.array_equal(got.estimate, want.reports.estimate), (form, t)
         assert pool.snapshot_bytes() == opipe.pool.snapshot_bytes(), (form, t)
+
+
+@pytest.mark.parametrize("floor,hosts0,two_calls", [(0.0, 900, False), (30.0, 900, False),
+                                                   (0.0, 30_000, False), (30.0, 30_000, True)])
+def test_lagged_step_equals_oracle(floor, hosts0, two_calls):
+    """Pipeline.step_lagged (vate_slice_step_lagged): slice t's reports arrive
+    with the call for slice t+1 and equal the oracle's, the ATP1 snapshot after
+    each call equals the oracle's after the same slice (scan + advance), with
+    host churn, an empty slice, prunes (t % k == 0), a floor, and -- with 30k new
+    hosts in the first slices -- registry growth and parked inserts completed
+    while the next scan runs."""
+    import torch
+    cfg = vb.EstimatorConfig(256, 16, 6, seed=12)
+    ocfg = vo.OracleConfig(256, 16, 6, seed=12)
+    pool = cfg.build_pool()
+    pipe = vb.Pipeline(pool, cfg, 5, floor=floor)
+    if two_calls:   # as for pools beyond the log table: np.log of P per slice, two calls
+        pipe._lzp_tab = None
+        import paper_1812_00282_b200.pipeline as pl
+        orig = pl.log_zp_table
+        pl.log_zp_table = lambda c: None
+    opipe = vo.OraclePipeline(ocfg, 5, floor=floor)
+    rng = np.random.default_rng(8)
+    want = {}
+    outs = [tuple(np.empty(40_000, dt) for dt in (np.uint64, np.float64, np.float64, np.uint8))
+            for _ in range(2)]
+
+    def check_rows(res):
+        if res is None:
+            return
+        tp, rows = res
+        w = want.pop(tp)
+        if w.reports is None or len(w.reports.host) == 0:
+            assert rows is None or len(rows.host) == 0, tp
+            return
+        assert np.array_equal(rows.host, w.reports.host), tp
+        assert np.array_equal(rows.estimate, w.reports.estimate), tp
+        assert np.array_equal(rows.z_v, w.reports.z_v), tp
+        assert np.array_equal(rows.saturated, w.reports.saturated), tp
+
+    for t in range(20):
+        n = 0 if t == 7 else int(rng.integers(5_000, 20_000))
+        span = hosts0 if t < 4 else 900
+        lo = 0 if t < 10 else 400
+        a = (0x0A000000 + rng.integers(lo, lo + span, n)).astype(np.uint32)
+        b = rng.integers(1, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+        pairs = torch.from_numpy(np.ascontiguousarray(np.stack([a, b], axis=1)).view(np.int32)).cuda()
+        res = pipe.step_lagged(t, pairs.data_ptr() if n else 0, n, "device", outs[t % 2])
+        pipe.wait_reports()
+        check_rows(res)
+        want[t] = opipe.process_slice(t, a.astype(np.uint64), b.astype(np.uint64))
+        assert pool.snapshot_bytes() == opipe.pool.snapshot_bytes(), t
+    res = pipe.flush_lagged(outs[0])
+    pipe.wait_reports()
+    check_rows(res)
+    assert not want
+    if two_calls:
+        pl.log_zp_table = orig
