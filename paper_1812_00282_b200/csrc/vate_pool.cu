@@ -582,18 +582,32 @@ __device__ __forceinline__ bool active_bits_simd(const uint4 (&r)[(int)sizeof(T)
       bits |= ((((m >> 7) * 0x01020408u) >> 24) & 0xFu) << (4 * q);
     }
   } else if (sizeof(T) == 2 && B < 32768) {
+    // Per 2-cell word: the guard-bit compares, then the two result bits (15, 31)
+    // go to bit q (even cell 2q) and bit 16+q (odd cell 2q+1) of an interleaved
+    // mask, un-interleaved once per 32 cells; the "value > 2k" check is one
+    // lane-wise max per word, tested once.  (The cfg-4 bitmap pass is
+    // issue-bound: this form retires ~35 % fewer instructions per cell.)
     const uint32_t H = 0x80008000u;
     const uint32_t AH = (act * 0x00010001u) | H;
     const uint32_t L2 = (uint32_t)(lo >= 0 ? lo : lo + (int)B) * 0x00010001u;
-    const uint32_t B2 = B * 0x00010001u, Bp1 = (B + 1) * 0x00010001u;
+    const uint32_t B2 = B * 0x00010001u;
+    uint32_t mx = 0, inter = 0;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
+      mx = __vmaxu2(mx, x[q]);
       const uint32_t xh = x[q] | H;
-      bad |= (x[q] & H) | ((xh - Bp1) & H);
       const uint32_t ge_lo = (xh - L2) & H, le_act = (AH - x[q]) & H;
       const uint32_t m = lo >= 0 ? (ge_lo & le_act) : (le_act | (ge_lo & ~((xh - B2) & H)));
-      bits |= (((m >> 15) & 1u) | ((m >> 30) & 2u)) << (2 * q);
+      inter |= ((m >> 15) & 0x00010001u) << q;
     }
+    bad = __vcmpgtu2(mx, B * 0x00010001u);
+    // interleave: low 16 bits -> even positions, high 16 bits -> odd positions
+    uint32_t e = inter & 0xFFFFu, o = inter >> 16;
+    e = (e | (e << 8)) & 0x00FF00FFu; e = (e | (e << 4)) & 0x0F0F0F0Fu;
+    e = (e | (e << 2)) & 0x33333333u; e = (e | (e << 1)) & 0x55555555u;
+    o = (o | (o << 8)) & 0x00FF00FFu; o = (o | (o << 4)) & 0x0F0F0F0Fu;
+    o = (o | (o << 2)) & 0x33333333u; o = (o | (o << 1)) & 0x55555555u;
+    bits = e | (o << 1);
   } else if (sizeof(T) == 1) {
     const uint32_t B4 = B * 0x01010101u, A4 = act * 0x01010101u;
     const uint32_t L4 = (uint32_t)(lo >= 0 ? lo : lo + (int)B) * 0x01010101u;
@@ -687,8 +701,6 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const uint4* src = reinterpret_cast<const uint4*>(cells + w * 32) + v;
-          // an L2-resident pool must stay resident for the next scan: normal
-          // priority; a pool beyond L2 is streamed evict-first
           r[q][v] = STREAM ? __ldcs(src) : __ldcg(src);
         }
       }
@@ -951,7 +963,9 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
     const uint32_t grid = grid_for((nwords + kw - 1) / kw, kThreads, 148u * 32u);
-    const bool stream = p->L.size * (uint64_t)p->cell_bytes > (64ull << 20);
+    // measured (scripts/micro_bitmap.py): evict-first reads are faster even for
+    // an L2-resident pool, so the normal-priority form stays off
+    const bool stream = true;
     if (kw == 4)
       VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 4>), (const T*)p->cells, p->L,
                   p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub);
