@@ -60,6 +60,11 @@ WORKLOADS = {
     "cfg4": dict(name="cfg4-long-window-k300", c=28, k=300, k_prime=300, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
                  base_aip=0x0A000000),
+    # configs[4]: 100M packets per slice in total (k=300, 2^28), split across the
+    # ranks (strong scaling); on one GPU the whole 100M-packet slice
+    "cfg5": dict(name="cfg5-100M-packets-per-slice-k300", c=28, k=300, k_prime=300, g=1024,
+                 hosts=1_000_000, packets=100_000_000, seed=0, partition="tail", floor=0.0,
+                 base_aip=0x0A000000, strong=True),
 }
 WORKLOAD = WORKLOADS["cfg2"]
 METRIC = "Mpackets/s AT scan+update (full slice: scan+estimate+maintain)"
@@ -234,8 +239,10 @@ def _dtype(w):
 
 
 def _config(w, world):
+    per_gpu = w["packets"] // world if w.get("strong") else w["packets"]
     return {"workload": w["name"], "c": w["c"], "k": w["k"], "k_prime": w["k_prime"],
-            "g": w["g"], "hosts": w["hosts"], "packets_per_slice_per_gpu": w["packets"],
+            "g": w["g"], "hosts": w["hosts"], "packets_per_slice_per_gpu": per_gpu,
+            "packets_per_slice_total": per_gpu * world,
             "floor": w["floor"], "partition": w["partition"], "seed": w["seed"],
             "parallelism": f"dp{world}" if world > 1 else "single",
             "l2": _l2_note(w)}
@@ -246,8 +253,11 @@ def _l2_note(w):
     cb = 1 if 2 * w["k"] <= 254 else 2
     pool_mib = (1 << w["c"]) * cb / 2**20
     total = w["packets"] * 8 / 1e6
-    return (f"every slice distinct ({total:.1f} MB of packets each, pre-generated; the timed "
-            f"region streams > L2 of never-reused input); the {pool_mib:.0f} MiB pool "
+    inputs = (f"every slice distinct ({total:.1f} MB of packets each, pre-generated; the timed "
+              f"region streams > L2 of never-reused input)" if total <= 256 else
+              f"slices of {total:.0f} MB cycle through a ring of 24 distinct ones (19 GB, "
+              f">> L2: no input is L2-hot)")
+    return (inputs + f"; the {pool_mib:.0f} MiB pool "
             + ("stays L2-resident by design" if pool_mib <= 64 else "exceeds L2 (HBM-bound)"))
 
 
@@ -289,7 +299,8 @@ def run_gpu(args, rank, world, local_rank):
     for kv in args.opt:                       # experiments: --opt spin_wait=0 ...
         name, val = kv.split("=")
         pool.set_option(name, int(val))
-    n = w["packets"]
+    # strong-scaling workloads fix the packets per slice of the whole job
+    n = w["packets"] // world if w.get("strong") else w["packets"]
     slice_bytes = n * 8
     torch.cuda.set_device(dev)
     # Every slice of the run is distinct (no ring reuse): a repeated slice would
@@ -308,12 +319,17 @@ def run_gpu(args, rank, world, local_rank):
             zt.packets(pool, t_, n, w["base_aip"], w["seed"], out_ptr)
         else:
             check(lib.vate_synth_packets(h, t_, n, w["hosts"], w["base_aip"], w["seed"], out_ptr))
+    # distinct device slices; 800 MB slices (cfg 5) cycle through a ring of 24 (19 GB,
+    # >> L2, so the timed region still never finds its input in L2)
     n_dev = args.warmup + 2 * args.steps
+    if slice_bytes > (256 << 20):
+        n_dev = min(n_dev, 24)
     scratch = torch.empty((n, 2), dtype=torch.int32, device=f"cuda:{dev}")
     dslices = torch.empty((n_dev, n, 2), dtype=torch.int32, device=f"cuda:{dev}")
     for i in range(n_dev):
         synth(t_base + prefill + i, dslices[i].data_ptr())
-    n_host = args.warmup + args.steps
+    # e2e host slices (pinned): every one distinct; 800 MB slices (cfg 5) capped at 4
+    n_host = args.warmup + (args.steps if slice_bytes <= (256 << 20) else min(args.steps, 4))
     hslices = torch.empty((n_host, n, 2), dtype=torch.int32, pin_memory=True)
     for i in range(n_host):
         synth(t_base + prefill + n_dev + i, scratch.data_ptr())
@@ -370,7 +386,7 @@ def run_gpu(args, rank, world, local_rank):
         t += 1
     di = 0
     for _ in range(args.warmup):
-        step(t, dslices[di].data_ptr(), True)
+        step(t, dslices[di % n_dev].data_ptr(), True)
         t += 1
         di += 1
 
@@ -395,7 +411,7 @@ def run_gpu(args, rank, world, local_rank):
         check(lib.vate_mark(h, 0))
         rows = 0
         for _ in range(args.steps):
-            rows += step(t, dslices[di].data_ptr(), True)
+            rows += step(t, dslices[di % n_dev].data_ptr(), True)
             t += 1
             di += 1
         rows += flush()                  # the last slice's reports are part of the work
@@ -412,7 +428,7 @@ def run_gpu(args, rank, world, local_rank):
         # --- per-kernel breakdown (separate pass, CUDA events around each launch) -----
         pool.set_timing(True)
         for _ in range(args.steps):
-            step(t, dslices[di].data_ptr(), True)
+            step(t, dslices[di % n_dev].data_ptr(), True)
             t += 1
             di += 1
         flush()
@@ -454,8 +470,9 @@ def run_gpu(args, rank, world, local_rank):
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         max_ms, max_e2e = float(v[0]), float(v[1])
     total_packets = n * world * args.steps
+    e2e_steps = n_host - args.warmup
     value = total_packets / (max_ms / 1e3) / 1e6
-    e2e_value = total_packets / max_e2e / 1e6
+    e2e_value = n * world * e2e_steps / max_e2e / 1e6
     if rank != 0:
         _teardown(dist)
         return
@@ -506,7 +523,8 @@ def run_gpu(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": _dtype(w),
+        "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
+        "dtype": _dtype(w),
         "data": "synthetic (csrc k_synth == oracle.synthetic_slice)",
         "config": dict(_config(w, world), counter=args.counter,
                        scan_form="heavy-hitter (load-before-store, CTA touch filter)"
@@ -529,8 +547,9 @@ def run_gpu(args, rank, world, local_rank):
                      "traffic_source": "profiles/*ncu_kernels.txt (ncu --set full, one launch)",
                      "algorithmic_bytes_per_launch": alg_bytes[dom]},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": slice_bytes,
-                "d2h_bytes_per_step": int(e2e_rows / args.steps * 25),
-                "host_ms_per_step": {k: v / args.steps for k, v in host_ms.items()}},
+                "d2h_bytes_per_step": int(e2e_rows / e2e_steps * 25),
+                "steps": e2e_steps,
+                "host_ms_per_step": {k: v / e2e_steps for k, v in host_ms.items()}},
         "gpu_launches": int(launches),
         "slice_step": "lagged (Pipeline.step_lagged)" if lagged else "Pipeline.step_fast",
         "active_set_ordering": pool.sort_stats(),
