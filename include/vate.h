@@ -88,7 +88,10 @@ int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
  * (exact), 0 recomputes every g0 by a full gather. */
 enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 2,
                    VATE_OPT_SCAN_CHECK = 3, VATE_OPT_L2_PERSIST = 4, VATE_OPT_BITMAP_KW = 5,
-                   VATE_OPT_CONCURRENT = 6, VATE_OPT_INC_SORT = 7, VATE_OPT_SPIN_WAIT = 8 };
+                   VATE_OPT_CONCURRENT = 6, VATE_OPT_INC_SORT = 7, VATE_OPT_SPIN_WAIT = 8,
+                   VATE_OPT_FUSE_SWEEP = 9 };
+/* VATE_OPT_FUSE_SWEEP (default 1): in the slice step the advance's two-block
+ * sweep runs inside the bitmap pass (after each word's bits are taken). */
 /* VATE_OPT_SPIN_WAIT (default 0): the slice's host round trip spins on a flag
  * a one-thread kernel writes to mapped pinned memory (bounded; falls back to
  * cudaStreamSynchronize).  Measured slower than the driver's wait on B200

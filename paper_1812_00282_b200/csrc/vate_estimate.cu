@@ -551,15 +551,26 @@ int vate_reports_from_counts(vate_pool* p, uint64_t g, const int32_t* g0, uint64
 // The estimate in two halves around its single host round trip.
 // enqueue: the bitmap pass (P, and the flipped cells when the index is live)
 // and the active-set compaction; their counters are copied to pinned memory.
+// with_advance: slice t's advance follows its bitmap pass on the main stream --
+// fused into the pass for the AT pool (no separate sweep launch), a separate
+// kernel for the comparators; collected with vate_advance_result.
+static int bitmap_and_advance(vate_pool* p, int k_prime, bool delta, bool with_advance) {
+  const bool fuse = with_advance && p->kind == VATE_AT && p->opt_fuse_sweep;
+  int rc = build_bitmap(p, k_prime, delta, fuse);
+  if (rc || !with_advance || fuse) return rc;
+  return vate_advance_async(p);
+}
+
 static int begin_enqueue(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_stream,
-                         int64_t t, int k_prime, bool whole_set = true) {
+                         int64_t t, int k_prime, bool whole_set = true,
+                         bool with_advance = false) {
   if (!hosts || hosts->pool != p) return set_error(VATE_EVALUE, "registry does not belong to pool");
   int rc = check_width(p, k_prime);
   if (rc) return rc;
   if (g < 1 || g > p->L.size) return set_error(VATE_ECONFIG, "g must be in [1, 2^c]");
   p->est_n = 0;
   if (!p->opt_concurrent) {
-    rc = build_bitmap(p, k_prime, inc_delta_ready(p, g, cell_stream, k_prime));
+    rc = bitmap_and_advance(p, k_prime, inc_delta_ready(p, g, cell_stream, k_prime), with_advance);
     if (rc) return rc;
     return hosts_active_launch(hosts, t, k_prime);  // pipeline.py:121
   }
@@ -572,10 +583,16 @@ static int begin_enqueue(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t c
   std::swap(p->stream, p->aux_stream);
   if (rc) return rc;
   VATE_CUDA(cudaEventRecord(p->ev_join, p->aux_stream));
-  rc = build_bitmap(p, k_prime, inc_delta_ready(p, g, cell_stream, k_prime));
+  const bool delta = inc_delta_ready(p, g, cell_stream, k_prime);
+  rc = build_bitmap(p, k_prime, delta,
+                    with_advance && p->kind == VATE_AT && p->opt_fuse_sweep);
   if (rc) return rc;
   if (whole_set) {  // the delta apply overlaps the round trip (behind active on aux)
     rc = inc_apply_early(p, hosts_nactive_dev(hosts), g);
+    if (rc) return rc;
+  }
+  if (with_advance && !(p->kind == VATE_AT && p->opt_fuse_sweep)) {
+    rc = vate_advance_async(p);  // comparators: the separate advance kernel
     if (rc) return rc;
   }
   VATE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_join, 0));
@@ -757,46 +774,29 @@ int vate_slice_step(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_s
     rc = vate_scan_packed(p, g, cell_stream, group_stream, pairs, n, where, hosts, t);
   }
   if (rc) return rc;
-  // estimate, first half; then the slice's one host round trip
-  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime);
-  if (rc) return rc;
-  rc = sync_small(p);
-  if (rc) return rc;
-  if (p->adv_pending) {  // the previous slice's sweep finished before this sync
+  if (p->adv_pending) {  // the previous slice's advance (its bitmap pass) is long done
     res->prev_collected = 1;
     rc = vate_advance_result(p, res->prev_blocks, &res->prev_maintained, &res->prev_cleared);
     if (rc) return rc;
   }
+  // estimate, first half, with this slice's advance fused into the bitmap pass
+  // (it touches cells, which nothing after the pass reads); then the slice's
+  // one host round trip
+  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime, true, true);
+  if (rc) return rc;
+  rc = sync_small(p);
+  if (rc) return rc;
   uint64_t nh = 0, pin = 0;
   rc = begin_complete(p, hosts, g, cell_stream, t, k_prime, &nh, &pin);
   if (rc) return rc;
   res->nhosts = nh;
   res->pool_inactive = pin;
-  // maintenance may run before the float path: it touches cells, not g0 --
-  // with opt_concurrent on the aux stream, beside g0 and the float path, and
-  // joined back so the next scan follows it
-  const bool fork = p->opt_concurrent != 0;
-  if (fork) {
-    VATE_CUDA(cudaEventRecord(p->ev_fork, p->stream));
-    VATE_CUDA(cudaStreamWaitEvent(p->aux_stream, p->ev_fork, 0));
-    std::swap(p->stream, p->aux_stream);
-  }
-  rc = vate_advance_async(p);
-  if (fork) {
-    std::swap(p->stream, p->aux_stream);
-    if (rc == VATE_OK) {
-      cudaError_t e = cudaEventRecord(p->ev_join, p->aux_stream);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
-    }
-  }
-  if (rc) return rc;
   uint64_t kept = 0;
   if (nh) {
     rc = vate_estimate_finish_async(p, g, pin, log_zp_table[pin], floor, out_host, out_est,
                                     out_zv, out_sat, cap, &kept);
     res->nkept = kept;
   }
-  if (fork) VATE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_join, 0));
   return rc;
 }
 
@@ -944,11 +944,9 @@ int vate_slice_lagged_end(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t 
     VATE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_post, 0));
     p->post_recorded = false;
   }
-  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime);
+  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime, true, true);  // + advance(t)
   if (rc) return rc;
   VATE_CUDA(cudaEventRecord(p->ev_counts, p->stream));
-  rc = vate_advance_async(p);
-  if (rc) return rc;
   p->lag_pending = true;
   p->lag_t = t;
   p->lag_kp = k_prime;

@@ -319,6 +319,7 @@ struct vate_pool {
   int opt_l2 = 0;             // L2 persisting window: 0 off, 1 registry, 2 cells
   int opt_bitmap_kw = 0;      // bitmap pass words per thread (0 auto)
   int opt_concurrent = 1;     // fork independent estimate phases onto aux_stream
+  int opt_fuse_sweep = 1;     // slice step: the advance sweep inside the bitmap pass
   cudaStream_t aux_stream = nullptr;   // second compute stream (fork/join with events)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // lagged slice step: the slice whose results the next call completes
@@ -342,6 +343,7 @@ struct vate_pool {
   uint64_t sorted_n = 0;
   uint64_t sorts_skipped = 0;
   uint64_t sorts_full = 0, sorts_incremental = 0;
+  uint64_t sweeps_fused = 0;
   int opt_inc_sort = 1;       // merge membership flips into the sorted active set
   int opt_spin = 0;           // host round trip: spin on a mapped flag (measured slower: off)
   volatile unsigned long long* h_flag = nullptr;  // mapped pinned sequence flag
@@ -391,7 +393,7 @@ struct vate_hosts {
 
 namespace vate {
 
-int build_bitmap(vate_pool* p, int k_prime, bool with_delta = false);
+int build_bitmap(vate_pool* p, int k_prime, bool with_delta = false, bool fused_advance = false);
 
 // error plumbing (thread-local message)
 int set_error(int code, const std::string& msg);

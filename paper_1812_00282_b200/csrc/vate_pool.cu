@@ -639,6 +639,39 @@ struct DeltaOut {
   unsigned long long* work;
 };
 
+// The slice advance fused into the bitmap pass (vate_slice_step): the bits are
+// taken with the slice's clocks, then the two blocks due under the advanced
+// clock are swept exactly as k_sweep does (pools.py:221-249): range 0 at clock
+// 0 (stale: v <= k), range 1 at clock k (stale: k <= v <= 2k-1 or v == 0).
+// Each cell is read and rewritten by the one thread that owns its word, after
+// its bit is taken, so the estimate sees the pre-advance pool as it must.
+struct SweepSpec {
+  uint64_t s0, e0, s1, e1;          // the two due ranges (e == s: none)
+  uint32_t k, B;
+  unsigned long long* cleared;      // nullptr: no fused sweep
+};
+
+// Out of line and register-free (re-reads the word's cells, L1-hot): passing
+// the pass's register copy by reference would push it to local memory.
+template <typename T>
+__device__ __noinline__ unsigned sweep_word(T* __restrict__ cells, uint64_t i0, uint32_t cnt,
+                                            uint64_t s0, uint64_t e0, uint64_t s1, uint64_t e1,
+                                            uint32_t k, uint32_t B) {
+  unsigned cleared = 0;
+  for (uint32_t j = 0; j < cnt; ++j) {
+    const uint64_t i = i0 + j;
+    const bool due0 = i >= s0 && i < e0, due1 = i >= s1 && i < e1;
+    if (!due0 && !due1) continue;
+    const uint32_t v = cells[i];
+    const bool stale = due0 ? v <= k : ((v >= k && v <= B - 1) || v == 0);
+    if (stale) {
+      cells[i] = (T)B;
+      ++cleared;
+    }
+  }
+  return cleared;
+}
+
 template <typename T>
 __device__ __forceinline__ uint32_t word_inactive_bits(const T* __restrict__ cells,
                                                        const uint4 (&r)[(int)sizeof(T) * 2],
@@ -673,12 +706,12 @@ __device__ __forceinline__ uint32_t word_inactive_bits(const T* __restrict__ cel
 // kW words per thread per iteration: all their 16-byte loads are issued before
 // any predicate, for memory-level parallelism.
 template <typename T, int kW, bool STREAM = true>
-__global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells, Layout L,
+__global__ void __launch_bounds__(kThreads) k_bitmap(T* __restrict__ cells, Layout L,
                                                      uint32_t bact0, uint32_t kp,
                                                      uint32_t* __restrict__ bitmap,
                                                      uint64_t nwords,
                                                      unsigned long long* pool_inactive,
-                                                     DeltaOut D, Publish pub) {
+                                                     DeltaOut D, Publish pub, SweepSpec SW) {
   constexpr int NV = (int)sizeof(T) * 2;
   constexpr unsigned kDeltaStage = 1024;
   __shared__ unsigned long long s_delta[kDeltaStage];
@@ -690,7 +723,7 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
   }
   __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  unsigned local = 0;
+  unsigned local = 0, swept = 0;
   for (uint64_t w0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w0 < nwords;
        w0 += kW * stride) {
     uint4 r[kW][NV];
@@ -714,6 +747,8 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
       const uint32_t bits = word_inactive_bits<T>(cells, r[q], i0, cnt, L, bact0, kp);
       bitmap[w] = bits;
       local += __popc(bits);
+      if (SW.cleared && ((i0 < SW.e0 && i0 + cnt > SW.s0) || (i0 < SW.e1 && i0 + cnt > SW.s1)))
+        swept += sweep_word(cells, i0, cnt, SW.s0, SW.e0, SW.s1, SW.e1, SW.k, SW.B);
       if (D.bprev) {
         uint32_t x = bits ^ D.bprev[w];
         if (x) {  // stage this CTA's flipped cells in shared memory
@@ -747,9 +782,13 @@ __global__ void __launch_bounds__(kThreads) k_bitmap(const T* __restrict__ cells
     for (unsigned i = threadIdx.x; i < nd; i += blockDim.x)
       if (s_base + i < D.cap) D.list[s_base + i] = s_delta[i];
   }
+  if (SW.cleared) {
+    const unsigned ws = __reduce_add_sync(0xffffffffu, swept);
+    if ((threadIdx.x & 31) == 0 && ws) atomicAdd(SW.cleared, (unsigned long long)ws);
+  }
   const unsigned s = block_sum(local);
   if (threadIdx.x == 0 && s) atomicAdd(pool_inactive, (unsigned long long)s);
-  publish_last_block(pub);  // P (and the delta counts) straight into pinned memory
+  publish_last_block(pub);  // P (and the delta / sweep counts) straight into pinned memory
 }
 
 template <typename T>
@@ -940,7 +979,7 @@ static int require_at(const vate_pool* p, const char* what) {
 }
 
 // Build the k' inactive bitmap and enqueue P into h_ctr[C_P] (not synced).
-int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
+int build_bitmap(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
   if (p->kind != VATE_AT) return cmp_build_bitmap(p, k_prime);  // opt_inc is 0 there
   const uint64_t nwords = (p->L.size + 31) / 32;
   int rc = p->bitmap.ensure(nwords * 4 + 16);
@@ -955,9 +994,23 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
                  p->d_ctr + C_DWORK};
   }
   // words per thread per iteration (p->opt_bitmap_kw overrides: 1, 2 or 4)
-  // counters [C_P .. C_DWORK] published by the last CTA (zero-copy)
+  // the fused advance: due blocks under the advanced clock (pools.py:228-232)
+  SweepSpec SW{};
+  uint32_t z = 0, qb = 0;
+  if (fused_advance) {
+    if (p->adv_pending) return set_error(VATE_EVALUE, "previous advance not collected");
+    const uint32_t B = p->L.B, k = p->L.k;
+    const uint32_t nb = (p->bact0 + 1) % B;
+    z = (B - nb) % B;
+    qb = (k + B - nb) % B;
+    SW = SweepSpec{block_start(z, p->L), block_start(z + 1, p->L), block_start(qb, p->L),
+                   block_start(qb + 1, p->L), k, B, p->d_ctr + C_CLEARED};
+    VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_CLEARED, 0, 8, p->stream));
+  }
+  // counters published by the last CTA (zero-copy)
   const Publish pub{p->d_done, p->d_ctr, p->h_ctr_dev,
-                    (1u << C_P) | (with_delta ? (1u << C_DCNT) | (1u << C_DWORK) : 0u)};
+                    (1u << C_P) | (with_delta ? (1u << C_DCNT) | (1u << C_DWORK) : 0u) |
+                        (fused_advance ? (1u << C_CLEARED) : 0u)};
   int kw = p->opt_bitmap_kw;
   if (kw == 0) kw = 1;  // measured best at c = 24, 26, 28 (scripts/micro_bitmap.py)
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
@@ -967,24 +1020,33 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
     // an L2-resident pool, so the normal-priority form stays off
     const bool stream = true;
     if (kw == 4)
-      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 4>), (const T*)p->cells, p->L,
-                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub);
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 4>), (T*)p->cells, p->L,
+                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub, SW);
     else if (kw == 2)
-      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 2>), (const T*)p->cells, p->L,
-                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub);
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 2>), (T*)p->cells, p->L,
+                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub, SW);
     else if (stream)
-      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1, true>), (const T*)p->cells,
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1, true>), (T*)p->cells,
                   p->L, p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords,
-                  p->d_ctr + C_P, D, pub);
+                  p->d_ctr + C_P, D, pub, SW);
     else
-      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1, false>), (const T*)p->cells,
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1, false>), (T*)p->cells,
                   p->L, p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords,
-                  p->d_ctr + C_P, D, pub);
+                  p->d_ctr + C_P, D, pub, SW);
     return VATE_OK;
   });
   if (rc) return rc;
   // P (and the delta counts) reach the host with the estimate's one round trip,
   // written into pinned memory by the kernel's last CTA
+  if (fused_advance) {  // AtPool.advance_slice bookkeeping; result via vate_advance_result
+    p->bact0 = (p->bact0 + 1) % p->L.B;
+    p->adv_blocks[0] = (int32_t)z;
+    p->adv_blocks[1] = (int32_t)qb;
+    p->adv_maint = (SW.e0 - SW.s0) + (SW.e1 - SW.s1);
+    VATE_CUDA(cudaEventRecord(p->ev_adv, p->stream));
+    p->adv_pending = true;
+    p->sweeps_fused++;
+  }
   return VATE_OK;
 }
 
@@ -1227,6 +1289,10 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
       VATE_CUDA(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
       VATE_CUDA(cudaCtxResetPersistingL2Cache());  // persisting lines would stay pinned
     }
+    return VATE_OK;
+  }
+  if (option == VATE_OPT_FUSE_SWEEP && (value == 0 || value == 1)) {
+    p->opt_fuse_sweep = (int)value;
     return VATE_OK;
   }
   if (option == VATE_OPT_SPIN_WAIT && (value == 0 || value == 1)) {

@@ -249,7 +249,7 @@ class _DevicePool:
         """Tuning switches: 'g0_kernel' (0 auto, 1 gather, 2 smem) and 'incremental' (0/1)."""
         check(lib.vate_pool_set_option(self._h, ("g0_kernel", "incremental", "scan_v", "scan_check",
                                                      "l2_persist", "bitmap_kw", "concurrent",
-                                                     "inc_sort", "spin_wait").index(option),
+                                                     "inc_sort", "spin_wait", "fuse_sweep").index(option),
                                        int(value)))
 
     def inc_stats(self) -> dict:
