@@ -536,8 +536,12 @@ def run_gpu(args, rank, world, local_rank):
         "scan_update_mpps": n / ((per_kind["scan"]["ms_total"] + per_kind["sweep"]["ms_total"])
                                  / args.steps / 1e3) / 1e6,
         "reports_per_slice": nh,
-        "maintain_ms_per_slice": per_kind["sweep"]["ms_total"] / args.steps,
-        "maintain_note": ("AT: the two due blocks (pools.py:221-249)" if args.counter == "at" else
+        "maintain_ms_per_slice": (per_kind["sweep"]["ms_total"] / args.steps
+                                  if per_kind["sweep"]["launches"] else None),
+        "maintain_note": (("AT: the two due blocks (pools.py:221-249)" +
+                           ("" if per_kind["sweep"]["launches"] else
+                            ", swept inside the bitmap pass (no separate launch)"))
+                          if args.counter == "at" else
                           "DR: every cell slides (pools.py:339-349)" if args.counter == "dr" else
                           "TS: no maintenance (pools.py:399-401)"),
         "kernels": per_kind,

@@ -6,6 +6,8 @@ timeout 300 python __graft_entry__.py smoke > gpurun_out/ev_smoke.log 2>&1; echo
 timeout 1500 python -m pytest tests -m gpu -q --timeout 400 -p no:cacheprovider > gpurun_out/ev_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ev_pytest_gpu.log
 python bench.py > gpurun_out/ev_bench_cfg2.json 2> gpurun_out/ev_bench_cfg2.err
 for C in cfg1 cfg3 cfg4; do timeout 600 python bench.py --config $C --steps 30 --warmup 3 > gpurun_out/ev_bench_$C.json 2>/dev/null; done
+timeout 900 python bench.py --config cfg5 --steps 10 --warmup 3 > gpurun_out/ev_bench_cfg5_1gpu.json 2>/dev/null
+timeout 600 python bench.py --lagged 0 --steps 60 --warmup 5 > gpurun_out/ev_bench_cfg2_step_fast.json 2>/dev/null
 timeout 600 python bench.py --incremental off --steps 30 --warmup 3 > gpurun_out/ev_bench_cfg2_full_recompute.json 2>/dev/null
 timeout 600 python bench.py --config cfg4 --counter dr --steps 20 --warmup 3 > gpurun_out/ev_bench_cfg4_dr.json 2>/dev/null
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/ev_bench_reference.json 2> gpurun_out/ev_bench_reference.err
