@@ -319,7 +319,7 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
 }
 
 template <typename T, bool REG, int V = 2, bool CHECK = false, typename Rule = AtRule>  // V uint4 loads per iteration
-__global__ void __launch_bounds__(kThreads, 6) k_scan_packed16(
+__global__ void __launch_bounds__(kThreads, 8) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
     Rule rule, RegRef R, long long t) {
   __shared__ unsigned filt[REG && CHECK ? kTouchSlots : 1];
