@@ -651,10 +651,10 @@ struct SweepSpec {
   unsigned long long* cleared;      // nullptr: no fused sweep
 };
 
-// Out of line and register-free (re-reads the word's cells, L1-hot): passing
+// Register-free (re-reads the word's cells, L1-hot): passing
 // the pass's register copy by reference would push it to local memory.
 template <typename T>
-__device__ __noinline__ unsigned sweep_word(T* __restrict__ cells, uint64_t i0, uint32_t cnt,
+__device__ __forceinline__ unsigned sweep_word(T* __restrict__ cells, uint64_t i0, uint32_t cnt,
                                             uint64_t s0, uint64_t e0, uint64_t s1, uint64_t e1,
                                             uint32_t k, uint32_t B) {
   unsigned cleared = 0;
@@ -706,7 +706,7 @@ __device__ __forceinline__ uint32_t word_inactive_bits(const T* __restrict__ cel
 // kW words per thread per iteration: all their 16-byte loads are issued before
 // any predicate, for memory-level parallelism.
 template <typename T, int kW, bool STREAM = true>
-__global__ void __launch_bounds__(kThreads) k_bitmap(T* __restrict__ cells, Layout L,
+__global__ void __launch_bounds__(kThreads, 6) k_bitmap(T* __restrict__ cells, Layout L,
                                                      uint32_t bact0, uint32_t kp,
                                                      uint32_t* __restrict__ bitmap,
                                                      uint64_t nwords,
