@@ -55,7 +55,7 @@ WORKLOADS = {
     # random peers), pool 2^26
     "cfg3": dict(name="cfg3-zipf-superspreaders", c=26, k=60, k_prime=60, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
-                 base_aip=0x0A000000, zipf=True, scan_check=1),
+                 base_aip=0x0A000000, zipf=True),
     # configs[3]: long window, 512 MiB of u16 cells beyond L2
     "cfg4": dict(name="cfg4-long-window-k300", c=28, k=300, k_prime=300, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
