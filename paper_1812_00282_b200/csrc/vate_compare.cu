@@ -47,8 +47,11 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_cmp_bitmap(const T* __restrict__ cells, uint64_t size,
                                                     CmpPred P, uint32_t* __restrict__ bitmap,
                                                     uint64_t nwords,
-                                                    unsigned long long* pool_inactive) {
+                                                    unsigned long long* pool_inactive,
+                                                    DeltaOut D) {
   constexpr int NV = (int)sizeof(T) * 2;  // uint4 per 32 cells
+  __shared__ DeltaStage ds;
+  if (D.bprev) delta_stage_init(ds);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   unsigned local = 0;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
@@ -66,7 +69,9 @@ __global__ void __launch_bounds__(256) k_cmp_bitmap(const T* __restrict__ cells,
     }
     bitmap[w] = bits;
     local += __popc(bits);
+    if (D.bprev) delta_word(D, ds, bits, w, i0);
   }
+  if (D.bprev) delta_flush(D, ds);
   local = __reduce_add_sync(0xffffffffu, local);
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(pool_inactive, (unsigned long long)local);
 }
@@ -158,21 +163,32 @@ int cmp_fill(vate_pool* p) {
   });
 }
 
-int cmp_build_bitmap(vate_pool* p, int k_prime) {
+int cmp_build_bitmap(vate_pool* p, int k_prime, bool with_delta) {
   const uint64_t nwords = (p->L.size + 31) / 32;
   int rc = p->bitmap.ensure(nwords * 4 + 16);
   if (rc) return rc;
   VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_P, 0, 8, p->stream));
+  DeltaOut D{};
+  if (with_delta) {  // the incremental g0's flipped cells, as in the AT pass
+    IncIndex& I = p->inc;
+    VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_DCNT, 0, 16, p->stream));
+    D = DeltaOut{I.bprev.as<const uint32_t>(), I.off.as<const uint32_t>(),
+                 I.dlist.as<unsigned long long>(), I.dlist_cap, p->d_ctr + C_DCNT,
+                 p->d_ctr + C_DWORK};
+  }
   const CmpPred P{p->kind, (uint32_t)k_prime, p->ts_now};
   rc = with_cmp_cell(p, [&](auto tag) -> int {
     using T = decltype(tag);
     VATE_LAUNCH(p, VATE_K_BITMAP, grid_for(nwords, 256, 148u * 16u), 256, 0, k_cmp_bitmap<T>,
                 (const T*)p->cells, p->L.size, P, p->bitmap.as<uint32_t>(), nwords,
-                p->d_ctr + C_P);
+                p->d_ctr + C_P, D);
     return VATE_OK;
   });
   if (rc) return rc;
   VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_P, p->d_ctr + C_P, 8, cudaMemcpyDeviceToHost, p->stream));
+  if (with_delta)
+    VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_DCNT, p->d_ctr + C_DCNT, 16, cudaMemcpyDeviceToHost,
+                              p->stream));
   return VATE_OK;
 }
 

@@ -160,6 +160,64 @@ struct ConstRule {
   __device__ __forceinline__ T value(uint64_t) const { return (T)v; }
 };
 
+// The incremental-g0 delta of a bitmap pass (vate_incremental.cu): with
+// `bprev` set, every word's bits are XORed with the previous estimate's bitmap
+// and the flipped cells are emitted, staged per CTA in shared memory with one
+// global reservation per CTA.  Shared by the AT and the comparator passes.
+struct DeltaOut {
+  const uint32_t* bprev;       // nullptr: no delta
+  const uint32_t* off;         // inverse-index offsets
+  unsigned long long* list;    // cell | (now_inactive << 32)
+  uint64_t cap;
+  unsigned long long* count;
+  unsigned long long* work;
+};
+constexpr unsigned kDeltaStage = 1024;
+struct DeltaStage {
+  unsigned long long delta[kDeltaStage];
+  unsigned nd;
+  unsigned long long work, base;
+};
+__device__ __forceinline__ void delta_stage_init(DeltaStage& ds) {
+  if (threadIdx.x == 0) {
+    ds.nd = 0;
+    ds.work = 0;
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void delta_word(const DeltaOut& D, DeltaStage& ds, uint32_t bits,
+                                           uint64_t w, uint64_t i0) {
+  uint32_t x = bits ^ D.bprev[w];
+  if (!x) return;
+  unsigned long long wsum = 0;
+  while (x) {
+    const int j = __ffs(x) - 1;
+    x &= x - 1;
+    const uint64_t cell = i0 + j;
+    wsum += D.off[cell + 1] - D.off[cell];
+    const unsigned long long v = cell | ((unsigned long long)((bits >> j) & 1u) << 32);
+    const unsigned slot = atomicAdd(&ds.nd, 1u);
+    if (slot < kDeltaStage) {
+      ds.delta[slot] = v;
+    } else {  // stage full: straight to the global list
+      const unsigned long long pos = atomicAdd(D.count, 1ull);
+      if (pos < D.cap) D.list[pos] = v;
+    }
+  }
+  atomicAdd(&ds.work, wsum);
+}
+__device__ __forceinline__ void delta_flush(const DeltaOut& D, DeltaStage& ds) {
+  __syncthreads();
+  const unsigned nd = ds.nd < kDeltaStage ? ds.nd : kDeltaStage;
+  if (threadIdx.x == 0) {
+    ds.base = nd ? atomicAdd(D.count, (unsigned long long)nd) : 0ull;
+    if (ds.work) atomicAdd(D.work, ds.work);
+  }
+  __syncthreads();
+  for (unsigned i = threadIdx.x; i < nd; i += blockDim.x)
+    if (ds.base + i < D.cap) D.list[ds.base + i] = ds.delta[i];
+}
+
 // Zero-copy publication of a kernel's counters for the slice's host round
 // trip: the last CTA to finish copies n device counters into pinned host
 // memory (mapped; UVA), replacing a small D2H memcpy whose copy-engine latency

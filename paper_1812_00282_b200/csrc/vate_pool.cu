@@ -630,15 +630,6 @@ __device__ __forceinline__ bool active_bits_simd(const uint4 (&r)[(int)sizeof(T)
 // `bprev` set it also emits the cells whose bit flipped against the previous
 // estimate's bitmap (the incremental g0 delta, vate_incremental.cu), so the
 // delta costs no second pass.
-struct DeltaOut {
-  const uint32_t* bprev;       // nullptr: no delta
-  const uint32_t* off;         // inverse-index offsets
-  unsigned long long* list;    // cell | (now_inactive << 32)
-  uint64_t cap;
-  unsigned long long* count;
-  unsigned long long* work;
-};
-
 // The slice advance fused into the bitmap pass (vate_slice_step): the bits are
 // taken with the slice's clocks, then the two blocks due under the advanced
 // clock are swept exactly as k_sweep does (pools.py:221-249): range 0 at clock
@@ -713,15 +704,8 @@ __global__ void __launch_bounds__(kThreads, 6) k_bitmap(T* __restrict__ cells, L
                                                      unsigned long long* pool_inactive,
                                                      DeltaOut D, Publish pub, SweepSpec SW) {
   constexpr int NV = (int)sizeof(T) * 2;
-  constexpr unsigned kDeltaStage = 1024;
-  __shared__ unsigned long long s_delta[kDeltaStage];
-  __shared__ unsigned s_nd;
-  __shared__ unsigned long long s_work, s_base;
-  if (threadIdx.x == 0) {
-    s_nd = 0;
-    s_work = 0;
-  }
-  __syncthreads();
+  __shared__ DeltaStage ds;
+  delta_stage_init(ds);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   unsigned local = 0, swept = 0;
   for (uint64_t w0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w0 < nwords;
@@ -749,39 +733,10 @@ __global__ void __launch_bounds__(kThreads, 6) k_bitmap(T* __restrict__ cells, L
       local += __popc(bits);
       if (SW.cleared && ((i0 < SW.e0 && i0 + cnt > SW.s0) || (i0 < SW.e1 && i0 + cnt > SW.s1)))
         swept += sweep_word(cells, i0, cnt, SW.s0, SW.e0, SW.s1, SW.e1, SW.k, SW.B);
-      if (D.bprev) {
-        uint32_t x = bits ^ D.bprev[w];
-        if (x) {  // stage this CTA's flipped cells in shared memory
-          unsigned long long wsum = 0;
-          while (x) {
-            const int j = __ffs(x) - 1;
-            x &= x - 1;
-            const uint64_t cell = i0 + j;
-            wsum += D.off[cell + 1] - D.off[cell];
-            const unsigned long long v = cell | ((unsigned long long)((bits >> j) & 1u) << 32);
-            const unsigned slot = atomicAdd(&s_nd, 1u);
-            if (slot < kDeltaStage) s_delta[slot] = v;
-            else {  // stage full: straight to the global list
-              const unsigned long long pos = atomicAdd(D.count, 1ull);
-              if (pos < D.cap) D.list[pos] = v;
-            }
-          }
-          atomicAdd(&s_work, wsum);
-        }
-      }
+      if (D.bprev) delta_word(D, ds, bits, w, i0);
     }
   }
-  if (D.bprev) {  // one global reservation per CTA
-    __syncthreads();
-    const unsigned nd = s_nd < kDeltaStage ? s_nd : kDeltaStage;
-    if (threadIdx.x == 0) {
-      s_base = nd ? atomicAdd(D.count, (unsigned long long)nd) : 0ull;
-      if (s_work) atomicAdd(D.work, s_work);
-    }
-    __syncthreads();
-    for (unsigned i = threadIdx.x; i < nd; i += blockDim.x)
-      if (s_base + i < D.cap) D.list[s_base + i] = s_delta[i];
-  }
+  if (D.bprev) delta_flush(D, ds);
   if (SW.cleared) {
     const unsigned ws = __reduce_add_sync(0xffffffffu, swept);
     if ((threadIdx.x & 31) == 0 && ws) atomicAdd(SW.cleared, (unsigned long long)ws);
@@ -966,7 +921,7 @@ using namespace vate;
 namespace vate {
 // comparator pools (vate_compare.cu)
 int cmp_fill(vate_pool* p);
-int cmp_build_bitmap(vate_pool* p, int k_prime);
+int cmp_build_bitmap(vate_pool* p, int k_prime, bool with_delta);
 int cmp_advance_async(vate_pool* p);
 int cmp_inactive_mask(vate_pool* p, const uint64_t* d_idx, uint64_t n, int k_prime,
                       uint8_t* out_dev);
@@ -980,7 +935,7 @@ static int require_at(const vate_pool* p, const char* what) {
 
 // Build the k' inactive bitmap and enqueue P into h_ctr[C_P] (not synced).
 int build_bitmap(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
-  if (p->kind != VATE_AT) return cmp_build_bitmap(p, k_prime);  // opt_inc is 0 there
+  if (p->kind != VATE_AT) return cmp_build_bitmap(p, k_prime, with_delta);
   const uint64_t nwords = (p->L.size + 31) / 32;
   int rc = p->bitmap.ensure(nwords * 4 + 16);
   if (rc) return rc;
@@ -1119,7 +1074,7 @@ static int pool_create(vate_pool** out, int kind, int c, int k, int partition, i
   if (kind == VATE_DR) p->width = 32u - (uint32_t)__builtin_clz((uint32_t)k);  // dr_bits
   if (kind == VATE_TS) p->width = 64;
   p->cell_bytes = p->width <= 8 ? 1 : (p->width <= 16 ? 2 : (p->width <= 32 ? 4 : 8));
-  if (kind != VATE_AT) p->opt_inc = 0;  // comparators: full g0 gather every estimate
+
   p->L = L;
   int rc = VATE_OK;
   cudaError_t e = cudaSetDevice(device);
@@ -1321,7 +1276,7 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     return VATE_OK;
   }
   if (option == VATE_OPT_INCREMENTAL && (value == 0 || value == 1)) {
-    p->opt_inc = p->kind == VATE_AT ? (int)value : 0;
+    p->opt_inc = (int)value;
     if (!value) p->inc.valid = false;
     return VATE_OK;
   }

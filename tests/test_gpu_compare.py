@@ -60,9 +60,10 @@ def test_device_pools_replay_the_reference(name, kind):
 
 @pytest.mark.parametrize("kind", ("dr", "ts"))
 def test_comparator_pipeline_equals_at_pipeline(kind):
-    """The fused device Pipeline (one host round trip per slice, incremental g0
-    off for comparators) gives the AT pipeline's reports, and the maintenance
-    the oracle's comparator pool reports (DR: every cell visited)."""
+    """The fused device Pipeline (one host round trip per slice, the incremental
+    g0 index on the comparator's bitmap too) gives the AT pipeline's reports,
+    and the maintenance the oracle's comparator pool reports (DR: every cell
+    visited)."""
     spec = dict(COMPARATORS["cmp_k6"], slices=20, pairs=20_000, hosts=1500)
     at_cfg = vb.EstimatorConfig(spec["g"], spec["c"], spec["k"], seed=spec["seed"])
     cfg = vb.EstimatorConfig(spec["g"], spec["c"], spec["k"], seed=spec["seed"], counter_kind=kind)
@@ -72,7 +73,8 @@ def test_comparator_pipeline_equals_at_pipeline(kind):
     opipe = vo.OraclePipeline(ocfg, spec["kp"], kind=kind)
     for t, a, b in gen_slices(spec):
         want, _ = at.process_slice_soa(t, a, b)
-        got, _ = cmp_.process_slice_soa(t, a, b)
+        got = cmp_.step_fast(t, *_pairs(a, b)) if t % 2 else cmp_.process_slice_soa(t, a, b)[0]
+        cmp_.wait_reports()
         ref = opipe.process_slice(t, a, b)
         if want is None:
             assert got is None
@@ -85,6 +87,18 @@ def test_comparator_pipeline_equals_at_pipeline(kind):
                                                                   ref.cleared), t
     assert np.array_equal(cmp_.pool.cells.get_range(0, cmp_.pool.size),
                           np.asarray(opipe.pool.cells, dtype=np.uint64))
+    assert cmp_.pool.inc_stats()["delta_slices"] > 0   # the index served the comparator
+
+
+def _pairs(a, b):
+    """(device pointer, n, 'device', out) for step_fast on a slice."""
+    import torch
+    pairs = torch.from_numpy(np.ascontiguousarray(
+        np.stack([a.astype(np.uint32), b.astype(np.uint32)], axis=1)).view(np.int32)).cuda()
+    _pairs.keep = pairs
+    n = len(a)
+    out = tuple(np.empty(4096, dt) for dt in (np.uint64, np.float64, np.float64, np.uint8))
+    return pairs.data_ptr(), n, "device", out
 
 
 def test_comparators_refuse_at_only_operations():
