@@ -18,13 +18,15 @@ NB = 140
 bufs = torch.empty((NB, n, 2), dtype=torch.int32, device="cuda:0")
 for i in range(NB):
     check(lib.vate_synth_packets(pool.handle, i, n, 1_000_000, 0x0A000000, 0, bufs[i].data_ptr()))
+lagged = os.environ.get("TL_LAGGED", "1") == "1"
+step = pipe.step_lagged if lagged else pipe.step_fast
 for t in range(130):
-    pipe.step_fast(t, bufs[t].data_ptr(), n, "device", None)
-pipe.wait_reports()
-pool.synchronize()
+    step(t, bufs[t].data_ptr(), n, "device", None)
 pool.set_timing(True)
 for t in range(130, 136):
-    pipe.step_fast(t, bufs[t].data_ptr(), n, "device", None)
+    step(t, bufs[t].data_ptr(), n, "device", None)
+if lagged:
+    pipe.flush_lagged(None)
 pipe.wait_reports()
 pool.synchronize()
 tl = pool.timeline()
