@@ -55,7 +55,7 @@ WORKLOADS = {
     # random peers), pool 2^26
     "cfg3": dict(name="cfg3-zipf-superspreaders", c=26, k=60, k_prime=60, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
-                 base_aip=0x0A000000, zipf=True),
+                 base_aip=0x0A000000, zipf=True, scan_check=2),
     # configs[3]: long window, 512 MiB of u16 cells beyond L2
     "cfg4": dict(name="cfg4-long-window-k300", c=28, k=300, k_prime=300, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
@@ -527,8 +527,9 @@ def run_gpu(args, rank, world, local_rank):
         "dtype": _dtype(w),
         "data": "synthetic (csrc k_synth == oracle.synthetic_slice)",
         "config": dict(_config(w, world), counter=args.counter,
-                       scan_form="heavy-hitter (load-before-store, CTA touch filter)"
-                       if scan_check else "plain stores"),
+                       scan_form={0: "plain stores",
+                                  1: "heavy-hitter (load-before-store, CTA stamp filter)",
+                                  2: "CTA registry-stamp filter (skewed traffic)"}[scan_check]),
         "estimate_ms_per_slice": sum(per_kind[k]["ms_total"] for k in
                                      ("registry", "sort", "bitmap", "g0", "final")) / args.steps,
         "estimate_ms_per_slice_note": "kernel time from the end of scan to the report rows "
@@ -606,7 +607,7 @@ def main():
     ap.add_argument("--impl", choices=("vate", "reference"), default="vate")
     ap.add_argument("--g0-kernel", choices=("auto", "gather", "smem"), default="auto",
                     help="g0 gather variant (VATE_OPT_G0)")
-    ap.add_argument("--scan-check", type=int, choices=(0, 1), default=None,
+    ap.add_argument("--scan-check", type=int, choices=(0, 1, 2), default=None,
                     help="load-before-store scan (VATE_OPT_SCAN_CHECK)")
     ap.add_argument("--l2-persist", type=int, choices=(0, 1, 2), default=0,
                     help="L2 persisting window: 1 host registry, 2 cells (VATE_OPT_L2_PERSIST)")

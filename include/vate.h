@@ -90,6 +90,11 @@ enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 
                    VATE_OPT_SCAN_CHECK = 3, VATE_OPT_L2_PERSIST = 4, VATE_OPT_BITMAP_KW = 5,
                    VATE_OPT_CONCURRENT = 6, VATE_OPT_INC_SORT = 7, VATE_OPT_SPIN_WAIT = 8,
                    VATE_OPT_FUSE_SWEEP = 9 };
+/* VATE_OPT_SCAN_V: packed-scan form (1 default: one uint4 = two packets per
+ * thread; 0 one packet; 2 / 4 uint4; 8 TMA-fed persistent).  VATE_OPT_SCAN_CHECK:
+ * 0 plain stores (default), 1 load-before-store cells + a per-CTA filter of
+ * registry stamps, 2 the stamp filter alone (skewed traffic).  All forms leave
+ * identical state. */
 /* VATE_OPT_FUSE_SWEEP (default 1): in the slice step the advance's two-block
  * sweep runs inside the bitmap pass (after each word's bits are taken). */
 /* VATE_OPT_SPIN_WAIT (default 0): the slice's host round trip spins on a flag

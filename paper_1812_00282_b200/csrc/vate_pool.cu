@@ -266,7 +266,9 @@ __device__ __forceinline__ void defer_drain(DeferQ* dq, const RegRef& R, long lo
   for (unsigned i = threadIdx.x; i < n; i += blockDim.x) reg_insert(R, dq->keys[i], t, false);
 }
 
-template <typename T, bool REG, int U, bool CHECK = false, typename Rule>
+// CHK: 0 plain stores; 1 heavy-hitter form (load-before-store cells + per-CTA
+// registry stamp filter); 2 the registry stamp filter alone
+template <typename T, bool REG, int U, int CHK = 0, typename Rule>
 __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint64_t (&bip)[U],
                                            int m, T* __restrict__ cells, const HashParams& H,
                                            const Rule& rule, const RegRef& R, long long t,
@@ -278,7 +280,7 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
       const T act = rule.template value<T>(cell);
       // CHECK: skew-tolerant form for heavy hitters -- read first (L1 keeps hot
       // lines) and store only if the cell does not already hold the clock
-      if (!CHECK || cells[cell] != act) cells[cell] = act;
+      if (CHK != 1 || cells[cell] != act) cells[cell] = act;
     }
   }
   if (REG) {
@@ -296,12 +298,12 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
       if (q >= m) continue;
       if (aip[q] != kEmptyKey && e[q].key == aip[q]) {
         if (e[q].last != t) {
-          if (CHECK) touch_last(R, filt, slot[q], t);
+          if (CHK) touch_last(R, filt, slot[q], t);
           else R.table[slot[q]].last = t;
         }
       } else if (aip[q] != kEmptyKey && f[q].key == aip[q]) {
         if (f[q].last != t) {
-          if (CHECK) touch_last(R, filt, slot[q] + 1, t);
+          if (CHK) touch_last(R, filt, slot[q] + 1, t);
           else R.table[slot[q] + 1].last = t;
         }
       } else {
@@ -318,7 +320,7 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
   }
 }
 
-template <typename T, bool REG, int V = 2, bool CHECK = false, typename Rule = AtRule>  // V uint4 loads per iteration
+template <typename T, bool REG, int V = 2, int CHECK = 0, typename Rule = AtRule>  // V uint4 loads per iteration
 __global__ void __launch_bounds__(kThreads, 8) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
     Rule rule, RegRef R, long long t) {
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_scan_packed16(
 // One 8-byte packet per thread (the default form, VATE_OPT_SCAN_V = 0): the
 // most threads, the shortest per-thread dependency chain; registry misses go
 // through the same per-CTA deferred queue, CHECK adds the heavy-hitter forms.
-template <typename T, bool REG, bool CHECK = false, typename Rule = AtRule>
+template <typename T, bool REG, int CHECK = 0, typename Rule = AtRule>
 __global__ void __launch_bounds__(kThreads) k_scan_packed8(
     const uint2* __restrict__ pairs, uint64_t n, T* __restrict__ cells, HashParams H,
     Rule rule, RegRef R, long long t) {
@@ -413,7 +415,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   } while (!done);
 }
 
-template <typename T, bool CHECK, typename Rule>
+template <typename T, int CHECK, typename Rule>
 __global__ void __launch_bounds__(kThreads, 4) k_scan_tma(
     const uint2* __restrict__ pairs, uint64_t ntiles, T* __restrict__ cells, HashParams H,
     Rule rule, RegRef R, long long t, unsigned* __restrict__ tile_counter) {
@@ -1266,7 +1268,7 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_bitmap_kw = (int)value;
     return VATE_OK;
   }
-  if (option == VATE_OPT_SCAN_CHECK && (value == 0 || value == 1)) {
+  if (option == VATE_OPT_SCAN_CHECK && (value == 0 || value == 1 || value == 2)) {
     p->opt_scan_check = (int)value;
     return VATE_OK;
   }
@@ -1445,60 +1447,64 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
         VATE_CUDA(cudaMemsetAsync(p->d_done + 2, 0, 4, p->stream));
         const uint32_t gt = (uint32_t)umin64(ntiles, 148u * 4u);
         if (p->opt_scan_check)
-          VATE_LAUNCH(p, VATE_K_SCAN, gt, kThreads, 0, (k_scan_tma<T, true, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, gt, kThreads, 0, (k_scan_tma<T, 1, Rl>),
                       (const uint2*)d_pairs, ntiles, (T*)p->cells, H, rule, R, (long long)t,
                       p->d_done + 2);
         else
-          VATE_LAUNCH(p, VATE_K_SCAN, gt, kThreads, 0, (k_scan_tma<T, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, gt, kThreads, 0, (k_scan_tma<T, 0, Rl>),
                       (const uint2*)d_pairs, ntiles, (T*)p->cells, H, rule, R, (long long)t,
                       p->d_done + 2);
         if (rest)
           VATE_LAUNCH(p, VATE_K_SCAN, grid_for(rest, kThreads, 148u * 64u), kThreads, 0,
-                      (k_scan_packed8<T, true, false, Rl>),
+                      (k_scan_packed8<T, true, 0, Rl>),
                       (const uint2*)d_pairs + ntiles * kTmaTile, rest, (T*)p->cells, H, rule, R,
                       (long long)t);
       } else if (aligned16 && n >= 2 && p->opt_scan_v > 0 && p->opt_scan_v <= 4) {
-        if (hosts && p->opt_scan_v == 1 && p->opt_scan_check)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, true, Rl>),
+        if (hosts && p->opt_scan_v == 1 && p->opt_scan_check == 2)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, 2, Rl>),
+                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
+                      (long long)t);
+        else if (hosts && p->opt_scan_v == 1 && p->opt_scan_check)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, 1, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else if (hosts && p->opt_scan_v == 1)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, 0, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else if (hosts && p->opt_scan_v == 4)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 4, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 4, 0, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else if (hosts)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 2, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 2, 0, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         else
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, false, 2, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, false, 2, 0, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
         if (n & 1) {
           const uint2* last = (const uint2*)d_pairs + (n - 1);
           if (hosts)
-            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, true, false, Rl>), last, 1,
+            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, true, 0, Rl>), last, 1,
                         (T*)p->cells, H, rule, R, (long long)t);
           else
-            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, false, false, Rl>), last, 1,
+            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, false, 0, Rl>), last, 1,
                         (T*)p->cells, H, rule, R, (long long)t);
         }
       } else {  // unaligned input, or scan_v == 0: one 8-byte packet per thread
         const uint32_t grid8 = grid_for(n, kThreads, 148u * 64u);
         if (hosts && p->opt_scan_check)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, true, true, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, true, 1, Rl>),
                       (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
                       (long long)t);
         else if (hosts)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, true, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, true, 0, Rl>),
                       (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
                       (long long)t);
         else
-          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, false, false, Rl>),
+          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, false, 0, Rl>),
                       (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
                       (long long)t);
       }

@@ -954,7 +954,7 @@ def test_active_set_merge_under_small_churn(inc_sort):
         assert st["incremental"] == 0, st
 
 
-@pytest.mark.parametrize("form", [(1, 0), (1, 1), (0, 0), (0, 1), (2, 0), (4, 0), (8, 0), (8, 1)])
+@pytest.mark.parametrize("form", [(1, 0), (1, 1), (1, 2), (0, 0), (0, 1), (2, 0), (4, 0), (8, 0), (8, 1)])
 def test_scan_forms_are_equivalent(form):
     """Every packed-scan form (VATE_OPT_SCAN_V: 0 one packet per thread, 1/2/4
     uint4 per thread, 8 TMA-fed persistent; VATE_OPT_SCAN_CHECK heavy-hitter
