@@ -55,7 +55,7 @@ WORKLOADS = {
     # random peers), pool 2^26
     "cfg3": dict(name="cfg3-zipf-superspreaders", c=26, k=60, k_prime=60, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
-                 base_aip=0x0A000000, zipf=True, scan_check=2),
+                 base_aip=0x0A000000, zipf=True),
     # configs[3]: long window, 512 MiB of u16 cells beyond L2
     "cfg4": dict(name="cfg4-long-window-k300", c=28, k=300, k_prime=300, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
@@ -290,8 +290,10 @@ def run_gpu(args, rank, world, local_rank):
     h = pool.handle
     check(lib.vate_pool_set_option(h, 0, ("auto", "gather", "smem").index(args.g0_kernel)))
     pool.set_option("incremental", 1 if args.incremental == "on" else 0)
-    scan_check = args.scan_check if args.scan_check is not None else w.get("scan_check", 0)
-    if scan_check:   # skewed traffic: load-before-store cells + per-CTA registry touch filter
+    # scan form: auto (the library picks the registry-stamp filter for skewed
+    # traffic) unless forced
+    scan_check = args.scan_check if args.scan_check is not None else w.get("scan_check", -1)
+    if scan_check != -1:
         pool.set_option("scan_check", scan_check)
     if args.l2_persist:
         pool.set_option("l2_persist", args.l2_persist)
@@ -527,7 +529,8 @@ def run_gpu(args, rank, world, local_rank):
         "dtype": _dtype(w),
         "data": "synthetic (csrc k_synth == oracle.synthetic_slice)",
         "config": dict(_config(w, world), counter=args.counter,
-                       scan_form={0: "plain stores",
+                       scan_form={-1: "auto (registry-stamp filter at >= 8 packets per host)",
+                                  0: "plain stores",
                                   1: "heavy-hitter (load-before-store, CTA stamp filter)",
                                   2: "CTA registry-stamp filter (skewed traffic)"}[scan_check]),
         "estimate_ms_per_slice": sum(per_kind[k]["ms_total"] for k in
@@ -607,7 +610,7 @@ def main():
     ap.add_argument("--impl", choices=("vate", "reference"), default="vate")
     ap.add_argument("--g0-kernel", choices=("auto", "gather", "smem"), default="auto",
                     help="g0 gather variant (VATE_OPT_G0)")
-    ap.add_argument("--scan-check", type=int, choices=(0, 1, 2), default=None,
+    ap.add_argument("--scan-check", type=int, choices=(-1, 0, 1, 2), default=None,
                     help="load-before-store scan (VATE_OPT_SCAN_CHECK)")
     ap.add_argument("--l2-persist", type=int, choices=(0, 1, 2), default=0,
                     help="L2 persisting window: 1 host registry, 2 cells (VATE_OPT_L2_PERSIST)")

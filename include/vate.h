@@ -92,9 +92,10 @@ enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 
                    VATE_OPT_FUSE_SWEEP = 9 };
 /* VATE_OPT_SCAN_V: packed-scan form (1 default: one uint4 = two packets per
  * thread; 0 one packet; 2 / 4 uint4; 8 TMA-fed persistent).  VATE_OPT_SCAN_CHECK:
- * 0 plain stores (default), 1 load-before-store cells + a per-CTA filter of
- * registry stamps, 2 the stamp filter alone (skewed traffic).  All forms leave
- * identical state. */
+ * -1 auto (default: the stamp filter when the last compacted slice saw >= 8
+ * packets per distinct host, else plain), 0 plain stores, 1 load-before-store
+ * cells + a per-CTA filter of registry stamps, 2 the stamp filter alone.  All
+ * forms leave identical state. */
 /* VATE_OPT_FUSE_SWEEP (default 1): in the slice step the advance's two-block
  * sweep runs inside the bitmap pass (after each word's bits are taken). */
 /* VATE_OPT_SPIN_WAIT (default 0): the slice's host round trip spins on a flag

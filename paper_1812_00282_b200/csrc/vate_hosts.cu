@@ -19,7 +19,7 @@
 namespace vate {
 
 enum HCtr { H_COUNT = 0, H_OVF = 1, H_SPECIAL = 2, H_MAXKEY = 3, H_NOUT = 4, H_CHANGES = 5, H_NOUT2 = 6,
-            H_ARR = 7, H_DEP = 8, H_N = 10 };
+            H_ARR = 7, H_DEP = 8, H_TOUCHED = 9, H_N = 10 };
 
 // Membership flips of one compaction, for the incremental sorted-set update:
 // keys that joined (arrivals) and left (departures) the window's active set.
@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
                                                 unsigned long long* nout,
                                                 unsigned long long* maxkey,
                                                 unsigned long long* changes, FlipLists F,
-                                                Publish pub) {
+                                                Publish pub, long long t_now,
+                                                unsigned long long* touched) {
   __shared__ unsigned s_n, s_flips;
   __shared__ unsigned long long s_max;
   if (threadIdx.x == 0) {
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
   const uint64_t total = cap + 1;
   const bool special_present = (*special & 0xFFFFFFFFull) != 0;
   unsigned long long kmax = 0;
-  unsigned mine = 0, flips = 0;
+  unsigned mine = 0, flips = 0, now = 0;
   for (uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < total;
        i0 += (uint64_t)gridDim.x * blockDim.x * 4) {
 #pragma unroll
@@ -111,12 +112,15 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
       }
       if (tk) {
         ++mine;
+        now += e.last == t_now;  // hosts seen in this very slice (scan-form heuristic)
         kmax = e.key > kmax ? e.key : kmax;
       }
     }
   }
   mine = __reduce_add_sync(0xffffffffu, mine);
   flips = __reduce_add_sync(0xffffffffu, flips);
+  now = __reduce_add_sync(0xffffffffu, now);
+  if ((threadIdx.x & 31) == 0 && now) atomicAdd(touched, (unsigned long long)now);
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     const unsigned long long other = __shfl_xor_sync(0xffffffffu, kmax, o);
@@ -499,7 +503,8 @@ int hosts_active_launch(vate_hosts* h, int64_t t, int k_prime) {
               h->table.as<const RegEntry>(), h->cap, h->d_count + H_SPECIAL,
               (long long)(t - k_prime), h->member.as<uint8_t>(), h->d_count + H_NOUT,
               h->d_count + H_MAXKEY, h->d_count + H_CHANGES, F,
-              Publish{p->d_done + 1, h->d_count, h->h_count_dev, (1u << H_N) - 1u});
+              Publish{p->d_done + 1, h->d_count, h->h_count_dev, (1u << H_N) - 1u}, (long long)t,
+              h->d_count + H_TOUCHED);
   return VATE_OK;
 }
 
@@ -580,6 +585,7 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
   }
   h->pending = 0;
   h->count_hint = h->h_count[H_COUNT];
+  h->last_touched = h->h_count[H_TOUCHED];
   if (h->count_hint * 5 > h->cap * 3 || (h->cap > (1u << 16) && h->count_hint * 16 < h->cap))
     h->needs_grow = true;
   *n = h->h_count[H_NOUT];

@@ -372,7 +372,8 @@ struct vate_pool {
   // options
   int opt_g0 = 0;
   int opt_inc = 1;            // incremental g0 through the inverse index
-  int opt_scan_check = 0;    // packed scan: load-before-store (heavy hitters)
+  int opt_scan_check = -1;   // packed scan form: -1 auto, 0 plain, 1 check + filter, 2 filter
+  int scan_form_used = 0;     // the form the last packed scan ran (auto resolved)
   int opt_scan_v = 1;         // packed scan form: 1 (default), 0, 2, 4 per-thread unroll; 8 TMA-fed persistent
   int opt_l2 = 0;             // L2 persisting window: 0 off, 1 registry, 2 cells
   int opt_bitmap_kw = 0;      // bitmap pass words per thread (0 auto)
@@ -441,6 +442,7 @@ struct vate_hosts {
   uint64_t count_hint = 0; // last count read back
   bool needs_grow = false; // load factor passed 1/2: grow at the next drain point
   bool lagged = false;     // completing a slice while the next one's scan may run
+  uint64_t last_touched = 0;  // hosts seen in the last compacted slice (scan-form heuristic)
   vate::DevBuf member;     // u8 per slot: in the active set of the last compaction
   bool member_valid = false;
   vate::DevBuf flips;      // arrivals, departures and their sorted copies (4 x flip_cap)

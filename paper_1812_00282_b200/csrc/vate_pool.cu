@@ -1268,7 +1268,7 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_bitmap_kw = (int)value;
     return VATE_OK;
   }
-  if (option == VATE_OPT_SCAN_CHECK && (value == 0 || value == 1 || value == 2)) {
+  if (option == VATE_OPT_SCAN_CHECK && value >= -1 && value <= 2) {
     p->opt_scan_check = (int)value;
     return VATE_OK;
   }
@@ -1429,6 +1429,13 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
   }
   rc = apply_l2_window(p, hosts);
   if (rc) return rc;
+  // scan form: auto picks the registry-stamp filter for skewed traffic -- when
+  // the last compacted slice saw 8 or more packets per distinct host (Zipf-like
+  // heads whose same-address stamps serialise); plain stores otherwise
+  int chk = p->opt_scan_check;
+  if (chk < 0)
+    chk = (hosts && hosts->last_touched && n >= 8 * hosts->last_touched) ? 2 : 0;
+  p->scan_form_used = chk;
   // packed16: one iteration of V uint4 (2V packets) per thread; others: grid-stride
   const uint64_t per_thread = 2ull * (uint64_t)(p->opt_scan_v > 0 ? p->opt_scan_v : 1);
   const uint32_t grid16 = grid_for((n + per_thread - 1) / per_thread, kThreads, 148u * 64u);
@@ -1446,7 +1453,7 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
         const uint64_t ntiles = n / kTmaTile, rest = n - ntiles * kTmaTile;
         VATE_CUDA(cudaMemsetAsync(p->d_done + 2, 0, 4, p->stream));
         const uint32_t gt = (uint32_t)umin64(ntiles, 148u * 4u);
-        if (p->opt_scan_check)
+        if (chk)
           VATE_LAUNCH(p, VATE_K_SCAN, gt, kThreads, 0, (k_scan_tma<T, 1, Rl>),
                       (const uint2*)d_pairs, ntiles, (T*)p->cells, H, rule, R, (long long)t,
                       p->d_done + 2);
@@ -1460,11 +1467,11 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
                       (const uint2*)d_pairs + ntiles * kTmaTile, rest, (T*)p->cells, H, rule, R,
                       (long long)t);
       } else if (aligned16 && n >= 2 && p->opt_scan_v > 0 && p->opt_scan_v <= 4) {
-        if (hosts && p->opt_scan_v == 1 && p->opt_scan_check == 2)
+        if (hosts && p->opt_scan_v == 1 && chk == 2)
           VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, 2, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
-        else if (hosts && p->opt_scan_v == 1 && p->opt_scan_check)
+        else if (hosts && p->opt_scan_v == 1 && chk)
           VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, 1, Rl>),
                       (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
                       (long long)t);
@@ -1495,7 +1502,7 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
         }
       } else {  // unaligned input, or scan_v == 0: one 8-byte packet per thread
         const uint32_t grid8 = grid_for(n, kThreads, 148u * 64u);
-        if (hosts && p->opt_scan_check)
+        if (hosts && chk)
           VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, true, 1, Rl>),
                       (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
                       (long long)t);
