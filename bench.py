@@ -540,8 +540,10 @@ def run_gpu(args, rank, world, local_rank):
                                   2: "CTA registry-stamp filter (skewed traffic)"}[scan_check]),
         "estimate_ms_per_slice": sum(per_kind[k]["ms_total"] for k in
                                      ("registry", "sort", "bitmap", "g0", "final")) / args.steps,
-        "estimate_ms_per_slice_note": "kernel time from the end of scan to the report rows "
-                                      "(registry compaction, sort, bitmap+delta, g0, float path)",
+        "estimate_ms_per_slice_note": "sum of the estimate kernels' event times (registry "
+                                      "compaction, sort, bitmap+delta, g0, float path); in the "
+                                      "pipelined step several run beside the scan, so this "
+                                      "overstates their share of ms_per_step",
         "scan_update_mpps": n / ((per_kind["scan"]["ms_total"] + per_kind["sweep"]["ms_total"])
                                  / args.steps / 1e3) / 1e6,
         "reports_per_slice": nh,
@@ -554,6 +556,10 @@ def run_gpu(args, rank, world, local_rank):
                           "DR: every cell slides (pools.py:339-349)" if args.counter == "dr" else
                           "TS: no maintenance (pools.py:399-401)"),
         "kernels": per_kind,
+        "kernels_note": "CUDA-event time per launch on each kernel's own stream; aux-stream "
+                        "kernels (registry compaction, delta apply, float path) overlap the "
+                        "scan or bitmap pass and their times include that overlap; "
+                        "profiles/*launches_summary.txt has the serialised ncu times",
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": _ncu_traffic(dom, args.config),
