@@ -175,12 +175,15 @@ class PeerStep(_SliceStepBase):
         dist.barrier()                   # every window mapped before anyone arrives
         self.touched_total = 0
 
-    def exchange(self, t: int, n_packets: int) -> None:
+    def exchange(self, t: int, n_packets: int, count_touched: bool = False) -> None:
+        """One slice's exchange; count_touched also sums the ranks' touched-host
+        counts (one small read per peer window, so off on the hot path)."""
         if n_packets > self.key_cap:
             raise ValueError(f"{n_packets} packets exceed the peer key_cap {self.key_cap}")
         tot = C.c_uint64()
-        check(lib.vate_peer_exchange(self.handle, t, C.byref(tot)))
-        self.touched_total = tot.value
+        check(lib.vate_peer_exchange(self.handle, t, C.byref(tot) if count_touched else None))
+        if count_touched:
+            self.touched_total = tot.value
 
     def info(self) -> dict:
         wb, nb, ts = C.c_uint64(), C.c_uint64(), C.c_int()
