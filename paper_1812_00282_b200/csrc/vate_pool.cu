@@ -241,9 +241,9 @@ __device__ __forceinline__ void touch_filter_init(unsigned* filt) {
 __device__ __forceinline__ void touch_last(const RegRef& R, unsigned* filt, uint64_t slot,
                                            long long t) {
   const unsigned tag = (unsigned)slot + 1u;
-  volatile unsigned* f = filt + (slot & (kTouchSlots - 1));
-  if (*f == tag) return;
-  *f = tag;
+  // one shared-memory exchange: exactly one thread of a racing group sees a
+  // different previous tag and stamps (race-free under compute-sanitizer)
+  if (atomicExch(filt + (slot & (kTouchSlots - 1)), tag) == tag) return;
   R.table[slot].last = t;
 }
 
