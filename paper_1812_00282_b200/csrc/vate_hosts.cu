@@ -93,16 +93,31 @@ __global__ void __launch_bounds__(256) k_active(const RegEntry* __restrict__ tab
   const bool special_present = (*special & 0xFFFFFFFFull) != 0;
   unsigned long long kmax = 0;
   unsigned mine = 0, flips = 0, now = 0;
-  for (uint64_t i0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < total;
-       i0 += (uint64_t)gridDim.x * blockDim.x * 4) {
+  // each warp takes tiles of 128 consecutive slots, lane l slots l, l+32, l+64,
+  // l+96: every load instruction moves 512 contiguous bytes (entries) or 32
+  // (membership flags), all four entry loads in flight before any is used
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 128; i0 < total;
+       i0 += warps * 128) {
+    RegEntry ev[4];
+    uint8_t mv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint64_t i = i0 + q;
+      const uint64_t i = i0 + lane + 32 * q;
+      if (i < total) {
+        ev[q] = table[i];
+        mv[q] = member[i];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = i0 + lane + 32 * q;
       if (i >= total) break;
-      const RegEntry e = table[i];
+      const RegEntry e = ev[q];
       const bool tk = (i < cap) ? (e.key != kEmptyKey && e.last > cut)
                                 : (special_present && e.last > cut);
-      if ((member[i] != 0) != tk) {
+      if ((mv[q] != 0) != tk) {
         member[i] = tk;
         ++flips;
         if (F.arr) {  // rare in steady traffic: one atomic per flip
