@@ -665,6 +665,50 @@ __device__ __forceinline__ unsigned sweep_word(T* __restrict__ cells, uint64_t i
   return cleared;
 }
 
+// Bits j of [i0, i0+32) that fall in [s, e).
+__device__ __forceinline__ uint32_t range_bits(uint64_t i0, uint64_t s, uint64_t e) {
+  const uint64_t lo = s > i0 ? s - i0 : 0, hi = e > i0 ? umin64(e - i0, 32) : 0;
+  if (lo >= hi) return 0u;
+  const uint32_t below_hi = hi >= 32 ? 0xffffffffu : (1u << hi) - 1u;
+  return below_hi & ~((1u << lo) - 1u);
+}
+
+// The same sweep for a full word of u8/u16 cells, on the pass's register copy:
+// stale cells are rewritten in the registers and only the 16-byte vectors that
+// changed are stored.  (The scalar form re-reads each cell from L2 -- the
+// pass's loads are evict-first -- and its 32 dependent round trips set the
+// kernel's tail on small pools.)
+template <typename T>
+__device__ __forceinline__ unsigned sweep_regs(T* __restrict__ cells, uint4 (&r)[(int)sizeof(T) * 2],
+                                               uint64_t i0, const SweepSpec& SW) {
+  static_assert(sizeof(T) <= 2, "u8/u16 cells");
+  const uint32_t due0 = range_bits(i0, SW.s0, SW.e0), due1 = range_bits(i0, SW.s1, SW.e1);
+  if (!(due0 | due1)) return 0;
+  constexpr int kPer = 4 / (int)sizeof(T), kBits = 8 * (int)sizeof(T);
+  constexpr uint32_t kMask = sizeof(T) == 1 ? 0xFFu : 0xFFFFu;
+  uint32_t* x = reinterpret_cast<uint32_t*>(r);
+  unsigned cleared = 0, changed = 0;
+#pragma unroll
+  for (int q = 0; q < 32 / kPer; ++q) {
+#pragma unroll
+    for (int h = 0; h < kPer; ++h) {
+      const int j = q * kPer + h;
+      const uint32_t v = (x[q] >> (h * kBits)) & kMask;
+      const bool stale = ((due0 >> j) & 1u) ? v <= SW.k
+                         : ((due1 >> j) & 1u) ? ((v >= SW.k && v <= SW.B - 1) || v == 0) : false;
+      if (stale) {
+        x[q] = (x[q] & ~(kMask << (h * kBits))) | (SW.B << (h * kBits));
+        ++cleared;
+        changed |= 1u << (q / 4);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < (int)sizeof(T) * 2; ++v)
+    if ((changed >> v) & 1u) reinterpret_cast<uint4*>(cells + i0)[v] = r[v];
+  return cleared;
+}
+
 template <typename T>
 __device__ __forceinline__ uint32_t word_inactive_bits(const T* __restrict__ cells,
                                                        const uint4 (&r)[(int)sizeof(T) * 2],
@@ -733,8 +777,16 @@ __global__ void __launch_bounds__(kThreads, 6) k_bitmap(T* __restrict__ cells, L
       const uint32_t bits = word_inactive_bits<T>(cells, r[q], i0, cnt, L, bact0, kp);
       bitmap[w] = bits;
       local += __popc(bits);
-      if (SW.cleared && ((i0 < SW.e0 && i0 + cnt > SW.s0) || (i0 < SW.e1 && i0 + cnt > SW.s1)))
-        swept += sweep_word(cells, i0, cnt, SW.s0, SW.e0, SW.s1, SW.e1, SW.k, SW.B);
+      if (SW.cleared && ((i0 < SW.e0 && i0 + cnt > SW.s0) || (i0 < SW.e1 && i0 + cnt > SW.s1))) {
+        if constexpr (sizeof(T) <= 2) {
+          if (cnt == 32)
+            swept += sweep_regs<T>(cells, r[q], i0, SW);
+          else
+            swept += sweep_word(cells, i0, cnt, SW.s0, SW.e0, SW.s1, SW.e1, SW.k, SW.B);
+        } else {
+          swept += sweep_word(cells, i0, cnt, SW.s0, SW.e0, SW.s1, SW.e1, SW.k, SW.B);
+        }
+      }
       if (D.bprev) delta_word(D, ds, bits, w, i0);
     }
   }
