@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) k_cmp_bitmap(const T* __restrict__ cells,
     }
     bitmap[w] = bits;
     local += __popc(bits);
-    if (D.bprev) delta_word(D, ds, bits, w, i0);
+    if (D.bprev) delta_word(D, ds, bits, D.bprev[w], i0);
   }
   if (D.bprev) delta_flush(D, ds);
   local = __reduce_add_sync(0xffffffffu, local);

@@ -185,9 +185,11 @@ __device__ __forceinline__ void delta_stage_init(DeltaStage& ds) {
   }
   __syncthreads();
 }
+// prev: D.bprev[w], loaded by the caller (the bitmap pass issues it with the
+// cell loads so its latency overlaps theirs)
 __device__ __forceinline__ void delta_word(const DeltaOut& D, DeltaStage& ds, uint32_t bits,
-                                           uint64_t w, uint64_t i0) {
-  uint32_t x = bits ^ D.bprev[w];
+                                           uint32_t prev, uint64_t i0) {
+  uint32_t x = bits ^ prev;
   if (!x) return;
   unsigned long long wsum = 0;
   while (x) {

@@ -757,9 +757,11 @@ __global__ void __launch_bounds__(kThreads, 6) k_bitmap(T* __restrict__ cells, L
   for (uint64_t w0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w0 < nwords;
        w0 += kW * stride) {
     uint4 r[kW][NV];
+    uint32_t prev[kW];
 #pragma unroll
     for (int q = 0; q < kW; ++q) {
       const uint64_t w = w0 + q * stride;
+      prev[q] = (D.bprev && w < nwords) ? __ldcs(D.bprev + w) : 0u;
       if (w < nwords && (w + 1) * 32 <= L.size) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
@@ -787,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_bitmap(T* __restrict__ cells, L
           swept += sweep_word(cells, i0, cnt, SW.s0, SW.e0, SW.s1, SW.e1, SW.k, SW.B);
         }
       }
-      if (D.bprev) delta_word(D, ds, bits, w, i0);
+      if (D.bprev) delta_word(D, ds, bits, prev[q], i0);
     }
   }
   if (D.bprev) delta_flush(D, ds);

@@ -1,4 +1,4 @@
-"""Device timeline of the cfg 2 slice step: every launch (CUDA events around
+"""Device timeline of the cfg 2 slice step (TL_C/TL_K/TL_N/TL_HOSTS: another shape): every launch (CUDA events around
 each kernel) and the idle gaps between them, for a few steady-state slices."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -7,17 +7,19 @@ import torch
 import paper_1812_00282_b200 as vb
 from paper_1812_00282_b200._lib import lib, check
 
-cfg = vb.EstimatorConfig(1024, 24, 60)
+C_, K_ = int(os.environ.get("TL_C", 24)), int(os.environ.get("TL_K", 60))
+cfg = vb.EstimatorConfig(1024, C_, K_)
 pool = cfg.build_pool()
 for kv in os.environ.get("TL_OPTS", "").split():
     k_, v_ = kv.split("=")
     pool.set_option(k_, int(v_))
-pipe = vb.Pipeline(pool, cfg, 60)
-n = 5_000_000
+pipe = vb.Pipeline(pool, cfg, K_)
+n = int(os.environ.get("TL_N", 5_000_000))
+HOSTS = int(os.environ.get("TL_HOSTS", 1_000_000))
 NB = 140
 bufs = torch.empty((NB, n, 2), dtype=torch.int32, device="cuda:0")
 for i in range(NB):
-    check(lib.vate_synth_packets(pool.handle, i, n, 1_000_000, 0x0A000000, 0, bufs[i].data_ptr()))
+    check(lib.vate_synth_packets(pool.handle, i, n, HOSTS, 0x0A000000, 0, bufs[i].data_ptr()))
 lagged = os.environ.get("TL_LAGGED", "1") == "1"
 step = pipe.step_lagged if lagged else pipe.step_fast
 for t in range(130):
