@@ -233,17 +233,22 @@ struct Publish {
 };
 __device__ __forceinline__ void publish_last_block(const Publish& P) {
   if (!P.dst) return;
+  __shared__ unsigned s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned ticket = atomicAdd(P.done, 1u);
-    if (ticket == gridDim.x - 1) {
-      __threadfence();
-      for (int i = 0; i < 32; ++i)
-        if ((P.mask >> i) & 1u) P.dst[i] = *((volatile const unsigned long long*)P.src + i);
-      __threadfence_system();
-      *P.done = 0u;
-    }
+    s_last = atomicAdd(P.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  // the last CTA's first warp copies the counters, one lane each (their L2
+  // round trips overlap instead of chaining)
+  if (s_last && threadIdx.x < 32) {
+    __threadfence();
+    const int i = threadIdx.x;
+    if ((P.mask >> i) & 1u) P.dst[i] = *((volatile const unsigned long long*)P.src + i);
+    __threadfence_system();
+    __syncwarp();
+    if (i == 0) *P.done = 0u;
   }
 }
 
