@@ -479,6 +479,8 @@ void timing_begin(vate_pool* p, int kind, cudaEvent_t* a);
 void timing_end(vate_pool* p, int kind, cudaEvent_t a);
 int collect_timing(vate_pool* p);
 uint32_t grid_for(uint64_t work, uint32_t per_block, uint32_t cap_blocks = 148u * 64u);
+// A/B knob: the CTA cap named by env var `name` if set, else dflt.
+uint32_t xp_cap(const char* name, uint32_t dflt);
 
 // counters in vate_pool::d_ctr
 enum Ctr { C_P = 0, C_CLEARED = 1, C_NSEL = 2, C_ERR = 3, C_DCNT = 4, C_DWORK = 5, C_MISS = 6,

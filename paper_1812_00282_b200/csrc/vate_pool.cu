@@ -166,6 +166,24 @@ int collect_timing(vate_pool* p) {
   return VATE_OK;
 }
 
+uint32_t xp_cap(const char* name, uint32_t dflt) {
+  // read once per call site (names are literals: the pointer is the key)
+  static thread_local const char* names[8];
+  static thread_local int vals[8];
+  for (int i = 0; i < 8; ++i) {
+    if (names[i] == name) return vals[i] > 0 ? (uint32_t)vals[i] : dflt;
+    if (!names[i]) {
+      const char* e = getenv(name);
+      names[i] = name;
+      vals[i] = e ? atoi(e) : 0;
+      return vals[i] > 0 ? (uint32_t)vals[i] : dflt;
+    }
+  }
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : 0;
+  return v > 0 ? (uint32_t)v : dflt;
+}
+
 uint32_t grid_for(uint64_t work, uint32_t per_block, uint32_t cap_blocks) {
   uint64_t g = (work + per_block - 1) / per_block;
   if (g < 1) g = 1;
