@@ -1044,10 +1044,10 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta, bool fused_advance)
   if (kw == 0) kw = 1;  // measured best at c = 24, 26, 28 (scripts/micro_bitmap.py)
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
-    // grid cap: an L2-resident pool (<= 32 MiB) gets 4 CTAs per SM, looping,
-    // which leaves SM slots to the registry compaction and delta apply running
-    // beside the pass (cfg 2: 0.141 -> 0.137 ms per slice); a larger, HBM-bound
-    // pool keeps one word per thread.  VATE_XP_BITMAP_CAP overrides (A/B runs,
+    // grid cap: a pool of <= 64 MiB gets one wave (6 CTAs per SM, the launch
+    // bound), looping, which leaves SM slots to the registry compaction and
+    // delta apply running beside the pass (cfg 2: 0.141 -> 0.134 ms per slice,
+    // cfg 3: 0.356 -> 0.348); a larger, HBM-bound pool keeps one word per thread.  VATE_XP_BITMAP_CAP overrides (A/B runs,
     // scripts/xp_bitmap_grid.sh).
     static const int cap_env = [] {
       const char* e = getenv("VATE_XP_BITMAP_CAP");
@@ -1055,7 +1055,7 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta, bool fused_advance)
     }();
     const uint64_t pool_bytes = p->L.size * (uint64_t)p->cell_bytes;
     const uint32_t cap = cap_env > 0 ? (uint32_t)cap_env
-                         : (pool_bytes <= (32ull << 20) ? 148u * 4u : 148u * 32u);
+                         : (pool_bytes <= (64ull << 20) ? 148u * 6u : 148u * 32u);
     const uint32_t grid = grid_for((nwords + kw - 1) / kw, kThreads, cap);
     // measured (scripts/micro_bitmap.py): evict-first reads are faster even for
     // an L2-resident pool, so the normal-priority form stays off

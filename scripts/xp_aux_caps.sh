@@ -1,5 +1,5 @@
-# aux-stream kernel CTA caps A/B: k_active (registry compaction)
-V="--steps 60 --warmup 5;--config cfg3 --steps 20 --warmup 3;--config cfg4 --steps 20 --warmup 3;--config cfg1 --steps 100 --warmup 5"
-for X in "VATE_XP_ACTIVE_CAP=148" "VATE_XP_ACTIVE_CAP=296" "VATE_XP_ACTIVE_CAP=444" "VATE_XP_ACTIVE_CAP=1184"; do
-  echo "== $X"; env $X VARIANTS="$V" bash scripts/bench_variants.sh | cut -c1-120
+# aux-stream / bitmap CTA caps A/B on top of the defaults (cfg 2, cfg 3)
+V="--steps 60 --warmup 5;--config cfg3 --steps 20 --warmup 3"
+for X in "VATE_XP_NONE=1" "VATE_XP_BITMAP_CAP=444" "VATE_XP_BITMAP_CAP=888" "VATE_XP_INC_CAP=1184" "VATE_XP_INC_CAP=3552" "VATE_XP_FINAL_CAP=1184" "VATE_XP_NONE=1"; do
+  echo "== $X"; env $X VARIANTS="$V" bash scripts/bench_variants.sh | cut -c1-110
 done
