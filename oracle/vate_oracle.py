@@ -48,6 +48,18 @@ class OracleConfigError(ValueError):
     """Mirrors ``ConfigError`` (errors.py:9-10) for the oracle's own checks."""
 
 
+def _unique(x) -> np.ndarray:
+    """Sorted distinct values (np.unique's result; sort-based, which is many times
+    faster than numpy 2.3's np.unique on large integer arrays)."""
+    s = np.sort(np.asarray(x))
+    if len(s) < 2:
+        return s
+    keep = np.empty(len(s), dtype=bool)
+    keep[0] = True
+    np.not_equal(s[1:], s[:-1], out=keep[1:])
+    return s[keep]
+
+
 # --------------------------------------------------------------------------
 # hashing (hashing.py:25-67)
 # --------------------------------------------------------------------------
@@ -184,6 +196,19 @@ class OraclePool:
         self.starts = block_starts(c, k, partition)
         self.cells = np.full(self.size, self.sentinel, dtype=np.uint32)
         self.bact0 = 0
+        self.hist = None
+
+    def track_histogram(self) -> "OraclePool":
+        """Keep the per-block value histogram hist[block, value] (pools.py:98-100)
+        so that count_inactive costs O(2k * k') per call instead of a pass over
+        the pool (pools.py:195-204).  Updated by set_cells (pools.py:167-174, with
+        bincount instead of ufunc.at) and by advance (pools.py:246-248)."""
+        nb = self.nblocks
+        self.hist = np.zeros((nb, nb + 1), dtype=np.int64)
+        for b in range(nb):
+            lo, hi = self.block_range(b)
+            self.hist[b] = np.bincount(self.cells[lo:hi], minlength=nb + 1)
+        return self
 
     # layout --------------------------------------------------------------
     def block_of(self, idx) -> np.ndarray:
@@ -210,6 +235,17 @@ class OraclePool:
         i = np.asarray(idx).astype(np.int64)
         if i.size and (i.min() < 0 or i.max() >= self.size):
             raise ValueError("cell index out of range")         # pools.py:106-107
+        if self.hist is not None:                              # pools.py:167-174
+            i = _unique(i)
+            blocks = self.block_of(i)
+            new = self.clock(blocks)
+            rows = blocks * (self.nblocks + 1)
+            nbins = self.nblocks * (self.nblocks + 1)
+            flat = self.hist.reshape(-1)
+            flat -= np.bincount(rows + self.cells[i], minlength=nbins)
+            flat += np.bincount(rows + new, minlength=nbins)
+            self.cells[i] = new.astype(np.uint32)
+            return
         self.cells[i] = self.clock(self.block_of(i)).astype(np.uint32)
 
     # queries ----------------------------------------------------------------
@@ -241,8 +277,14 @@ class OraclePool:
         return out
 
     def count_inactive(self, k_prime: int) -> int:
-        """Pool-wide inactive count P (pools.py:195-210), by a full pass."""
+        """Pool-wide inactive count P (pools.py:195-210): from the histogram when
+        tracked (pools.py:198-204), else by a full pass."""
         self._check_width(k_prime)
+        if self.hist is not None:
+            acts = self.clock(np.arange(self.nblocks))
+            recent = (acts[:, None] - np.arange(k_prime)[None, :]) % self.nblocks
+            rows = np.arange(self.nblocks)[:, None]
+            return self.size - int(self.hist[rows, recent].sum())
         total = 0
         for b, act in enumerate(self.clock(np.arange(self.nblocks)).tolist()):
             lo, hi = self.block_range(b)
@@ -270,6 +312,8 @@ class OraclePool:
             cleared += int(stale.sum())
             visited += hi - lo
             v[stale] = self.sentinel
+            if self.hist is not None:                          # pools.py:246-248
+                self.hist[bi] = np.bincount(v, minlength=nb + 1)
         return due, visited, cleared
 
     # snapshots --------------------------------------------------------------
@@ -512,7 +556,7 @@ class OracleHosts:
         self.last: dict = {}
 
     def update(self, aips, t: int) -> None:
-        for a in np.unique(np.asarray(aips).astype(U64)).tolist():
+        for a in _unique(np.asarray(aips).astype(U64)).tolist():
             self.last[a] = t
 
     def active(self, t: int, k_prime: int) -> np.ndarray:
@@ -523,6 +567,38 @@ class OracleHosts:
         cut = t - self.k
         for a in [a for a, s in self.last.items() if s <= cut]:
             del self.last[a]
+
+
+class OracleHostsVec:
+    """OracleHosts (pipeline.py:43-64) as two sorted arrays (keys, last seen):
+    the same semantics at a million hosts without a per-slice Python sort."""
+
+    def __init__(self, k: int):
+        self.k = k
+        self.keys = np.empty(0, dtype=U64)
+        self.last = np.empty(0, dtype=np.int64)
+
+    def update(self, aips, t: int) -> None:
+        u = _unique(np.asarray(aips).astype(U64))
+        pos = np.searchsorted(self.keys, u)
+        hit = pos < len(self.keys)
+        hit[hit] = self.keys[pos[hit]] == u[hit]
+        self.last[pos[hit]] = t
+        new = u[~hit]
+        if len(new):
+            at = np.searchsorted(self.keys, new)
+            self.keys = np.insert(self.keys, at, new)
+            self.last = np.insert(self.last, at, t)
+
+    def __len__(self):
+        return len(self.keys)
+
+    def active(self, t: int, k_prime: int) -> np.ndarray:
+        return self.keys[self.last > t - k_prime]                # pipeline.py:54-58
+
+    def prune(self, t: int) -> None:
+        keep = self.last > t - self.k                            # pipeline.py:59-64
+        self.keys, self.last = self.keys[keep], self.last[keep]
 
 
 @dataclass
