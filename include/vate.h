@@ -244,6 +244,12 @@ int vate_estimate_wait(vate_pool* p);
 int vate_reports_device(vate_pool* p, uint64_t** host, double** est, double** zv,
                         uint8_t** sat);
 
+/* Synchronous copy of rows [first, first+n) of the last finished report set
+ * (the rows a caller's too-small output arrays did not receive: the async
+ * forms copy at most `cap` rows and report the full count in *nkept). */
+int vate_reports_copy(vate_pool* p, uint64_t first, uint64_t n, uint64_t* host, double* est,
+                      double* zv, uint8_t* sat);
+
 /* ---- one whole slice (pipeline.py:142-160) in one call, streaming form ---
  * scan (pairs: host/device pointer, or the staging slot when where ==
  * VATE_STAGED) -> estimate begin -> the slice's single host round trip ->

@@ -89,6 +89,7 @@ _SIGS = {
     "vate_estimate_finish_async": ([_p, _u64, _u64, _dbl, _dbl, _p, _p, _p, _p, _u64, _pu64], _int),
     "vate_estimate_wait": ([_p], _int),
     "vate_reports_device": ([_p, _p, _p, _p, _p], _int),
+    "vate_reports_copy": ([_p, _u64, _u64, _p, _p, _p, _p], _int),
     "vate_slice_step": ([_p, _p, _u64, _u64, _u64, _p, _u64, _int, _i64, _int, _dbl, _p,
                          _p, _p, _p, _p, _u64, C.POINTER(StepResult)], _int),
     "vate_slice_step_lagged": ([_p, _p, _u64, _u64, _u64, _p, _u64, _int, _i64, _int, _dbl, _p,

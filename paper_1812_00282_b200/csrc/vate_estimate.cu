@@ -1001,6 +1001,25 @@ int vate_reports_device(vate_pool* p, uint64_t** host, double** est, double** zv
   return VATE_OK;
 }
 
+int vate_reports_copy(vate_pool* p, uint64_t first, uint64_t n, uint64_t* host, double* est,
+                      double* zv, uint8_t* sat) {
+  int rc = enter(p);
+  if (rc) return rc;
+  const int slot = p->out_slot ^ 1;  // the set the last finish wrote
+  const uint64_t avail = p->host_out[slot].bytes / 8;
+  if (first + n > avail)
+    return set_error(VATE_EVALUE, "report rows [" + std::to_string(first) + ", " +
+                                      std::to_string(first + n) + ") beyond the last slice's " +
+                                      std::to_string(avail) + "-row buffer");
+  VATE_CUDA(cudaEventSynchronize(p->ev_fin[slot]));
+  if (n == 0) return VATE_OK;
+  if (host) VATE_CUDA(cudaMemcpy(host, p->host_out[slot].as<uint64_t>() + first, n * 8, cudaMemcpyDeviceToHost));
+  if (est) VATE_CUDA(cudaMemcpy(est, p->est_out[slot].as<double>() + first, n * 8, cudaMemcpyDeviceToHost));
+  if (zv) VATE_CUDA(cudaMemcpy(zv, p->zv_out[slot].as<double>() + first, n * 8, cudaMemcpyDeviceToHost));
+  if (sat) VATE_CUDA(cudaMemcpy(sat, p->sat_out[slot].as<uint8_t>() + first, n, cudaMemcpyDeviceToHost));
+  return VATE_OK;
+}
+
 int vate_estimate_wait(vate_pool* p) {
   int rc = enter(p);
   if (rc) return rc;

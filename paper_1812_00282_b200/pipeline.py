@@ -194,8 +194,21 @@ class Pipeline:
                      ptr(est), ptr(zv), ptr(sat), len(host), C.byref(kept)))
         m = kept.value
         self.last_pool_inactive = p.value
+        host, est, zv, sat = self._full_rows(out, m, wait)
         return HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool), z_p,
                            t - self.k_prime + 1, self.k_prime)
+
+    def _full_rows(self, out, m: int, wait: bool = False):
+        """``out`` if it holds all m rows; otherwise fresh arrays with every row
+        (the async copy filled only len(out[0]) of them; the rest come from the
+        device synchronously -- no row is ever dropped)."""
+        host = out[0]
+        if len(host) >= m:
+            return out
+        full = (np.empty(m, np.uint64), np.empty(m, np.float64), np.empty(m, np.float64),
+                np.empty(m, np.uint8))
+        check(lib.vate_reports_copy(self.pool.handle, 0, m, *(ptr(a) for a in full)))
+        return full
 
     def _collect(self, t: int) -> MaintenanceReport:
         """Finish an advance enqueued by estimate_soa(advance=True); prune every k."""
@@ -291,6 +304,7 @@ class Pipeline:
         m = res.nkept
         if out is None:
             return m
+        host, est, zv, sat = self._full_rows(out, m)
         return HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool),
                            res.pool_inactive / float(self.pool.size), t - self.k_prime + 1,
                            self.k_prime)
@@ -353,6 +367,7 @@ class Pipeline:
         m = res.nkept
         if out is None:
             return tp, m
+        host, est, zv, sat = self._full_rows(out, m)
         return tp, HostReports(host[:m], est[:m], zv[:m], sat[:m].view(bool),
                                res.pool_inactive / float(self.pool.size), tp - self.k_prime + 1,
                                self.k_prime)

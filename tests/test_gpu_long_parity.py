@@ -45,7 +45,7 @@ def _run_long(c, k, hosts, pkts, slices, rows_at, snaps_at, seed=0, zipf=False):
     pipe = vb.Pipeline(pool, cfg, k, floor=0.0)
     opool = vo.OraclePool(c, k).track_histogram()
     ohosts = vo.OracleHostsVec(k)
-    cap = hosts + 16
+    cap = hosts + 16   # cfg 3 (1M ranks + 64 spreaders) overflows it: rows come back in full anyway
     outs = [(torch.empty(cap, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64),
              torch.empty(cap, dtype=torch.float64, pin_memory=True).numpy(),
              torch.empty(cap, dtype=torch.float64, pin_memory=True).numpy(),
