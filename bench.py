@@ -292,11 +292,11 @@ def run_gpu(args, rank, world, local_rank):
     pool.set_option("incremental", 1 if args.incremental == "on" else 0)
     # scan form: auto (the library picks the registry-stamp filter for skewed
     # traffic) unless forced
-    scan_check = args.scan_check if args.scan_check is not None else w.get("scan_check", -1)
-    if scan_check != -1:
-        pool.set_option("scan_check", scan_check)
-    if args.l2_persist:
-        pool.set_option("l2_persist", args.l2_persist)
+    scan_filter = args.scan_filter
+    if scan_filter != -1:
+        pool.set_option("scan_filter", scan_filter)
+    if args.deferred != -1:
+        pool.set_option("deferred", args.deferred)
     pool.set_option("concurrent", args.concurrent)
     for kv in args.opt:                       # experiments: --opt spin_wait=0 ...
         name, val = kv.split("=")
@@ -338,7 +338,7 @@ def run_gpu(args, rank, world, local_rank):
         pool.synchronize()
         hslices[i].copy_(scratch)
     pool.synchronize()
-    nh_cap = w["hosts"] + 16
+    nh_cap = w["hosts"] + 1024   # (+ cfg 3's 64 super-spreaders)
 
     def pinned_outs():
         return (torch.empty(nh_cap, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64),
@@ -534,10 +534,9 @@ def run_gpu(args, rank, world, local_rank):
         "dtype": _dtype(w),
         "data": "synthetic (csrc k_synth == oracle.synthetic_slice)",
         "config": dict(_config(w, world), counter=args.counter,
-                       scan_form={-1: "auto (registry-stamp filter at >= 8 packets per host)",
-                                  0: "plain stores",
-                                  1: "heavy-hitter (load-before-store, CTA stamp filter)",
-                                  2: "CTA registry-stamp filter (skewed traffic)"}[scan_check]),
+                       scan_filter={-1: "auto (registry-stamp filter at >= 8 packets per host)",
+                                    0: "off", 1: "on"}[scan_filter],
+                       deferred_scatter=bool(pool.deferred)),
         "estimate_ms_per_slice": sum(per_kind[k]["ms_total"] for k in
                                      ("registry", "sort", "bitmap", "g0", "final")) / args.steps,
         "estimate_ms_per_slice_note": "sum of the estimate kernels' event times (registry "
@@ -621,10 +620,11 @@ def main():
     ap.add_argument("--impl", choices=("vate", "reference"), default="vate")
     ap.add_argument("--g0-kernel", choices=("auto", "gather", "smem"), default="auto",
                     help="g0 gather variant (VATE_OPT_G0)")
-    ap.add_argument("--scan-check", type=int, choices=(-1, 0, 1, 2), default=None,
-                    help="load-before-store scan (VATE_OPT_SCAN_CHECK)")
-    ap.add_argument("--l2-persist", type=int, choices=(0, 1, 2), default=0,
-                    help="L2 persisting window: 1 host registry, 2 cells (VATE_OPT_L2_PERSIST)")
+    ap.add_argument("--scan-filter", type=int, choices=(-1, 0, 1), default=-1,
+                    help="per-CTA registry-stamp filter in the scan (VATE_OPT_SCAN_FILTER)")
+    ap.add_argument("--deferred", type=int, choices=(-1, 0, 1), default=-1,
+                    help="deferred scatter: scans mark an L2-resident pending-set bitmap and "
+                         "the pool pass stores the clocks (VATE_OPT_DEFERRED; auto: cells > 64 MiB)")
     ap.add_argument("--opt", action="append", default=[],
                     help="extra pool option name=value (AtPool.set_option), for A/B runs")
     ap.add_argument("--lagged", type=int, choices=(0, 1), default=1,

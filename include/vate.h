@@ -66,6 +66,9 @@ int vate_pool_kind(const vate_pool* p, int* kind, uint64_t* slice_index);
 int vate_pool_destroy(vate_pool* p);
 /* bact0 (pools.py:96), cell storage bytes (1, 2 or 4), the stream (cudaStream_t) */
 int vate_pool_info(const vate_pool* p, int32_t* bact0, int32_t* cell_bytes, void** stream);
+/* HBM the pool's cells occupy (unpacked) plus a deferred pool's pending-set
+ * bitmap; the reference's packed accounting (pools.py:257-259) is host-side. */
+int vate_pool_device_bytes(const vate_pool* p, int64_t* bytes);
 int vate_pool_sync(vate_pool* p);
 /* cumulative count of kernels this pool (and its registries) launched */
 int vate_pool_launches(const vate_pool* p, uint64_t* n);
@@ -86,22 +89,14 @@ int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
  * 2 shared-memory / cluster-DSMEM kernel (c <= 24 only).  VATE_OPT_INCREMENTAL
  * = 1 (default) lets the fused estimate update g0 through an inverse index
  * (exact), 0 recomputes every g0 by a full gather. */
-enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 2,
-                   VATE_OPT_SCAN_CHECK = 3, VATE_OPT_L2_PERSIST = 4, VATE_OPT_BITMAP_KW = 5,
-                   VATE_OPT_CONCURRENT = 6, VATE_OPT_INC_SORT = 7, VATE_OPT_SPIN_WAIT = 8,
-                   VATE_OPT_FUSE_SWEEP = 9 };
-/* VATE_OPT_SCAN_V: packed-scan form (1 default: one uint4 = two packets per
- * thread; 0 one packet; 2 / 4 uint4; 8 TMA-fed persistent).  VATE_OPT_SCAN_CHECK:
- * -1 auto (default: the stamp filter when the last compacted slice saw >= 8
- * packets per distinct host, else plain), 0 plain stores, 1 load-before-store
- * cells + a per-CTA filter of registry stamps, 2 the stamp filter alone.  All
- * forms leave identical state. */
+enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_FILTER = 2,
+                   VATE_OPT_CONCURRENT = 3, VATE_OPT_INC_SORT = 4, VATE_OPT_FUSE_SWEEP = 5,
+                   VATE_OPT_DEFERRED = 6 };
+/* VATE_OPT_SCAN_FILTER: -1 auto (default: the per-CTA registry-stamp filter
+ * when the last compacted slice saw >= 8 packets per distinct host, else
+ * plain stamps), 0 off, 1 on.  Both forms leave identical state. */
 /* VATE_OPT_FUSE_SWEEP (default 1): in the slice step the advance's two-block
  * sweep runs inside the bitmap pass (after each word's bits are taken). */
-/* VATE_OPT_SPIN_WAIT (default 0): the slice's host round trip spins on a flag
- * a one-thread kernel writes to mapped pinned memory (bounded; falls back to
- * cudaStreamSynchronize).  Measured slower than the driver's wait on B200
- * (scripts/timeline.py), kept for the record. */
 /* VATE_OPT_INC_SORT (default 1): when few hosts join or leave the window, the
  * sorted active set (SlidingHostSet.active, pipeline.py:54-58) is updated by
  * merging the sorted arrivals and removing the departures instead of a full
@@ -109,8 +104,10 @@ enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_V = 
 /* VATE_OPT_CONCURRENT (default 1): the estimate's registry compaction runs
  * beside the bitmap pass, and the slice advance beside g0 + float path, on a
  * second stream of the pool (fork/join by events; results unchanged). */
-/* VATE_OPT_L2_PERSIST: 0 off (default), 1 an L2 persisting access-policy window
- * over the host registry (the scan's random probe target), 2 over the cells. */
+/* VATE_OPT_DEFERRED: -1 auto (default: on for AT pools whose cells exceed
+ * 64 MiB), 0 off, 1 on.  On: scans and set_many set one bit per cell in an
+ * L2-resident pending-set bitmap; the next pool pass stores the block clocks
+ * (identical state). */
 int vate_pool_set_option(vate_pool* p, int option, int64_t value);
 /* incremental-estimate counters: [rebuilds, delta slices, refresh slices, full
  * slices, last delta cells, last delta work, identity slices, hosts indexed,
@@ -178,6 +175,13 @@ int vate_advance(vate_pool* p, int32_t blocks[2], uint64_t* maintained, uint64_t
 int vate_advance_async(vate_pool* p);
 int vate_advance_result(vate_pool* p, int32_t blocks[2], uint64_t* maintained,
                         uint64_t* cleared);
+/* PackedArray write API on the device cells (bitpack.py:57-78, :97-140):
+ * put: cells[idx[i]] = values[i] & (2^width - 1) (set / set_one / set_range;
+ * duplicate indices must carry equal values); fill: every cell = value
+ * (ValueError if value exceeds the width).  Any AT/DR/TS pool. */
+int vate_put_cells(vate_pool* p, const uint64_t* idx, const uint64_t* values, uint64_t n,
+                   int where);
+int vate_fill_cells(vate_pool* p, uint64_t value);
 
 /* ---- queries ----------------------------------------------------------- */
 /* AtPool.count_inactive (pools.py:195-210); 1 <= k_prime <= k. */

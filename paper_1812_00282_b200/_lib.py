@@ -53,6 +53,9 @@ _SIGS = {
     "vate_pool_create_kind": ([C.POINTER(_p), _int, _int, _int, _int, _int], _int),
     "vate_pool_kind": ([_p, C.POINTER(_int), _pu64], _int),
     "vate_get_cells64": ([_p, _p, _u64, _p, _int], _int),
+    "vate_put_cells": ([_p, _p, _p, _u64, _int], _int),
+    "vate_fill_cells": ([_p, _u64], _int),
+    "vate_pool_device_bytes": ([_p, _p], _int),
     "vate_pool_destroy": ([_p], _int),
     "vate_pool_info": ([_p, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_p)], _int),
     "vate_pool_sync": ([_p], _int),

@@ -107,6 +107,23 @@ __global__ void k_get64(const T* __restrict__ cells, uint64_t size, const uint64
   }
 }
 
+// PackedArray.set / set_one / set_range (bitpack.py:97-140): cells[idx] =
+// value & mask; duplicate indices carry equal values (the reference's contract).
+template <typename T>
+__global__ void k_put64(T* __restrict__ cells, uint64_t size, const uint64_t* __restrict__ idx,
+                        const unsigned long long* __restrict__ vals, uint64_t n,
+                        unsigned long long mask, unsigned long long* err) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t c = idx[i];
+    if (c >= size) {
+      *err = 1;
+      continue;
+    }
+    cells[c] = (T)(vals[i] & mask);
+  }
+}
+
 // DrPool.advance_slice (pools.py:339-349): every recorder slides by one,
 // saturating at k; a streaming read-modify-write of the whole pool, 16 bytes
 // per thread per step (HBM-bound: 2 * cell_bytes * 2^c per slice).
@@ -228,11 +245,72 @@ int cmp_inactive_mask(vate_pool* p, const uint64_t* d_idx, uint64_t n, int k_pri
   });
 }
 
+template <typename F>
+static int with_any_cell(vate_pool* p, F f) {
+  if (p->kind == VATE_TS) return f(uint64_t{});
+  if (p->cell_bytes == 1) return f(uint8_t{});
+  if (p->cell_bytes == 2) return f(uint16_t{});
+  return f(uint32_t{});
+}
+
+static unsigned long long width_mask(const vate_pool* p) {
+  return p->width >= 64 ? ~0ull : ((1ull << p->width) - 1);
+}
+
 }  // namespace vate
 
 using namespace vate;
 
 extern "C" {
+
+int vate_put_cells(vate_pool* p, const uint64_t* idx, const uint64_t* values, uint64_t n,
+                   int where) {
+  int rc = enter(p);
+  if (rc || n == 0) return rc;
+  if (where == VATE_HOST) {
+    for (uint64_t i = 0; i < n; ++i)
+      if (idx[i] >= p->L.size)
+        return set_error(VATE_EVALUE, "cell index " + std::to_string(idx[i]) + " outside [0, " +
+                                          std::to_string(p->L.size) + ")");
+  }
+  const void *d_idx, *d_val;
+  rc = stage_in(p, p->in_a, idx, n * 8, where, &d_idx);
+  if (rc) return rc;
+  rc = stage_in(p, p->in_b, values, n * 8, where, &d_val);
+  if (rc) return rc;
+  rc = flush_pending(p);  // an older mark must not overwrite the value
+  if (rc) return rc;
+  rc = with_any_cell(p, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(n, kThreads), kThreads, 0, k_put64<T>, (T*)p->cells,
+                p->L.size, (const uint64_t*)d_idx, (const unsigned long long*)d_val, n,
+                width_mask(p), p->d_ctr + C_ERR);
+    return VATE_OK;
+  });
+  if (rc) return rc;
+  return sync_small(p);
+}
+
+int vate_fill_cells(vate_pool* p, uint64_t value) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (p->width < 64 && (value >> p->width))  // PackedArray.fill (bitpack.py:57-60)
+    return set_error(VATE_EVALUE, "value " + std::to_string(value) + " exceeds " +
+                                      std::to_string(p->width) + " bits");
+  if (p->pend_dirty) {  // every cell is overwritten: earlier marks are void
+    VATE_CUDA(cudaMemsetAsync(p->pend.ptr, 0, p->pend.bytes, p->stream));
+    p->pend_dirty = false;
+  }
+  const uint64_t S = p->L.size;
+  rc = with_any_cell(p, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(S, kThreads), kThreads, 0, k_cmp_fill<T>, (T*)p->cells,
+                S, (T)value);
+    return VATE_OK;
+  });
+  if (rc) return rc;
+  return sync_small(p);
+}
 
 int vate_get_cells64(vate_pool* p, const uint64_t* idx, uint64_t n, uint64_t* out, int where) {
   int rc = enter(p);
@@ -241,6 +319,8 @@ int vate_get_cells64(vate_pool* p, const uint64_t* idx, uint64_t n, uint64_t* ou
   rc = stage_in(p, p->in_a, idx, n * 8, where, &d_idx);
   if (rc) return rc;
   rc = p->out_buf.ensure(n * 8);
+  if (rc) return rc;
+  rc = flush_pending(p);
   if (rc) return rc;
   auto launch = [&](auto tag) -> int {
     using T = decltype(tag);

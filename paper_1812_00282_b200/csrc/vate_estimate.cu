@@ -435,7 +435,7 @@ static int run_float_path(vate_pool* p, const uint64_t* hosts_dev, const int32_t
                 tile_off, p->host_out[slot].as<uint64_t>(), p->est_out[slot].as<double>(),
                 p->zv_out[slot].as<double>(), p->sat_out[slot].as<uint8_t>());
   else
-    VATE_LAUNCH(p, VATE_K_FINAL, grid_for(n, 256, xp_cap("VATE_XP_FINAL_CAP", 148u * 16u)), 256, 0, k_final_all, hosts_dev,
+    VATE_LAUNCH(p, VATE_K_FINAL, grid_for(n, 256, p->cap_final), 256, 0, k_final_all, hosts_dev,
                 g0_dev, n, F, p->host_out[slot].as<uint64_t>(), p->est_out[slot].as<double>(),
                 p->zv_out[slot].as<double>(), p->sat_out[slot].as<uint8_t>());
   if (F.floor > 0.0) {

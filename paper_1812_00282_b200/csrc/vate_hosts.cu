@@ -516,7 +516,7 @@ int hosts_active_launch(vate_hosts* h, int64_t t, int k_prime) {
   F.n_dep = h->d_count + H_DEP;
   // 3 CTAs per SM, looping: the compaction runs beside the bitmap pass and
   // leaves it SM slots (scripts/xp_aux_caps.sh: cfg 2 0.137 -> 0.134 ms/slice)
-  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for((h->cap + 4) / 4, 256, xp_cap("VATE_XP_ACTIVE_CAP", 148u * 3u)), 256, 0, k_active,
+  VATE_LAUNCH(p, VATE_K_REGISTRY, grid_for((h->cap + 4) / 4, 256, p->cap_active), 256, 0, k_active,
               h->table.as<const RegEntry>(), h->cap, h->d_count + H_SPECIAL,
               (long long)(t - k_prime), h->member.as<uint8_t>(), h->d_count + H_NOUT,
               h->d_count + H_MAXKEY, h->d_count + H_CHANGES, F,

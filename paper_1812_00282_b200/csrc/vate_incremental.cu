@@ -459,7 +459,7 @@ int inc_apply_early(vate_pool* p, const unsigned long long* nhosts_dev, uint64_t
   std::swap(p->stream, p->aux_stream);
   cudaEvent_t ta = nullptr;
   timing_begin(p, VATE_K_G0, &ta);
-  k_inc_apply<<<xp_cap("VATE_XP_INC_CAP", 148u * 16u), kThreads, 0, p->stream>>>(
+  k_inc_apply<<<p->cap_inc, kThreads, 0, p->stream>>>(
       I.dlist.as<const unsigned long long>(), p->d_ctr + C_DCNT, I.dlist_cap,
       I.off.as<const uint32_t>(), I.ent.as<const uint32_t>(), I.g0x.as<int32_t>(),
       ApplyGuard{p->d_ctr + C_DWORK, nhosts_dev, g});

@@ -149,6 +149,7 @@ __device__ __forceinline__ void for_word_clocks(uint64_t i0, uint32_t cnt, const
 struct AtRule {
   Layout L;
   uint32_t bact0;
+  static constexpr bool kMark = false;
   template <typename T>
   __device__ __forceinline__ T value(uint64_t cell) const {
     return (T)clock_of(bact0, block_of(cell, L), L.B);
@@ -156,9 +157,27 @@ struct AtRule {
 };
 struct ConstRule {
   unsigned long long v;  // DrPool: 0 (pools.py:314-315); TsPool: the slice index (:363-364)
+  static constexpr bool kMark = false;
   template <typename T>
   __device__ __forceinline__ T value(uint64_t) const { return (T)v; }
 };
+// A deferred AT pool (cells beyond L2): the write is one bit in the
+// L2-resident pending-set bitmap; the next pool pass (k_bitmap, or
+// flush_pending) stores the block clock into every marked cell.  Same result:
+// nothing reads or re-clocks a cell between the two (flush_pending runs
+// before any other cell access and before every advance).
+struct MarkRule {
+  uint32_t* pend;
+  static constexpr bool kMark = true;
+};
+
+template <typename T, typename Rule>
+__device__ __forceinline__ void store_cell(T* __restrict__ cells, uint64_t c, const Rule& rule) {
+  if constexpr (Rule::kMark)
+    atomicOr(rule.pend + (c >> 5), 1u << (c & 31));  // result unused: one RED
+  else
+    cells[c] = rule.template value<T>(c);
+}
 
 // The incremental-g0 delta of a bitmap pass (vate_incremental.cu): with
 // `bprev` set, every word's bits are XORed with the previous estimate's bitmap
@@ -343,6 +362,16 @@ struct vate_pool {
   vate::Layout L{};
   uint32_t bact0 = 0;
   void* cells = nullptr;
+  // deferred scatter (AT pools whose cells exceed L2): the
+  // pending-set bitmap, one bit per cell, L2-resident; set by scans and
+  // set_many, applied and cleared by the next pool pass
+  vate::DevBuf pend;
+  bool deferred = false;     // scans mark pend instead of storing into cells
+  bool pend_dirty = false;   // pend may hold marks
+  int opt_deferred = -1;     // -1 auto (cells > kDeferBytes), 0 off, 1 on
+  // grid caps of the kernels that share the SMs in the slice step, fixed at
+  // pool creation from its shape (co-scheduling)
+  uint32_t cap_bitmap = 0, cap_active = 0, cap_inc = 0, cap_final = 0;
 
   vate::DevBuf bitmap;      // (S+31)/32 words
   vate::DevBuf in_a, in_b;  // staging for host inputs
@@ -379,11 +408,8 @@ struct vate_pool {
   // options
   int opt_g0 = 0;
   int opt_inc = 1;            // incremental g0 through the inverse index
-  int opt_scan_check = -1;   // packed scan form: -1 auto, 0 plain, 1 check + filter, 2 filter
+  int opt_scan_check = -1;   // registry-stamp filter: -1 auto, 0 off, 1 on
   int scan_form_used = 0;     // the form the last packed scan ran (auto resolved)
-  int opt_scan_v = 1;         // packed scan form: 1 (default), 0, 2, 4 per-thread unroll; 8 TMA-fed persistent
-  int opt_l2 = 0;             // L2 persisting window: 0 off, 1 registry, 2 cells
-  int opt_bitmap_kw = 0;      // bitmap pass words per thread (0 auto)
   int opt_concurrent = 1;     // fork independent estimate phases onto aux_stream
   int opt_fuse_sweep = 1;     // slice step: the advance sweep inside the bitmap pass
   cudaStream_t aux_stream = nullptr;   // second compute stream (fork/join with events)
@@ -403,18 +429,12 @@ struct vate_pool {
   cudaEvent_t ev_counts = nullptr;
   cudaEvent_t ev_post = nullptr;       // the completed slice's post-round-trip work
   bool post_recorded = false;
-  void* l2_base = nullptr;    // window currently set on the stream
-  size_t l2_bytes = 0;
   const void* sorted_owner = nullptr;  // registry whose active set hosts_sorted holds
   uint64_t sorted_n = 0;
   uint64_t sorts_skipped = 0;
   uint64_t sorts_full = 0, sorts_incremental = 0;
   uint64_t sweeps_fused = 0;
   int opt_inc_sort = 1;       // merge membership flips into the sorted active set
-  int opt_spin = 0;           // host round trip: spin on a mapped flag (measured slower: off)
-  volatile unsigned long long* h_flag = nullptr;  // mapped pinned sequence flag
-  unsigned long long* d_flag = nullptr;
-  unsigned long long flag_seq = 0;
   uint64_t sorted_version = 1;         // bumps whenever hosts_sorted changes content
   const int32_t* g0_src = nullptr;     // g0 array the float path reads (p->g0 or inc.g0x)
   cudaEvent_t ev_adv = nullptr;        // advance counters landed in h_ctr
@@ -461,6 +481,13 @@ struct vate_hosts {
 namespace vate {
 
 int build_bitmap(vate_pool* p, int k_prime, bool with_delta = false, bool fused_advance = false);
+// Apply and clear the pending-set marks of a deferred pool (no-op otherwise):
+// every cell access other than the bitmap pass calls it first.
+int flush_pending(vate_pool* p);
+// Start or stop deferring for the pool (flushes first when stopping).
+int set_deferred(vate_pool* p, bool on);
+constexpr uint64_t kDeferBytes = 64ull << 20;
+bool default_deferred(const vate_pool* p);
 
 // error plumbing (thread-local message)
 int set_error(int code, const std::string& msg);
@@ -480,7 +507,6 @@ void timing_end(vate_pool* p, int kind, cudaEvent_t a);
 int collect_timing(vate_pool* p);
 uint32_t grid_for(uint64_t work, uint32_t per_block, uint32_t cap_blocks = 148u * 64u);
 // A/B knob: the CTA cap named by env var `name` if set, else dflt.
-uint32_t xp_cap(const char* name, uint32_t dflt);
 
 // counters in vate_pool::d_ctr
 enum Ctr { C_P = 0, C_CLEARED = 1, C_NSEL = 2, C_ERR = 3, C_DCNT = 4, C_DWORK = 5, C_MISS = 6,

@@ -137,9 +137,15 @@ __global__ void k_dirty_into(const T* __restrict__ cells, Layout L, uint32_t bac
   }
 }
 
+// Dirty cells take their block clock; on a deferred pool (pend set) the
+// union becomes the pending marks instead, which the bitmap pass applies.
 template <typename T>
 __device__ __forceinline__ void apply_word(T* __restrict__ cells, const Layout& L, uint32_t bact0,
-                                           uint64_t w, uint32_t bits) {
+                                           uint64_t w, uint32_t bits, uint32_t* pend) {
+  if (pend) {
+    pend[w] = bits;
+    return;
+  }
   if (!bits) return;
   const uint64_t i0 = w * 32;
   const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
@@ -153,14 +159,14 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_merge_oneshot(
     T* __restrict__ cells, Layout L, uint32_t bact0, uint8_t* const* __restrict__ bases,
     uint64_t off_bits, int world, uint64_t nwords, unsigned long long epoch,
-    const unsigned long long* arrive, unsigned long long* err) {
+    const unsigned long long* arrive, unsigned long long* err, uint32_t* __restrict__ pend) {
   wait_arrivals(arrive, world, epoch, err);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
     uint32_t bits = 0;
     for (int r = 0; r < world; ++r)
       bits |= __ldcg(reinterpret_cast<const uint32_t*>(bases[r] + off_bits) + w);
-    apply_word(cells, L, bact0, w, bits);
+    apply_word(cells, L, bact0, w, bits, pend);
   }
 }
 
@@ -169,7 +175,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_merge_reduce(
     T* __restrict__ cells, Layout L, uint32_t bact0, uint8_t* const* __restrict__ bases,
     uint64_t off_bits, uint64_t off_red, int me, int world, uint64_t nwords, uint64_t seg,
-    unsigned long long epoch, const unsigned long long* arrive, unsigned long long* err) {
+    unsigned long long epoch, const unsigned long long* arrive, unsigned long long* err,
+    uint32_t* __restrict__ pend) {
   wait_arrivals(arrive, world, epoch, err);
   const uint64_t lo = (uint64_t)me * seg, hi = umin64(nwords, lo + seg);
   uint32_t* red = reinterpret_cast<uint32_t*>(bases[me] + off_red);
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(256) k_merge_reduce(
     for (int r = 0; r < world; ++r)
       bits |= __ldcg(reinterpret_cast<const uint32_t*>(bases[r] + off_bits) + w);
     red[w - lo] = bits;
-    apply_word(cells, L, bact0, w, bits);
+    apply_word(cells, L, bact0, w, bits, pend);
   }
 }
 
@@ -188,7 +195,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_merge_gather(
     T* __restrict__ cells, Layout L, uint32_t bact0, uint8_t* const* __restrict__ bases,
     uint64_t off_red, int me, int world, uint64_t nwords, uint64_t seg,
-    unsigned long long epoch, const unsigned long long* arrive, unsigned long long* err) {
+    unsigned long long epoch, const unsigned long long* arrive, unsigned long long* err,
+    uint32_t* __restrict__ pend) {
   wait_arrivals(arrive, world, epoch, err);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t lo_me = (uint64_t)me * seg, hi_me = umin64(nwords, lo_me + seg);
@@ -198,7 +206,7 @@ __global__ void __launch_bounds__(256) k_merge_gather(
     const uint64_t owner = w / seg;
     const uint32_t bits = __ldcg(
         reinterpret_cast<const uint32_t*>(bases[owner] + off_red) + (w - owner * seg));
-    apply_word(cells, L, bact0, w, bits);
+    apply_word(cells, L, bact0, w, bits, pend);
   }
 }
 
@@ -336,15 +344,26 @@ int vate_peer_exchange(vate_peer* x, int64_t t, uint64_t* touched_total) {
   const bool two_shot = x->mode == 2 || (x->mode == 0 && x->world > 2);
   const uint32_t grid = 148u * 8u;
 
-  // 1. this rank's dirty bitmap and touched keys into its window
-  rc = with_cell_t(p->cell_bytes, [&](auto tag) -> int {
-    using T = decltype(tag);
-    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(x->nwords, kThreads), kThreads, 0, k_dirty_into<T>,
-                (const T*)p->cells, p->L, p->bact0, reinterpret_cast<uint32_t*>(x->win + W.bits[par]),
-                x->nwords);
-    return VATE_OK;
-  });
-  if (rc) return rc;
+  // 1. this rank's dirty bitmap and touched keys into its window: a deferred
+  // pool's pending marks are exactly the cells it set (a 2^c/8-byte copy); a
+  // direct-store pool derives them from a pass over its cells
+  uint32_t* pend = p->deferred ? p->pend.as<uint32_t>() : nullptr;
+  if (pend) {
+    if (p->pend_dirty)
+      VATE_CUDA(cudaMemcpyAsync(x->win + W.bits[par], pend, x->nwords * 4,
+                                cudaMemcpyDeviceToDevice, p->stream));
+    else
+      VATE_CUDA(cudaMemsetAsync(x->win + W.bits[par], 0, x->nwords * 4, p->stream));
+  } else {
+    rc = with_cell_t(p->cell_bytes, [&](auto tag) -> int {
+      using T = decltype(tag);
+      VATE_LAUNCH(p, VATE_K_OTHER, grid_for(x->nwords, kThreads), kThreads, 0, k_dirty_into<T>,
+                  (const T*)p->cells, p->L, p->bact0,
+                  reinterpret_cast<uint32_t*>(x->win + W.bits[par]), x->nwords);
+      return VATE_OK;
+    });
+    if (rc) return rc;
+  }
   rc = hosts_touched_launch(h, t, reinterpret_cast<uint64_t*>(x->win + W.keys[par]), x->key_cap,
                             own_count);
   if (rc) return rc;
@@ -357,20 +376,21 @@ int vate_peer_exchange(vate_peer* x, int64_t t, uint64_t* touched_total) {
     using T = decltype(tag);
     if (!two_shot) {
       VATE_LAUNCH(p, VATE_K_OTHER, grid, 256, 0, k_merge_oneshot<T>, (T*)p->cells, p->L, p->bact0,
-                  x->d_bases, W.bits[par], x->world, x->nwords, epoch, own_arrive, x->d_err);
+                  x->d_bases, W.bits[par], x->world, x->nwords, epoch, own_arrive, x->d_err, pend);
     } else {
       VATE_LAUNCH(p, VATE_K_OTHER, grid, 256, 0, k_merge_reduce<T>, (T*)p->cells, p->L, p->bact0,
                   x->d_bases, W.bits[par], W.red[par], x->rank, x->world, x->nwords, x->seg, epoch, own_arrive,
-                  x->d_err);
+                  x->d_err, pend);
       VATE_LAUNCH(p, VATE_K_OTHER, 1, 64, 0, k_arrive, x->d_bases, W.arrive, 1, x->rank, x->world,
                   epoch);
       VATE_LAUNCH(p, VATE_K_OTHER, grid, 256, 0, k_merge_gather<T>, (T*)p->cells, p->L, p->bact0,
                   x->d_bases, W.red[par], x->rank, x->world, x->nwords, x->seg, epoch,
-                  own_arrive + kMaxWorld, x->d_err);
+                  own_arrive + kMaxWorld, x->d_err, pend);
     }
     return VATE_OK;
   });
   if (rc) return rc;
+  if (pend) p->pend_dirty = true;
   const uint64_t wb = x->nwords * 4;
   x->nvlink_bytes = two_shot ? 2 * (wb / x->world) * (x->world - 1) : wb * (x->world - 1);
 

@@ -78,31 +78,9 @@ int stage_in(vate_pool* p, DevBuf& buf, const void* src, size_t bytes, int where
   return VATE_OK;
 }
 
-// The host round trip of a slice: a one-thread kernel stores a sequence number
-// into mapped pinned memory after everything enqueued so far, and the host
-// spins on it (a few hundred ns after the GPU gets there, instead of the
-// driver's wait); after 2 ms of spinning, or without a flag, it falls back to
-// cudaStreamSynchronize (which also surfaces any sticky error).
-__global__ void k_signal(unsigned long long* flag, unsigned long long seq) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(seq) : "memory");
-}
-
+// The host round trip of a slice.  (Spinning on a mapped flag stored by a
+// one-thread kernel was measured slower than the driver's wait and removed.)
 static int wait_stream(vate_pool* p) {
-  if (p->opt_spin && p->h_flag) {
-    const unsigned long long seq = ++p->flag_seq;
-    k_signal<<<1, 1, 0, p->stream>>>(p->d_flag, seq);
-    p->launches++;
-    if (cudaGetLastError() == cudaSuccess) {
-      const auto t0 = std::chrono::steady_clock::now();
-      unsigned spins = 0;
-      while (*p->h_flag < seq) {
-        if ((++spins & 1023u) == 0 &&
-            std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2))
-          break;
-      }
-      if (*p->h_flag >= seq) return VATE_OK;
-    }
-  }
   VATE_CUDA(cudaStreamSynchronize(p->stream));
   return VATE_OK;
 }
@@ -166,24 +144,6 @@ int collect_timing(vate_pool* p) {
   return VATE_OK;
 }
 
-uint32_t xp_cap(const char* name, uint32_t dflt) {
-  // read once per call site (names are literals: the pointer is the key)
-  static thread_local const char* names[8];
-  static thread_local int vals[8];
-  for (int i = 0; i < 8; ++i) {
-    if (names[i] == name) return vals[i] > 0 ? (uint32_t)vals[i] : dflt;
-    if (!names[i]) {
-      const char* e = getenv(name);
-      names[i] = name;
-      vals[i] = e ? atoi(e) : 0;
-      return vals[i] > 0 ? (uint32_t)vals[i] : dflt;
-    }
-  }
-  const char* e = getenv(name);
-  const int v = e ? atoi(e) : 0;
-  return v > 0 ? (uint32_t)v : dflt;
-}
-
 uint32_t grid_for(uint64_t work, uint32_t per_block, uint32_t cap_blocks) {
   uint64_t g = (work + per_block - 1) / per_block;
   if (g < 1) g = 1;
@@ -202,8 +162,14 @@ static int with_cell(int bytes, F f) {
 
 // Cell type and store rule of a pool: AT stores its block clock; the DR / TS
 // comparators store a constant per slice (0, or the slice index).
+// A deferred AT pool marks the pending-set bitmap instead (MarkRule).
 template <typename F>
 static int with_store(vate_pool* p, F f) {
+  if (p->kind == VATE_AT && p->deferred) {
+    p->pend_dirty = true;
+    return with_cell(p->cell_bytes,
+                     [&](auto tag) { return f(tag, MarkRule{p->pend.as<uint32_t>()}); });
+  }
   if (p->kind == VATE_AT)
     return with_cell(p->cell_bytes, [&](auto tag) { return f(tag, AtRule{p->L, p->bact0}); });
   const ConstRule r{p->kind == VATE_DR ? 0ull : p->ts_now};
@@ -237,18 +203,21 @@ __global__ void k_fill(T* cells, uint64_t n, T value) {
     cells[i] = value;
 }
 
-// A batch of U packets per thread: BH, H, block clock, store (pools.py:153-178
+// A batch of U packets per thread: BH, H, then the cell write (pools.py:153-178
 // with estimator.py:96-99), then the host-registry touch.  Same-cell writers
 // of a slice store the same clock, so plain stores suffice -- no atomics, no
-// read-modify-write.  The registry step issues all U first-probe loads (one
-// 16-byte sector each) before resolving any, so a thread keeps U independent
-// requests in flight; only misses take the probing insert.
-// Heavy-hitter form (CHECK, VATE_OPT_SCAN_CHECK): registry touches are
-// filtered per CTA by a small direct-mapped table of the slots this CTA already
-// stamped with t in shared memory.  Loads of `last`
-// come from L1 and are stale within a launch, so without it every packet of a
-// heavy hitter would store into the same 8 bytes -- hundreds of thousands of
-// same-address stores serialised at one L2 slice (cfg 3's Zipf head).
+// read-modify-write.  A deferred pool (MarkRule: cells beyond L2) instead
+// sets the cell's bit in the L2-resident pending-set bitmap (one red.or) and
+// the next pool pass writes the clock (store_cell).  The registry step issues
+// all U first-probe loads (one 32-byte sector each) before resolving any, so
+// a thread keeps U independent requests in flight; only misses take the
+// probing insert.
+// FILTER (skewed traffic): registry stamps are filtered per CTA by a small
+// direct-mapped table of the slots this CTA already stamped with t in shared
+// memory.  Loads of `last` come from L1 and are stale within a launch, so
+// without it every packet of a heavy hitter would store into the same 8 bytes
+// -- hundreds of thousands of same-address stores serialised at one L2 slice
+// (cfg 3's Zipf head).
 constexpr int kTouchSlots = 1024;
 
 __device__ __forceinline__ void touch_filter_init(unsigned* filt) {
@@ -284,23 +253,14 @@ __device__ __forceinline__ void defer_drain(DeferQ* dq, const RegRef& R, long lo
   for (unsigned i = threadIdx.x; i < n; i += blockDim.x) reg_insert(R, dq->keys[i], t, false);
 }
 
-// CHK: 0 plain stores; 1 heavy-hitter form (load-before-store cells + per-CTA
-// registry stamp filter); 2 the registry stamp filter alone
-template <typename T, bool REG, int U, int CHK = 0, typename Rule>
+template <typename T, bool REG, int U, bool FILTER, typename Rule>
 __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint64_t (&bip)[U],
                                            int m, T* __restrict__ cells, const HashParams& H,
                                            const Rule& rule, const RegRef& R, long long t,
                                            unsigned* filt, DeferQ* dq = nullptr) {
 #pragma unroll
-  for (int q = 0; q < U; ++q) {
-    if (q < m) {
-      const uint64_t cell = cell_of(aip[q], slot_of(bip[q], H), H);
-      const T act = rule.template value<T>(cell);
-      // CHECK: skew-tolerant form for heavy hitters -- read first (L1 keeps hot
-      // lines) and store only if the cell does not already hold the clock
-      if (CHK != 1 || cells[cell] != act) cells[cell] = act;
-    }
-  }
+  for (int q = 0; q < U; ++q)
+    if (q < m) store_cell<T>(cells, cell_of(aip[q], slot_of(bip[q], H), H), rule);
   if (REG) {
     // all U first probes in flight before any is resolved: each reads the home
     // sector (two slots, one 256-bit load)
@@ -316,12 +276,12 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
       if (q >= m) continue;
       if (aip[q] != kEmptyKey && e[q].key == aip[q]) {
         if (e[q].last != t) {
-          if (CHK) touch_last(R, filt, slot[q], t);
+          if (FILTER) touch_last(R, filt, slot[q], t);
           else R.table[slot[q]].last = t;
         }
       } else if (aip[q] != kEmptyKey && f[q].key == aip[q]) {
         if (f[q].last != t) {
-          if (CHK) touch_last(R, filt, slot[q] + 1, t);
+          if (FILTER) touch_last(R, filt, slot[q] + 1, t);
           else R.table[slot[q] + 1].last = t;
         }
       } else {
@@ -338,154 +298,51 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
   }
 }
 
-template <typename T, bool REG, int V = 2, int CHECK = 0, typename Rule = AtRule>  // V uint4 loads per iteration
+// The packed scan: one uint4 (two 8-byte packets) per thread per iteration,
+// 8 CTAs per SM at <= 32 registers (measured best on cfg 2/3/4 against one
+// packet, two or four uint4 per thread, and a TMA-fed persistent form).
+template <typename T, bool REG, bool FILTER, typename Rule>
 __global__ void __launch_bounds__(kThreads, 8) k_scan_packed16(
     const uint4* __restrict__ pairs2, uint64_t npairs2, T* __restrict__ cells, HashParams H,
     Rule rule, RegRef R, long long t) {
-  __shared__ unsigned filt[REG && CHECK ? kTouchSlots : 1];
+  __shared__ unsigned filt[REG && FILTER ? kTouchSlots : 1];
   __shared__ __align__(16) unsigned char dq_raw[REG ? sizeof(DeferQ) : 16];
   DeferQ* dq = REG ? reinterpret_cast<DeferQ*>(dq_raw) : nullptr;
   if (REG) defer_init(dq);
-  if (REG && CHECK) touch_filter_init(filt);  // (its barrier also publishes dq->n = 0)
+  if (REG && FILTER) touch_filter_init(filt);  // (its barrier also publishes dq->n = 0)
   else if (REG) __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  for (; i < npairs2; i += V * stride) {
-    uint64_t a[2 * V], b[2 * V];
-    int m = 0;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const uint64_t j = i + v * stride;
-      if (j < npairs2) {
-        const uint4 q = __ldcs(pairs2 + j);  // streamed once: evict-first
-        a[2 * v] = q.x; b[2 * v] = q.y; a[2 * v + 1] = q.z; b[2 * v + 1] = q.w;
-        m += 2;
-      } else {
-        a[2 * v] = b[2 * v] = a[2 * v + 1] = b[2 * v + 1] = 0;
-      }
-    }
-    scan_batch<T, REG, 2 * V, CHECK>(a, b, m, cells, H, rule, R, t, filt, dq);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < npairs2; i += stride) {
+    const uint4 q = __ldcs(pairs2 + i);  // streamed once: evict-first
+    const uint64_t a[2] = {q.x, q.z}, b[2] = {q.y, q.w};
+    scan_batch<T, REG, 2, FILTER>(a, b, 2, cells, H, rule, R, t, filt, dq);
   }
   if (REG) defer_drain(dq, R, t);
 }
 
-// One 8-byte packet per thread (the default form, VATE_OPT_SCAN_V = 0): the
-// most threads, the shortest per-thread dependency chain; registry misses go
-// through the same per-CTA deferred queue, CHECK adds the heavy-hitter forms.
-template <typename T, bool REG, int CHECK = 0, typename Rule = AtRule>
+// One 8-byte packet per thread: input that is not 16-byte aligned, and the odd
+// last packet of a 16-byte aligned batch.
+template <typename T, bool REG, bool FILTER, typename Rule>
 __global__ void __launch_bounds__(kThreads) k_scan_packed8(
     const uint2* __restrict__ pairs, uint64_t n, T* __restrict__ cells, HashParams H,
     Rule rule, RegRef R, long long t) {
-  __shared__ unsigned filt[REG && CHECK ? kTouchSlots : 1];
+  __shared__ unsigned filt[REG && FILTER ? kTouchSlots : 1];
   __shared__ __align__(16) unsigned char dq_raw[REG ? sizeof(DeferQ) : 16];
   DeferQ* dq = REG ? reinterpret_cast<DeferQ*>(dq_raw) : nullptr;
   if (REG) defer_init(dq);
-  if (REG && CHECK) touch_filter_init(filt);
+  if (REG && FILTER) touch_filter_init(filt);
   else if (REG) __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint2 q = __ldcs(pairs + i);  // streamed once: evict-first
     const uint64_t a[1] = {q.x}, b[1] = {q.y};
-    scan_batch<T, REG, 1, CHECK>(a, b, 1, cells, H, rule, R, t, filt, dq);
+    scan_batch<T, REG, 1, FILTER>(a, b, 1, cells, H, rule, R, t, filt, dq);
   }
   if (REG) defer_drain(dq, R, t);
 }
 
-// ---------------------------------------------------------------------------
-// Persistent scan with the packet stream moved by TMA (VATE_OPT_SCAN_V = 8, for
-// 16-byte-aligned input; measured no faster than the default one-uint4-per-
-// thread form on cfg 2/3/4 -- the stream is not what bounds the scan, the
-// random cell stores and registry probes are): each CTA pulls 8 KB tiles (1024
-// packets) into a two-stage shared-memory ring with cp.async.bulk, signalled on
-// an mbarrier, while its threads hash, store and probe the previous tile -- the
-// stream never sits on the per-packet dependency chain.  Tiles are handed out
-// by an atomic counter (balanced tails); each thread takes 4 packets at a time
-// so 4 registry home-sector loads are in flight together.
-// ---------------------------------------------------------------------------
-constexpr int kTmaTile = 1024;                       // packets per tile (8 KB)
-constexpr int kTmaPerThread = kTmaTile / kThreads;   // 4
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
-               "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(bar)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          (unsigned)__cvta_generic_to_shared(dst)),
-      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  unsigned done = 0;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-
-template <typename T, int CHECK, typename Rule>
-__global__ void __launch_bounds__(kThreads, 4) k_scan_tma(
-    const uint2* __restrict__ pairs, uint64_t ntiles, T* __restrict__ cells, HashParams H,
-    Rule rule, RegRef R, long long t, unsigned* __restrict__ tile_counter) {
-  __shared__ __align__(128) uint2 buf[2][kTmaTile];
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ unsigned next_tile[2];
-  __shared__ unsigned filt[CHECK ? kTouchSlots : 1];
-  __shared__ __align__(16) unsigned char dq_raw[sizeof(DeferQ)];
-  DeferQ* dq = reinterpret_cast<DeferQ*>(dq_raw);
-  defer_init(dq);
-  if (CHECK) touch_filter_init(filt);
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const unsigned first = atomicAdd(tile_counter, 1u);
-    next_tile[0] = first;
-    if (first < ntiles) {
-      mbar_expect_tx(&bar[0], kTmaTile * 8);
-      bulk_g2s(buf[0], pairs + (uint64_t)first * kTmaTile, kTmaTile * 8, &bar[0]);
-    }
-  }
-  __syncthreads();
-  for (unsigned k = 0;; ++k) {
-    const int s = k & 1;
-    const unsigned tile = next_tile[s];
-    if (tile >= ntiles) break;
-    if (threadIdx.x == 0) {  // claim and prefetch the next tile into the other stage
-      const unsigned nt = atomicAdd(tile_counter, 1u);
-      next_tile[s ^ 1] = nt;
-      if (nt < ntiles) {
-        // the stage was read through the generic proxy before the last barrier
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[s ^ 1], kTmaTile * 8);
-        bulk_g2s(buf[s ^ 1], pairs + (uint64_t)nt * kTmaTile, kTmaTile * 8, &bar[s ^ 1]);
-      }
-    }
-    mbar_wait(&bar[s], (k >> 1) & 1);
-    uint64_t a[kTmaPerThread], b[kTmaPerThread];
-#pragma unroll
-    for (int q = 0; q < kTmaPerThread; ++q) {
-      const uint2 v = buf[s][threadIdx.x + q * kThreads];
-      a[q] = v.x;
-      b[q] = v.y;
-    }
-    scan_batch<T, true, kTmaPerThread, CHECK>(a, b, kTmaPerThread, cells, H, rule, R, t, filt, dq);
-    __syncthreads();  // stage s is read; next_tile[s ^ 1] is visible
-  }
-  defer_drain(dq, R, t);
-}
-
-template <typename T, bool REG, typename Rule = AtRule>
+// The u64 form (record_pairs on u64 aips / bips, estimator.py:96-104).
+template <typename T, bool REG, typename Rule>
 __global__ void __launch_bounds__(kThreads) k_scan_u64(
     const uint64_t* __restrict__ aips, const uint64_t* __restrict__ bips, uint64_t n,
     T* __restrict__ cells, HashParams H, Rule rule, RegRef R, long long t) {
@@ -505,7 +362,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_u64(
         m = q + 1;
       }
     }
-    scan_batch<T, REG, U>(a, b, m, cells, H, rule, R, t, filt);
+    scan_batch<T, REG, U, false>(a, b, m, cells, H, rule, R, t, filt);
   }
 }
 
@@ -534,7 +391,7 @@ __global__ void k_set_cells(const uint64_t* __restrict__ idx, uint64_t n, T* __r
       *err = 1;
       continue;
     }
-    cells[c] = rule.template value<T>(c);
+    store_cell<T>(cells, c, rule);
   }
 }
 
@@ -561,18 +418,6 @@ __global__ void __launch_bounds__(kThreads) k_sweep(T* __restrict__ cells, uint6
   }
   const unsigned s = block_sum(local);
   if (threadIdx.x == 0 && s) atomicAdd(cleared, (unsigned long long)s);
-}
-
-// 32 consecutive cells into registers with 16-byte loads (i0 is 32-aligned).
-template <typename T>
-__device__ __forceinline__ void load32(const T* __restrict__ p, uint32_t (&v)[32]) {
-  constexpr int NV = (int)sizeof(T) * 32 / 16;
-  uint4 r[NV];
-#pragma unroll
-  for (int q = 0; q < NV; ++q) r[q] = __ldcs(reinterpret_cast<const uint4*>(p) + q);
-  const T* e = reinterpret_cast<const T*>(r);
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = e[j];
 }
 
 // Active bits of 32 cells that share one clock, SIMD-in-register for u8/u16
@@ -607,18 +452,27 @@ __device__ __forceinline__ bool active_bits_simd(const uint4 (&r)[(int)sizeof(T)
     // mask, un-interleaved once per 32 cells; the "value > 2k" check is one
     // lane-wise max per word, tested once.  (The cfg-4 bitmap pass is
     // issue-bound: this form retires ~35 % fewer instructions per cell.)
+    // Every stored value fits the pool's width (<= 15 bits here), so each
+    // lane is < 0x8000 and x | H == x + H: one add per compare.  The flags
+    // (bits 15, 31) shift into the interleaved mask: after the 16 steps bit
+    // 15 of step q sits at bit q and bit 31 at bit 16 + q.
     const uint32_t H = 0x80008000u;
     const uint32_t AH = (act * 0x00010001u) | H;
-    const uint32_t L2 = (uint32_t)(lo >= 0 ? lo : lo + (int)B) * 0x00010001u;
-    const uint32_t B2 = B * 0x00010001u;
+    const uint32_t GL = H - (uint32_t)(lo >= 0 ? lo : lo + (int)B) * 0x00010001u;
+    const uint32_t GB = H - B * 0x00010001u;
     uint32_t mx = 0, inter = 0;
+    if (lo >= 0) {
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      mx = __vmaxu2(mx, x[q]);
-      const uint32_t xh = x[q] | H;
-      const uint32_t ge_lo = (xh - L2) & H, le_act = (AH - x[q]) & H;
-      const uint32_t m = lo >= 0 ? (ge_lo & le_act) : (le_act | (ge_lo & ~((xh - B2) & H)));
-      inter |= ((m >> 15) & 0x00010001u) << q;
+      for (int q = 0; q < 16; ++q) {
+        mx = __vmaxu2(mx, x[q]);
+        inter = (inter >> 1) | ((x[q] + GL) & (AH - x[q]) & H);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        mx = __vmaxu2(mx, x[q]);
+        inter = (inter >> 1) | (((AH - x[q]) | ((x[q] + GL) & ~(x[q] + GB))) & H);
+      }
     }
     bad = __vcmpgtu2(mx, B * 0x00010001u);
     // interleave: low 16 bits -> even positions, high 16 bits -> odd positions
@@ -650,20 +504,29 @@ __device__ __forceinline__ bool active_bits_simd(const uint4 (&r)[(int)sizeof(T)
 // `bprev` set it also emits the cells whose bit flipped against the previous
 // estimate's bitmap (the incremental g0 delta, vate_incremental.cu), so the
 // delta costs no second pass.
+// Deferred pools (PEND): the pass first applies its word's pending-set marks
+// -- marked cells take their block clock, the write set_many would have made
+// (pools.py:164-178) -- and clears them, so the scan's scattered writes reach
+// HBM as part of this streaming pass instead of one sector read + write per
+// packet.
 // The slice advance fused into the bitmap pass (vate_slice_step): the bits are
 // taken with the slice's clocks, then the two blocks due under the advanced
 // clock are swept exactly as k_sweep does (pools.py:221-249): range 0 at clock
 // 0 (stale: v <= k), range 1 at clock k (stale: k <= v <= 2k-1 or v == 0).
 // Each cell is read and rewritten by the one thread that owns its word, after
 // its bit is taken, so the estimate sees the pre-advance pool as it must.
+// Write-back: only the 32-byte sectors of a word that changed, always whole
+// sectors -- a 16-byte store into a sector the pass read evict-first makes the
+// L2 fill the other half from DRAM (scripts/probes/probe_marks.cu: 634 vs
+// 165 us for a 512 MiB pass applying 5M marks).
 struct SweepSpec {
   uint64_t s0, e0, s1, e1;          // the two due ranges (e == s: none)
   uint32_t k, B;
   unsigned long long* cleared;      // nullptr: no fused sweep
 };
 
-// Register-free (re-reads the word's cells, L1-hot): passing
-// the pass's register copy by reference would push it to local memory.
+// Register-free (re-reads the word's cells, L1-hot): words of u32 cells and the
+// partial last word of a tiny pool.
 template <typename T>
 __device__ __forceinline__ unsigned sweep_word(T* __restrict__ cells, uint64_t i0, uint32_t cnt,
                                             uint64_t s0, uint64_t e0, uint64_t s1, uint64_t e1,
@@ -692,20 +555,20 @@ __device__ __forceinline__ uint32_t range_bits(uint64_t i0, uint64_t s, uint64_t
 }
 
 // The same sweep for a full word of u8/u16 cells, on the pass's register copy:
-// stale cells are rewritten in the registers and only the 16-byte vectors that
-// changed are stored.  (The scalar form re-reads each cell from L2 -- the
-// pass's loads are evict-first -- and its 32 dependent round trips set the
-// kernel's tail on small pools.)
+// stale cells are rewritten in the registers; bit v of `chg` marks a changed
+// uint4.  (The scalar form re-reads each cell from L2 -- the pass's loads are
+// evict-first -- and its 32 dependent round trips set the kernel's tail on
+// small pools.)
 template <typename T>
-__device__ __forceinline__ unsigned sweep_regs(T* __restrict__ cells, uint4 (&r)[(int)sizeof(T) * 2],
-                                               uint64_t i0, const SweepSpec& SW) {
+__device__ __forceinline__ unsigned sweep_regs(uint4 (&r)[(int)sizeof(T) * 2], uint64_t i0,
+                                               const SweepSpec& SW, unsigned& chg) {
   static_assert(sizeof(T) <= 2, "u8/u16 cells");
   const uint32_t due0 = range_bits(i0, SW.s0, SW.e0), due1 = range_bits(i0, SW.s1, SW.e1);
   if (!(due0 | due1)) return 0;
   constexpr int kPer = 4 / (int)sizeof(T), kBits = 8 * (int)sizeof(T);
   constexpr uint32_t kMask = sizeof(T) == 1 ? 0xFFu : 0xFFFFu;
   uint32_t* x = reinterpret_cast<uint32_t*>(r);
-  unsigned cleared = 0, changed = 0;
+  unsigned cleared = 0;
 #pragma unroll
   for (int q = 0; q < 32 / kPer; ++q) {
 #pragma unroll
@@ -717,98 +580,197 @@ __device__ __forceinline__ unsigned sweep_regs(T* __restrict__ cells, uint4 (&r)
       if (stale) {
         x[q] = (x[q] & ~(kMask << (h * kBits))) | (SW.B << (h * kBits));
         ++cleared;
-        changed |= 1u << (q / 4);
+        chg |= 1u << (q / 4);
       }
     }
   }
-#pragma unroll
-  for (int v = 0; v < (int)sizeof(T) * 2; ++v)
-    if ((changed >> v) & 1u) reinterpret_cast<uint4*>(cells + i0)[v] = r[v];
   return cleared;
 }
 
+// Pending-set marks of a word whose 32 cells share clock `act`, applied to the
+// register copy (u8: 4 cells per 32-bit lane, u16: 2); bit v of the result
+// marks a changed uint4.
 template <typename T>
-__device__ __forceinline__ uint32_t word_inactive_bits(const T* __restrict__ cells,
-                                                       const uint4 (&r)[(int)sizeof(T) * 2],
-                                                       uint64_t i0, uint32_t cnt, const Layout& L,
-                                                       uint32_t bact0, uint32_t kp) {
+__device__ __forceinline__ unsigned apply_marks_regs(uint4 (&r)[(int)sizeof(T) * 2], uint32_t m,
+                                                     uint32_t act) {
+  static_assert(sizeof(T) <= 2, "u8/u16 cells");
+  uint32_t* x = reinterpret_cast<uint32_t*>(r);
+  unsigned chg = 0;
+  if (sizeof(T) == 1) {
+    const uint32_t a4 = act * 0x01010101u;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t nib = (m >> (4 * q)) & 0xFu;
+      const uint32_t bm = ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;  // bit j -> byte j
+      x[q] = (x[q] & ~bm) | (a4 & bm);
+    }
+    chg = m ? 3u : 0u;  // (see below: a marked cell changes)
+  } else {
+    // lane masks by sign-replicating byte permutes: copy s[k] = m << k puts bit
+    // 8j + 7 - k of m at the sign of byte j, and prmt with a selector nibble's
+    // bit 3 set writes that sign into a whole byte -- one prmt per two cells
+    const uint32_t a2 = act * 0x00010001u;
+    uint32_t sh[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sh[k] = m << k;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int j = (2 * q) >> 3, k = 7 - ((2 * q) & 7);  // bit 2q: byte j of sh[k]; 2q+1: of sh[k-1]
+      const uint32_t sel = (8u | j) | ((8u | j) << 4) | ((12u | j) << 8) | ((12u | j) << 12);
+      uint32_t bm;
+      asm("prmt.b32 %0, %1, %2, %3;" : "=r"(bm) : "r"(sh[k]), "r"(sh[k - 1]), "r"(sel));
+      x[q] = (x[q] & ~bm) | (a2 & bm);
+    }
+    // a marked cell never already holds its clock (it would have been set in
+    // this slice, and this slice's sets are the marks): a sector with a mark
+    // changed
+    chg = ((m & 0xFFFFu) ? 3u : 0u) | ((m >> 16) ? 12u : 0u);
+  }
+  return chg;
+}
+
+// Marks of a word that straddles a block boundary (or holds u32 cells), in
+// memory: each marked cell takes its own block's clock.
+template <typename T>
+__device__ __forceinline__ void apply_marks_scalar(T* __restrict__ cells, uint64_t i0, uint32_t cnt,
+                                                   uint32_t m, const Layout& L, uint32_t bact0) {
+  for_word_clocks(i0, cnt, L, bact0, [&](uint32_t j, uint32_t act) {
+    if ((m >> j) & 1u) cells[i0 + j] = (T)act;
+  });
+}
+
+// Changed 32-byte sectors of a word back to HBM (uint4 pairs, whole sectors).
+template <typename T>
+__device__ __forceinline__ void store_sectors(T* __restrict__ cells, uint64_t i0,
+                                              const uint4 (&r)[(int)sizeof(T) * 2], unsigned chg) {
+  constexpr int NV = (int)sizeof(T) * 2;
+  uint4* dst = reinterpret_cast<uint4*>(cells + i0);
+#pragma unroll
+  for (int s = 0; s < NV / 2; ++s)
+    if ((chg >> (2 * s)) & 3u) {
+      dst[2 * s] = r[2 * s];
+      dst[2 * s + 1] = r[2 * s + 1];
+    }
+}
+
+// The rare words, entirely in memory (re-reads are L1/L2 hits): a word that
+// straddles a block boundary (2k of them), u32 cells (k = 2^15), the partial
+// last word of a pool smaller than 32 cells, and -- with m = 0, no sweep --
+// the bits of a word holding values above 2k (hand-made snapshots only).
+// Out of line, so the common path keeps its registers.
+template <typename T>
+__device__ __forceinline__ uint32_t slow_word(T* __restrict__ cells, uint32_t m, uint64_t i0,
+                                           uint32_t cnt, Layout L, uint32_t bact0, uint32_t kp,
+                                           SweepSpec SW, unsigned* swept) {
   uint32_t b = block_of(i0, L);
   uint64_t next = block_start(b + 1, L);
-  uint32_t act = clock_of(bact0, b, L.B);
-  if (cnt == 32 && i0 + 32 <= next) {  // the whole word in one block: one clock
-    if (sizeof(T) <= 2) {
-      uint32_t active;
-      if (active_bits_simd<T>(r, act, L.B, kp, &active)) return ~active;
-    }
-    const T* e = reinterpret_cast<const T*>(r);
-    uint32_t bits = 0;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) bits |= (uint32_t)is_inactive(e[j], act, L.B, kp) << j;
-    return bits;
-  }
-  uint32_t bits = 0;  // block boundary (or pool end) inside the word
+  uint32_t a = clock_of(bact0, b, L.B);
+  uint32_t bits = 0;
+#pragma unroll 1
   for (uint32_t j = 0; j < cnt; ++j) {
     while (i0 + j >= next) {
       ++b;
       next = block_start(b + 1, L);
-      act = (act + 1 == L.B) ? 0 : act + 1;
+      a = (a + 1 == L.B) ? 0 : a + 1;
     }
-    bits |= (uint32_t)is_inactive(cells[i0 + j], act, L.B, kp) << j;
+    if ((m >> j) & 1u) cells[i0 + j] = (T)a;
+    bits |= (uint32_t)is_inactive(cells[i0 + j], a, L.B, kp) << j;
   }
+  if (swept && SW.cleared && ((i0 < SW.e0 && i0 + cnt > SW.s0) || (i0 < SW.e1 && i0 + cnt > SW.s1)))
+    *swept += sweep_word(cells, i0, cnt, SW.s0, SW.e0, SW.s1, SW.e1, SW.k, SW.B);
   return bits;
 }
 
-// kW words per thread per iteration: all their 16-byte loads are issued before
-// any predicate, for memory-level parallelism.
-template <typename T, int kW, bool STREAM = true>
-__global__ void __launch_bounds__(kThreads, 6) k_bitmap(T* __restrict__ cells, Layout L,
+// One word of the pass: marks, bits, sweep, write-back.  Returns the inactive
+// bits; adds the swept-clear count to `swept`.
+template <typename T, bool PEND>
+__device__ __forceinline__ uint32_t pass_word(T* __restrict__ cells, uint4 (&r)[(int)sizeof(T) * 2],
+                                              uint32_t m, uint64_t i0, uint32_t cnt,
+                                              uint64_t next, uint32_t act,
+                                              const Layout& L, uint32_t bact0, uint32_t kp,
+                                              const SweepSpec& SW, unsigned& swept) {
+  if (sizeof(T) > 2 || cnt != 32 || i0 + 32 > next)
+    return slow_word<T>(cells, PEND ? m : 0u, i0, cnt, L, bact0, kp, SW, &swept);
+  if constexpr (sizeof(T) <= 2) {
+    unsigned chg = 0;
+    if (PEND && m) chg = apply_marks_regs<T>(r, m, act);
+    uint32_t active, bits;
+    if (active_bits_simd<T>(r, act, L.B, kp, &active)) {
+      bits = ~active;
+    } else {  // a value above 2k: the exact scalar predicate, from memory
+      if (chg) store_sectors<T>(cells, i0, r, chg);
+      chg = 0;
+      bits = slow_word<T>(cells, 0u, i0, 32, L, bact0, kp, SW, nullptr);
+    }
+    if (SW.cleared && ((i0 < SW.e0 && i0 + 32 > SW.s0) || (i0 < SW.e1 && i0 + 32 > SW.s1)))
+      swept += sweep_regs<T>(r, i0, SW, chg);
+    if (chg) store_sectors<T>(cells, i0, r, chg);
+    return bits;
+  }
+  return 0u;
+}
+
+// One 32-cell word per thread per iteration; its 16-byte cell loads, the
+// previous bitmap word and the pending marks are all issued before any
+// predicate, for memory-level parallelism.  Each CTA walks a contiguous run
+// of words (256 consecutive words per step, coalesced), so a thread stays in
+// one block for many steps and recomputes the block and its clock (a 64-bit
+// division) only when it crosses a block boundary.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <typename T, bool PEND, int PF = 0>
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 1 ? 5 : 4) k_bitmap(T* __restrict__ cells, Layout L,
                                                      uint32_t bact0, uint32_t kp,
                                                      uint32_t* __restrict__ bitmap,
                                                      uint64_t nwords,
                                                      unsigned long long* pool_inactive,
-                                                     DeltaOut D, Publish pub, SweepSpec SW) {
+                                                     DeltaOut D, Publish pub, SweepSpec SW,
+                                                     uint32_t* __restrict__ pend) {
   constexpr int NV = (int)sizeof(T) * 2;
   __shared__ DeltaStage ds;
   delta_stage_init(ds);
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t per_cta = ((nwords + gridDim.x - 1) / gridDim.x + kThreads - 1) / kThreads * kThreads;
+  const uint64_t w_lo = blockIdx.x * per_cta, w_hi = umin64(nwords, w_lo + per_cta);
   unsigned local = 0, swept = 0;
-  for (uint64_t w0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w0 < nwords;
-       w0 += kW * stride) {
-    uint4 r[kW][NV];
-    uint32_t prev[kW];
-#pragma unroll
-    for (int q = 0; q < kW; ++q) {
-      const uint64_t w = w0 + q * stride;
-      prev[q] = (D.bprev && w < nwords) ? __ldcs(D.bprev + w) : 0u;
-      if (w < nwords && (w + 1) * 32 <= L.size) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const uint4* src = reinterpret_cast<const uint4*>(cells + w * 32) + v;
-          r[q][v] = STREAM ? __ldcs(src) : __ldcg(src);
-        }
+  uint64_t bnext = 0;  // end of the cached block (words only move forward)
+  uint32_t act = 0;
+  if (PF && threadIdx.x == 0) {  // the first PF steps' cells into L2
+    for (int q = 0; q < PF; ++q) {
+      const uint64_t f = w_lo + (uint64_t)q * kThreads;
+      if (f + kThreads <= w_hi) prefetch_l2(cells + f * 32, kThreads * 32 * sizeof(T));
+    }
+  }
+  for (uint64_t w = w_lo + threadIdx.x; w < w_hi; w += kThreads) {
+    if (PF && threadIdx.x == 0) {  // L2 bulk prefetch PF steps ahead (one instruction)
+      const uint64_t f = w + (uint64_t)PF * kThreads;
+      if (f + kThreads <= w_hi) {
+        prefetch_l2(cells + f * 32, kThreads * 32 * sizeof(T));
+        if (PEND) prefetch_l2(pend + f, kThreads * 4);
+        if (D.bprev) prefetch_l2(D.bprev + f, kThreads * 4);
       }
     }
+    uint4 r[NV];
+    const uint32_t prev = D.bprev ? __ldcs(D.bprev + w) : 0u;
+    const uint32_t m = PEND ? __ldcg(pend + w) : 0u;
+    const uint64_t i0 = w * 32;
+    const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
+    if (cnt == 32) {
 #pragma unroll
-    for (int q = 0; q < kW; ++q) {
-      const uint64_t w = w0 + q * stride;
-      if (w >= nwords) break;
-      const uint64_t i0 = w * 32;
-      const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
-      const uint32_t bits = word_inactive_bits<T>(cells, r[q], i0, cnt, L, bact0, kp);
-      bitmap[w] = bits;
-      local += __popc(bits);
-      if (SW.cleared && ((i0 < SW.e0 && i0 + cnt > SW.s0) || (i0 < SW.e1 && i0 + cnt > SW.s1))) {
-        if constexpr (sizeof(T) <= 2) {
-          if (cnt == 32)
-            swept += sweep_regs<T>(cells, r[q], i0, SW);
-          else
-            swept += sweep_word(cells, i0, cnt, SW.s0, SW.e0, SW.s1, SW.e1, SW.k, SW.B);
-        } else {
-          swept += sweep_word(cells, i0, cnt, SW.s0, SW.e0, SW.s1, SW.e1, SW.k, SW.B);
-        }
-      }
-      if (D.bprev) delta_word(D, ds, bits, prev[q], i0);
+      for (int v = 0; v < NV; ++v) r[v] = __ldcs(reinterpret_cast<const uint4*>(cells + i0) + v);
     }
+    if (i0 >= bnext) {
+      const uint32_t b = block_of(i0, L);
+      bnext = block_start(b + 1, L);
+      act = clock_of(bact0, b, L.B);
+    }
+    const uint32_t bits = pass_word<T, PEND>(cells, r, m, i0, cnt, bnext, act, L, bact0, kp, SW,
+                                             swept);
+    if (PEND && m) pend[w] = 0u;
+    bitmap[w] = bits;
+    local += __popc(bits);
+    if (D.bprev) delta_word(D, ds, bits, prev, i0);
   }
   if (D.bprev) delta_flush(D, ds);
   if (SW.cleared) {
@@ -818,6 +780,38 @@ __global__ void __launch_bounds__(kThreads, 6) k_bitmap(T* __restrict__ cells, L
   const unsigned s = block_sum(local);
   if (threadIdx.x == 0 && s) atomicAdd(pool_inactive, (unsigned long long)s);
   publish_last_block(pub);  // P (and the delta / sweep counts) straight into pinned memory
+}
+
+// flush_pending: the marks alone (no bitmap), reading only the 2^c/8-byte
+// pending-set bitmap and the words it marks -- for the point queries,
+// snapshots and standalone advances that read cells outside the slice step.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_apply_pending(T* __restrict__ cells, Layout L,
+                                                            uint32_t bact0,
+                                                            uint32_t* __restrict__ pend,
+                                                            uint64_t nwords) {
+  constexpr int NV = (int)sizeof(T) * 2;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
+    const uint32_t m = __ldcg(pend + w);
+    if (!m) continue;
+    const uint64_t i0 = w * 32;
+    const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
+    const uint32_t b = block_of(i0, L);
+    bool done = false;
+    if constexpr (sizeof(T) <= 2) {
+      if (cnt == 32 && i0 + 32 <= block_start(b + 1, L)) {
+        uint4 r[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) r[v] = reinterpret_cast<const uint4*>(cells + i0)[v];
+        const unsigned chg = apply_marks_regs<T>(r, m, clock_of(bact0, b, L.B));
+        store_sectors<T>(cells, i0, r, chg);
+        done = true;
+      }
+    }
+    if (!done) apply_marks_scalar<T>(cells, i0, cnt, m, L, bact0);
+    pend[w] = 0u;
+  }
 }
 
 template <typename T>
@@ -908,11 +902,16 @@ __global__ void k_dirty(const T* __restrict__ cells, Layout L, uint32_t bact0,
 // their block clock.  Equals the newest-timestamp max of SURVEY.md §8e.
 template <typename T>
 __global__ void k_merge(T* __restrict__ cells, Layout L, uint32_t bact0,
-                        const uint32_t* __restrict__ bitmaps, uint64_t nwords, int nranks) {
+                        const uint32_t* __restrict__ bitmaps, uint64_t nwords, int nranks,
+                        uint32_t* __restrict__ pend) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
     uint32_t bits = 0;
     for (int r = 0; r < nranks; ++r) bits |= bitmaps[(uint64_t)r * nwords + w];
+    if (pend) {  // deferred pool: the union becomes the pending marks
+      pend[w] = bits;
+      continue;
+    }
     if (!bits) continue;
     const uint64_t i0 = w * 32;
     const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
@@ -1022,7 +1021,6 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta, bool fused_advance)
                  I.dlist.as<unsigned long long>(), I.dlist_cap, p->d_ctr + C_DCNT,
                  p->d_ctr + C_DWORK};
   }
-  // words per thread per iteration (p->opt_bitmap_kw overrides: 1, 2 or 4)
   // the fused advance: due blocks under the advanced clock (pools.py:228-232)
   SweepSpec SW{};
   uint32_t z = 0, qb = 0;
@@ -1040,43 +1038,38 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta, bool fused_advance)
   const Publish pub{p->d_done, p->d_ctr, p->h_ctr_dev,
                     (1u << C_P) | (with_delta ? (1u << C_DCNT) | (1u << C_DWORK) : 0u) |
                         (fused_advance ? (1u << C_CLEARED) : 0u)};
-  int kw = p->opt_bitmap_kw;
-  if (kw == 0) kw = 1;  // measured best at c = 24, 26, 28 (scripts/micro_bitmap.py)
+  const bool pend = p->pend_dirty;
+  uint32_t* pend_words = p->pend.as<uint32_t>();
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
-    // grid cap: a pool of <= 64 MiB gets one wave (6 CTAs per SM, the launch
-    // bound), looping, which leaves SM slots to the registry compaction and
-    // delta apply running beside the pass (cfg 2: 0.141 -> 0.134 ms per slice,
-    // cfg 3: 0.356 -> 0.348); a larger, HBM-bound pool keeps one word per thread.  VATE_XP_BITMAP_CAP overrides (A/B runs,
-    // scripts/xp_bitmap_grid.sh).
-    static const int cap_env = [] {
-      const char* e = getenv("VATE_XP_BITMAP_CAP");
-      return e ? atoi(e) : -1;
-    }();
-    const uint64_t pool_bytes = p->L.size * (uint64_t)p->cell_bytes;
-    const uint32_t cap = cap_env > 0 ? (uint32_t)cap_env
-                         : (pool_bytes <= (64ull << 20) ? 148u * 6u : 148u * 32u);
-    const uint32_t grid = grid_for((nwords + kw - 1) / kw, kThreads, cap);
-    // measured (scripts/micro_bitmap.py): evict-first reads are faster even for
-    // an L2-resident pool, so the normal-priority form stays off
-    const bool stream = true;
-    if (kw == 4)
-      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 4>), (T*)p->cells, p->L,
-                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub, SW);
-    else if (kw == 2)
-      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 2>), (T*)p->cells, p->L,
-                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P, D, pub, SW);
-    else if (stream)
-      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1, true>), (T*)p->cells,
-                  p->L, p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords,
-                  p->d_ctr + C_P, D, pub, SW);
+    // pools beyond L2 stream from HBM: each CTA bulk-prefetches its cells two
+    // steps ahead into L2 (one instruction per step), which takes the pass
+    // from 177 to 166 us at cfg 4 (profiles/r02c_ab_pass.txt); an L2-resident
+    // pool gains nothing from it
+    const uint32_t grid = grid_for(nwords, kThreads, p->cap_bitmap);
+    if (p->L.size * (uint64_t)sizeof(T) > kDeferBytes) {
+      if (pend)
+        VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, true, 2>), (T*)p->cells,
+                    p->L, p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords,
+                    p->d_ctr + C_P, D, pub, SW, pend_words);
+      else
+        VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, false, 2>), (T*)p->cells,
+                    p->L, p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords,
+                    p->d_ctr + C_P, D, pub, SW, pend_words);
+      return VATE_OK;
+    }
+    if (pend)
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, true>), (T*)p->cells, p->L,
+                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P,
+                  D, pub, SW, pend_words);
     else
-      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, 1, false>), (T*)p->cells,
-                  p->L, p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords,
-                  p->d_ctr + C_P, D, pub, SW);
+      VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, false>), (T*)p->cells, p->L,
+                  p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords, p->d_ctr + C_P,
+                  D, pub, SW, pend_words);
     return VATE_OK;
   });
   if (rc) return rc;
+  p->pend_dirty = false;
   // P (and the delta counts) reach the host with the estimate's one round trip,
   // written into pinned memory by the kernel's last CTA
   if (fused_advance) {  // AtPool.advance_slice bookkeeping; result via vate_advance_result
@@ -1088,6 +1081,45 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta, bool fused_advance)
     p->adv_pending = true;
     p->sweeps_fused++;
   }
+  return VATE_OK;
+}
+
+int flush_pending(vate_pool* p) {
+  if (!p->pend_dirty) return VATE_OK;
+  const uint64_t nwords = (p->L.size + 31) / 32;
+  int rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
+    using T = decltype(tag);
+    VATE_LAUNCH(p, VATE_K_OTHER, grid_for(nwords, kThreads, p->cap_bitmap), kThreads, 0,
+                k_apply_pending<T>, (T*)p->cells, p->L, p->bact0, p->pend.as<uint32_t>(), nwords);
+    return VATE_OK;
+  });
+  if (rc) return rc;
+  p->pend_dirty = false;
+  return VATE_OK;
+}
+
+// Auto: defer when the cells exceed 64 MiB (the part of the 126 MB L2 a pool
+// can keep beside the registry and the packet stream): cfg 4 / 5's 512 MiB.
+bool default_deferred(const vate_pool* p) {
+  return p->kind == VATE_AT && p->L.size * (uint64_t)p->cell_bytes > kDeferBytes;
+}
+
+int set_deferred(vate_pool* p, bool on) {
+  if (on && p->kind != VATE_AT) on = false;  // the comparators store constants directly
+  if (on == p->deferred) return VATE_OK;
+  if (!on) {
+    int rc = flush_pending(p);
+    if (rc) return rc;
+    p->deferred = false;
+    return VATE_OK;
+  }
+  const uint64_t bytes = ((p->L.size + 31) / 32) * 4;
+  if (p->pend.bytes < bytes) {
+    int rc = p->pend.ensure(bytes);
+    if (rc) return rc;
+    VATE_CUDA(cudaMemsetAsync(p->pend.ptr, 0, bytes, p->stream));
+  }
+  p->deferred = true;
   return VATE_OK;
 }
 
@@ -1177,11 +1209,6 @@ static int pool_create(vate_pool** out, int kind, int c, int k, int partition, i
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->aux_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaHostAlloc((void**)&p->h_flag, 64, cudaHostAllocMapped);
-  if (e == cudaSuccess) {
-    *p->h_flag = 0;
-    e = cudaHostGetDevicePointer((void**)&p->d_flag, (void*)p->h_flag, 0);
-  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
     for (cudaEvent_t* ev : {&p->ev_fin[i], &p->ev_d2h[i], &p->ev_h2d[i], &p->ev_used[i]})
@@ -1203,6 +1230,18 @@ static int pool_create(vate_pool** out, int kind, int c, int k, int partition, i
         return VATE_OK;
       });
   }
+  // grid caps of the kernels that share SMs in the slice step (round-1 A/B
+  // runs at cfg 2-4): a pool of <= 64 MiB gets a one-wave bitmap pass (its
+  // launch bound: 5 CTAs per SM for u8 cells, 4 for u16, looping), leaving SM
+  // slots to the registry compaction and the delta apply beside it; a larger,
+  // HBM-bound pool a contiguous run of ~1800 words per CTA; the compaction 3
+  // CTAs per SM.
+  const uint64_t pool_bytes = S * (uint64_t)p->cell_bytes;
+  p->cap_bitmap = pool_bytes <= (64ull << 20) ? 148u * (p->cell_bytes == 1 ? 5u : 4u) : 148u * 32u;
+  p->cap_active = 148u * 3u;
+  p->cap_inc = 148u * 16u;
+  p->cap_final = 148u * 16u;
+  if (rc == VATE_OK) rc = set_deferred(p, default_deferred(p));
   if (rc == VATE_OK) rc = sync_small(p);
   if (rc != VATE_OK) {
     vate_pool_destroy(p);
@@ -1243,7 +1282,7 @@ int vate_pool_destroy(vate_pool* p) {
   if (p->ev_counts) cudaEventDestroy(p->ev_counts);
   if (p->ev_post) cudaEventDestroy(p->ev_post);
   if (p->timeline_ref) cudaEventDestroy(p->timeline_ref);
-  if (p->h_flag) cudaFreeHost((void*)p->h_flag);
+  p->pend.release();
   if (p->d_done) cudaFree(p->d_done);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   inc_release(p);
@@ -1269,6 +1308,13 @@ int vate_pool_info(const vate_pool* p, int32_t* bact0, int32_t* cell_bytes, void
   if (bact0) *bact0 = (int32_t)p->bact0;
   if (cell_bytes) *cell_bytes = p->cell_bytes;
   if (stream) *stream = (void*)p->stream;
+  return VATE_OK;
+}
+
+int vate_pool_device_bytes(const vate_pool* p, int64_t* bytes) {
+  if (!p || !bytes) return set_error(VATE_EVALUE, "null argument");
+  const uint64_t cb = p->kind == VATE_TS ? 8 : (uint64_t)p->cell_bytes;
+  *bytes = (int64_t)(p->L.size * cb + (p->deferred ? p->pend.bytes : 0));
   return VATE_OK;
 }
 
@@ -1321,23 +1367,8 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_g0 = (int)value;
     return VATE_OK;
   }
-  if (option == VATE_OPT_L2_PERSIST && value >= 0 && value <= 2) {
-    p->opt_l2 = (int)value;
-    p->l2_base = nullptr;  // re-apply at the next scan
-    if (value == 0) {
-      cudaStreamAttrValue v{};
-      v.accessPolicyWindow.num_bytes = 0;
-      VATE_CUDA(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
-      VATE_CUDA(cudaCtxResetPersistingL2Cache());  // persisting lines would stay pinned
-    }
-    return VATE_OK;
-  }
   if (option == VATE_OPT_FUSE_SWEEP && (value == 0 || value == 1)) {
     p->opt_fuse_sweep = (int)value;
-    return VATE_OK;
-  }
-  if (option == VATE_OPT_SPIN_WAIT && (value == 0 || value == 1)) {
-    p->opt_spin = (int)value;
     return VATE_OK;
   }
   if (option == VATE_OPT_INC_SORT && (value == 0 || value == 1)) {
@@ -1348,23 +1379,20 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_concurrent = (int)value;
     return VATE_OK;
   }
-  if (option == VATE_OPT_BITMAP_KW && (value == 0 || value == 1 || value == 2 || value == 4)) {
-    p->opt_bitmap_kw = (int)value;
-    return VATE_OK;
-  }
-  if (option == VATE_OPT_SCAN_CHECK && value >= -1 && value <= 2) {
+  if (option == VATE_OPT_SCAN_FILTER && value >= -1 && value <= 1) {
     p->opt_scan_check = (int)value;
-    return VATE_OK;
-  }
-  if (option == VATE_OPT_SCAN_V &&
-      (value == 0 || value == 1 || value == 2 || value == 4 || value == 8)) {
-    p->opt_scan_v = (int)value;
     return VATE_OK;
   }
   if (option == VATE_OPT_INCREMENTAL && (value == 0 || value == 1)) {
     p->opt_inc = (int)value;
     if (!value) p->inc.valid = false;
     return VATE_OK;
+  }
+  if (option == VATE_OPT_DEFERRED && value >= -1 && value <= 1) {
+    int rc = enter(p);
+    if (rc) return rc;
+    p->opt_deferred = (int)value;
+    return set_deferred(p, value == 1 || (value == -1 && default_deferred(p)));
   }
   return set_error(VATE_EVALUE, "unknown option or value");
 }
@@ -1456,48 +1484,6 @@ int vate_set_cells(vate_pool* p, const uint64_t* idx, uint64_t n, int where) {
   });
 }
 
-// L2 persistence for the scan's random-access target (VATE_OPT_L2_PERSIST):
-// 1 = the host registry (one random 16-B probe per packet), 2 = the cells.
-// Streamed packets are loaded evict-first, so the persisting lines survive the
-// 40 MB per slice of packet traffic.  The window is a stream attribute; it is
-// re-set only when the target moved (registry growth) or changed size.
-static int apply_l2_window(vate_pool* p, vate_hosts* hosts) {
-  if (p->opt_l2 == 0) return VATE_OK;
-  void* base = nullptr;
-  size_t bytes = 0;
-  if (p->opt_l2 == 1 && hosts) {
-    base = hosts->table.ptr;
-    bytes = (hosts->cap + 1) * sizeof(RegEntry);
-  } else if (p->opt_l2 == 2) {
-    base = p->cells;
-    bytes = p->L.size * (size_t)p->cell_bytes;
-  }
-  if (!base || (base == p->l2_base && bytes == p->l2_bytes)) return VATE_OK;
-  static int configured[64] = {0};
-  int maxp = 0, maxw = 0;
-  VATE_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, p->device));
-  VATE_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, p->device));
-  if (maxp <= 0 || maxw <= 0) {
-    p->opt_l2 = 0;  // no persistence on this device
-    return VATE_OK;
-  }
-  if (p->device >= 0 && p->device < 64 && !configured[p->device]) {
-    VATE_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
-    configured[p->device] = 1;
-  }
-  const size_t win = std::min(bytes, (size_t)maxw);
-  cudaStreamAttrValue v{};
-  v.accessPolicyWindow.base_ptr = base;
-  v.accessPolicyWindow.num_bytes = win;
-  v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxp / (double)win);
-  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  VATE_CUDA(cudaStreamSetAttribute(p->stream, cudaStreamAttributeAccessPolicyWindow, &v));
-  p->l2_base = base;
-  p->l2_bytes = bytes;
-  return VATE_OK;
-}
-
 static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const uint64_t* bips,
                        const uint32_t* pairs, uint64_t n, int where, vate_hosts* hosts,
                        int64_t t) {
@@ -1511,19 +1497,12 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     if (rc) return rc;
     R = hosts->ref();
   }
-  rc = apply_l2_window(p, hosts);
-  if (rc) return rc;
-  // scan form: auto picks the registry-stamp filter for skewed traffic -- when
-  // the last compacted slice saw 8 or more packets per distinct host (Zipf-like
-  // heads whose same-address stamps serialise); plain stores otherwise
-  int chk = p->opt_scan_check;
-  if (chk < 0)
-    chk = (hosts && hosts->last_touched && n >= 8 * hosts->last_touched) ? 2 : 0;
-  p->scan_form_used = chk;
-  // packed16: one iteration of V uint4 (2V packets) per thread; others: grid-stride
-  const uint64_t per_thread = 2ull * (uint64_t)(p->opt_scan_v > 0 ? p->opt_scan_v : 1);
-  const uint32_t grid16 = grid_for((n + per_thread - 1) / per_thread, kThreads, 148u * 64u);
-  const uint32_t grid = grid_for(n, kThreads, 148u * 16u);
+  // registry-stamp filter: auto takes it for skewed traffic -- when the last
+  // compacted slice saw 8 or more packets per distinct host (Zipf-like heads
+  // whose same-address stamps serialise); plain stamps otherwise
+  int filt = p->opt_scan_check;
+  if (filt < 0) filt = (hosts && hosts->last_touched && n >= 8 * hosts->last_touched) ? 1 : 0;
+  p->scan_form_used = filt;
   if (pairs) {
     const void* d_pairs;
     rc = stage_in(p, p->in_a, pairs, n * 8, where, &d_pairs);
@@ -1532,72 +1511,36 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     return with_store(p, [&](auto tag, auto rule) -> int {
       using T = decltype(tag);
       using Rl = decltype(rule);
-      if (aligned16 && hosts && p->opt_scan_v == 8 && n >= (uint64_t)kTmaTile) {
-        // TMA-fed persistent scan over the full tiles; the remainder below
-        const uint64_t ntiles = n / kTmaTile, rest = n - ntiles * kTmaTile;
-        VATE_CUDA(cudaMemsetAsync(p->d_done + 2, 0, 4, p->stream));
-        const uint32_t gt = (uint32_t)umin64(ntiles, 148u * 4u);
-        if (chk)
-          VATE_LAUNCH(p, VATE_K_SCAN, gt, kThreads, 0, (k_scan_tma<T, 1, Rl>),
-                      (const uint2*)d_pairs, ntiles, (T*)p->cells, H, rule, R, (long long)t,
-                      p->d_done + 2);
-        else
-          VATE_LAUNCH(p, VATE_K_SCAN, gt, kThreads, 0, (k_scan_tma<T, 0, Rl>),
-                      (const uint2*)d_pairs, ntiles, (T*)p->cells, H, rule, R, (long long)t,
-                      p->d_done + 2);
-        if (rest)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid_for(rest, kThreads, 148u * 64u), kThreads, 0,
-                      (k_scan_packed8<T, true, 0, Rl>),
-                      (const uint2*)d_pairs + ntiles * kTmaTile, rest, (T*)p->cells, H, rule, R,
-                      (long long)t);
-      } else if (aligned16 && n >= 2 && p->opt_scan_v > 0 && p->opt_scan_v <= 4) {
-        if (hosts && p->opt_scan_v == 1 && chk == 2)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, 2, Rl>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
-                      (long long)t);
-        else if (hosts && p->opt_scan_v == 1 && chk)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, 1, Rl>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
-                      (long long)t);
-        else if (hosts && p->opt_scan_v == 1)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 1, 0, Rl>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
-                      (long long)t);
-        else if (hosts && p->opt_scan_v == 4)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 4, 0, Rl>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
-                      (long long)t);
+      T* cells = (T*)p->cells;
+      uint64_t done = 0;
+      if (aligned16 && n >= 2) {  // one uint4 (two packets) per thread
+        const uint64_t n2 = n / 2;
+        const uint32_t grid = grid_for(n2, kThreads, 148u * 64u);
+        const uint4* src = (const uint4*)d_pairs;
+        if (hosts && filt)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, true, Rl>),
+                      src, n2, cells, H, rule, R, (long long)t);
         else if (hosts)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, true, 2, 0, Rl>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
-                      (long long)t);
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, false, Rl>),
+                      src, n2, cells, H, rule, R, (long long)t);
         else
-          VATE_LAUNCH(p, VATE_K_SCAN, grid16, kThreads, 0, (k_scan_packed16<T, false, 2, 0, Rl>),
-                      (const uint4*)d_pairs, n / 2, (T*)p->cells, H, rule, R,
-                      (long long)t);
-        if (n & 1) {
-          const uint2* last = (const uint2*)d_pairs + (n - 1);
-          if (hosts)
-            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, true, 0, Rl>), last, 1,
-                        (T*)p->cells, H, rule, R, (long long)t);
-          else
-            VATE_LAUNCH(p, VATE_K_SCAN, 1, 32, 0, (k_scan_packed8<T, false, 0, Rl>), last, 1,
-                        (T*)p->cells, H, rule, R, (long long)t);
-        }
-      } else {  // unaligned input, or scan_v == 0: one 8-byte packet per thread
-        const uint32_t grid8 = grid_for(n, kThreads, 148u * 64u);
-        if (hosts && chk)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, true, 1, Rl>),
-                      (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
-                      (long long)t);
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, false, false, Rl>),
+                      src, n2, cells, H, rule, R, (long long)t);
+        done = 2 * n2;
+      }
+      if (done < n) {  // unaligned input, or the odd last packet: one packet per thread
+        const uint64_t m = n - done;
+        const uint32_t grid = grid_for(m, kThreads, 148u * 64u);
+        const uint2* src = (const uint2*)d_pairs + done;
+        if (hosts && filt)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, true, true, Rl>),
+                      src, m, cells, H, rule, R, (long long)t);
         else if (hosts)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, true, 0, Rl>),
-                      (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
-                      (long long)t);
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, true, false, Rl>),
+                      src, m, cells, H, rule, R, (long long)t);
         else
-          VATE_LAUNCH(p, VATE_K_SCAN, grid8, kThreads, 0, (k_scan_packed8<T, false, 0, Rl>),
-                      (const uint2*)d_pairs, n, (T*)p->cells, H, rule, R,
-                      (long long)t);
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed8<T, false, false, Rl>),
+                      src, m, cells, H, rule, R, (long long)t);
       }
       return VATE_OK;
     });
@@ -1607,6 +1550,7 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
   if (rc) return rc;
   rc = stage_in(p, p->in_b, bips, n * 8, where, &d_b);
   if (rc) return rc;
+  const uint32_t grid = grid_for(n, kThreads, 148u * 16u);
   return with_store(p, [&](auto tag, auto rule) -> int {
     using T = decltype(tag);
     using Rl = decltype(rule);
@@ -1712,6 +1656,8 @@ int vate_advance_async(vate_pool* p) {
   if (rc) return rc;
   if (p->adv_pending) return set_error(VATE_EVALUE, "previous advance not collected");
   if (p->kind != VATE_AT) return cmp_advance_async(p);
+  rc = flush_pending(p);  // marks take the clocks of the slice that made them
+  if (rc) return rc;
   const uint32_t B = p->L.B, k = p->L.k;
   p->bact0 = (p->bact0 + 1) % B;  // pools.py:228
   const uint32_t z = (B - p->bact0) % B, q = (k + B - p->bact0) % B;  // pools.py:231-232
@@ -1784,6 +1730,8 @@ int vate_inactive_mask(vate_pool* p, const uint64_t* idx, uint64_t n, int k_prim
   if (rc) return rc;
   rc = p->out_buf.ensure(n);
   if (rc) return rc;
+  rc = flush_pending(p);
+  if (rc) return rc;
   if (p->kind != VATE_AT)
     rc = cmp_inactive_mask(p, (const uint64_t*)d_idx, n, k_prime, p->out_buf.as<uint8_t>());
   else rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
@@ -1808,6 +1756,8 @@ int vate_get_cells(vate_pool* p, const uint64_t* idx, uint64_t n, uint32_t* out,
   rc = stage_in(p, p->in_a, idx, n * 8, where, &d_idx);
   if (rc) return rc;
   rc = p->out_buf.ensure(n * 4);
+  if (rc) return rc;
+  rc = flush_pending(p);
   if (rc) return rc;
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
@@ -1854,6 +1804,8 @@ int vate_snapshot(vate_pool* p, uint8_t* buf, uint64_t cap, uint64_t* len) {
   buf[9] = (uint8_t)((p->bact0 >> 8) & 0xFF);
   rc = p->out_buf.ensure(nwords * 8);
   if (rc) return rc;
+  rc = flush_pending(p);
+  if (rc) return rc;
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
     VATE_LAUNCH(p, VATE_K_OTHER, grid_for(nwords, kThreads), kThreads, 0, k_pack<T>,
@@ -1888,6 +1840,10 @@ int vate_load(vate_pool* p, const uint8_t* buf, uint64_t len) {
   rc = p->in_a.ensure(nwords * 8 + 8);
   if (rc) return rc;
   VATE_CUDA(cudaMemcpyAsync(p->in_a.ptr, buf + 16, nwords * 8, cudaMemcpyHostToDevice, p->stream));
+  if (p->pend_dirty) {  // every cell is overwritten: earlier marks are void
+    VATE_CUDA(cudaMemsetAsync(p->pend.ptr, 0, p->pend.bytes, p->stream));
+    p->pend_dirty = false;
+  }
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
     VATE_LAUNCH(p, VATE_K_OTHER, grid_for(p->L.size, kThreads), kThreads, 0, k_unpack<T>,
@@ -1908,6 +1864,14 @@ int vate_dirty_bitmap(vate_pool* p, uint32_t* bitmap_dev) {
   if (rc) return rc;
   rc = enter(p);
   if (rc) return rc;
+  const uint64_t nw = (p->L.size + 31) / 32;
+  if (p->deferred) {  // the pending marks are exactly the cells this rank set
+    if (!p->pend_dirty) VATE_CUDA(cudaMemsetAsync(bitmap_dev, 0, nw * 4, p->stream));
+    else VATE_CUDA(cudaMemcpyAsync(bitmap_dev, p->pend.ptr, nw * 4, cudaMemcpyDeviceToDevice, p->stream));
+    return VATE_OK;
+  }
+  rc = flush_pending(p);
+  if (rc) return rc;
   const uint64_t nwords = (p->L.size + 31) / 32;
   return with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
@@ -1927,7 +1891,9 @@ int vate_merge_dirty(vate_pool* p, const uint32_t* bitmaps_dev, int nranks) {
   return with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
     VATE_LAUNCH(p, VATE_K_OTHER, grid_for(nwords, kThreads), kThreads, 0, k_merge<T>, (T*)p->cells,
-                p->L, p->bact0, bitmaps_dev, nwords, nranks);
+                p->L, p->bact0, bitmaps_dev, nwords, nranks,
+                p->deferred ? p->pend.as<uint32_t>() : nullptr);
+    if (p->deferred) p->pend_dirty = true;
     return VATE_OK;
   });
 }

@@ -232,8 +232,22 @@ class _DevicePool:
 
     @property
     def memory_bytes(self) -> int:
-        """Device bytes of the cell array (unpacked cells)."""
-        return self.size * self.cell_bytes
+        """The reference's accounting of the pool (pools.py:257-259, :355-356,
+        :409-410): its packed words (AT: plus the snapshot header)."""
+        return self.packed_bytes
+
+    @property
+    def deferred(self) -> bool:
+        """Scans mark the pending-set bitmap instead of storing cells (VATE_OPT_DEFERRED)."""
+        return self.device_bytes > self.size * self.cell_bytes
+
+    @property
+    def device_bytes(self) -> int:
+        """What the pool occupies in HBM: unpacked cells (u8 / u16 / u32 / u64)
+        plus the pending-set bitmap of a deferred AT pool."""
+        pend = C.c_int64()
+        check(lib.vate_pool_device_bytes(self._h, C.byref(pend)))
+        return pend.value
 
     @property
     def cells(self) -> "DeviceCells":
@@ -245,12 +259,15 @@ class _DevicePool:
         check(lib.vate_pool_launches(self._h, C.byref(n)))
         return n.value
 
+    OPTIONS = ("g0_kernel", "incremental", "scan_filter", "concurrent", "inc_sort",
+               "fuse_sweep", "deferred")
+
     def set_option(self, option: str, value: int) -> None:
-        """Tuning switches: 'g0_kernel' (0 auto, 1 gather, 2 smem) and 'incremental' (0/1)."""
-        check(lib.vate_pool_set_option(self._h, ("g0_kernel", "incremental", "scan_v", "scan_check",
-                                                     "l2_persist", "bitmap_kw", "concurrent",
-                                                     "inc_sort", "spin_wait", "fuse_sweep").index(option),
-                                       int(value)))
+        """Tuning switches (include/vate.h enum vate_option): 'g0_kernel' (0 auto,
+        1 gather, 2 smem), 'incremental' (0/1), 'scan_filter' (-1 auto, 0, 1),
+        'concurrent', 'inc_sort', 'fuse_sweep' (0/1), 'deferred' (-1 auto, 0, 1).
+        Every setting leaves identical results."""
+        check(lib.vate_pool_set_option(self._h, self.OPTIONS.index(option), int(value)))
 
     def inc_stats(self) -> dict:
         """Counters of the incremental estimate."""
@@ -392,9 +409,36 @@ class DeviceCells:
         blob = self._pool.snapshot_bytes()
         return np.frombuffer(blob[_SNAPSHOT_HEADER.size:], dtype="<u8").copy()
 
+    # --- write API (bitpack.py:57-78, :97-140), device kernels -------------------
+    def set(self, idx, values) -> None:
+        """cells[idx] = values & mask; duplicate indices must carry equal values."""
+        idx = _as_u64(idx)
+        vals = np.ascontiguousarray(np.broadcast_to(
+            np.asarray(values, dtype=np.uint64), idx.shape)).reshape(-1)
+        idx = np.ascontiguousarray(idx.reshape(-1))
+        if idx.size:
+            check(lib.vate_put_cells(self._pool.handle, ptr(idx), ptr(vals), idx.size, VATE_HOST))
+
+    def set_one(self, i: int, value: int) -> None:
+        if not 0 <= i < self.size:
+            raise ValueError(f"cell index {i} outside [0, {self.size})")
+        self.set(np.array([i], dtype=np.uint64), np.array([int(value) & int(self.mask)],
+                                                           dtype=np.uint64))
+
+    def set_range(self, start: int, values) -> None:
+        values = np.asarray(values, dtype=np.uint64)
+        self.set(np.arange(start, start + len(values), dtype=np.uint64), values)
+
+    def fill(self, value: int) -> None:
+        """Every cell = value (ValueError if it exceeds the width, bitpack.py:57-60)."""
+        if int(value) >> self.width:
+            raise ValueError(f"value {value} exceeds {self.width} bits")
+        check(lib.vate_fill_cells(self._pool.handle, int(value)))
+
     @property
     def nbytes(self) -> int:
-        return self._pool.memory_bytes
+        """PackedArray.nbytes: packed words plus the guard word (bitpack.py:53-55)."""
+        return (-(-self.size * self.width // 64) + 1) * 8 if self.width < 64 else self.size * 8
 
 
 class DrPool(_DevicePool):

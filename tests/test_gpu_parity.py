@@ -954,20 +954,22 @@ def test_active_set_merge_under_small_churn(inc_sort):
         assert st["incremental"] == 0, st
 
 
-@pytest.mark.parametrize("form", [(1, 0), (1, 1), (1, 2), (0, 0), (0, 1), (2, 0), (4, 0), (8, 0), (8, 1)])
+@pytest.mark.parametrize("form", [(f, d, m) for f in (0, 1) for d in (0, 1) for m in (0, 1)])
 def test_scan_forms_are_equivalent(form):
-    """Every packed-scan form (VATE_OPT_SCAN_V: 0 one packet per thread, 1/2/4
-    uint4 per thread, 8 TMA-fed persistent; VATE_OPT_SCAN_CHECK heavy-hitter
-    form) leaves the reference's cells and host set: ATP1 bytes, reports and
-    the registry after skewed traffic (a heavy host, odd packet counts, tiles
-    plus remainders) equal the oracle's, slice by slice."""
+    """Every packed-scan form -- the per-CTA registry-stamp filter on / off
+    (VATE_OPT_SCAN_FILTER), direct cell stores or the deferred pending-set
+    marks (VATE_OPT_DEFERRED), 16-byte aligned input (two packets per thread,
+    plus the odd last packet) or misaligned input (one packet per thread) --
+    leaves the reference's cells and host set: ATP1 bytes, reports and the
+    registry after skewed traffic (a heavy host, odd packet counts) equal the
+    oracle's, slice by slice."""
     import torch
-    v, chk = form
+    filt, deferred, misaligned = form
     cfg = vb.EstimatorConfig(256, 16, 6, seed=5)
     ocfg = vo.OracleConfig(256, 16, 6, seed=5)
     pool = cfg.build_pool()
-    pool.set_option("scan_v", v)
-    pool.set_option("scan_check", chk)
+    pool.set_option("scan_filter", filt)
+    pool.set_option("deferred", deferred)
     pipe = vb.Pipeline(pool, cfg, 5)
     opipe = vo.OraclePipeline(ocfg, 5)
     rng = np.random.default_rng(31)
@@ -976,8 +978,10 @@ def test_scan_forms_are_equivalent(form):
         a = (0x0A000000 + rng.integers(0, 900, n)).astype(np.uint32)
         a[rng.random(n) < 0.3] = 0x0A0000FF                      # a heavy hitter
         b = rng.integers(1, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
-        pairs = torch.from_numpy(np.ascontiguousarray(np.stack([a, b], axis=1)).view(np.int32)).cuda()
-        got = pipe.step_fast(t, pairs.data_ptr(), n, "device",
+        flat = np.ascontiguousarray(np.stack([a, b], axis=1)).view(np.int32).reshape(-1)
+        buf = torch.zeros(flat.size + 2, dtype=torch.int32, device="cuda")
+        buf[misaligned * 2: misaligned * 2 + flat.size] = torch.from_numpy(flat).cuda()
+        got = pipe.step_fast(t, buf.data_ptr() + 8 * misaligned, n, "device",
                              (np.empty(2048, np.uint64), np.empty(2048), np.empty(2048),
                               np.empty(2048, np.uint8)))
         pipe.wait_reports()
@@ -1043,3 +1047,54 @@ def test_lagged_step_equals_oracle(floor, hosts0, two_calls):
     assert not want
     if two_calls:
         pl.log_zp_table = orig
+
+
+@pytest.mark.parametrize("deferred", [0, 1])
+def test_u16_pass_forms_over_two_windows(deferred):
+    """u16 cells (k = 300, the cfg 4 width) on a small pool for 2k + 5 slices:
+    direct or deferred stores, through the lagged slice step; the ATP1 bytes, P, maintenance and every report equal
+    the oracle's, with the clock wrapping and every block swept twice."""
+    k, c = 300, 16
+    cfg = vb.EstimatorConfig(64, c, k, seed=9)
+    ocfg = vo.OracleConfig(64, c, k, seed=9)
+    pool = cfg.build_pool()
+    pool.set_option("deferred", deferred)
+    pipe = vb.Pipeline(pool, cfg, k - 7)
+    opipe = vo.OraclePipeline(ocfg, k - 7)
+    rng = np.random.default_rng(77)
+    outs = [tuple(np.empty(4096, dt) for dt in (np.uint64, np.float64, np.float64, np.uint8))
+            for _ in range(2)]
+    want = {}
+
+    def check(res):
+        if res is None:
+            return
+        tp, rows = res
+        ww = want.pop(tp)
+        assert pipe.last_pool_inactive == ww.pool_inactive or ww.reports is None, tp
+        m = pipe.last_maintenance
+        assert (m.blocks, m.cells_maintained, m.cells_cleared) == (ww.due, ww.visited, ww.cleared)
+        if ww.reports is None or len(ww.reports.host) == 0:
+            assert rows is None or len(rows.host) == 0, tp
+        else:
+            assert np.array_equal(rows.host, ww.reports.host), tp
+            assert np.array_equal(rows.estimate, ww.reports.estimate), tp
+            assert np.array_equal(rows.z_v, ww.reports.z_v), tp
+
+    for t in range(2 * k + 5):
+        n = int(rng.integers(0, 300))
+        a = (0x0A000000 + rng.integers(0, 500, n)).astype(np.uint32)
+        b = rng.integers(1, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+        pairs = np.ascontiguousarray(np.stack([a, b], axis=1))
+        res = pipe.step_lagged(t, pairs.ctypes.data, n, "host", outs[t % 2])
+        want[t] = opipe.process_slice(t, a.astype(np.uint64), b.astype(np.uint64))
+        pipe.wait_reports()
+        check(res)
+        if t % 50 == 0:     # slice t's scan, pass and sweep are enqueued: the pool after t
+            assert pool.snapshot_bytes() == opipe.pool.snapshot_bytes(), t
+    check(pipe.flush_lagged(outs[(2 * k + 5) % 2]))
+    pipe.wait_reports()
+    assert not want
+    assert pool.snapshot_bytes() == opipe.pool.snapshot_bytes()
+    pipe.close()
+    pool.close()
