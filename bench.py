@@ -1,29 +1,33 @@
 #!/usr/bin/env python
 """Benchmark of the VATE hot path on B200 (contract: one JSON line on rank 0).
 
-A step is one whole slice of the reference's pipeline (pipeline.py:142-160)
-on BASELINE.json configs[1] -- the 40 Gb/s-equivalent trace: 5,000,000
-packets per slice from 1,000,000 hosts, pool 2^24, k = k' = 60, g = 1024,
-tail partition, seed 0, floor 0 (every active host's report is produced):
+A step is one whole slice of the reference's pipeline (pipeline.py:142-160).
+The default workload is BASELINE.json configs[3] (cfg 4), the largest
+single-GPU shape and the north star's k = 300 window: 5,000,000 packets per
+slice from 1,000,000 hosts, pool 2^28 (512 MiB of u16 cells, beyond L2),
+k = k' = 300, g = 1024, tail partition, seed 0, floor 0 (every active host's
+report is produced):
 
-    scan (hash + scatter 5M packets, register hosts)
+    scan (hash 5M packets, mark their cells, register hosts)
     -> estimate (sorted active hosts, Z_p + inactive bitmap, g0 of every
        active host, float path; SoA reports land in host memory)
     -> maintain (advance clocks, sweep the two due blocks), prune every k.
 
 `value`  = packets / device time of K steps with packets resident in HBM and
-           the SoA report rows left in HBM (every slice distinct and
-           pre-generated, 40 MB each: inputs are not L2-hot).
+           the SoA report rows left in HBM (every slice distinct, 40 MB each).
 `e2e`    = the same K steps through the public API from pinned HOST packet
            buffers: H2D of every slice's packets + D2H of every report row.
-The pool (16 MiB) is L2-resident by design across steps; it is state, not input.
+--config cfg1/cfg2/cfg3/cfg5 select the other BASELINE shapes (cfg 5: 100M
+packets per slice).
 
---impl reference: the CPU oracle port of the reference algorithm (oracle/;
-the reference itself is pure Python and cannot travel to the GPU box) on the
-same config, all host cores, each step a bounded sample extrapolated to the
-full slice.  Multi-GPU (torchrun, N > 1): each rank scans its own 5M-packet
-shard into a replica pool; replicas merge every slice by an all-gather of
-dirty bitmaps over NCCL; the active-host union is range-split for the estimate.
+--impl reference: the reference algorithm on the box's host cores, through
+the oracle port (oracle/: the reference is pure Python and cannot travel to
+the GPU box): per step one full slice -- the whole scan, host-set update,
+Z_p, advance -- with g0 + float path timed on a sample of the active hosts
+and scaled to all of them (the factor is in the line).  Multi-GPU (torchrun,
+N > 1): each rank scans its own shard into a replica pool; replicas merge
+every slice (fused peer-memory merge, or NCCL all-gathers); the active-host
+union is range-split for the estimate.
 """
 
 from __future__ import annotations
@@ -43,7 +47,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # BASELINE.json configs[1] -- the headline (default)
+    # BASELINE.json configs[1]: the 40 Gb/s-equivalent trace, L2-resident pool
     "cfg2": dict(name="cfg2-40Gbps-equivalent", c=24, k=60, k_prime=60, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
                  base_aip=0x0A000000),
@@ -56,7 +60,8 @@ WORKLOADS = {
     "cfg3": dict(name="cfg3-zipf-superspreaders", c=26, k=60, k_prime=60, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
                  base_aip=0x0A000000, zipf=True),
-    # configs[3]: long window, 512 MiB of u16 cells beyond L2
+    # configs[3]: long window, 512 MiB of u16 cells beyond L2 -- the headline
+    # (default): the largest single-GPU config and the north star's k = 300
     "cfg4": dict(name="cfg4-long-window-k300", c=28, k=300, k_prime=300, g=1024,
                  hosts=1_000_000, packets=5_000_000, seed=0, partition="tail", floor=0.0,
                  base_aip=0x0A000000),
@@ -66,7 +71,7 @@ WORKLOADS = {
                  hosts=1_000_000, packets=100_000_000, seed=0, partition="tail", floor=0.0,
                  base_aip=0x0A000000, strong=True),
 }
-WORKLOAD = WORKLOADS["cfg2"]
+WORKLOAD = WORKLOADS["cfg4"]
 METRIC = "Mpackets/s AT scan+update (full slice: scan+estimate+maintain)"
 UNIT = "Mpackets/s"
 PEAKS_FALLBACK = dict(hbm_gbs=6650.0)
@@ -76,26 +81,20 @@ KERNEL_SYMBOL = {"scan": "k_scan_packed16", "bitmap": "k_bitmap", "g0": "k_g0", 
                  "registry": "k_active", "sweep": "k_sweep"}
 
 
-def _ncu_traffic(kind, cfg="cfg2"):
+def _ncu_traffic(kind, cfg):
     """dram read+write bytes per launch of the kernel behind `kind` for this workload,
-    from the committed ncu --set full summaries (profiles/*ncu_kernels.txt; captures of
-    other configs are named *_<cfg>_*, cfg 2's carry no config tag); None if not captured."""
+    from the committed ncu --set full summaries (profiles/*ncu_kernels.txt, sections
+    "## <tag>_<cfg>_<kernel>..."; newest file first); None if not captured."""
     import glob
     sym = KERNEL_SYMBOL.get(kind)
     if sym is None:
         return None
-
-    def mine(header):
-        if "_full" in header or sym not in header:
-            return False
-        return f"_{cfg}_" in header if cfg != "cfg2" else "_cfg" not in header
-
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_kernels.txt")), reverse=True):
         cur, vals = None, {}
         for line in open(path):
             if line.startswith("## "):
                 cur = line
-            elif cur and mine(cur) and "dram__bytes" in line:
+            elif cur and sym in cur and f"_{cfg}_" in cur and "dram__bytes" in line:
                 parts = line.split()
                 v, unit = float(parts[1]), parts[2] if len(parts) > 2 else "byte"
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
@@ -164,67 +163,102 @@ class ClockSampler:
 # CPU arm: the oracle port on the box's host cores
 # ----------------------------------------------------------------------------------
 
-def cpu_sample(w, seconds_budget=20.0, workers=None, sample_packets=1_000_000,
-               sample_hosts=1000, steps=1, kind="at"):
-    """Time the oracle pipeline on a bounded sample of the workload, per slice.
+def cpu_sample(w, steps=1, host_sample=100_000, kind="at", warmup=0):
+    """The reference algorithm on the host cores, per slice of the workload.
 
-    Scan: `sample_packets` of the slice's packets (rate extrapolated to the full
-    slice).  Estimate: Z_p over the whole pool plus g0 + float path for
-    `sample_hosts` active hosts, extrapolated to the full active set.  Maintain:
-    the real two-block advance.  Returns seconds per full slice and details.
+    AT pools: the oracle's C half (oracle/native.py, OpenMP over every host
+    thread) plus its numpy parts, one FULL slice per step: hashing and setting
+    all of the slice's packets with the reference's per-block value histogram
+    (pools.py:163-178), the host-set update and active set (pipeline.py:43-64),
+    Z_p from the histogram (pools.py:195-204), g0 + float path for
+    `host_sample` of the active hosts (estimator.py:107-181; the one phase that
+    is sampled: its time is scaled by active / sampled hosts), and the
+    two-block advance (pools.py:221-249).  DR / TS comparators: the numpy
+    oracle pipeline on a 1M-packet sample.  Returns (mean seconds per full
+    slice by phase, threads, sample description).
     """
     from oracle import vate_oracle as vo
-    workers = workers or os.cpu_count()
+    threads = len(os.sched_getaffinity(0))
     cfg = vo.OracleConfig(w["g"], w["c"], w["k"], seed=w["seed"], partition=w["partition"])
-    pipe = vo.OraclePipeline(cfg, w["k_prime"], floor=w["floor"], workers=workers, kind=kind)
-    per_step = []
-    sample_packets = min(sample_packets, w["packets"])
     tables = (vo.zipf_cdf(w["hosts"]), vo.spreader_cdf()) if w.get("zipf") else None
-    for t in range(steps):
-        if tables is not None:
-            a, b = vo.synthetic_zipf_slice(t, sample_packets, w["hosts"], *tables,
-                                           base_aip=w["base_aip"])
-        else:
-            a, b = vo.synthetic_slice(t, sample_packets, w["hosts"], w["base_aip"])
-        t0 = time.perf_counter()
-        pipe.scan(a, b)
-        t1 = time.perf_counter()
-        hosts = np.unique(a)[:sample_hosts]
-        p = pipe.pool.count_inactive(w["k_prime"])
-        t2 = time.perf_counter()
-        g0 = pipe.g0(hosts)
-        vo.reports_soa(cfg, hosts, g0, p, t, w["k_prime"])
-        t3 = time.perf_counter()
-        pipe.pool.advance()
-        t4 = time.perf_counter()
-        scan_s = (t1 - t0) * w["packets"] / sample_packets
-        est_s = (t2 - t1) + (t3 - t2) * w["hosts"] / len(hosts)
-        per_step.append(dict(scan_s=scan_s, estimate_s=est_s, maintain_s=t4 - t3,
-                             slice_s=scan_s + est_s + (t4 - t3)))
-    pipe.close()
-    mean = {k: float(np.mean([s[k] for s in per_step])) for k in per_step[0]}
-    return mean, workers
+    n = w["packets"]
+    per_step = []
+    if kind != "at":
+        pipe = vo.OraclePipeline(cfg, w["k_prime"], floor=w["floor"], workers=threads, kind=kind)
+        m = min(n, 1_000_000)
+        for t in range(warmup + steps):
+            a, b = vo.synthetic_slice(t, m, w["hosts"], w["base_aip"])
+            t0 = time.perf_counter()
+            pipe.scan(a, b)
+            t1 = time.perf_counter()
+            hosts = np.unique(a)[:1000]
+            p = pipe.pool.count_inactive(w["k_prime"])
+            g0 = pipe.g0(hosts)
+            vo.reports_soa(cfg, hosts, g0, p, t, w["k_prime"])
+            t2 = time.perf_counter()
+            pipe.pool.advance()
+            t3 = time.perf_counter()
+            if t >= warmup:
+                per_step.append(dict(scan_s=(t1 - t0) * n / m, estimate_s=(t2 - t1) * w["hosts"] / 1000,
+                                     maintain_s=t3 - t2))
+        pipe.close()
+        sample = (f"numpy oracle ({kind} pool), {m:,} of {n:,} packets and g0 of 1,000 hosts "
+                  f"per step, both scaled to the full slice")
+    else:
+        from oracle import native
+        pool = vo.OraclePool(w["c"], w["k"], w["partition"]).track_histogram()
+        hosts = vo.OracleHostsVec(w["k"])
+        scale = []
+        for t in range(warmup + steps):
+            if tables is not None:
+                a, b = vo.synthetic_zipf_slice(t, n, w["hosts"], *tables, base_aip=w["base_aip"])
+            else:
+                a, b = native.synthetic_slice(t, n, w["hosts"], w["base_aip"])
+            t0 = time.perf_counter()
+            native.set_cells(pool, native.pair_cells(cfg, a, b))     # scan (estimator.py:96-104)
+            hosts.update(a.astype(np.uint32), t)                       # SlidingHostSet.update
+            t1 = time.perf_counter()
+            act = hosts.active(t, w["k_prime"])
+            p = pool.count_inactive(w["k_prime"])
+            sub = act[:host_sample] if len(act) > host_sample else act
+            t2 = time.perf_counter()
+            g0 = native.host_g0(pool, cfg, sub, w["k_prime"])
+            rep = vo.reports_soa(cfg, sub, g0, p, t, w["k_prime"])
+            if w["floor"] > 0:
+                rep = rep.select(rep.estimate >= w["floor"])
+            t3 = time.perf_counter()
+            pool.advance()
+            if t % w["k"] == 0:
+                hosts.prune(t)
+            t4 = time.perf_counter()
+            f = len(act) / max(1, len(sub))
+            if t >= warmup:
+                scale.append(f)
+                per_step.append(dict(scan_s=t1 - t0, estimate_s=(t2 - t1) + (t3 - t2) * f,
+                                     maintain_s=t4 - t3))
+        sample = (f"oracle port (C half, {threads} threads + numpy): per step one full slice -- "
+                  f"all {n:,} packets scanned, host set, Z_p, advance -- with g0 + float path "
+                  f"for {min(host_sample, w['hosts']):,} of the ~{w['hosts']:,} active hosts, "
+                  f"scaled by x{float(np.mean(scale)):.1f}")
+    mean = {k: float(np.mean([s_[k] for s_ in per_step])) for k in per_step[0]}
+    mean["slice_s"] = mean["scan_s"] + mean["estimate_s"] + mean["maintain_s"]
+    return mean, threads, sample
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     w = WORKLOAD
-    for _ in range(args.warmup):
-        cpu_sample(w, steps=1, kind=args.counter)
-    mean, cores = cpu_sample(w, steps=args.steps, kind=args.counter)
+    mean, cores, sample = cpu_sample(w, steps=args.steps, kind=args.counter, warmup=args.warmup)
     value = w["packets"] / mean["slice_s"] / 1e6
-    sample = (f"per step: scan of {min(1_000_000, w['packets']):,} of the slice's "
-              f"{w['packets']:,} packets and g0 of 1,000 of its ~{w['hosts']:,} active hosts "
-              f"(both extrapolated), full-pool Z_p and the real two-block advance; oracle port "
-              f"with {cores} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean["slice_s"] * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype(w),
-        "data": "synthetic (oracle.synthetic_slice)",
-        "config": dict(_config(w, world), counter=args.counter),
-        "estimate_ms_per_slice": mean["estimate_s"] * 1e3,
+        "data": "synthetic (oracle.synthetic_slice == csrc k_synth)",
+        "config": _config(w, world),
+        "path": {"counter": args.counter},
+        "phases_ms_per_slice": {k[:-2]: v * 1e3 for k, v in mean.items() if k != "slice_s"},
         "scan_mpps": w["packets"] / mean["scan_s"] / 1e6,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
@@ -479,106 +513,104 @@ def run_gpu(args, rank, world, local_rank):
         _teardown(dist)
         return
 
+    # --- after the timed regions (rank 0): latency, the list API, ceilings -----------
+    extra = {}
+    if world == 1 and args.counter == "at":
+        extra = after_timing(args, w, vb, pipe, pool, n, t, dslices, n_dev, di, out_sets, lagged)
+        t = extra.pop("_t")
+
     # speed of light of the scan's memory pattern on this pool shape: one random
     # 32-B registry-sized load + one random cell store per packet, no hashing,
     # no input stream (scratch pool; csrc vate_bench_sol_scatter)
-    sol = None
-    if rank == 0:
-        scratch_pool = vb.AtPool(w["c"], w["k"], w["partition"], device=dev)
-        table_bytes = 16 * (1 << max(12, (2 * w["hosts"] - 1).bit_length()))
-        sol_ms = C.c_double()
-        check(lib.vate_bench_sol_scatter(scratch_pool.handle, n, table_bytes, 10,
-                                         C.byref(sol_ms)))
-        scratch_pool.close()
-        sol = {"ms_per_slice_of_packets": sol_ms.value, "registry_table_bytes": table_bytes,
-               "pool_bytes": (1 << w["c"]) * (1 if 2 * w["k"] <= 254 else 2)}
+    scratch_pool = vb.AtPool(w["c"], w["k"], w["partition"], device=dev)
+    table_bytes = 16 * (1 << max(12, (2 * w["hosts"] - 1).bit_length()))
+    sol_ms = C.c_double()
+    check(lib.vate_bench_sol_scatter(scratch_pool.handle, n, table_bytes, 10, C.byref(sol_ms)))
+    l2 = scratch_pool.l2_ceilings()
+    scratch_pool.close()
+    sol = {"ms_per_slice_of_packets": sol_ms.value, "registry_table_bytes": table_bytes,
+           "pool_bytes": (1 << w["c"]) * pool.cell_bytes}
 
     peaks, peak_src = _peaks()
     hbm = float(peaks["hbm_gbs"])
-    # dominant kernel by event time; algorithmic bytes per launch
     per_kind = {k: {"ms_total": v[0], "launches": v[1],
                     "ms_per_launch": (v[0] / v[1] if v[1] else 0.0)} for k, v in kt.items()}
     nh = pipe.last_active
     S = 1 << w["c"]
+    cb = pool.cell_bytes
+    deferred = bool(pool.deferred)
+    inc_on = args.incremental == "on"
+    # algorithmic bytes per launch: the scan 40 B per
+    # packet (8 B streamed pair + one 32-B sector for its scattered cell write);
+    # the pool pass reads every cell and writes the bitmap, plus the previous
+    # bitmap (incremental delta) and the pending marks (deferred pools)
     alg_bytes = {
-        "g0": (nh * (32 * w["g"] + 12) if args.incremental == "off" else None),
-        "scan": n * 40,                                # 8 B pair + one 32 B sector write
-        "bitmap": S * pool.cell_bytes + S // 8,        # pool read + bitmap write
-        "sweep": (2 * pool.cell_bytes * 2 * pool.max_block_size if args.counter == "at" else
-                  2 * pool.cell_bytes * S if args.counter == "dr" else 0),
+        "scan": n * 40,
+        "bitmap": S * cb + S // 8 + (S // 8 if inc_on else 0) + (S // 8 if deferred else 0),
+        "g0": (nh * (32 * w["g"] + 12) if not inc_on else None),
+        "sweep": (2 * cb * 2 * pool.max_block_size if args.counter == "at" else
+                  2 * cb * S if args.counter == "dr" else 0),
         "final": nh * (4 + 8 + 8 + 8 + 8 + 1),
         "registry": nh * 32,
         "sort": nh * 8 * 4 * 2,
         "other": 0,
     }
-    # the dominant kernel among those with a defined per-unit figure (the incremental
-    # g0 family has none in SURVEY §8(d); its work is reported in "incremental").
-    # Kernels on the aux stream run beside the scan, so their event times include
-    # waiting for SMs; only main-stream kernels compete (ncu's serialised launch list,
-    # profiles/*launches_summary.txt, gives the same answer: the scan, or the
-    # full-recompute gather)
-    main_stream = ("scan", "bitmap", "g0") if args.incremental == "off" else ("scan", "bitmap")
-    dom = max((k for k in main_stream if alg_bytes.get(k)), key=lambda k: per_kind[k]["ms_total"])
-    dk = per_kind[dom]
-    achieved = alg_bytes[dom] / (dk["ms_per_launch"] / 1e3) / 1e9 if dk["ms_per_launch"] else 0.0
     for kind, v in per_kind.items():   # the same accounting for every kernel, for context
         if v["ms_per_launch"] and alg_bytes.get(kind):
             v["alg_gbs"] = alg_bytes[kind] / (v["ms_per_launch"] / 1e3) / 1e9
             v["frac_of_hbm"] = v["alg_gbs"] / hbm
+    # the dominant kernel: largest event time among the main-stream kernels (the
+    # aux-stream ones run beside them; profiles/*launches* has the serialised view)
+    main_stream = ("scan", "bitmap", "g0") if not inc_on else ("scan", "bitmap")
+    rooflines = {k: _roofline(k, per_kind[k], alg_bytes[k], hbm, peak_src, l2, n, S, cb, w,
+                              deferred, args.config)
+                 for k in main_stream if alg_bytes.get(k) and per_kind[k]["ms_per_launch"]}
+    dom = max(rooflines, key=lambda k: per_kind[k]["ms_total"])
     step_ms = max_ms / args.steps
-    cpu_mean, cores = cpu_sample(w, steps=1, kind=args.counter) if world == 1 else (None, None)
+    cpu = cpu_sample(w, steps=1, kind=args.counter) if world == 1 else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "strong" if w.get("strong") else "weak", "vs_baseline": None,
         "dtype": _dtype(w),
         "data": "synthetic (csrc k_synth == oracle.synthetic_slice)",
-        "config": dict(_config(w, world), counter=args.counter,
-                       scan_filter={-1: "auto (registry-stamp filter at >= 8 packets per host)",
-                                    0: "off", 1: "on"}[scan_filter],
-                       deferred_scatter=bool(pool.deferred)),
-        "estimate_ms_per_slice": sum(per_kind[k]["ms_total"] for k in
-                                     ("registry", "sort", "bitmap", "g0", "final")) / args.steps,
-        "estimate_ms_per_slice_note": "sum of the estimate kernels' event times (registry "
-                                      "compaction, sort, bitmap+delta, g0, float path); in the "
-                                      "pipelined step several run beside the scan, so this "
-                                      "overstates their share of ms_per_step",
+        "config": _config(w, world),
+        "path": {"counter": args.counter,
+                 "scan_filter": {-1: "auto (registry-stamp filter at >= 8 packets per host)",
+                                 0: "off", 1: "on"}[args.scan_filter],
+                 "deferred_scatter": deferred, "incremental_g0": inc_on,
+                 "slice_step": "lagged (Pipeline.step_lagged)" if lagged else "Pipeline.step_fast"},
+        "roofline": rooflines[dom],
+        "rooflines": rooflines,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": slice_bytes,
+                "d2h_bytes_per_step": int(e2e_rows / e2e_steps * 25),
+                "steps": e2e_steps,
+                "host_ms_per_step": {k: v / e2e_steps for k, v in host_ms.items()}},
+        "gpu_launches": int(launches),
+        **extra,
         "scan_update_mpps": n / ((per_kind["scan"]["ms_total"] + per_kind["sweep"]["ms_total"])
                                  / args.steps / 1e3) / 1e6,
         "reports_per_slice": nh,
-        "maintain_ms_per_slice": (per_kind["sweep"]["ms_total"] / args.steps
-                                  if per_kind["sweep"]["launches"] else None),
         "maintain_note": (("AT: the two due blocks (pools.py:221-249)" +
                            ("" if per_kind["sweep"]["launches"] else
-                            ", swept inside the bitmap pass (no separate launch)"))
+                            ", swept inside the pool pass (no separate launch)"))
                           if args.counter == "at" else
                           "DR: every cell slides (pools.py:339-349)" if args.counter == "dr" else
                           "TS: no maintenance (pools.py:399-401)"),
         "kernels": per_kind,
         "kernels_note": "CUDA-event time per launch on each kernel's own stream; aux-stream "
                         "kernels (registry compaction, delta apply, float path) overlap the "
-                        "scan or bitmap pass and their times include that overlap; "
-                        "profiles/*launches_summary.txt has the serialised ncu times",
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": _ncu_traffic(dom, args.config),
-                     "traffic_source": "profiles/*ncu_kernels.txt (ncu --set full, one launch)",
-                     "algorithmic_bytes_per_launch": alg_bytes[dom]},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": slice_bytes,
-                "d2h_bytes_per_step": int(e2e_rows / e2e_steps * 25),
-                "steps": e2e_steps,
-                "host_ms_per_step": {k: v / e2e_steps for k, v in host_ms.items()}},
-        "gpu_launches": int(launches),
-        "slice_step": "lagged (Pipeline.step_lagged)" if lagged else "Pipeline.step_fast",
-        "active_set_ordering": pool.sort_stats(),
+                        "scan or the pool pass and their times include that overlap; "
+                        "profiles/*launches* has the serialised ncu times",
+        "l2_ceilings": l2,
         "scan_speed_of_light": dict(sol, scan_ms_per_launch=per_kind["scan"]["ms_per_launch"],
                                     scan_over_sol=per_kind["scan"]["ms_per_launch"]
                                     / sol["ms_per_slice_of_packets"],
                                     note="random 32-B load (registry-sized table) + random "
                                          "cell store per packet, no hashing or packet "
-                                         "stream: the L2/HBM random-access ceiling") if sol else None,
-        "g0_kernel": args.g0_kernel,
-        "incremental": {"enabled": args.incremental == "on",
+                                         "stream: the L2/HBM random-access ceiling"),
+        "active_set_ordering": pool.sort_stats(),
+        "incremental": {"enabled": inc_on,
                         **{k: inc1[k] - inc0[k] for k in ("rebuilds", "delta_slices",
                                                           "refresh_slices", "full_slices",
                                                           "extends")},
@@ -595,15 +627,130 @@ def run_gpu(args, rank, world, local_rank):
                             **(replica.info() if args.exchange == "p2p" else {})}
         if args.share_device:
             line["config"]["parallelism"] += " (ranks share cuda:0: functional check, not scaling)"
-    if cpu_mean is not None:
-        line["cpu_baseline"] = {
-            "value": w["packets"] / cpu_mean["slice_s"] / 1e6, "unit": UNIT, "cores": cores,
-            "kind": "port",
-            "sample": f"one slice: scan of {min(1_000_000, w['packets']):,} of {w['packets']:,} "
-                      f"packets, g0 of 1,000 of ~{w['hosts']:,} hosts (extrapolated), full Z_p "
-                      f"and advance; numpy oracle, all host threads"}
+    if cpu is not None:
+        cpu_mean, cores, sample = cpu
+        line["cpu_baseline"] = {"value": w["packets"] / cpu_mean["slice_s"] / 1e6, "unit": UNIT,
+                                "cores": cores, "kind": "port", "sample": sample}
     print(json.dumps(line), flush=True)
     _teardown(dist)
+
+
+def _roofline(kind, k, alg, hbm, peak_src, l2, n, S, cb, w, deferred, cfg):
+    """One kernel's roofline: HBM (algorithmic bytes / launch time against the
+    measured copy bandwidth) and, for work L2 serves, the L2 ceiling: the time
+    the L2 probes need for the kernel's random accesses (or its stream) over
+    the launch time."""
+    t = k["ms_per_launch"] / 1e3
+    achieved = alg / t / 1e9
+    r = {"bound": "hbm", "kernel": kind, "achieved": achieved, "peak": hbm,
+         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
+         "traffic": _ncu_traffic(kind, cfg),
+         "traffic_source": "profiles/*ncu_kernels.txt (ncu --set full, one launch)",
+         "algorithmic_bytes_per_launch": alg}
+    pool_in_l2 = S * cb <= (64 << 20)
+    if kind == "scan":
+        # per packet: its cell write (a red.or into the L2-resident mark bitmap when
+        # deferred, a random store into an L2-resident pool otherwise -- beyond L2 it
+        # is the HBM sector above) and one random sector read of the host registry
+        write_rate = l2["random_red_or_G_per_s"] if deferred else l2["random_u16_stores_G_per_s"]
+        t_l2 = n / (l2["random_sector_reads_G_per_s"] * 1e9)
+        if deferred or pool_in_l2:
+            t_l2 += n / (write_rate * 1e9)
+        r["l2"] = {"ceiling_ms": t_l2 * 1e3, "frac": t_l2 / t,
+                   "model": "n random 32-B registry reads + n random cell writes "
+                            "(red.or marks when deferred) at the probed L2 rates"}
+        if deferred or pool_in_l2:
+            r["bound"] = "l2"
+    elif kind == "bitmap" and pool_in_l2:
+        t_l2 = (S * cb + 3 * S // 8) / (l2["stream_read_GB_per_s"] * 1e9)
+        r["l2"] = {"ceiling_ms": t_l2 * 1e3, "frac": t_l2 / t,
+                   "model": "the pool and bitmaps streamed at the probed L2 read rate"}
+        r["bound"] = "l2"
+    elif kind == "g0":
+        t_l2 = w["g"] * (alg / (32 * w["g"] + 12)) / (l2["random_sector_reads_G_per_s"] * 1e9)
+        r["l2"] = {"ceiling_ms": t_l2 * 1e3, "frac": t_l2 / t,
+                   "model": "g random 32-B bitmap reads per host at the probed L2 rate"}
+        r["bound"] = "l2"
+    return r
+
+
+def after_timing(args, w, vb, pipe, pool, n, t, dslices, n_dev, di, out_sets, lagged):
+    """Measurements after the timed regions (rank 0, N = 1): the per-slice
+    estimate latency (CUDA events from the end of a slice's scan to its SoA
+    report rows in pinned host memory) for the one-call step
+    with the incremental g0 and with the full recompute, and for the lagged
+    step; then the reference's own list API (Pipeline.process_slice from u64
+    host arrays -> list[EstimateReport], pipeline.py:142-166), with the
+    EstimateReport materialisation timed apart."""
+    import torch
+    res = {}
+
+    def lat_run(fn, m):
+        nonlocal t
+        for i in range(2):   # unmeasured: index rebuilds after a switch land here
+            fn(t, dslices[(di + i) % n_dev].data_ptr(), n, "device", out_sets[t % 2])
+            t += 1
+        pipe.wait_reports()
+        pool.set_latency(True)
+        for i in range(m):
+            fn(t, dslices[(di + i) % n_dev].data_ptr(), n, "device", out_sets[t % 2])
+            t += 1
+        pipe.wait_reports()
+        r = pool.latency()
+        pool.set_latency(False)
+        return r
+
+    def fast(t_, ptr_, n_, where, out):
+        rep = pipe.step_fast(t_, ptr_, n_, where, out)
+        pipe.wait_reports()
+        return rep
+
+    m = 6
+    res_lat = {"definition": "CUDA events: end of the slice's scan (compute stream) -> its "
+                             "SoA report rows (host, estimate, z_v, saturated) landed in "
+                             "pinned host memory (copy stream)",
+               "hosts": None}
+    res_lat["step_fast_incremental"] = lat_run(fast, m)
+    res_lat["hosts"] = pipe.last_active
+    inc_was = args.incremental == "on"
+    pool.set_option("incremental", 0)
+    res_lat["step_fast_full_recompute"] = lat_run(fast, m)
+    pool.set_option("incremental", 1 if inc_was else 0)
+    if lagged:
+        lat = lat_run(lambda *a: pipe.step_lagged(*a), m)
+        pipe.flush_lagged(out_sets[t % 2])
+        pipe.wait_reports()
+        lat["note"] = ("the lagged step completes slice t during the call for slice t+1, "
+                       "so this includes the next slice's scan")
+        res_lat["step_lagged"] = lat
+    res["estimate_latency_ms"] = res_lat
+
+    # the reference's list API from u64 host arrays (two slices)
+    rows = []
+    for i in range(2):
+        pr = dslices[(di + i) % n_dev].cpu().numpy().view(np.uint32)
+        a, b = pr[:, 0].astype(np.uint64), pr[:, 1].astype(np.uint64)
+        t0 = time.perf_counter()
+        soa, stats = pipe.process_slice_soa(t, a, b)
+        t1 = time.perf_counter()
+        lst = [] if soa is None else soa.to_list()
+        t2 = time.perf_counter()
+        rows.append({"slice_ms": (t1 - t0) * 1e3, "to_list_ms": (t2 - t1) * 1e3,
+                     "reports": len(lst), "slice_stats_us": {"scan": stats.scan_us,
+                                                              "estimate": stats.estimate_us,
+                                                              "maintain": stats.maintain_us}})
+        t += 1
+        del lst
+    res["list_api"] = {
+        "call": "Pipeline.process_slice(t, u64 aips, u64 bips) -> list[EstimateReport]",
+        "slices": rows,
+        "mpps_without_objects": n / (np.mean([r["slice_ms"] for r in rows]) / 1e3) / 1e6,
+        "mpps_with_objects": n / (np.mean([r["slice_ms"] + r["to_list_ms"] for r in rows]) / 1e3)
+                             / 1e6,
+        "note": "the u64 arrays (16 B per packet) cross PCIe each slice; the 1M Python "
+                "EstimateReport objects are the reference's own output type"}
+    res["_t"] = t
+    return res
 
 
 def _teardown(dist):
@@ -633,8 +780,8 @@ def main():
     ap.add_argument("--concurrent", type=int, choices=(0, 1), default=1,
                     help="registry compaction beside the bitmap pass, advance beside g0 + float "
                          "path, on a second stream (VATE_OPT_CONCURRENT)")
-    ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2",
-                    help="workload shape (BASELINE.json configs); cfg2 is the headline")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg4",
+                    help="workload shape (BASELINE.json configs); cfg4 is the headline")
     ap.add_argument("--incremental", choices=("on", "off"), default="on",
                     help="exact incremental g0 through the inverse index (VATE_OPT_INCREMENTAL)")
     ap.add_argument("--counter", choices=("at", "dr", "ts"), default="at",

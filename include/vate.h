@@ -69,6 +69,15 @@ int vate_pool_info(const vate_pool* p, int32_t* bact0, int32_t* cell_bytes, void
 /* HBM the pool's cells occupy (unpacked) plus a deferred pool's pending-set
  * bitmap; the reference's packed accounting (pools.py:257-259) is host-side. */
 int vate_pool_device_bytes(const vate_pool* p, int64_t* bytes);
+/* Per-slice estimate latency of the slice steps (vate_slice_step and the
+ * lagged step): with on = 1, CUDA events mark the end of each slice's scan
+ * (compute stream) and the landing of its report rows in host memory (copy
+ * stream).  out = [slices measured, mean ms, max ms, last ms]. */
+int vate_pool_set_latency(vate_pool* p, int on);
+int vate_pool_latency(vate_pool* p, double out[4]);
+/* The same marks for a slice driven by separate calls (scan, then the
+ * estimate's begin/finish): which = 0 after the scan, 1 after the finish. */
+int vate_pool_lat_mark(vate_pool* p, int64_t t, int which);
 int vate_pool_sync(vate_pool* p);
 /* cumulative count of kernels this pool (and its registries) launched */
 int vate_pool_launches(const vate_pool* p, uint64_t* n);
@@ -382,6 +391,12 @@ int vate_trace_bucket(vate_pool* p, const uint8_t* records, uint64_t n, int wher
 
 /* stream-ordered device-to-device copy on the pool's stream (ingest carry) */
 int vate_copy_device(vate_pool* p, void* dst, const void* src, uint64_t bytes);
+/* L2 ceilings for bench.py's rooflines (measurement only): over an
+ * L2-resident buffer of buf_bytes (power of two), n random accesses per
+ * launch, reps timed launches after a warm-up; out = [random 32-B sector
+ * reads G/s, random 2-byte stores G/s, random 32-bit red.or G/s, streaming
+ * read GB/s]. */
+int vate_bench_l2(vate_pool* p, uint64_t buf_bytes, uint64_t n, int reps, double out[4]);
 
 /* ---- speed-of-light probe (bench only) -----------------------------------
  * n "packets" of the scan's memory pattern without its arithmetic or input

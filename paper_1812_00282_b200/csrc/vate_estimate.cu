@@ -774,6 +774,8 @@ int vate_slice_step(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_s
     rc = vate_scan_packed(p, g, cell_stream, group_stream, pairs, n, where, hosts, t);
   }
   if (rc) return rc;
+  rc = lat_scan_end(p, t);
+  if (rc) return rc;
   if (p->adv_pending) {  // the previous slice's advance (its bitmap pass) is long done
     res->prev_collected = 1;
     rc = vate_advance_result(p, res->prev_blocks, &res->prev_maintained, &res->prev_cleared);
@@ -796,6 +798,7 @@ int vate_slice_step(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_s
     rc = vate_estimate_finish_async(p, g, pin, log_zp_table[pin], floor, out_host, out_est,
                                     out_zv, out_sat, cap, &kept);
     res->nkept = kept;
+    if (rc == VATE_OK) rc = lat_rows(p, t);
   }
   return rc;
 }
@@ -853,6 +856,7 @@ static int lagged_end_prev(vate_pool* p, vate_hosts* hosts, uint64_t g, double f
     rc = vate_estimate_finish_async(p, g, res->pool_inactive, log_zp, floor, out_host, out_est,
                                     out_zv, out_sat, cap, &kept);
     res->nkept = kept;
+    if (rc == VATE_OK) rc = lat_rows(p, t);
   }
   // everything above (g0 delta / lookups read the delta list and bitmap buffers
   // the next bitmap pass rewrites) must finish before slice t+1's bitmap pass
@@ -903,6 +907,8 @@ int vate_slice_lagged_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_
     rc = vate_scan_packed(p, g, cell_stream, group_stream, pairs, n, where, hosts, t);
   }
   if (rc) return rc;
+  rc = lat_scan_end(p, t);
+  if (rc) return rc;
   return lagged_begin_prev(p, hosts, g, cell_stream, res);
 }
 
@@ -937,6 +943,8 @@ int vate_slice_lagged_end(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t 
       rc = vate_scan_packed(p, g, cell_stream, group_stream, p->lag_scan_pairs, p->lag_scan_n,
                             p->lag_scan_where, hosts, t);
     }
+    if (rc) return rc;
+    rc = lat_scan_end(p, t);
     if (rc) return rc;
   }
   // slice t up to its counters; then its sweep (it reads no g0, only cells already counted)

@@ -372,6 +372,15 @@ struct vate_pool {
   // grid caps of the kernels that share the SMs in the slice step, fixed at
   // pool creation from its shape (co-scheduling)
   uint32_t cap_bitmap = 0, cap_active = 0, cap_inc = 0, cap_final = 0;
+  // per-slice estimate latency (vate_pool_set_latency): CUDA events at the end
+  // of slice t's scan (main stream) and after its report rows' D2H (copy
+  // stream), one pair per slice parity
+  bool lat_on = false;
+  cudaEvent_t lat_a[2] = {nullptr, nullptr}, lat_b[2] = {nullptr, nullptr};
+  int64_t lat_t[2] = {-1, -1};
+  bool lat_b_set[2] = {false, false};
+  uint64_t lat_n = 0;
+  double lat_sum_ms = 0, lat_max_ms = 0, lat_last_ms = 0;
 
   vate::DevBuf bitmap;      // (S+31)/32 words
   vate::DevBuf in_a, in_b;  // staging for host inputs
@@ -484,6 +493,9 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta = false, bool fused_
 // Apply and clear the pending-set marks of a deferred pool (no-op otherwise):
 // every cell access other than the bitmap pass calls it first.
 int flush_pending(vate_pool* p);
+// estimate-latency marks (no-ops unless vate_pool_set_latency(p, 1))
+int lat_scan_end(vate_pool* p, int64_t t);
+int lat_rows(vate_pool* p, int64_t t);
 // Start or stop deferring for the pool (flushes first when stopping).
 int set_deferred(vate_pool* p, bool on);
 constexpr uint64_t kDeferBytes = 64ull << 20;

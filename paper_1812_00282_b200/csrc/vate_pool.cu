@@ -1123,6 +1123,39 @@ int set_deferred(vate_pool* p, bool on) {
   return VATE_OK;
 }
 
+static int lat_harvest(vate_pool* p, int slot) {
+  if (!p->lat_b_set[slot]) return VATE_OK;
+  VATE_CUDA(cudaEventSynchronize(p->lat_b[slot]));
+  float ms = 0.f;
+  VATE_CUDA(cudaEventElapsedTime(&ms, p->lat_a[slot], p->lat_b[slot]));
+  p->lat_n++;
+  p->lat_sum_ms += ms;
+  p->lat_last_ms = ms;
+  if (ms > p->lat_max_ms) p->lat_max_ms = ms;
+  p->lat_b_set[slot] = false;
+  p->lat_t[slot] = -1;
+  return VATE_OK;
+}
+
+int lat_scan_end(vate_pool* p, int64_t t) {
+  if (!p->lat_on) return VATE_OK;
+  const int slot = (int)(t & 1);
+  int rc = lat_harvest(p, slot);
+  if (rc) return rc;
+  VATE_CUDA(cudaEventRecord(p->lat_a[slot], p->stream));
+  p->lat_t[slot] = t;
+  return VATE_OK;
+}
+
+int lat_rows(vate_pool* p, int64_t t) {
+  if (!p->lat_on) return VATE_OK;
+  const int slot = (int)(t & 1);
+  if (p->lat_t[slot] != t) return VATE_OK;
+  VATE_CUDA(cudaEventRecord(p->lat_b[slot], p->d2h_stream));
+  p->lat_b_set[slot] = true;
+  return VATE_OK;
+}
+
 int check_width(vate_pool* p, int k_prime) {
   if (k_prime < 1 || k_prime > p->k)
     return set_error(VATE_EVALUE, "k'=" + std::to_string(k_prime) + " outside [1, " +
@@ -1283,6 +1316,10 @@ int vate_pool_destroy(vate_pool* p) {
   if (p->ev_post) cudaEventDestroy(p->ev_post);
   if (p->timeline_ref) cudaEventDestroy(p->timeline_ref);
   p->pend.release();
+  for (int i = 0; i < 2; ++i) {
+    if (p->lat_a[i]) cudaEventDestroy(p->lat_a[i]);
+    if (p->lat_b[i]) cudaEventDestroy(p->lat_b[i]);
+  }
   if (p->d_done) cudaFree(p->d_done);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   inc_release(p);
@@ -1315,6 +1352,41 @@ int vate_pool_device_bytes(const vate_pool* p, int64_t* bytes) {
   if (!p || !bytes) return set_error(VATE_EVALUE, "null argument");
   const uint64_t cb = p->kind == VATE_TS ? 8 : (uint64_t)p->cell_bytes;
   *bytes = (int64_t)(p->L.size * cb + (p->deferred ? p->pend.bytes : 0));
+  return VATE_OK;
+}
+
+int vate_pool_set_latency(vate_pool* p, int on) {
+  int rc = enter(p);
+  if (rc) return rc;
+  for (int i = 0; i < 2; ++i) {
+    if (!p->lat_a[i]) VATE_CUDA(cudaEventCreate(&p->lat_a[i]));
+    if (!p->lat_b[i]) VATE_CUDA(cudaEventCreate(&p->lat_b[i]));
+    p->lat_t[i] = -1;
+    p->lat_b_set[i] = false;
+  }
+  p->lat_on = on != 0;
+  p->lat_n = 0;
+  p->lat_sum_ms = p->lat_max_ms = p->lat_last_ms = 0;
+  return VATE_OK;
+}
+
+int vate_pool_lat_mark(vate_pool* p, int64_t t, int which) {
+  int rc = enter(p);
+  if (rc) return rc;
+  return which == 0 ? lat_scan_end(p, t) : lat_rows(p, t);
+}
+
+int vate_pool_latency(vate_pool* p, double out[4]) {
+  int rc = enter(p);
+  if (rc) return rc;
+  for (int i = 0; i < 2; ++i) {
+    rc = lat_harvest(p, i);
+    if (rc) return rc;
+  }
+  out[0] = (double)p->lat_n;
+  out[1] = p->lat_n ? p->lat_sum_ms / (double)p->lat_n : 0.0;
+  out[2] = p->lat_max_ms;
+  out[3] = p->lat_last_ms;
   return VATE_OK;
 }
 

@@ -13,6 +13,7 @@ has no host thread fan-out and its output never depended on it.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import time
 from dataclasses import dataclass
 
@@ -158,6 +159,7 @@ class Pipeline:
         ``part``/``nparts`` estimate only that contiguous share of the sorted
         active set (the multi-GPU split, parallel.ReplicaStep).
         """
+        _ensure_log_table(self.pool, self.cfg.g)   # an ad-hoc estimate may have swapped it
         nh, p = C.c_uint64(), C.c_uint64()
         if nparts > 1:
             check(lib.vate_estimate_begin_part(self.pool.handle, self.hosts.handle, self.cfg.g,
@@ -270,6 +272,7 @@ class Pipeline:
         stay in device memory (reports_device()) and the call returns the row
         count.  The advance of slice t is accounted during the next call or
         wait_reports()."""
+        _ensure_log_table(self.pool, self.cfg.g)
         tab = getattr(self, "_lzp_tab", None)
         if tab is None:
             tab = self._lzp_tab = log_zp_table(self.pool.c)
@@ -280,8 +283,10 @@ class Pipeline:
                                            self.hosts.handle, t))
             else:
                 self.scan_packed(t, pairs, n, where == "device")
+            check(lib.vate_pool_lat_mark(self.pool.handle, t, 0))
             rep = self.estimate_soa(t, out, advance=True, wait=False,
                                     keep_on_device=out is None)
+            check(lib.vate_pool_lat_mark(self.pool.handle, t, 1))
             self._deferred_t = t
             return rep
         host, est, zv, sat = out if out is not None else (None, None, None, None)
@@ -325,6 +330,7 @@ class Pipeline:
         return self._lagged(None, out)
 
     def _lagged(self, fn, out, t=None, pairs=0, n=0, where="device"):
+        _ensure_log_table(self.pool, self.cfg.g)
         tab = getattr(self, "_lzp_tab", None)
         if tab is None:
             tab = self._lzp_tab = log_zp_table(self.pool.c)
@@ -385,38 +391,54 @@ class Pipeline:
         return self._estimate_advance(t, out, wait)
 
     # --- driving ---------------------------------------------------------------------
-    def process_slice_soa(self, t: int, aips, bips, out=None):
-        """All three phases for slice t; returns (HostReports | None, SliceStats)."""
-        t0 = time.perf_counter_ns()
-        self._t = t
-        n = self._scan(aips, bips)
-        t1 = time.perf_counter_ns()
-        reports = self.estimate_soa(t, out)
-        t2 = time.perf_counter_ns()
-        rep = self._maintain(t)
-        t3 = time.perf_counter_ns()
-        stats = SliceStats(t, n, (t1 - t0) // 1000, (t2 - t1) // 1000, (t3 - t2) // 1000,
+    # SliceStats phase times (pipeline.py:144-159 measures each phase's wall
+    # time on the CPU): here each phase is timed by CUDA events on the pool's
+    # stream around it -- the scan (with its H2D and host registration), the
+    # estimate up to its report rows in host memory, the advance -- read after
+    # the phase's own synchronisation, so timing adds no sync.
+    _M0, _M1, _M2, _M3 = 12, 13, 14, 15
+
+    def _phase_us(self, a: int, b: int) -> int:
+        ms = C.c_double()
+        check(lib.vate_mark_elapsed(self.pool.handle, a, b, C.byref(ms)))
+        return int(ms.value * 1000)
+
+    def _phases(self, t: int, n: int, scan, out=None):
+        h = self.pool.handle
+        check(lib.vate_mark(h, self._M0))
+        scan()
+        check(lib.vate_mark(h, self._M1))
+        reports = self.estimate_soa(t, out)     # returns once the rows are in host memory
+        check(lib.vate_mark(h, self._M2))
+        rep = self._maintain(t)                  # returns once the advance is collected
+        check(lib.vate_mark(h, self._M3))
+        stats = SliceStats(t, n, self._phase_us(self._M0, self._M1),
+                           self._phase_us(self._M1, self._M2),
+                           self._phase_us(self._M2, self._M3),
                            rep.cells_maintained, rep.cells_cleared)
         return reports, stats
+
+    def process_slice_soa(self, t: int, aips, bips, out=None):
+        """All three phases for slice t; returns (HostReports | None, SliceStats)."""
+        self._t = t
+        n = len(aips)
+        return self._phases(t, n, lambda: self._scan(aips, bips), out)
 
     def process_packed(self, t: int, pairs_dev: int, n: int):
         """All three phases for a slice of packed {u32 aip, u32 bip} records already
         on the device (e.g. from traceio.DeviceSlices); (HostReports | None, SliceStats)."""
-        t0 = time.perf_counter_ns()
-        if n:
-            self.scan_packed(t, pairs_dev, n, True)
-        t1 = time.perf_counter_ns()
-        reports = self.estimate_soa(t)
-        t2 = time.perf_counter_ns()
-        rep = self._maintain(t)
-        t3 = time.perf_counter_ns()
-        return reports, SliceStats(t, n, (t1 - t0) // 1000, (t2 - t1) // 1000,
-                                   (t3 - t2) // 1000, rep.cells_maintained, rep.cells_cleared)
+        return self._phases(t, n, lambda: n and self.scan_packed(t, pairs_dev, n, True))
 
     def process_slice(self, t: int, aips, bips):
-        """Run all three phases for slice t; returns (reports, stats) (pipeline.py:142-160)."""
+        """Run all three phases for slice t; returns (reports, stats) (pipeline.py:142-160).
+        estimate_us includes building the EstimateReport list, as the reference's
+        _estimate does (pipeline.py:120-138)."""
         soa, stats = self.process_slice_soa(t, aips, bips)
-        return ([] if soa is None else soa.to_list()), stats
+        t0 = time.perf_counter_ns()
+        reports = [] if soa is None else soa.to_list()
+        stats = dataclasses.replace(stats, estimate_us=stats.estimate_us
+                                    + (time.perf_counter_ns() - t0) // 1000)
+        return reports, stats
 
     def run(self, sliced):
         """Process a (slice, aips, bips) stream; yields (t, reports, stats)."""

@@ -294,6 +294,24 @@ class _DevicePool:
         return [(_lib.KERNEL_KINDS[int(out[3 * i])], out[3 * i + 1], out[3 * i + 2])
                 for i in range(len(out) // 3)]
 
+    def set_latency(self, on: bool) -> None:
+        """Per-slice estimate latency of the slice steps (CUDA events: end of the
+        slice's scan -> its report rows in host memory); resets the counters."""
+        check(lib.vate_pool_set_latency(self._h, int(on)))
+
+    def latency(self) -> dict:
+        out = (C.c_double * 4)()
+        check(lib.vate_pool_latency(self._h, out))
+        return {"slices": int(out[0]), "mean_ms": out[1], "max_ms": out[2], "last_ms": out[3]}
+
+    def l2_ceilings(self, buf_bytes: int = 32 << 20, n: int = 20_000_000, reps: int = 5) -> dict:
+        """L2 ceilings over an L2-resident buffer (vate_bench_l2; measurement only)."""
+        out = (C.c_double * 4)()
+        check(lib.vate_bench_l2(self._h, buf_bytes, n, reps, out))
+        return {"buffer_bytes": buf_bytes, "random_sector_reads_G_per_s": out[0],
+                "random_u16_stores_G_per_s": out[1], "random_red_or_G_per_s": out[2],
+                "stream_read_GB_per_s": out[3]}
+
     def set_timing(self, on: bool) -> None:
         check(lib.vate_pool_set_timing(self._h, int(on)))
 
