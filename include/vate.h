@@ -78,6 +78,8 @@ int vate_pool_latency(vate_pool* p, double out[4]);
 /* The same marks for a slice driven by separate calls (scan, then the
  * estimate's begin/finish): which = 0 after the scan, 1 after the finish. */
 int vate_pool_lat_mark(vate_pool* p, int64_t t, int which);
+/* out = [deferred scatter on, bit-plane mode on, its window k', its ring slots]. */
+int vate_pool_mode(const vate_pool* p, int32_t out[4]);
 int vate_pool_sync(vate_pool* p);
 /* cumulative count of kernels this pool (and its registries) launched */
 int vate_pool_launches(const vate_pool* p, uint64_t* n);
@@ -100,7 +102,12 @@ int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
  * (exact), 0 recomputes every g0 by a full gather. */
 enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_FILTER = 2,
                    VATE_OPT_CONCURRENT = 3, VATE_OPT_INC_SORT = 4, VATE_OPT_FUSE_SWEEP = 5,
-                   VATE_OPT_DEFERRED = 6 };
+                   VATE_OPT_DEFERRED = 6, VATE_OPT_BITPLANE = 7 };
+/* VATE_OPT_BITPLANE: -1 auto (default: on for deferred pools, when the HBM
+ * fits it), 0 off, 1 on.  On: the pool keeps one mark bitmap per epoch, the
+ * estimate for k' = the first estimate's k' reads ~(S | P | M_e) instead of
+ * the cells, and the cells are brought up to date block by block as blocks
+ * fall due.  Identical results. */
 /* VATE_OPT_SCAN_FILTER: -1 auto (default: the per-CTA registry-stamp filter
  * when the last compacted slice saw >= 8 packets per distinct host, else
  * plain stamps), 0 off, 1 on.  Both forms leave identical state. */

@@ -56,6 +56,7 @@ _SIGS = {
     "vate_put_cells": ([_p, _p, _p, _u64, _int], _int),
     "vate_fill_cells": ([_p, _u64], _int),
     "vate_pool_device_bytes": ([_p, _p], _int),
+    "vate_pool_mode": ([_p, _p], _int),
     "vate_pool_set_latency": ([_p, _int], _int),
     "vate_bench_l2": ([_p, _u64, _u64, _int, _p], _int),
     "vate_pool_latency": ([_p, _p], _int),

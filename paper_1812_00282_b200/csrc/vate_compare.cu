@@ -288,7 +288,9 @@ int vate_put_cells(vate_pool* p, const uint64_t* idx, const uint64_t* values, ui
     return VATE_OK;
   });
   if (rc) return rc;
-  return sync_small(p);
+  rc = sync_small(p);
+  if (rc) return rc;
+  return bp_rebuild(p);  // bit-plane mode: the new values' history
 }
 
 int vate_fill_cells(vate_pool* p, uint64_t value) {
@@ -297,10 +299,12 @@ int vate_fill_cells(vate_pool* p, uint64_t value) {
   if (p->width < 64 && (value >> p->width))  // PackedArray.fill (bitpack.py:57-60)
     return set_error(VATE_EVALUE, "value " + std::to_string(value) + " exceeds " +
                                       std::to_string(p->width) + " bits");
-  if (p->pend_dirty) {  // every cell is overwritten: earlier marks are void
+  if (p->pend_dirty && !p->bp) {  // every cell is overwritten: earlier marks are void
     VATE_CUDA(cudaMemsetAsync(p->pend.ptr, 0, p->pend.bytes, p->stream));
     p->pend_dirty = false;
   }
+  rc = bp_wait_aux(p);
+  if (rc) return rc;
   const uint64_t S = p->L.size;
   rc = with_any_cell(p, [&](auto tag) -> int {
     using T = decltype(tag);
@@ -309,7 +313,9 @@ int vate_fill_cells(vate_pool* p, uint64_t value) {
     return VATE_OK;
   });
   if (rc) return rc;
-  return sync_small(p);
+  rc = sync_small(p);
+  if (rc) return rc;
+  return bp_rebuild(p);
 }
 
 int vate_get_cells64(vate_pool* p, const uint64_t* idx, uint64_t n, uint64_t* out, int where) {

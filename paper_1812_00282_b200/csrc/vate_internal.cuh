@@ -369,6 +369,25 @@ struct vate_pool {
   bool deferred = false;     // scans mark pend instead of storing into cells
   bool pend_dirty = false;   // pend may hold marks
   int opt_deferred = -1;     // -1 auto (cells > kDeferBytes), 0 off, 1 on
+  // bit-plane mode (vate_bitplane.cu): the pool's recent
+  // history as one mark bitmap per epoch (advance) in a ring, a prefix OR of
+  // the current L-epoch block and suffix ORs of the previous one, so the
+  // estimate's inactive bitmap for k' = L is ~(S | P | M_e) -- three bitmaps
+  // instead of the 2^c cells; cells are brought up to date block by block
+  // when a block is due for its sweep (and wholesale before any other read)
+  int opt_bp = -1;           // -1 auto (on for deferred pools), 0 off, 1 on
+  bool bp = false;
+  uint32_t bp_L = 0, bp_R = 0;   // window width (epochs), ring slots
+  int64_t bp_e = 0;              // current epoch
+  bool bp_folded = false;        // M_e already ORed into P in this epoch
+  bool bp_failed = false;        // enabling was refused (memory, values > 2k)
+  int64_t bp_flushed_e = -1;     // epoch of the last whole-pool materialization
+  vate::DevBuf bp_ring, bp_S, bp_P, bp_applied, bp_acc, bp_planes;
+  cudaEvent_t ev_bp = nullptr;  // the last due-block work (aux stream)
+  bool bp_join = false;         // cell accesses must wait for ev_bp
+  uint64_t bp_wmax = 0;      // words of the largest block (+1), scratch row length
+  uint32_t bp_gmax = 0;      // 16-epoch groups the ring spans
+  std::vector<int64_t> bp_applied_h;  // per block: epochs <= this are in the cells
   // grid caps of the kernels that share the SMs in the slice step, fixed at
   // pool creation from its shape (co-scheduling)
   uint32_t cap_bitmap = 0, cap_active = 0, cap_inc = 0, cap_final = 0;
@@ -490,6 +509,7 @@ struct vate_hosts {
 namespace vate {
 
 int build_bitmap(vate_pool* p, int k_prime, bool with_delta = false, bool fused_advance = false);
+int build_bitmap_direct(vate_pool* p, int k_prime, bool with_delta, bool fused_advance);
 // Apply and clear the pending-set marks of a deferred pool (no-op otherwise):
 // every cell access other than the bitmap pass calls it first.
 int flush_pending(vate_pool* p);
@@ -498,6 +518,15 @@ int lat_scan_end(vate_pool* p, int64_t t);
 int lat_rows(vate_pool* p, int64_t t);
 // Start or stop deferring for the pool (flushes first when stopping).
 int set_deferred(vate_pool* p, bool on);
+// bit-plane mode (vate_bitplane.cu)
+uint32_t* pend_ptr(vate_pool* p);       // where this epoch's marks go
+int bp_maybe_enable(vate_pool* p, int k_prime);
+int bp_disable(vate_pool* p);
+int bp_materialize_all(vate_pool* p);
+int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance);
+int bp_advance(vate_pool* p);
+int bp_rebuild(vate_pool* p);           // after cells were overwritten (load, put, fill)
+int bp_wait_aux(vate_pool* p);          // order a cell access after the due-block work
 constexpr uint64_t kDeferBytes = 64ull << 20;
 bool default_deferred(const vate_pool* p);
 

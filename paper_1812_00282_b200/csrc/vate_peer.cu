@@ -347,7 +347,7 @@ int vate_peer_exchange(vate_peer* x, int64_t t, uint64_t* touched_total) {
   // 1. this rank's dirty bitmap and touched keys into its window: a deferred
   // pool's pending marks are exactly the cells it set (a 2^c/8-byte copy); a
   // direct-store pool derives them from a pass over its cells
-  uint32_t* pend = p->deferred ? p->pend.as<uint32_t>() : nullptr;
+  uint32_t* pend = p->deferred ? pend_ptr(p) : nullptr;
   if (pend) {
     if (p->pend_dirty)
       VATE_CUDA(cudaMemcpyAsync(x->win + W.bits[par], pend, x->nwords * 4,

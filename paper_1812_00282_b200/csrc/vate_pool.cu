@@ -15,6 +15,7 @@
 
 #include "vate_internal.cuh"
 #include "vate_registry.cuh"
+#include "vate_cells.cuh"
 
 namespace vate {
 
@@ -167,8 +168,7 @@ template <typename F>
 static int with_store(vate_pool* p, F f) {
   if (p->kind == VATE_AT && p->deferred) {
     p->pend_dirty = true;
-    return with_cell(p->cell_bytes,
-                     [&](auto tag) { return f(tag, MarkRule{p->pend.as<uint32_t>()}); });
+    return with_cell(p->cell_bytes, [&](auto tag) { return f(tag, MarkRule{pend_ptr(p)}); });
   }
   if (p->kind == VATE_AT)
     return with_cell(p->cell_bytes, [&](auto tag) { return f(tag, AtRule{p->L, p->bact0}); });
@@ -519,140 +519,6 @@ __device__ __forceinline__ bool active_bits_simd(const uint4 (&r)[(int)sizeof(T)
 // sectors -- a 16-byte store into a sector the pass read evict-first makes the
 // L2 fill the other half from DRAM (scripts/probes/probe_marks.cu: 634 vs
 // 165 us for a 512 MiB pass applying 5M marks).
-struct SweepSpec {
-  uint64_t s0, e0, s1, e1;          // the two due ranges (e == s: none)
-  uint32_t k, B;
-  unsigned long long* cleared;      // nullptr: no fused sweep
-};
-
-// Register-free (re-reads the word's cells, L1-hot): words of u32 cells and the
-// partial last word of a tiny pool.
-template <typename T>
-__device__ __forceinline__ unsigned sweep_word(T* __restrict__ cells, uint64_t i0, uint32_t cnt,
-                                            uint64_t s0, uint64_t e0, uint64_t s1, uint64_t e1,
-                                            uint32_t k, uint32_t B) {
-  unsigned cleared = 0;
-  for (uint32_t j = 0; j < cnt; ++j) {
-    const uint64_t i = i0 + j;
-    const bool due0 = i >= s0 && i < e0, due1 = i >= s1 && i < e1;
-    if (!due0 && !due1) continue;
-    const uint32_t v = cells[i];
-    const bool stale = due0 ? v <= k : ((v >= k && v <= B - 1) || v == 0);
-    if (stale) {
-      cells[i] = (T)B;
-      ++cleared;
-    }
-  }
-  return cleared;
-}
-
-// Bits j of [i0, i0+32) that fall in [s, e).
-__device__ __forceinline__ uint32_t range_bits(uint64_t i0, uint64_t s, uint64_t e) {
-  const uint64_t lo = s > i0 ? s - i0 : 0, hi = e > i0 ? umin64(e - i0, 32) : 0;
-  if (lo >= hi) return 0u;
-  const uint32_t below_hi = hi >= 32 ? 0xffffffffu : (1u << hi) - 1u;
-  return below_hi & ~((1u << lo) - 1u);
-}
-
-// The same sweep for a full word of u8/u16 cells, on the pass's register copy:
-// stale cells are rewritten in the registers; bit v of `chg` marks a changed
-// uint4.  (The scalar form re-reads each cell from L2 -- the pass's loads are
-// evict-first -- and its 32 dependent round trips set the kernel's tail on
-// small pools.)
-template <typename T>
-__device__ __forceinline__ unsigned sweep_regs(uint4 (&r)[(int)sizeof(T) * 2], uint64_t i0,
-                                               const SweepSpec& SW, unsigned& chg) {
-  static_assert(sizeof(T) <= 2, "u8/u16 cells");
-  const uint32_t due0 = range_bits(i0, SW.s0, SW.e0), due1 = range_bits(i0, SW.s1, SW.e1);
-  if (!(due0 | due1)) return 0;
-  constexpr int kPer = 4 / (int)sizeof(T), kBits = 8 * (int)sizeof(T);
-  constexpr uint32_t kMask = sizeof(T) == 1 ? 0xFFu : 0xFFFFu;
-  uint32_t* x = reinterpret_cast<uint32_t*>(r);
-  unsigned cleared = 0;
-#pragma unroll
-  for (int q = 0; q < 32 / kPer; ++q) {
-#pragma unroll
-    for (int h = 0; h < kPer; ++h) {
-      const int j = q * kPer + h;
-      const uint32_t v = (x[q] >> (h * kBits)) & kMask;
-      const bool stale = ((due0 >> j) & 1u) ? v <= SW.k
-                         : ((due1 >> j) & 1u) ? ((v >= SW.k && v <= SW.B - 1) || v == 0) : false;
-      if (stale) {
-        x[q] = (x[q] & ~(kMask << (h * kBits))) | (SW.B << (h * kBits));
-        ++cleared;
-        chg |= 1u << (q / 4);
-      }
-    }
-  }
-  return cleared;
-}
-
-// Pending-set marks of a word whose 32 cells share clock `act`, applied to the
-// register copy (u8: 4 cells per 32-bit lane, u16: 2); bit v of the result
-// marks a changed uint4.
-template <typename T>
-__device__ __forceinline__ unsigned apply_marks_regs(uint4 (&r)[(int)sizeof(T) * 2], uint32_t m,
-                                                     uint32_t act) {
-  static_assert(sizeof(T) <= 2, "u8/u16 cells");
-  uint32_t* x = reinterpret_cast<uint32_t*>(r);
-  unsigned chg = 0;
-  if (sizeof(T) == 1) {
-    const uint32_t a4 = act * 0x01010101u;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t nib = (m >> (4 * q)) & 0xFu;
-      const uint32_t bm = ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;  // bit j -> byte j
-      x[q] = (x[q] & ~bm) | (a4 & bm);
-    }
-    chg = m ? 3u : 0u;  // (see below: a marked cell changes)
-  } else {
-    // lane masks by sign-replicating byte permutes: copy s[k] = m << k puts bit
-    // 8j + 7 - k of m at the sign of byte j, and prmt with a selector nibble's
-    // bit 3 set writes that sign into a whole byte -- one prmt per two cells
-    const uint32_t a2 = act * 0x00010001u;
-    uint32_t sh[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) sh[k] = m << k;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int j = (2 * q) >> 3, k = 7 - ((2 * q) & 7);  // bit 2q: byte j of sh[k]; 2q+1: of sh[k-1]
-      const uint32_t sel = (8u | j) | ((8u | j) << 4) | ((12u | j) << 8) | ((12u | j) << 12);
-      uint32_t bm;
-      asm("prmt.b32 %0, %1, %2, %3;" : "=r"(bm) : "r"(sh[k]), "r"(sh[k - 1]), "r"(sel));
-      x[q] = (x[q] & ~bm) | (a2 & bm);
-    }
-    // a marked cell never already holds its clock (it would have been set in
-    // this slice, and this slice's sets are the marks): a sector with a mark
-    // changed
-    chg = ((m & 0xFFFFu) ? 3u : 0u) | ((m >> 16) ? 12u : 0u);
-  }
-  return chg;
-}
-
-// Marks of a word that straddles a block boundary (or holds u32 cells), in
-// memory: each marked cell takes its own block's clock.
-template <typename T>
-__device__ __forceinline__ void apply_marks_scalar(T* __restrict__ cells, uint64_t i0, uint32_t cnt,
-                                                   uint32_t m, const Layout& L, uint32_t bact0) {
-  for_word_clocks(i0, cnt, L, bact0, [&](uint32_t j, uint32_t act) {
-    if ((m >> j) & 1u) cells[i0 + j] = (T)act;
-  });
-}
-
-// Changed 32-byte sectors of a word back to HBM (uint4 pairs, whole sectors).
-template <typename T>
-__device__ __forceinline__ void store_sectors(T* __restrict__ cells, uint64_t i0,
-                                              const uint4 (&r)[(int)sizeof(T) * 2], unsigned chg) {
-  constexpr int NV = (int)sizeof(T) * 2;
-  uint4* dst = reinterpret_cast<uint4*>(cells + i0);
-#pragma unroll
-  for (int s = 0; s < NV / 2; ++s)
-    if ((chg >> (2 * s)) & 3u) {
-      dst[2 * s] = r[2 * s];
-      dst[2 * s + 1] = r[2 * s + 1];
-    }
-}
-
 // The rare words, entirely in memory (re-reads are L1/L2 hits): a word that
 // straddles a block boundary (2k of them), u32 cells (k = 2^15), the partial
 // last word of a pool smaller than 32 cells, and -- with m = 0, no sweep --
@@ -1009,6 +875,22 @@ static int require_at(const vate_pool* p, const char* what) {
 // Build the k' inactive bitmap and enqueue P into h_ctr[C_P] (not synced).
 int build_bitmap(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
   if (p->kind != VATE_AT) return cmp_build_bitmap(p, k_prime, with_delta);
+  int rc = bp_maybe_enable(p, k_prime);
+  if (rc) return rc;
+  if (p->bp) {
+    if ((uint32_t)k_prime == p->bp_L) return bp_window(p, k_prime, with_delta, fused_advance);
+    // another width: the cells, brought up to date, through the direct pass;
+    // the advance keeps the bit-plane bookkeeping
+    rc = bp_materialize_all(p);
+    if (rc) return rc;
+    rc = build_bitmap_direct(p, k_prime, with_delta, false);
+    if (rc || !fused_advance) return rc;
+    return bp_advance(p);
+  }
+  return build_bitmap_direct(p, k_prime, with_delta, fused_advance);
+}
+
+int build_bitmap_direct(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
   const uint64_t nwords = (p->L.size + 31) / 32;
   int rc = p->bitmap.ensure(nwords * 4 + 16);
   if (rc) return rc;
@@ -1039,7 +921,7 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta, bool fused_advance)
                     (1u << C_P) | (with_delta ? (1u << C_DCNT) | (1u << C_DWORK) : 0u) |
                         (fused_advance ? (1u << C_CLEARED) : 0u)};
   const bool pend = p->pend_dirty;
-  uint32_t* pend_words = p->pend.as<uint32_t>();
+  uint32_t* pend_words = pend_ptr(p);
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
     // pools beyond L2 stream from HBM: each CTA bulk-prefetches its cells two
@@ -1085,6 +967,7 @@ int build_bitmap(vate_pool* p, int k_prime, bool with_delta, bool fused_advance)
 }
 
 int flush_pending(vate_pool* p) {
+  if (p->bp) return bp_materialize_all(p);
   if (!p->pend_dirty) return VATE_OK;
   const uint64_t nwords = (p->L.size + 31) / 32;
   int rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
@@ -1108,7 +991,9 @@ int set_deferred(vate_pool* p, bool on) {
   if (on && p->kind != VATE_AT) on = false;  // the comparators store constants directly
   if (on == p->deferred) return VATE_OK;
   if (!on) {
-    int rc = flush_pending(p);
+    int rc = bp_disable(p);  // bit-plane mode needs marks
+    if (rc) return rc;
+    rc = flush_pending(p);
     if (rc) return rc;
     p->deferred = false;
     return VATE_OK;
@@ -1316,8 +1201,15 @@ int vate_pool_destroy(vate_pool* p) {
   if (p->ev_post) cudaEventDestroy(p->ev_post);
   if (p->timeline_ref) cudaEventDestroy(p->timeline_ref);
   p->pend.release();
+  p->bp_ring.release();
+  p->bp_S.release();
+  p->bp_P.release();
+  p->bp_applied.release();
+  p->bp_acc.release();
+  p->bp_planes.release();
   for (int i = 0; i < 2; ++i) {
     if (p->lat_a[i]) cudaEventDestroy(p->lat_a[i]);
+    if (i == 0 && p->ev_bp) cudaEventDestroy(p->ev_bp);
     if (p->lat_b[i]) cudaEventDestroy(p->lat_b[i]);
   }
   if (p->d_done) cudaFree(p->d_done);
@@ -1351,7 +1243,8 @@ int vate_pool_info(const vate_pool* p, int32_t* bact0, int32_t* cell_bytes, void
 int vate_pool_device_bytes(const vate_pool* p, int64_t* bytes) {
   if (!p || !bytes) return set_error(VATE_EVALUE, "null argument");
   const uint64_t cb = p->kind == VATE_TS ? 8 : (uint64_t)p->cell_bytes;
-  *bytes = (int64_t)(p->L.size * cb + (p->deferred ? p->pend.bytes : 0));
+  *bytes = (int64_t)(p->L.size * cb + (p->deferred ? p->pend.bytes : 0) +
+                     (p->bp ? p->bp_ring.bytes + p->bp_S.bytes + p->bp_P.bytes : 0));
   return VATE_OK;
 }
 
@@ -1459,6 +1352,14 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_inc = (int)value;
     if (!value) p->inc.valid = false;
     return VATE_OK;
+  }
+  if (option == VATE_OPT_BITPLANE && value >= -1 && value <= 1) {
+    int rc = enter(p);
+    if (rc) return rc;
+    p->opt_bp = (int)value;
+    p->bp_failed = false;
+    if (value == 0) return bp_disable(p);
+    return VATE_OK;  // enabled at the next estimate (its k' is the window)
   }
   if (option == VATE_OPT_DEFERRED && value >= -1 && value <= 1) {
     int rc = enter(p);
@@ -1728,6 +1629,7 @@ int vate_advance_async(vate_pool* p) {
   if (rc) return rc;
   if (p->adv_pending) return set_error(VATE_EVALUE, "previous advance not collected");
   if (p->kind != VATE_AT) return cmp_advance_async(p);
+  if (p->bp) return bp_advance(p);
   rc = flush_pending(p);  // marks take the clocks of the slice that made them
   if (rc) return rc;
   const uint32_t B = p->L.B, k = p->L.k;
@@ -1912,10 +1814,12 @@ int vate_load(vate_pool* p, const uint8_t* buf, uint64_t len) {
   rc = p->in_a.ensure(nwords * 8 + 8);
   if (rc) return rc;
   VATE_CUDA(cudaMemcpyAsync(p->in_a.ptr, buf + 16, nwords * 8, cudaMemcpyHostToDevice, p->stream));
-  if (p->pend_dirty) {  // every cell is overwritten: earlier marks are void
+  if (p->pend_dirty && !p->bp) {  // every cell is overwritten: earlier marks are void
     VATE_CUDA(cudaMemsetAsync(p->pend.ptr, 0, p->pend.bytes, p->stream));
     p->pend_dirty = false;
   }
+  rc = bp_wait_aux(p);
+  if (rc) return rc;
   rc = with_cell(p->cell_bytes, [&](auto tag) -> int {
     using T = decltype(tag);
     VATE_LAUNCH(p, VATE_K_OTHER, grid_for(p->L.size, kThreads), kThreads, 0, k_unpack<T>,
@@ -1926,7 +1830,7 @@ int vate_load(vate_pool* p, const uint8_t* buf, uint64_t len) {
   rc = sync_small(p);
   if (rc) return rc;
   p->bact0 = bact0;
-  return VATE_OK;
+  return bp_rebuild(p);  // bit-plane mode: the history of the loaded cells
 }
 
 // ---- replica merge --------------------------------------------------------------
@@ -1939,7 +1843,7 @@ int vate_dirty_bitmap(vate_pool* p, uint32_t* bitmap_dev) {
   const uint64_t nw = (p->L.size + 31) / 32;
   if (p->deferred) {  // the pending marks are exactly the cells this rank set
     if (!p->pend_dirty) VATE_CUDA(cudaMemsetAsync(bitmap_dev, 0, nw * 4, p->stream));
-    else VATE_CUDA(cudaMemcpyAsync(bitmap_dev, p->pend.ptr, nw * 4, cudaMemcpyDeviceToDevice, p->stream));
+    else VATE_CUDA(cudaMemcpyAsync(bitmap_dev, pend_ptr(p), nw * 4, cudaMemcpyDeviceToDevice, p->stream));
     return VATE_OK;
   }
   rc = flush_pending(p);
@@ -1964,7 +1868,7 @@ int vate_merge_dirty(vate_pool* p, const uint32_t* bitmaps_dev, int nranks) {
     using T = decltype(tag);
     VATE_LAUNCH(p, VATE_K_OTHER, grid_for(nwords, kThreads), kThreads, 0, k_merge<T>, (T*)p->cells,
                 p->L, p->bact0, bitmaps_dev, nwords, nranks,
-                p->deferred ? p->pend.as<uint32_t>() : nullptr);
+                p->deferred ? pend_ptr(p) : nullptr);
     if (p->deferred) p->pend_dirty = true;
     return VATE_OK;
   });

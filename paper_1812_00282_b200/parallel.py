@@ -3,10 +3,11 @@
 The packet stream shards across ranks; every rank scans its shard into a
 private replica pool.  Replicas share bact0 and hold identical cells at slice
 start, so the only per-slice exchange is "which cells were set this slice":
-each rank builds a 1-bit-per-cell dirty bitmap on the device
-(vate_dirty_bitmap), the bitmaps are all-gathered (NCCL over NVLink), and
-every rank ORs them and writes its block clock into the dirty cells
-(vate_merge_dirty).  That is the reference's single-pool state exactly (the
+each rank has a 1-bit-per-cell dirty bitmap on the device (vate_dirty_bitmap:
+a deferred pool's pending-set marks as they are, a direct-store pool's cells
+holding their block clock), the bitmaps are all-gathered (NCCL over NVLink),
+and every rank ORs them and writes its block clock into the dirty cells, or,
+deferred, takes the union as its pending marks (vate_merge_dirty).  That is the reference's single-pool state exactly (the
 window-aware newest-timestamp max of SURVEY.md §8e).
 
 Host estimation then splits by aip range without leaving the device: each
@@ -77,12 +78,17 @@ class _SliceStepBase:
     def exchange(self, t: int, n_packets: int) -> None:  # pragma: no cover - abstract
         raise NotImplementedError
 
+    def check_shard(self, n_packets: int) -> None:
+        """Reject a shard the exchange cannot carry BEFORE it is scanned (a
+        failure after the scan would leave this replica ahead of its peers)."""
+
     def __call__(self, t: int, pairs: int, n: int, where: str = "device", out=None):
         """Rows of this rank's share (HostReports, or a count with out=None), streamed.
 
         ``pairs``/``where`` as Pipeline.step_fast (device or host pointer, or a
         staging slot from stage_packed)."""
         pipe = self.pipe
+        self.check_shard(n)
         if where == "staged":
             check(lib.vate_scan_staged(pipe.pool.handle, pipe.cfg.g, pipe.cfg.cell_stream,
                                        pipe.cfg.group_stream, int(pairs), int(n),
@@ -128,6 +134,10 @@ class ReplicaStep(_SliceStepBase):
         dist.all_gather_into_tensor(self.all, self.mine)
         counts = self.counts.tolist()
         cap = max(counts + [1])
+        if self.keys.numel() < cap:   # a smaller shard than a peer's touched set
+            grown = torch.empty(cap, dtype=torch.int64, device=self.dev)
+            grown[:nt] = self.keys[:nt]
+            self.keys = grown
         if self.keys_all.numel() < self.world * cap:
             self.keys_all = torch.empty(self.world * cap, dtype=torch.int64, device=self.dev)
         dist.all_gather_into_tensor(self.keys_all[: self.world * cap], self.keys[:cap])
@@ -175,11 +185,14 @@ class PeerStep(_SliceStepBase):
         dist.barrier()                   # every window mapped before anyone arrives
         self.touched_total = 0
 
+    def check_shard(self, n_packets: int) -> None:
+        if n_packets > self.key_cap:
+            raise ValueError(f"{n_packets} packets exceed the peer key_cap {self.key_cap}")
+
     def exchange(self, t: int, n_packets: int, count_touched: bool = False) -> None:
         """One slice's exchange; count_touched also sums the ranks' touched-host
         counts (one small read per peer window, so off on the hot path)."""
-        if n_packets > self.key_cap:
-            raise ValueError(f"{n_packets} packets exceed the peer key_cap {self.key_cap}")
+        self.check_shard(n_packets)
         tot = C.c_uint64()
         check(lib.vate_peer_exchange(self.handle, t, C.byref(tot) if count_touched else None))
         if count_touched:

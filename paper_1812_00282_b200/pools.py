@@ -236,10 +236,17 @@ class _DevicePool:
         :409-410): its packed words (AT: plus the snapshot header)."""
         return self.packed_bytes
 
+    def mode(self) -> dict:
+        """The pool's storage mode: deferred scatter, bit-plane mode and its window."""
+        out = (C.c_int32 * 4)()
+        check(lib.vate_pool_mode(self._h, out))
+        return {"deferred": bool(out[0]), "bitplane": bool(out[1]), "window": out[2],
+                "ring_slots": out[3]}
+
     @property
     def deferred(self) -> bool:
         """Scans mark the pending-set bitmap instead of storing cells (VATE_OPT_DEFERRED)."""
-        return self.device_bytes > self.size * self.cell_bytes
+        return self.mode()["deferred"]
 
     @property
     def device_bytes(self) -> int:
@@ -260,12 +267,13 @@ class _DevicePool:
         return n.value
 
     OPTIONS = ("g0_kernel", "incremental", "scan_filter", "concurrent", "inc_sort",
-               "fuse_sweep", "deferred")
+               "fuse_sweep", "deferred", "bitplane")
 
     def set_option(self, option: str, value: int) -> None:
         """Tuning switches (include/vate.h enum vate_option): 'g0_kernel' (0 auto,
         1 gather, 2 smem), 'incremental' (0/1), 'scan_filter' (-1 auto, 0, 1),
-        'concurrent', 'inc_sort', 'fuse_sweep' (0/1), 'deferred' (-1 auto, 0, 1).
+        'concurrent', 'inc_sort', 'fuse_sweep' (0/1), 'deferred' (-1 auto, 0, 1),
+        'bitplane' (-1 auto, 0, 1).
         Every setting leaves identical results."""
         check(lib.vate_pool_set_option(self._h, self.OPTIONS.index(option), int(value)))
 

@@ -228,6 +228,69 @@ def test_cell_widths_and_memory():
     assert p.packed_bytes == (-(-(1 << 20) * 10 // 64) + 1) * 8 + 16   # test_pools.py:249-254
 
 
+def test_reference_memory_and_width_gates():
+    """The reference's own gates on the drop-in: ACCEPTANCE 4
+    (test_acceptance.py:130-143), test_pools.py:245-254, test_bitpack.py:49-52."""
+    at_bits = vb.AtPool(20, 300).bits_per_counter
+    dr_bits = vb.DrPool(20, 300).bits_per_counter
+    mem = vb.AtPool(20, 300).memory_bytes
+    bound = (1 << 20) * 10 // 8 + 16
+    assert at_bits == 10 and dr_bits == 9
+    assert abs(mem - bound) / bound <= 0.01
+    assert vb.AtPool(10, 300).bits_per_counter == 10
+    assert vb.DrPool(10, 300).bits_per_counter == 9
+    assert vb.TsPool(10, 300).bits_per_counter == 64
+    pool = vb.AtPool(20, 300)
+    words = -(-(1 << 20) * 10 // 64) + 1
+    assert pool.memory_bytes == words * 8 + 16
+    assert pool.cells.nbytes == (163_840 + 1) * 8
+    assert pool.device_bytes >= (1 << 20) * pool.cell_bytes   # the HBM footprint, separately
+    assert vb.DrPool(12, 300).memory_bytes == (-(-(1 << 12) * 9 // 64) + 1) * 8
+    assert vb.TsPool(12, 300).memory_bytes == (1 << 12) * 8
+
+
+@pytest.mark.parametrize("deferred", [0, 1, 2])
+def test_device_cells_write_api(deferred):
+    """AtPool.cells set / set_one / set_range / fill on the device, against the
+    reference's PackedArray semantics (bitpack.py:57-140): values masked to the
+    width, fill rejects values beyond it, reads and snapshots agree, and a
+    pending deferred mark never overwrites a later explicit value."""
+    k, c = 300, 12
+    pool = vb.AtPool(c, k)
+    pool.set_option("deferred", min(deferred, 1))
+    pool.set_option("bitplane", 1 if deferred == 2 else 0)
+    pool.count_inactive(k)              # (bit-plane mode starts at the first estimate)
+    assert pool.mode()["bitplane"] == (deferred == 2)
+    opool = vo.OraclePool(c, k)
+    cells = pool.cells
+    cells.fill(3)
+    opool.cells[:] = 3
+    assert np.all(cells.get_range(0, 1 << c) == 3)
+    with pytest.raises(ValueError):
+        cells.fill(1 << 10)
+    rng = np.random.default_rng(5)
+    idx = rng.integers(0, 1 << c, 500).astype(np.uint64)
+    vals = rng.integers(0, 1 << 12, 500).astype(np.uint64)     # wider than 10 bits: masked
+    idx, first = np.unique(idx, return_index=True)
+    vals = vals[first]
+    cells.set(idx, vals)
+    opool.cells[idx.astype(np.int64)] = (vals & 0x3FF).astype(opool.cells.dtype)
+    cells.set_one(7, 1000)
+    opool.cells[7] = 1000
+    cells.set_range(100, np.arange(20, dtype=np.uint64))
+    opool.cells[100:120] = np.arange(20)
+    # a set_many mark followed by an explicit value: the value wins
+    pool.set_many(np.array([9, 11], dtype=np.uint64))
+    opool.set_cells(np.array([9, 11], dtype=np.uint64))
+    cells.set_one(9, 5)
+    opool.cells[9] = 5
+    assert np.array_equal(cells.get_range(0, 1 << c), opool.cells.astype(np.uint64))
+    assert cells.get_one(7) == 1000
+    assert pool.snapshot_bytes() == opool.snapshot_bytes()
+    with pytest.raises(ValueError):
+        cells.set_one(1 << c, 1)
+
+
 # --- snapshots ------------------------------------------------------------------------
 
 def test_snapshot_load_of_reference_bytes(tmp_path):
@@ -954,11 +1017,12 @@ def test_active_set_merge_under_small_churn(inc_sort):
         assert st["incremental"] == 0, st
 
 
-@pytest.mark.parametrize("form", [(f, d, m) for f in (0, 1) for d in (0, 1) for m in (0, 1)])
+@pytest.mark.parametrize("form", [(f, d, m) for f in (0, 1) for d in (0, 1, 2) for m in (0, 1)])
 def test_scan_forms_are_equivalent(form):
     """Every packed-scan form -- the per-CTA registry-stamp filter on / off
     (VATE_OPT_SCAN_FILTER), direct cell stores or the deferred pending-set
-    marks (VATE_OPT_DEFERRED), 16-byte aligned input (two packets per thread,
+    marks (VATE_OPT_DEFERRED) or the bit-plane history (d = 2,
+    VATE_OPT_BITPLANE), 16-byte aligned input (two packets per thread,
     plus the odd last packet) or misaligned input (one packet per thread) --
     leaves the reference's cells and host set: ATP1 bytes, reports and the
     registry after skewed traffic (a heavy host, odd packet counts) equal the
@@ -969,7 +1033,8 @@ def test_scan_forms_are_equivalent(form):
     ocfg = vo.OracleConfig(256, 16, 6, seed=5)
     pool = cfg.build_pool()
     pool.set_option("scan_filter", filt)
-    pool.set_option("deferred", deferred)
+    pool.set_option("deferred", min(deferred, 1))
+    pool.set_option("bitplane", 1 if deferred == 2 else 0)
     pipe = vb.Pipeline(pool, cfg, 5)
     opipe = vo.OraclePipeline(ocfg, 5)
     rng = np.random.default_rng(31)
@@ -1049,16 +1114,18 @@ def test_lagged_step_equals_oracle(floor, hosts0, two_calls):
         pl.log_zp_table = orig
 
 
-@pytest.mark.parametrize("deferred", [0, 1])
+@pytest.mark.parametrize("deferred", [0, 1, 2])
 def test_u16_pass_forms_over_two_windows(deferred):
     """u16 cells (k = 300, the cfg 4 width) on a small pool for 2k + 5 slices:
-    direct or deferred stores, through the lagged slice step; the ATP1 bytes, P, maintenance and every report equal
+    direct or deferred stores or the bit-plane history (2; window k' = 293, so
+    two suffix builds), through the lagged slice step; the ATP1 bytes, P, maintenance and every report equal
     the oracle's, with the clock wrapping and every block swept twice."""
     k, c = 300, 16
     cfg = vb.EstimatorConfig(64, c, k, seed=9)
     ocfg = vo.OracleConfig(64, c, k, seed=9)
     pool = cfg.build_pool()
-    pool.set_option("deferred", deferred)
+    pool.set_option("deferred", min(deferred, 1))
+    pool.set_option("bitplane", 1 if deferred == 2 else 0)
     pipe = vb.Pipeline(pool, cfg, k - 7)
     opipe = vo.OraclePipeline(ocfg, k - 7)
     rng = np.random.default_rng(77)
@@ -1096,5 +1163,51 @@ def test_u16_pass_forms_over_two_windows(deferred):
     pipe.wait_reports()
     assert not want
     assert pool.snapshot_bytes() == opipe.pool.snapshot_bytes()
+    assert pool.mode()["bitplane"] == (deferred == 2)
     pipe.close()
+    pool.close()
+
+
+@pytest.mark.parametrize("c,k,kp", [(12, 6, 6), (12, 6, 4), (14, 40, 33), (10, 2, 2)])
+def test_bitplane_mixed_api(c, k, kp):
+    """Bit-plane mode under the whole pool protocol, not just the slice step:
+    set_many batches, the estimate's width and other widths (count_inactive,
+    inactive_mask), advances with and without an estimate in the epoch,
+    snapshots mid-epoch, loading a snapshot and writing cells (the history is
+    rebuilt), for many windows (block boundaries every k' epochs) -- the cells,
+    P and the maintenance reports equal the oracle pool's throughout."""
+    pool = vb.AtPool(c, k)
+    pool.set_option("bitplane", 1)
+    opool = vo.OraclePool(c, k)
+    rng = np.random.default_rng(c * 100 + k)
+    S = 1 << c
+    assert pool.count_inactive(kp) == opool.count_inactive(kp)
+    assert pool.mode()["bitplane"] and pool.mode()["window"] == kp
+    for t in range(6 * k + 9):
+        for _ in range(int(rng.integers(0, 3))):
+            idx = rng.integers(0, S, int(rng.integers(0, S // 8 + 1))).astype(np.uint64)
+            pool.set_many(idx)
+            opool.set_cells(idx)
+        if t % 3 != 2:
+            assert pool.count_inactive(kp) == opool.count_inactive(kp), t
+        if t % 7 == 3:
+            k2 = int(rng.integers(1, k + 1))
+            assert pool.count_inactive(k2) == opool.count_inactive(k2), (t, k2)
+            q = rng.integers(0, S, 64).astype(np.uint64)
+            assert np.array_equal(pool.inactive_mask(q, kp), opool.inactive_mask(q, kp)), t
+        if t % 11 == 5:
+            assert pool.snapshot_bytes() == opool.snapshot_bytes(), t
+        if t % 17 == 9:        # reload from bytes: the history is rebuilt from the cells
+            blob = pool.snapshot_bytes()
+            pool.close()
+            pool = vb.AtPool.from_bytes(blob)
+            pool.set_option("bitplane", 1)
+        if t % 19 == 12:       # explicit cell values: the history is rebuilt
+            i = int(rng.integers(0, S))
+            pool.cells.set_one(i, 2 * k)
+            opool.cells[i] = 2 * k
+        rep = pool.advance_slice()
+        want = opool.advance()
+        assert (rep.blocks, rep.cells_maintained, rep.cells_cleared) == want, t
+    assert pool.snapshot_bytes() == opool.snapshot_bytes()
     pool.close()

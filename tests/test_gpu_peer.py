@@ -29,7 +29,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, mode, c, k, result_q):
+def _worker(rank, world, port, mode, c, k, result_q, kind="peer", deferred=-1, uneven=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -37,7 +37,7 @@ def _worker(rank, world, port, mode, c, k, result_q):
 
     import paper_1812_00282_b200 as vb
     from oracle import vate_oracle as vo
-    from paper_1812_00282_b200.parallel import PeerStep, split_range
+    from paper_1812_00282_b200.parallel import PeerStep, ReplicaStep, split_range
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -47,16 +47,27 @@ def _worker(rank, world, port, mode, c, k, result_q):
         kp, g = 5, 256
         cfg = vb.EstimatorConfig(g, c, k, seed=9)
         ocfg = vo.OracleConfig(g, c, k, seed=9)
-        pipe = vb.Pipeline(cfg.build_pool(device=0), cfg, kp)
+        pool = cfg.build_pool(device=0)
+        if deferred != -1:
+            pool.set_option("deferred", deferred)
+        pipe = vb.Pipeline(pool, cfg, kp)
         ref = vo.OraclePipeline(ocfg, kp)
-        step = PeerStep(pipe, dist, key_cap=40_000, mode=mode)
+        torch.cuda.set_device(0)
+        step = (PeerStep(pipe, dist, key_cap=40_000, mode=mode) if kind == "peer"
+                else ReplicaStep(pipe, dist, torch))
         rng = np.random.default_rng(11)
         for t in range(18):
             n = int(rng.integers(0, 30_000)) if t != 5 else 0
             lo_host = 0 if t < 9 else 600        # host churn: half the hosts expire
             a = (0x0A000000 + rng.integers(lo_host, lo_host + 1200, n)).astype(np.uint32)
             b = rng.integers(1, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
-            mine = np.ascontiguousarray(np.stack([a, b], axis=1)[rank::world])
+            allp = np.stack([a, b], axis=1)
+            if uneven:   # rank 0 gets 95 % of the packets, the rest a sliver
+                cut = [0, (n * 95) // 100] + [(n * (95 + 5 * r)) // 100 for r in range(1, world)]
+                cut[-1] = n
+                mine = np.ascontiguousarray(allp[cut[rank]:cut[rank + 1]])
+            else:
+                mine = np.ascontiguousarray(allp[rank::world])
             cap = 4096
             out = (np.empty(cap, np.uint64), np.empty(cap, np.float64), np.empty(cap, np.float64),
                    np.empty(cap, np.uint8))
@@ -80,10 +91,11 @@ def _worker(rank, world, port, mode, c, k, result_q):
                 msgs.append(f"rank {rank} t {t}: estimates differ")
             if pipe.last_pool_inactive != want.pool_inactive:
                 msgs.append(f"rank {rank} t {t}: pool_inactive differs")
-        info = step.info()
-        if info["two_shot"] != (mode == 2 or (mode == 0 and world > 2)):
-            msgs.append(f"rank {rank}: unexpected merge form {info}")
-        step.close()
+        if kind == "peer":
+            info = step.info()
+            if info["two_shot"] != (mode == 2 or (mode == 0 and world > 2)):
+                msgs.append(f"rank {rank}: unexpected merge form {info}")
+            step.close()
         pipe.close()
         pipe.pool.close()
     except Exception as e:  # report, do not hang the peers' barrier
@@ -92,11 +104,12 @@ def _worker(rank, world, port, mode, c, k, result_q):
     dist.destroy_process_group()
 
 
-def _run(world, mode, c=15, k=6):
+def _run(world, mode, c=15, k=6, kind="peer", deferred=-1, uneven=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, c, k, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, c, k, q, kind, deferred,
+                                                uneven)) for r in range(world)]
     for p in procs:
         p.start()
     results = {}
@@ -125,3 +138,20 @@ def test_peer_exchange_three_ranks_auto_two_shot_u16():
     """world 3 (auto picks two-shot): 2^13 cells = 256 words split into 128-B
     segments of 96, 96 and 64 words; k = 130 makes the cells u16."""
     _run(3, 0, c=13, k=130)
+
+
+@pytest.mark.timeout(500)
+def test_peer_exchange_deferred_pools_uneven_shards():
+    """Deferred pools (the pending marks are the dirty bitmap; the merge writes
+    the union back as marks) with 95 % / 5 % shards."""
+    _run(2, 0, kind="peer", deferred=1, uneven=True)
+
+
+@pytest.mark.timeout(500)
+@pytest.mark.parametrize("deferred", [0, 1])
+def test_replica_step_two_ranks_uneven_shards(deferred):
+    """The NCCL-form exchange (all-gathers of bitmaps and touched keys, here
+    over gloo on one device) with a rank whose shard is smaller than the
+    other rank's touched-host set (the key buffer grows to the
+    gathered maximum before the key all-gather)."""
+    _run(2, 0, kind="replica", deferred=deferred, uneven=True)
