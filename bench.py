@@ -77,24 +77,26 @@ UNIT = "Mpackets/s"
 PEAKS_FALLBACK = dict(hbm_gbs=6650.0)
 
 
-KERNEL_SYMBOL = {"scan": "k_scan_packed16", "bitmap": "k_bitmap", "g0": "k_g0", "final": "k_final_write",
-                 "registry": "k_active", "sweep": "k_sweep"}
+KERNEL_SYMBOL = {"scan": ("k_scan_packed16",), "bitmap": ("k_bp_window", "k_bitmap"),
+                 "g0": ("k_g0",), "final": ("k_final_all",), "registry": ("k_active",),
+                 "sweep": ("k_bp_groups", "k_sweep")}
 
 
-def _ncu_traffic(kind, cfg):
+def _ncu_traffic(kind, cfg, bitplane=False):
     """dram read+write bytes per launch of the kernel behind `kind` for this workload,
     from the committed ncu --set full summaries (profiles/*ncu_kernels.txt, sections
     "## <tag>_<cfg>_<kernel>..."; newest file first); None if not captured."""
     import glob
-    sym = KERNEL_SYMBOL.get(kind)
-    if sym is None:
+    syms = KERNEL_SYMBOL.get(kind)
+    if syms is None:
         return None
+    sym = syms[0] if bitplane else syms[-1]
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_kernels.txt")), reverse=True):
         cur, vals = None, {}
         for line in open(path):
             if line.startswith("## "):
                 cur = line
-            elif cur and sym in cur and f"_{cfg}_" in cur and "dram__bytes" in line:
+            elif cur and f"_{cfg}_{sym}" in cur and "dram__bytes" in line:
                 parts = line.split()
                 v, unit = float(parts[1]), parts[2] if len(parts) > 2 else "byte"
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
@@ -331,6 +333,8 @@ def run_gpu(args, rank, world, local_rank):
         pool.set_option("scan_filter", scan_filter)
     if args.deferred != -1:
         pool.set_option("deferred", args.deferred)
+    if args.bitplane != -1:
+        pool.set_option("bitplane", args.bitplane)
     pool.set_option("concurrent", args.concurrent)
     for kv in args.opt:                       # experiments: --opt spin_wait=0 ...
         name, val = kv.split("=")
@@ -538,17 +542,25 @@ def run_gpu(args, rank, world, local_rank):
     nh = pipe.last_active
     S = 1 << w["c"]
     cb = pool.cell_bytes
-    deferred = bool(pool.deferred)
+    mode = pool.mode()
+    deferred, bitplane = mode["deferred"], mode["bitplane"]
     inc_on = args.incremental == "on"
+    nblocks = 2 * w["k"]
+    block_words = (S // nblocks + 31) // 32
     # algorithmic bytes per launch: the scan 40 B per
     # packet (8 B streamed pair + one 32-B sector for its scattered cell write);
     # the pool pass reads every cell and writes the bitmap, plus the previous
     # bitmap (incremental delta) and the pending marks (deferred pools)
+    # bit-plane mode: the pass reads S, P, M_e (+ the previous bitmap) and writes
+    # the bitmap and P, 2^c/8 bytes each; the due-block work reads the two blocks'
+    # k pending epochs of marks and reads + writes their cells
     alg_bytes = {
         "scan": n * 40,
-        "bitmap": S * cb + S // 8 + (S // 8 if inc_on else 0) + (S // 8 if deferred else 0),
+        "bitmap": ((S // 8) * (5 + (1 if inc_on else 0)) if bitplane else
+                   S * cb + S // 8 + (S // 8 if inc_on else 0) + (S // 8 if deferred else 0)),
         "g0": (nh * (32 * w["g"] + 12) if not inc_on else None),
-        "sweep": (2 * cb * 2 * pool.max_block_size if args.counter == "at" else
+        "sweep": ((w["k"] * block_words * 4 + 2 * cb * pool.max_block_size) if bitplane else
+                  2 * cb * 2 * pool.max_block_size if args.counter == "at" else
                   2 * cb * S if args.counter == "dr" else 0),
         "final": nh * (4 + 8 + 8 + 8 + 8 + 1),
         "registry": nh * 32,
@@ -563,7 +575,7 @@ def run_gpu(args, rank, world, local_rank):
     # aux-stream ones run beside them; profiles/*launches* has the serialised view)
     main_stream = ("scan", "bitmap", "g0") if not inc_on else ("scan", "bitmap")
     rooflines = {k: _roofline(k, per_kind[k], alg_bytes[k], hbm, peak_src, l2, n, S, cb, w,
-                              deferred, args.config)
+                              deferred, args.config, bitplane)
                  for k in main_stream if alg_bytes.get(k) and per_kind[k]["ms_per_launch"]}
     dom = max(rooflines, key=lambda k: per_kind[k]["ms_total"])
     step_ms = max_ms / args.steps
@@ -578,7 +590,9 @@ def run_gpu(args, rank, world, local_rank):
         "path": {"counter": args.counter,
                  "scan_filter": {-1: "auto (registry-stamp filter at >= 8 packets per host)",
                                  0: "off", 1: "on"}[args.scan_filter],
-                 "deferred_scatter": deferred, "incremental_g0": inc_on,
+                 "deferred_scatter": deferred, "bitplane": bitplane,
+                 "bitplane_window": mode["window"] if bitplane else None,
+                 "incremental_g0": inc_on,
                  "slice_step": "lagged (Pipeline.step_lagged)" if lagged else "Pipeline.step_fast"},
         "roofline": rooflines[dom],
         "rooflines": rooflines,
@@ -635,7 +649,7 @@ def run_gpu(args, rank, world, local_rank):
     _teardown(dist)
 
 
-def _roofline(kind, k, alg, hbm, peak_src, l2, n, S, cb, w, deferred, cfg):
+def _roofline(kind, k, alg, hbm, peak_src, l2, n, S, cb, w, deferred, cfg, bitplane=False):
     """One kernel's roofline: HBM (algorithmic bytes / launch time against the
     measured copy bandwidth) and, for work L2 serves, the L2 ceiling: the time
     the L2 probes need for the kernel's random accesses (or its stream) over
@@ -644,7 +658,7 @@ def _roofline(kind, k, alg, hbm, peak_src, l2, n, S, cb, w, deferred, cfg):
     achieved = alg / t / 1e9
     r = {"bound": "hbm", "kernel": kind, "achieved": achieved, "peak": hbm,
          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
-         "traffic": _ncu_traffic(kind, cfg),
+         "traffic": _ncu_traffic(kind, cfg, bitplane),
          "traffic_source": "profiles/*ncu_kernels.txt (ncu --set full, one launch)",
          "algorithmic_bytes_per_launch": alg}
     pool_in_l2 = S * cb <= (64 << 20)
@@ -772,6 +786,8 @@ def main():
     ap.add_argument("--deferred", type=int, choices=(-1, 0, 1), default=-1,
                     help="deferred scatter: scans mark an L2-resident pending-set bitmap and "
                          "the pool pass stores the clocks (VATE_OPT_DEFERRED; auto: cells > 64 MiB)")
+    ap.add_argument("--bitplane", type=int, choices=(-1, 0, 1), default=-1,
+                    help="bit-plane mode for deferred pools (VATE_OPT_BITPLANE; auto: on)")
     ap.add_argument("--opt", action="append", default=[],
                     help="extra pool option name=value (AtPool.set_option), for A/B runs")
     ap.add_argument("--lagged", type=int, choices=(0, 1), default=1,

@@ -60,15 +60,10 @@ __device__ __forceinline__ unsigned block_sum_bp(unsigned v) {
   return total;  // valid in thread 0
 }
 
-__global__ void k_bp_set_applied(int64_t* applied, uint32_t z, uint32_t q, int64_t e) {
-  applied[z] = e;
-  applied[q] = e;
-}
-
 // Block clock at epoch ep, given the clock of block 0 at epoch e_hi.
 __device__ __forceinline__ uint32_t clock_at(uint32_t bact0_hi, int64_t e_hi, int64_t ep,
                                              uint32_t b, uint32_t B) {
-  const uint32_t back = (uint32_t)((e_hi - ep) % (int64_t)B);
+  const uint32_t back = (uint32_t)(e_hi - ep) % B;  // e_hi - ep < the ring length
   return (bact0_hi + B - back + b) % B;
 }
 
@@ -159,12 +154,16 @@ __global__ void __launch_bounds__(256) k_bp_suffix(const uint32_t* __restrict__ 
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
     uint32_t acc = 0;
     int j = (int)L - 1;
+    uint32_t slot = slot_of_epoch(base + j, R);
     while (j >= 1) {
       uint32_t v[8];
       const int n = j >= 8 ? 8 : j;
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (u < n) v[u] = __ldcs(ring + (uint64_t)slot_of_epoch(base + j - u, R) * nwords + w);
+        if (u < n) {
+          v[u] = __ldcs(ring + (uint64_t)slot * nwords + w);
+          slot = slot ? slot - 1 : R - 1;
+        }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
         if (u < n) {
@@ -237,12 +236,16 @@ __global__ void __launch_bounds__(256) k_bp_apply(T* __restrict__ cells, Layout 
       const int64_t ap = applied[b];
       uint32_t acc = 0;
       int64_t ep = e_hi;
+      uint32_t slot = slot_of_epoch(ep, R);
       while (ep > ap && acc != rm) {
         uint32_t v[8];
         const int n = (int)((ep - ap) >= 8 ? 8 : (ep - ap));
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (u < n) v[u] = __ldcg(ring + (uint64_t)slot_of_epoch(ep - u, R) * nwords + w);
+          if (u < n) {
+            v[u] = __ldcg(ring + (uint64_t)slot * nwords + w);
+            slot = slot ? slot - 1 : R - 1;
+          }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (u >= n) break;
@@ -321,9 +324,12 @@ __global__ void __launch_bounds__(256) k_bp_groups(const uint32_t* __restrict__ 
     const int64_t newest = e_hi - (int64_t)g * kGroup;
     const int n = (int)((npend - (int64_t)g * kGroup) < kGroup ? (npend - (int64_t)g * kGroup) : kGroup);
     uint32_t v[kGroup];
+    uint32_t slot = slot_of_epoch(newest, R);  // one 64-bit modulo, then steps
 #pragma unroll
-    for (int u = 0; u < kGroup; ++u)
-      v[u] = u < n ? __ldcg(ring + (uint64_t)slot_of_epoch(newest - u, R) * nwords + w0 + wi) : 0u;
+    for (int u = 0; u < kGroup; ++u) {
+      v[u] = u < n ? __ldcg(ring + (uint64_t)slot * nwords + w0 + wi) : 0u;
+      slot = slot ? slot - 1 : R - 1;
+    }
     uint32_t acc = 0, p0 = 0, p1 = 0, p2 = 0, p3 = 0;
 #pragma unroll
     for (int u = 0; u < kGroup; ++u) {
@@ -340,8 +346,10 @@ __global__ void __launch_bounds__(256) k_bp_groups(const uint32_t* __restrict__ 
   }
 }
 
+constexpr int kResolveThreads = 64;  // small CTAs: the few thousand words spread over every SM
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_bp_resolve(T* __restrict__ cells, Layout L,
+__global__ void __launch_bounds__(kResolveThreads) k_bp_resolve(T* __restrict__ cells, Layout L,
                                                     DueRange r0, DueRange r1, int range_base,
                                                     int64_t e_hi, uint32_t bact0_hi,
                                                     const uint32_t* __restrict__ acc_in,
@@ -349,7 +357,7 @@ __global__ void __launch_bounds__(256) k_bp_resolve(T* __restrict__ cells, Layou
                                                     uint64_t wstride, uint32_t gstride,
                                                     unsigned long long* cleared) {
   constexpr int kChunk = 8;
-  __shared__ uint32_t cs[256 * 33];
+  __shared__ uint32_t cs[kResolveThreads * 33];
   uint32_t* c = cs + threadIdx.x * 33;
   const int slot_y = range_base + (int)blockIdx.y;
   const DueRange D = slot_y ? r1 : r0;
@@ -364,7 +372,17 @@ __global__ void __launch_bounds__(256) k_bp_resolve(T* __restrict__ cells, Layou
     const uint64_t w = w0 + wi, i0 = w * 32;
     const uint32_t cnt = (uint32_t)umin64(32, L.size - i0);
     const uint32_t rm = range_bits(i0, D.s, D.e);
-    for (uint32_t j = 0; j < cnt; ++j) c[j] = cells[i0 + j];
+    if (cnt == 32 && sizeof(T) <= 2) {  // 32 or 64 bytes: vector loads
+      constexpr int NV = (int)sizeof(T) * 2;
+      uint4 r[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) r[v] = reinterpret_cast<const uint4*>(cells + i0)[v];
+      const T* e = reinterpret_cast<const T*>(r);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) c[j] = e[j];
+    } else {
+      for (uint32_t j = 0; j < cnt; ++j) c[j] = cells[i0 + j];
+    }
     uint32_t done = 0;
     bool changed = false;
     for (uint32_t g0 = 0; g0 < G && done != rm; g0 += kChunk) {
@@ -409,8 +427,19 @@ __global__ void __launch_bounds__(256) k_bp_resolve(T* __restrict__ cells, Layou
         changed = true;
       }
     }
-    if (changed)
-      for (uint32_t j = 0; j < cnt; ++j) cells[i0 + j] = (T)c[j];
+    if (changed) {
+      if (cnt == 32 && sizeof(T) <= 2) {
+        constexpr int NV = (int)sizeof(T) * 2;
+        uint4 r[NV];
+        T* e = reinterpret_cast<T*>(r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) e[j] = (T)c[j];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) reinterpret_cast<uint4*>(cells + i0)[v] = r[v];
+      } else {
+        for (uint32_t j = 0; j < cnt; ++j) cells[i0 + j] = (T)c[j];
+      }
+    }
   }
   local = __reduce_add_sync(0xffffffffu, local);
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(cleared, (unsigned long long)local);
@@ -667,7 +696,6 @@ int bp_advance(vate_pool* p) {
   // the due blocks' pending epochs (applied[b], e]: newest marking epoch per
   // cell by 16-epoch groups, then clocks and the sweep rule per range
   const int64_t e = p->bp_e;
-  int64_t* dev_applied = p->bp_applied.as<int64_t>();
   const DueRange r0{s0, e0, p->bp_applied_h[z], z, 0}, r1{s1, e1, p->bp_applied_h[q], q, 1};
   const uint64_t wstride = p->bp_wmax;
   const uint32_t gstride = p->bp_gmax;
@@ -684,23 +712,19 @@ int bp_advance(vate_pool* p) {
     // both ranges in one launch unless they share a word (adjacent blocks: k = 1)
     const bool share = (e0 + 31) / 32 > s1 / 32 && (e1 + 31) / 32 > s0 / 32;
     for (int r = 0; r < (share ? 2 : 1); ++r)
-      VATE_LAUNCH(p, VATE_K_SWEEP, dim3(grid_for(nw, 256, 148u * 8u), share ? 1 : 2), 256, 0,
-                  k_bp_resolve<T>, (T*)p->cells, p->L, r0, r1, r, e, old_bact0,
+      VATE_LAUNCH(p, VATE_K_SWEEP, dim3(grid_for(nw, kResolveThreads, 148u * 32u), share ? 1 : 2),
+                  kResolveThreads, 0, k_bp_resolve<T>, (T*)p->cells, p->L, r0, r1, r, e, old_bact0,
                   p->bp_acc.as<const uint32_t>(), p->bp_planes.as<const uint4>(), wstride,
                   gstride, p->d_ctr + C_CLEARED);
     return VATE_OK;
   });
   if (rc == VATE_OK) {
-    // the two blocks now hold every epoch through e (host mirror, and the device
-    // entries by a one-thread kernel after the kernels above read the old ones)
+    // the two blocks now hold every epoch through e (the host mirror; the device
+    // copy is uploaded before its one reader, bp_materialize_all)
     p->bp_applied_h[z] = e;
     p->bp_applied_h[q] = e;
-    k_bp_set_applied<<<1, 1, 0, p->stream>>>(dev_applied, z, q, e);
-    p->launches++;
-    cudaError_t ce = cudaGetLastError();
-    if (ce == cudaSuccess)
-      ce = cudaMemcpyAsync(p->h_ctr + C_CLEARED, p->d_ctr + C_CLEARED, 8, cudaMemcpyDeviceToHost,
-                           p->stream);
+    cudaError_t ce = cudaMemcpyAsync(p->h_ctr + C_CLEARED, p->d_ctr + C_CLEARED, 8,
+                                     cudaMemcpyDeviceToHost, p->stream);
     if (ce == cudaSuccess) ce = cudaEventRecord(p->ev_adv, p->stream);
     if (ce != cudaSuccess) rc = cuda_fail(ce, "bit-plane advance");
   }
