@@ -651,9 +651,10 @@ def run_gpu(args, rank, world, local_rank):
 
 def _roofline(kind, k, alg, hbm, peak_src, l2, n, S, cb, w, deferred, cfg, bitplane=False):
     """One kernel's roofline: HBM (algorithmic bytes / launch time against the
-    measured copy bandwidth) and, for work L2 serves, the L2 ceiling: the time
-    the L2 probes need for the kernel's random accesses (or its stream) over
-    the launch time."""
+    measured copy bandwidth; `bound` stays "hbm", the contract's memory bound)
+    and, for work L2 serves, `l2`: the time the L2 probes need for the
+    kernel's random accesses (or its stream) over the launch time, with
+    `binding` set when L2, not HBM, is what limits the kernel."""
     t = k["ms_per_launch"] / 1e3
     achieved = alg / t / 1e9
     r = {"bound": "hbm", "kernel": kind, "achieved": achieved, "peak": hbm,
@@ -672,19 +673,18 @@ def _roofline(kind, k, alg, hbm, peak_src, l2, n, S, cb, w, deferred, cfg, bitpl
             t_l2 += n / (write_rate * 1e9)
         r["l2"] = {"ceiling_ms": t_l2 * 1e3, "frac": t_l2 / t,
                    "model": "n random 32-B registry reads + n random cell writes "
-                            "(red.or marks when deferred) at the probed L2 rates"}
-        if deferred or pool_in_l2:
-            r["bound"] = "l2"
+                            "(red.or marks when deferred) at the probed L2 rates",
+                   "binding": bool(deferred or pool_in_l2)}
     elif kind == "bitmap" and pool_in_l2:
         t_l2 = (S * cb + 3 * S // 8) / (l2["stream_read_GB_per_s"] * 1e9)
         r["l2"] = {"ceiling_ms": t_l2 * 1e3, "frac": t_l2 / t,
-                   "model": "the pool and bitmaps streamed at the probed L2 read rate"}
-        r["bound"] = "l2"
+                   "model": "the pool and bitmaps streamed at the probed L2 read rate",
+                   "binding": True}
     elif kind == "g0":
         t_l2 = w["g"] * (alg / (32 * w["g"] + 12)) / (l2["random_sector_reads_G_per_s"] * 1e9)
         r["l2"] = {"ceiling_ms": t_l2 * 1e3, "frac": t_l2 / t,
-                   "model": "g random 32-B bitmap reads per host at the probed L2 rate"}
-        r["bound"] = "l2"
+                   "model": "g random 32-B bitmap reads per host at the probed L2 rate",
+                   "binding": True}
     return r
 
 

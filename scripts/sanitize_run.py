@@ -26,8 +26,9 @@ for kind in ("at", "dr", "ts"):
                 pipe.flush_lagged(outs[0])
             pipe.process_slice_soa(t, a.astype(np.uint64), b.astype(np.uint64))
         pipe.wait_reports()
-        if kind == "at" and t in (4, 9):   # deferred marks for slices 4-8, flushed at 9
+        if kind == "at" and t in (4, 9):   # deferred marks + bit-plane history for slices 4-8
             pool.set_option("deferred", 1 if t == 4 else 0)
+            pool.set_option("bitplane", 1 if t == 4 else 0)
         if kind == "at" and t == 9:
             for form in (0, 1):
                 pool.set_option("scan_filter", form)
