@@ -398,6 +398,22 @@ int vate_trace_bucket(vate_pool* p, const uint8_t* records, uint64_t n, int wher
 
 /* stream-ordered device-to-device copy on the pool's stream (ingest carry) */
 int vate_copy_device(vate_pool* p, void* dst, const void* src, uint64_t bytes);
+
+/* ---- line-rate trace ingest (traceio.DeviceSlices; traceio.py:77-106,
+ * :188-230): two pinned staging buffers the reader fills from the file, async
+ * H2D, packing + slice runs on the device, carried slices across chunks. */
+typedef struct vate_tracer vate_tracer;
+int vate_tracer_create(vate_tracer** out, vate_pool* p, uint64_t chunk_records,
+                       uint64_t slice_us);
+int vate_tracer_destroy(vate_tracer* x);
+/* the slot's pinned staging buffer (16-byte records), once its last H2D is done */
+int vate_tracer_buffer(vate_tracer* x, int slot, uint8_t** host);
+int vate_tracer_submit(vate_tracer* x, int slot, uint64_t n, int64_t first_slice,
+                       uint64_t prev_ts, int has_prev, uint64_t carry_off, uint64_t carry_n);
+/* runs = (slice - first_slice, pair offset) per slice change, unsorted */
+int vate_tracer_collect(vate_tracer* x, int slot, uint64_t* runs, uint64_t cap,
+                        uint64_t* nruns, int64_t* violation, uint32_t** pairs_dev);
+int vate_tracer_release(vate_tracer* x, int slot);
 /* L2 ceilings for bench.py's rooflines (measurement only): over an
  * L2-resident buffer of buf_bytes (power of two), n random accesses per
  * launch, reps timed launches after a warm-up; out = [random 32-B sector

@@ -58,6 +58,12 @@ _SIGS = {
     "vate_pool_device_bytes": ([_p, _p], _int),
     "vate_pool_mode": ([_p, _p], _int),
     "vate_pool_set_latency": ([_p, _int], _int),
+    "vate_tracer_create": ([_p, _p, _u64, _u64], _int),
+    "vate_tracer_destroy": ([_p], _int),
+    "vate_tracer_buffer": ([_p, _int, _p], _int),
+    "vate_tracer_submit": ([_p, _int, _u64, _i64, _u64, _int, _u64, _u64], _int),
+    "vate_tracer_collect": ([_p, _int, _p, _u64, _p, _p, _p], _int),
+    "vate_tracer_release": ([_p, _int], _int),
     "vate_bench_l2": ([_p, _u64, _u64, _int, _p], _int),
     "vate_pool_latency": ([_p, _p], _int),
     "vate_pool_lat_mark": ([_p, _i64, _int], _int),

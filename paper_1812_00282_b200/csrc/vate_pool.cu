@@ -31,6 +31,9 @@ int set_error(int code, const std::string& msg) {
 }
 
 int cuda_fail(cudaError_t e, const char* what) {
+  // consume the runtime's last-error state: a non-sticky failure (a bad device
+  // ordinal, a failed allocation) must not resurface at the next launch check
+  (void)cudaGetLastError();
   return set_error(e == cudaErrorMemoryAllocation ? VATE_ENOMEM : VATE_ECUDA,
                    std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }

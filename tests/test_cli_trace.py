@@ -165,6 +165,73 @@ def test_cli_input_errors(tmp_path):
     assert cli.main(["estimate", "--trace", str(trace), "--c", "2"]) == cli.EXIT_CONFIG
 
 
+def _device_items(pool, path, fmt, slice_us, chunk, cudart):
+    import ctypes
+    from paper_1812_00282_b200 import traceio as tio
+    got = []
+    for t, dptr, n in tio.DeviceSlices(pool, path, fmt, slice_us, chunk=chunk):
+        pool.synchronize()
+        buf = np.empty(2 * n, dtype=np.uint32)
+        if n:
+            assert cudart.cudaMemcpy(ctypes.c_void_p(buf.ctypes.data), ctypes.c_void_p(dptr),
+                                     ctypes.c_size_t(8 * n), 2) == 0
+        got.append((t, buf[0::2].astype(np.uint64), buf[1::2].astype(np.uint64)))
+    return got
+
+
+def _cudart():
+    import ctypes
+    import nvidia.cuda_runtime
+    return ctypes.CDLL(os.path.join(os.path.dirname(nvidia.cuda_runtime.__file__), "lib",
+                                    "libcudart.so.12"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", [traceio.BINARY, traceio.TEXT])
+@pytest.mark.parametrize("bad_at", [5, 40_000, 70_001])
+def test_device_slices_order_errors_like_the_reference(tmp_path, fmt, bad_at):
+    """An out-of-order record: DeviceSlices yields exactly the slices the
+    reference's reader + slice_stream yield before the error (those completed
+    in the 32K-record batches before the failing one, traceio.py:60-145,
+    188-230), then raises TraceOrderError at the same position."""
+    import paper_1812_00282_b200 as vb
+    rng = np.random.default_rng(bad_at)
+    n = 90_000
+    ts = np.cumsum(rng.integers(0, 40, n)).astype(np.uint64)
+    ts[bad_at] = ts[bad_at - 1] - np.uint64(1) if ts[bad_at - 1] else np.uint64(0)
+    if ts[bad_at] >= ts[bad_at - 1]:
+        ts[bad_at - 1] += np.uint64(5)
+    recs = traceio.make_records(ts, (0x0A000000 + rng.integers(0, 50, n)).astype(np.uint32),
+                                rng.integers(1, 1 << 32, n, dtype=np.uint64).astype(np.uint32))
+    path = tmp_path / ("t.bin" if fmt == traceio.BINARY else "t.csv")
+    traceio.write_trace(path, recs, fmt)
+    want, want_err = [], None
+    try:
+        for t, a, b in traceio.slice_stream(traceio.read_batches(path, fmt), 997):
+            want.append((t, a, b))
+    except traceio.TraceOrderError as e:
+        want_err = str(e)
+    assert want_err is not None
+    pool = vb.AtPool(8, 2)
+    cudart = _cudart()
+    gen_items, got_err = [], None
+    try:
+        import ctypes
+        for t, dptr, n_ in traceio.DeviceSlices(pool, path, fmt, 997):
+            pool.synchronize()
+            buf = np.empty(2 * n_, dtype=np.uint32)
+            if n_:
+                cudart.cudaMemcpy(ctypes.c_void_p(buf.ctypes.data), ctypes.c_void_p(dptr),
+                                  ctypes.c_size_t(8 * n_), 2)
+            gen_items.append((t, buf[0::2].astype(np.uint64), buf[1::2].astype(np.uint64)))
+    except traceio.TraceOrderError as e:
+        got_err = str(e)
+    assert got_err == want_err
+    assert [g[0] for g in gen_items] == [w[0] for w in want]
+    for (t, a, b), (_, wa, wb) in zip(gen_items, want):
+        assert np.array_equal(a, wa) and np.array_equal(b, wb), t
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("chunk", [1, 7, 100, 1 << 22])
 def test_device_slices_equal_slice_stream(tmp_path, chunk):
