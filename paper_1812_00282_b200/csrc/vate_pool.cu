@@ -984,10 +984,13 @@ int flush_pending(vate_pool* p) {
   return VATE_OK;
 }
 
-// Auto: defer when the cells exceed 64 MiB (the part of the 126 MB L2 a pool
-// can keep beside the registry and the packet stream): cfg 4 / 5's 512 MiB.
+// Auto: defer (and keep the bit-plane history) when the cells take 64 MiB or
+// more -- half the 126 MB L2, beside the registry and the packet stream: cfg
+// 3's 64 MiB (0.380 -> 0.352 ms per slice) and cfg 4 / 5's 512 MiB; an
+// L2-resident pool below that is faster with direct stores (cfg 2: 0.140 vs
+// 0.148, cfg 1: 0.056 vs 0.066; profiles/r02h_ab_modes.txt).
 bool default_deferred(const vate_pool* p) {
-  return p->kind == VATE_AT && p->L.size * (uint64_t)p->cell_bytes > kDeferBytes;
+  return p->kind == VATE_AT && p->L.size * (uint64_t)p->cell_bytes >= kDeferBytes;
 }
 
 int set_deferred(vate_pool* p, bool on) {
