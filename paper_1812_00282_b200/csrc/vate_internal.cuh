@@ -149,7 +149,7 @@ __device__ __forceinline__ void for_word_clocks(uint64_t i0, uint32_t cnt, const
 struct AtRule {
   Layout L;
   uint32_t bact0;
-  static constexpr bool kMark = false;
+  static constexpr bool kMark = false, kSkip = false;
   template <typename T>
   __device__ __forceinline__ T value(uint64_t cell) const {
     return (T)clock_of(bact0, block_of(cell, L), L.B);
@@ -157,7 +157,7 @@ struct AtRule {
 };
 struct ConstRule {
   unsigned long long v;  // DrPool: 0 (pools.py:314-315); TsPool: the slice index (:363-364)
-  static constexpr bool kMark = false;
+  static constexpr bool kMark = false, kSkip = false;
   template <typename T>
   __device__ __forceinline__ T value(uint64_t) const { return (T)v; }
 };
@@ -168,12 +168,18 @@ struct ConstRule {
 // before any other cell access and before every advance).
 struct MarkRule {
   uint32_t* pend;
-  static constexpr bool kMark = true;
+  static constexpr bool kMark = true, kSkip = false;
+};
+// No cell write (a registry-only pass).
+struct SkipRule {
+  static constexpr bool kMark = false, kSkip = true;
 };
 
 template <typename T, typename Rule>
 __device__ __forceinline__ void store_cell(T* __restrict__ cells, uint64_t c, const Rule& rule) {
-  if constexpr (Rule::kMark)
+  if constexpr (Rule::kSkip)
+    return;
+  else if constexpr (Rule::kMark)
     atomicOr(rule.pend + (c >> 5), 1u << (c & 31));  // result unused: one RED
   else
     cells[c] = rule.template value<T>(c);
@@ -437,6 +443,7 @@ struct vate_pool {
   int opt_g0 = 0;
   int opt_inc = 1;            // incremental g0 through the inverse index
   int opt_scan_check = -1;   // registry-stamp filter: -1 auto, 0 off, 1 on
+  int opt_scan_split = 0;    // A/B: cell writes and registry in two passes
   int scan_form_used = 0;     // the form the last packed scan ran (auto resolved)
   int opt_concurrent = 1;     // fork independent estimate phases onto aux_stream
   int opt_fuse_sweep = 1;     // slice step: the advance sweep inside the bitmap pass

@@ -1359,6 +1359,10 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     if (!value) p->inc.valid = false;
     return VATE_OK;
   }
+  if (option == 8 && (value == 0 || value == 1)) {  // A/B: the scan split in two passes
+    p->opt_scan_split = (int)value;
+    return VATE_OK;
+  }
   if (option == VATE_OPT_BITPLANE && value >= -1 && value <= 1) {
     int rc = enter(p);
     if (rc) return rc;
@@ -1492,7 +1496,20 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
       using Rl = decltype(rule);
       T* cells = (T*)p->cells;
       uint64_t done = 0;
-      if (aligned16 && n >= 2) {  // one uint4 (two packets) per thread
+      if (aligned16 && n >= 2 && hosts && p->opt_scan_split) {  // A/B: cells, then registry
+        const uint64_t n2 = n / 2;
+        const uint32_t grid = grid_for(n2, kThreads, 148u * 64u);
+        const uint4* src = (const uint4*)d_pairs;
+        VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, false, false, Rl>),
+                    src, n2, cells, H, rule, R, (long long)t);
+        if (filt)
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, true, SkipRule>),
+                      src, n2, cells, H, SkipRule{}, R, (long long)t);
+        else
+          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, false, SkipRule>),
+                      src, n2, cells, H, SkipRule{}, R, (long long)t);
+        done = 2 * n2;
+      } else if (aligned16 && n >= 2) {  // one uint4 (two packets) per thread
         const uint64_t n2 = n / 2;
         const uint32_t grid = grid_for(n2, kThreads, 148u * 64u);
         const uint4* src = (const uint4*)d_pairs;
