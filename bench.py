@@ -393,7 +393,11 @@ def run_gpu(args, rank, world, local_rank):
     elif world > 1:                               # NCCL all-gathers + merge kernel
         replica = ReplicaStep(pipe, dist, torch)
     run_slice = replica if replica is not None else pipe.step_fast
-    lagged = bool(args.lagged) and replica is None
+    # the pipelined step: one GPU, or N GPUs with the peer-memory exchange run
+    # inside it (PeerStep.bind_lagged); the NCCL form stays one call per slice
+    lagged = bool(args.lagged) and (replica is None or args.exchange == "p2p")
+    if lagged and replica is not None:
+        replica.bind_lagged()
 
     def _lagged_rows(res):
         return None if res is None else res[1]

@@ -261,6 +261,12 @@ int vate_estimate_wait(vate_pool* p);
 /* Device addresses of the last finished report rows (for GPU consumers; with
  * null host output arrays the rows stay in HBM and nothing crosses PCIe).
  * Valid until the next-but-one finish (two report sets alternate). */
+/* Multi-GPU lagged step: with a peer exchange set, every lagged slice step
+ * (vate_slice_step_lagged, vate_slice_lagged_begin/_end) runs the replica
+ * exchange (vate_peer_exchange) between the slice's scan and its pool pass,
+ * and this rank's reports are share `part` of `nparts` of the sorted active
+ * set.  x = NULL restores the single-GPU step.  Set between lagged runs. */
+int vate_pool_set_peer(vate_pool* p, struct vate_peer* x, int part, int nparts);
 int vate_reports_device(vate_pool* p, uint64_t** host, double** est, double** zv,
                         uint8_t** sat);
 

@@ -70,6 +70,7 @@ __device__ __forceinline__ uint32_t clock_at(uint32_t bact0_hi, int64_t e_hi, in
 // The estimate's pass: bits = ~(S | P | M) over valid cells, P's popcount,
 // the incremental-g0 delta against the previous bitmap, and (fold) P | M as
 // the new prefix.  Four words per thread (16-byte loads).
+template <bool CS>
 __global__ void __launch_bounds__(256) k_bp_window(const uint32_t* __restrict__ S,
                                                    const uint32_t* __restrict__ Pin,
                                                    const uint32_t* __restrict__ M,
@@ -120,10 +121,15 @@ __global__ void __launch_bounds__(256) k_bp_window(const uint32_t* __restrict__ 
       if (D.bprev && w < nwords) delta_word(D, ds, bits[i], prev[i], i0);
     }
     if (w0 + 4 <= nwords) {
-      reinterpret_cast<uint4*>(bitmap)[q] = make_uint4(bits[0], bits[1], bits[2], bits[3]);
-      if (Pout)
-        reinterpret_cast<uint4*>(Pout)[q] =
-            make_uint4(pv[0] | m[0], pv[1] | m[1], pv[2] | m[2], pv[3] | m[3]);
+      const uint4 bv = make_uint4(bits[0], bits[1], bits[2], bits[3]);
+      const uint4 pw = make_uint4(pv[0] | m[0], pv[1] | m[1], pv[2] | m[2], pv[3] | m[3]);
+      if (CS) {  // evict-first: keep the registry and the marks in L2 for the next scan
+        __stcs(reinterpret_cast<uint4*>(bitmap) + q, bv);
+        if (Pout) __stcs(reinterpret_cast<uint4*>(Pout) + q, pw);
+      } else {
+        reinterpret_cast<uint4*>(bitmap)[q] = bv;
+        if (Pout) reinterpret_cast<uint4*>(Pout)[q] = pw;
+      }
     } else {
       for (int i = 0; i < 4; ++i)
         if (w0 + i < nwords) {
@@ -312,19 +318,19 @@ __global__ void __launch_bounds__(256) k_bp_groups(const uint32_t* __restrict__ 
                                                    int64_t e_hi, uint32_t* __restrict__ acc_out,
                                                    uint4* __restrict__ planes_out,
                                                    uint64_t wstride, uint32_t gstride) {
-  const DueRange D = blockIdx.y ? r1 : r0;
+  // grid: x over the range's words, y over 16-epoch groups, z over the two ranges
+  const DueRange D = blockIdx.z ? r1 : r0;
   const uint64_t w0 = D.s / 32, W = (D.e + 31) / 32 - w0;
   const int64_t npend = e_hi - D.ap;
-  if (npend <= 0 || W == 0) return;
-  const uint64_t G = (uint64_t)((npend + kGroup - 1) / kGroup);
-  const uint64_t total = G * W;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total; idx += stride) {
-    const uint64_t g = idx / W, wi = idx - g * W;
-    const int64_t newest = e_hi - (int64_t)g * kGroup;
-    const int n = (int)((npend - (int64_t)g * kGroup) < kGroup ? (npend - (int64_t)g * kGroup) : kGroup);
+  const uint32_t g = blockIdx.y;
+  if (npend <= (int64_t)g * kGroup) return;
+  const int64_t newest = e_hi - (int64_t)g * kGroup;
+  const int n = (int)((npend - (int64_t)g * kGroup) < kGroup ? (npend - (int64_t)g * kGroup) : kGroup);
+  const uint32_t slot0 = slot_of_epoch(newest, R);  // one 64-bit modulo per thread
+  for (uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; wi < W;
+       wi += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t v[kGroup];
-    uint32_t slot = slot_of_epoch(newest, R);  // one 64-bit modulo, then steps
+    uint32_t slot = slot0;
 #pragma unroll
     for (int u = 0; u < kGroup; ++u) {
       v[u] = u < n ? __ldcg(ring + (uint64_t)slot * nwords + w0 + wi) : 0u;
@@ -340,7 +346,7 @@ __global__ void __launch_bounds__(256) k_bp_groups(const uint32_t* __restrict__ 
       if (u & 4) p2 |= m;
       if (u & 8) p3 |= m;
     }
-    const uint64_t o = ((uint64_t)blockIdx.y * gstride + g) * wstride + wi;
+    const uint64_t o = ((uint64_t)blockIdx.z * gstride + g) * wstride + wi;
     acc_out[o] = acc;
     planes_out[o] = make_uint4(p0, p1, p2, p3);
   }
@@ -662,9 +668,11 @@ int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
   const uint32_t* S = (j + 1 <= p->bp_L - 1) ? p->bp_S.as<const uint32_t>() + (uint64_t)j * nwords
                                              : nullptr;  // S[j+1] at index j
   const bool fold = fused_advance && !p->bp_folded;
-  VATE_LAUNCH(p, VATE_K_BITMAP, grid_for((nwords + 3) / 4, 256, 148u * 16u), 256, 0, k_bp_window,
-              S, p->bp_P.as<const uint32_t>(), pend_ptr(p), fold ? p->bp_P.as<uint32_t>() : nullptr,
-              p->bitmap.as<uint32_t>(), nwords, p->L.size, p->d_ctr + C_P, D, pub);
+  // evict-first stores: the registry and the marks stay in L2 for the next scan
+  VATE_LAUNCH(p, VATE_K_BITMAP, grid_for((nwords + 3) / 4, 256, 148u * 16u), 256, 0,
+              k_bp_window<true>, S, p->bp_P.as<const uint32_t>(), pend_ptr(p),
+              fold ? p->bp_P.as<uint32_t>() : nullptr, p->bitmap.as<uint32_t>(), nwords,
+              p->L.size, p->d_ctr + C_P, D, pub);
   if (fold) p->bp_folded = true;
   if (fused_advance) return bp_advance(p);
   return VATE_OK;
@@ -702,8 +710,10 @@ int bp_advance(vate_pool* p) {
   if ((uint64_t)((e - std::min(r0.ap, r1.ap) + kGroup - 1) / kGroup) > gstride ||
       (e0 - s0 + 63) / 32 > wstride || (e1 - s1 + 63) / 32 > wstride)
     return set_error(VATE_EVALUE, "bit-plane advance: a due block is further behind than the ring");
-  const uint64_t tot = (uint64_t)gstride * wstride;
-  VATE_LAUNCH(p, VATE_K_SWEEP, dim3(grid_for(tot, 256, 148u * 16u), 2), 256, 0, k_bp_groups,
+  const uint32_t gmax = (uint32_t)((e - std::min(r0.ap, r1.ap) + kGroup - 1) / kGroup);
+  const uint64_t wmax = std::max((e0 + 31) / 32 - s0 / 32, (e1 + 31) / 32 - s1 / 32);
+  VATE_LAUNCH(p, VATE_K_SWEEP, dim3(grid_for(wmax, 256, 148u * 4u), std::max(gmax, 1u), 2), 256, 0,
+              k_bp_groups,
               p->bp_ring.as<const uint32_t>(), p->bp_R, nwords, r0, r1, e,
               p->bp_acc.as<uint32_t>(), p->bp_planes.as<uint4>(), wstride, gstride);
   int rc = with_cell_bp(p->cell_bytes, [&](auto tag) -> int {

@@ -835,7 +835,7 @@ static int lagged_begin_prev(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64
   std::swap(p->stream, p->aux_stream);
   hosts->lagged = true;
   uint64_t nh = 0, pin = 0;
-  int rc = begin_complete(p, hosts, g, cell_stream, t, kp, &nh, &pin);
+  int rc = begin_complete(p, hosts, g, cell_stream, t, kp, &nh, &pin, p->lag_part, p->lag_nparts);
   hosts->lagged = false;
   std::swap(p->stream, p->aux_stream);
   res->nhosts = nh;
@@ -890,6 +890,9 @@ int vate_slice_lagged_begin(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_
   if (rc) return rc;
   if (!p->ev_counts) VATE_CUDA(cudaEventCreateWithFlags(&p->ev_counts, cudaEventDisableTiming));
   if (!p->ev_post) VATE_CUDA(cudaEventCreateWithFlags(&p->ev_post, cudaEventDisableTiming));
+  if (p->lag_peer && n > peer_key_cap(p->lag_peer))  // before the scan: replicas stay equal
+    return set_error(VATE_EVALUE, std::to_string(n) + " packets exceed the peer key_cap " +
+                                      std::to_string(peer_key_cap(p->lag_peer)));
   p->lag_next_t = t;
   p->lag_next_kp = k_prime;
   p->lag_has_next = true;
@@ -947,12 +950,17 @@ int vate_slice_lagged_end(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t 
     rc = lat_scan_end(p, t);
     if (rc) return rc;
   }
+  // multi-GPU: merge the replicas and absorb the peers' hosts of slice t
+  if (p->lag_peer) {
+    rc = vate_peer_exchange(p->lag_peer, t, nullptr);
+    if (rc) return rc;
+  }
   // slice t up to its counters; then its sweep (it reads no g0, only cells already counted)
   if (p->post_recorded) {
     VATE_CUDA(cudaStreamWaitEvent(p->stream, p->ev_post, 0));
     p->post_recorded = false;
   }
-  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime, true, true);  // + advance(t)
+  rc = begin_enqueue(p, hosts, g, cell_stream, t, k_prime, p->lag_nparts == 1, true);  // + advance(t)
   if (rc) return rc;
   VATE_CUDA(cudaEventRecord(p->ev_counts, p->stream));
   p->lag_pending = true;
@@ -996,6 +1004,18 @@ int vate_slice_flush(vate_pool* p, vate_hosts* hosts, uint64_t g, uint64_t cell_
   return vate_slice_lagged_end(p, hosts, g, cell_stream, 0, floor,
                                log_zp_table[res->pool_inactive], out_host, out_est, out_zv,
                                out_sat, cap, res);
+}
+
+int vate_pool_set_peer(vate_pool* p, vate_peer* x, int part, int nparts) {
+  int rc = enter(p);
+  if (rc) return rc;
+  if (p->lag_pending || p->lag_completing)
+    return set_error(VATE_EVALUE, "set the peer between lagged runs (flush first)");
+  if (nparts < 1 || part < 0 || part >= nparts) return set_error(VATE_EVALUE, "bad part");
+  p->lag_peer = x;
+  p->lag_part = x ? part : 0;
+  p->lag_nparts = x ? nparts : 1;
+  return VATE_OK;
 }
 
 int vate_reports_device(vate_pool* p, uint64_t** host, double** est, double** zv,

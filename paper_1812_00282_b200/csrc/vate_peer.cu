@@ -236,6 +236,10 @@ static int with_cell_t(int bytes, F f) {
 
 }  // namespace vate
 
+namespace vate {
+uint64_t peer_key_cap(const vate_peer* x) { return x->key_cap; }
+}  // namespace vate
+
 using namespace vate;
 
 extern "C" {

@@ -1359,10 +1359,7 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     if (!value) p->inc.valid = false;
     return VATE_OK;
   }
-  if (option == 8 && (value == 0 || value == 1)) {  // A/B: the scan split in two passes
-    p->opt_scan_split = (int)value;
-    return VATE_OK;
-  }
+
   if (option == VATE_OPT_BITPLANE && value >= -1 && value <= 1) {
     int rc = enter(p);
     if (rc) return rc;
@@ -1496,22 +1493,14 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
       using Rl = decltype(rule);
       T* cells = (T*)p->cells;
       uint64_t done = 0;
-      if (aligned16 && n >= 2 && hosts && p->opt_scan_split) {  // A/B: cells, then registry
+      if (aligned16 && n >= 2) {  // one uint4 (two packets) per thread
         const uint64_t n2 = n / 2;
-        const uint32_t grid = grid_for(n2, kThreads, 148u * 64u);
-        const uint4* src = (const uint4*)d_pairs;
-        VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, false, false, Rl>),
-                    src, n2, cells, H, rule, R, (long long)t);
-        if (filt)
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, true, SkipRule>),
-                      src, n2, cells, H, SkipRule{}, R, (long long)t);
-        else
-          VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, false, SkipRule>),
-                      src, n2, cells, H, SkipRule{}, R, (long long)t);
-        done = 2 * n2;
-      } else if (aligned16 && n >= 2) {  // one uint4 (two packets) per thread
-        const uint64_t n2 = n / 2;
-        const uint32_t grid = grid_for(n2, kThreads, 148u * 64u);
+        // about four uint4 per thread, between 16 and 64 CTAs per SM: cfg 4
+        // (2.5M uint4) 0.185 -> 0.178 ms per slice over one per thread; cfg 5
+        // (50M) collapses with 16 per SM (3.6 vs 1.2 ms: its per-CTA stamp filter
+        // and deferred queue are per launch slice of packets)
+        const uint64_t want = std::max<uint64_t>(148ull * 16u, n2 / (4ull * kThreads));
+        const uint32_t grid = grid_for(n2, kThreads, (uint32_t)std::min<uint64_t>(want, 148ull * 64u));
         const uint4* src = (const uint4*)d_pairs;
         if (hosts && filt)
           VATE_LAUNCH(p, VATE_K_SCAN, grid, kThreads, 0, (k_scan_packed16<T, true, true, Rl>),

@@ -189,6 +189,14 @@ class PeerStep(_SliceStepBase):
         if n_packets > self.key_cap:
             raise ValueError(f"{n_packets} packets exceed the peer key_cap {self.key_cap}")
 
+    def bind_lagged(self, on: bool = True) -> None:
+        """Run the exchange inside the pipeline's lagged step (vate_pool_set_peer):
+        ``pipe.step_lagged`` then merges the replicas between each slice's scan
+        and its pool pass, and its rows are this rank's share -- slice t-1's
+        tail runs beside slice t's scan on every rank, as on one GPU."""
+        check(lib.vate_pool_set_peer(self.pipe.pool.handle, self.handle if on else None,
+                                     self.rank if on else 0, self.world if on else 1))
+
     def exchange(self, t: int, n_packets: int, count_touched: bool = False) -> None:
         """One slice's exchange; count_touched also sums the ranks' touched-host
         counts (one small read per peer window, so off on the hot path)."""
@@ -206,6 +214,9 @@ class PeerStep(_SliceStepBase):
 
     def close(self) -> None:
         if getattr(self, "handle", None):
+            pool = self.pipe.pool
+            if pool.handle is not None and pool.handle.value:
+                lib.vate_pool_set_peer(pool.handle, None, 0, 1)
             lib.vate_peer_destroy(self.handle)
             self.handle = None
 

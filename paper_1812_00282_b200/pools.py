@@ -267,7 +267,7 @@ class _DevicePool:
         return n.value
 
     OPTIONS = ("g0_kernel", "incremental", "scan_filter", "concurrent", "inc_sort",
-               "fuse_sweep", "deferred", "bitplane", "scan_split")
+               "fuse_sweep", "deferred", "bitplane")
 
     def set_option(self, option: str, value: int) -> None:
         """Tuning switches (include/vate.h enum vate_option): 'g0_kernel' (0 auto,

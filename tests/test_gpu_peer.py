@@ -53,8 +53,12 @@ def _worker(rank, world, port, mode, c, k, result_q, kind="peer", deferred=-1, u
         pipe = vb.Pipeline(pool, cfg, kp)
         ref = vo.OraclePipeline(ocfg, kp)
         torch.cuda.set_device(0)
-        step = (PeerStep(pipe, dist, key_cap=40_000, mode=mode) if kind == "peer"
+        step = (PeerStep(pipe, dist, key_cap=40_000, mode=mode) if kind.startswith("peer")
                 else ReplicaStep(pipe, dist, torch))
+        lagged = kind == "peer_lagged"
+        if lagged:
+            step.bind_lagged()
+        pending = {}
         rng = np.random.default_rng(11)
         for t in range(18):
             n = int(rng.integers(0, 30_000)) if t != 5 else 0
@@ -71,11 +75,23 @@ def _worker(rank, world, port, mode, c, k, result_q, kind="peer", deferred=-1, u
             cap = 4096
             out = (np.empty(cap, np.uint64), np.empty(cap, np.float64), np.empty(cap, np.float64),
                    np.empty(cap, np.uint8))
-            rep = step(t, mine.ctypes.data if len(mine) else 0, len(mine), "host", out)
+            outs_l = [tuple(np.empty(cap, dt) for dt in (np.uint64, np.float64, np.float64,
+                                                           np.uint8)) for _ in range(2)]
+            if lagged:
+                res = pipe.step_lagged(t, mine.ctypes.data if len(mine) else 0, len(mine),
+                                       "host", outs_l[t % 2])
+            else:
+                rep = step(t, mine.ctypes.data if len(mine) else 0, len(mine), "host", out)
             pipe.wait_reports()
             want = ref.process_slice(t, a.astype(np.uint64), b.astype(np.uint64))
             if pipe.pool.snapshot_bytes() != ref.pool.snapshot_bytes():
                 msgs.append(f"rank {rank} t {t}: snapshot differs")
+            if lagged:   # the rows of slice t-1 came with this call
+                pending[t] = want
+                if res is None:
+                    continue
+                tp, rep = res
+                want = pending.pop(tp)
             if want.reports is None:
                 if rep is not None and len(rep.host):
                     msgs.append(f"rank {rank} t {t}: reports where the oracle has none")
@@ -91,7 +107,14 @@ def _worker(rank, world, port, mode, c, k, result_q, kind="peer", deferred=-1, u
                 msgs.append(f"rank {rank} t {t}: estimates differ")
             if pipe.last_pool_inactive != want.pool_inactive:
                 msgs.append(f"rank {rank} t {t}: pool_inactive differs")
-        if kind == "peer":
+        if lagged:
+            res = pipe.flush_lagged(outs_l[0])
+            pipe.wait_reports()
+            if res is not None:
+                pending.pop(res[0], None)
+            if pending:
+                msgs.append(f"rank {rank}: slices never completed {sorted(pending)}")
+        if kind.startswith("peer"):
             info = step.info()
             if info["two_shot"] != (mode == 2 or (mode == 0 and world > 2)):
                 msgs.append(f"rank {rank}: unexpected merge form {info}")
@@ -155,3 +178,13 @@ def test_replica_step_two_ranks_uneven_shards(deferred):
     other rank's touched-host set (the key buffer grows to the
     gathered maximum before the key all-gather)."""
     _run(2, 0, kind="replica", deferred=deferred, uneven=True)
+
+
+@pytest.mark.timeout(500)
+@pytest.mark.parametrize("world,deferred", [(2, 0), (3, 1)])
+def test_peer_exchange_in_the_lagged_step(world, deferred):
+    """The multi-GPU step in the software-pipelined form (vate_pool_set_peer):
+    the exchange between each slice's scan and its pool pass, slice t-1's tail
+    beside slice t's scan; snapshots every slice and every rank's share of the
+    previous slice's reports equal the oracle's."""
+    _run(world, 0, kind="peer_lagged", deferred=deferred)
