@@ -648,6 +648,9 @@ int bp_rebuild(vate_pool* p) {
   return rc;
 }
 
+static int bp_due(vate_pool* p);
+static int bp_next_epoch(vate_pool* p);
+
 int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
   (void)k_prime;
   const uint64_t nwords = bp_nwords(p);
@@ -668,13 +671,34 @@ int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
   const uint32_t* S = (j + 1 <= p->bp_L - 1) ? p->bp_S.as<const uint32_t>() + (uint64_t)j * nwords
                                              : nullptr;  // S[j+1] at index j
   const bool fold = fused_advance && !p->bp_folded;
+  const uint32_t* M = pend_ptr(p);
+  if (fused_advance) {
+    // the due blocks on the aux stream beside the window pass (they read only
+    // ring slots up to this epoch and write only cells, which the pass does
+    // not touch); bp_wait_aux orders every later cell access after them.
+    // cfg 4: 0.183 -> 0.169 ms per slice (profiles/r02l_ab_bp_aux.txt); beside
+    // the next slice's scan instead they slowed both down (0.240 -> 0.268)
+    if (p->adv_pending) return set_error(VATE_EVALUE, "previous advance not collected");
+    if (!p->ev_bp) VATE_CUDA(cudaEventCreateWithFlags(&p->ev_bp, cudaEventDisableTiming));
+    VATE_CUDA(cudaEventRecord(p->ev_fork, p->stream));
+    VATE_CUDA(cudaStreamWaitEvent(p->aux_stream, p->ev_fork, 0));
+    std::swap(p->stream, p->aux_stream);
+    rc = bp_due(p);
+    if (rc == VATE_OK) {
+      const cudaError_t ce = cudaEventRecord(p->ev_bp, p->stream);
+      if (ce != cudaSuccess) rc = cuda_fail(ce, "bit-plane advance");
+    }
+    std::swap(p->stream, p->aux_stream);
+    if (rc) return rc;
+    p->bp_join = true;
+  }
   // evict-first stores: the registry and the marks stay in L2 for the next scan
   VATE_LAUNCH(p, VATE_K_BITMAP, grid_for((nwords + 3) / 4, 256, 148u * 16u), 256, 0,
-              k_bp_window<true>, S, p->bp_P.as<const uint32_t>(), pend_ptr(p),
+              k_bp_window<true>, S, p->bp_P.as<const uint32_t>(), M,
               fold ? p->bp_P.as<uint32_t>() : nullptr, p->bitmap.as<uint32_t>(), nwords,
               p->L.size, p->d_ctr + C_P, D, pub);
   if (fold) p->bp_folded = true;
-  if (fused_advance) return bp_advance(p);
+  if (fused_advance) return bp_next_epoch(p);
   return VATE_OK;
 }
 
@@ -689,6 +713,14 @@ int bp_advance(vate_pool* p) {
   if (!p->bp_folded)
     VATE_LAUNCH(p, VATE_K_OTHER, grid_for(nwords, 256, 148u * 16u), 256, 0, k_bp_fold,
                 p->bp_P.as<uint32_t>(), pend_ptr(p), nwords);
+  int rc = bp_due(p);
+  if (rc) return rc;
+  return bp_next_epoch(p);
+}
+
+// The clock advance and the two due blocks (their kernels on p->stream).
+static int bp_due(vate_pool* p) {
+  const uint64_t nwords = bp_nwords(p);
   const uint32_t B = p->L.B, k = p->L.k;
   const uint32_t old_bact0 = p->bact0;
   p->bact0 = (p->bact0 + 1) % B;  // pools.py:228
@@ -698,8 +730,6 @@ int bp_advance(vate_pool* p) {
   p->adv_blocks[0] = (int32_t)z;
   p->adv_blocks[1] = (int32_t)q;
   p->adv_maint = (e0 - s0) + (e1 - s1);
-  // (On the aux stream beside the next slice's scan the due blocks only
-  // slowed both down, cfg 4 0.240 -> 0.268 ms per slice: they stay in order.)
   VATE_CUDA(cudaMemsetAsync(p->d_ctr + C_CLEARED, 0, 8, p->stream));
   // the due blocks' pending epochs (applied[b], e]: newest marking epoch per
   // cell by 16-epoch groups, then clocks and the sweep rule per range
@@ -738,9 +768,15 @@ int bp_advance(vate_pool* p) {
     if (ce == cudaSuccess) ce = cudaEventRecord(p->ev_adv, p->stream);
     if (ce != cudaSuccess) rc = cuda_fail(ce, "bit-plane advance");
   }
-  if (rc) return rc;
-  // the next epoch: its ring slot (held epoch e + 1 - R, past every use) emptied
-  p->bp_e = e + 1;
+  return rc;
+}
+
+// Open the next epoch: its ring slot (held epoch e + 1 - R, past every use)
+// emptied; at a block boundary the suffix ORs of the finished block.
+static int bp_next_epoch(vate_pool* p) {
+  const uint64_t nwords = bp_nwords(p);
+  int rc = VATE_OK;
+  p->bp_e = p->bp_e + 1;
   p->bp_folded = false;
   VATE_CUDA(cudaMemsetAsync(ring_slot(p, p->bp_e), 0, nwords * 4, p->stream));
   if (p->bp_e % (int64_t)p->bp_L == 0) {
