@@ -80,6 +80,9 @@ int vate_pool_latency(vate_pool* p, double out[4]);
 int vate_pool_lat_mark(vate_pool* p, int64_t t, int which);
 /* out = [deferred scatter on, bit-plane mode on, its window k', its ring slots]. */
 int vate_pool_mode(const vate_pool* p, int32_t out[4]);
+/* CUDA runtime calls other than launches made by this thread so far (the
+ * library's host cost per slice, with vate_pool_launches). */
+int vate_api_calls(uint64_t* n);
 int vate_pool_sync(vate_pool* p);
 /* cumulative count of kernels this pool (and its registries) launched */
 int vate_pool_launches(const vate_pool* p, uint64_t* n);

@@ -59,6 +59,7 @@ _SIGS = {
     "vate_pool_mode": ([_p, _p], _int),
     "vate_pool_set_latency": ([_p, _int], _int),
     "vate_pool_set_peer": ([_p, _p, _int, _int], _int),
+    "vate_api_calls": ([_p], _int),
     "vate_tracer_create": ([_p, _p, _u64, _u64], _int),
     "vate_tracer_destroy": ([_p], _int),
     "vate_tracer_buffer": ([_p, _int, _p], _int),

@@ -680,15 +680,21 @@ int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
     // the next slice's scan instead they slowed both down (0.240 -> 0.268)
     if (p->adv_pending) return set_error(VATE_EVALUE, "previous advance not collected");
     if (!p->ev_bp) VATE_CUDA(cudaEventCreateWithFlags(&p->ev_bp, cudaEventDisableTiming));
-    VATE_CUDA(cudaEventRecord(p->ev_fork, p->stream));
-    VATE_CUDA(cudaStreamWaitEvent(p->aux_stream, p->ev_fork, 0));
-    std::swap(p->stream, p->aux_stream);
+    if (!p->ev_bp_fork) VATE_CUDA(cudaEventCreateWithFlags(&p->ev_bp_fork, cudaEventDisableTiming));
+    if (!p->bp_stream) VATE_CUDA(cudaStreamCreateWithFlags(&p->bp_stream, cudaStreamNonBlocking));
+    // their own stream: they start with the pass instead of queueing behind the
+    // registry compaction on aux, so the advance result (which the next call
+    // waits for) lands early
+    VATE_CUDA(cudaEventRecord(p->ev_bp_fork, p->stream));
+    VATE_CUDA(cudaStreamWaitEvent(p->bp_stream, p->ev_bp_fork, 0));
+    cudaStream_t main_stream = p->stream;
+    p->stream = p->bp_stream;
     rc = bp_due(p);
     if (rc == VATE_OK) {
       const cudaError_t ce = cudaEventRecord(p->ev_bp, p->stream);
       if (ce != cudaSuccess) rc = cuda_fail(ce, "bit-plane advance");
     }
-    std::swap(p->stream, p->aux_stream);
+    p->stream = main_stream;
     if (rc) return rc;
     p->bp_join = true;
   }

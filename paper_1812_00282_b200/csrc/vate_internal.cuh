@@ -392,7 +392,9 @@ struct vate_pool {
   bool bp_failed = false;        // enabling was refused (memory, values > 2k)
   int64_t bp_flushed_e = -1;     // epoch of the last whole-pool materialization
   vate::DevBuf bp_ring, bp_S, bp_P, bp_applied, bp_acc, bp_planes;
-  cudaEvent_t ev_bp = nullptr;  // the last due-block work (aux stream)
+  cudaEvent_t ev_bp = nullptr;  // the last due-block work (bp_stream)
+  cudaEvent_t ev_bp_fork = nullptr;
+  cudaStream_t bp_stream = nullptr;  // the due blocks, beside the window pass
   bool bp_join = false;         // cell accesses must wait for ev_bp
   uint64_t bp_wmax = 0;      // words of the largest block (+1), scratch row length
   uint32_t bp_gmax = 0;      // 16-epoch groups the ring spans
@@ -548,8 +550,10 @@ bool default_deferred(const vate_pool* p);
 // error plumbing (thread-local message)
 int set_error(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
+extern thread_local unsigned long long g_api_calls;  // CUDA runtime calls (host-cost accounting)
 #define VATE_CUDA(call)                                  \
   do {                                                   \
+    ++::vate::g_api_calls;                               \
     cudaError_t _e = (call);                             \
     if (_e != cudaSuccess) return ::vate::cuda_fail(_e, #call); \
   } while (0)

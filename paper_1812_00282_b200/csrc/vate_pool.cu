@@ -24,6 +24,7 @@ namespace vate {
 // ---------------------------------------------------------------------------
 
 static thread_local std::string g_err;
+thread_local unsigned long long g_api_calls = 0;
 
 int set_error(int code, const std::string& msg) {
   g_err = msg;
@@ -1190,6 +1191,7 @@ int vate_pool_destroy(vate_pool* p) {
   if (p->d2h_stream) cudaStreamSynchronize(p->d2h_stream);
   if (p->h2d_stream) cudaStreamSynchronize(p->h2d_stream);
   if (p->aux_stream) cudaStreamSynchronize(p->aux_stream);
+  if (p->bp_stream) cudaStreamSynchronize(p->bp_stream);
   for (DevBuf* b : {&p->bitmap, &p->in_a, &p->in_b, &p->out_buf, &p->hosts_sorted, &p->hosts_tmp,
                     &p->g0, &p->flags, &p->sel_idx, &p->cub_tmp, &p->lzv})
     b->release();
@@ -1202,6 +1204,7 @@ int vate_pool_destroy(vate_pool* p) {
   if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
   if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
   if (p->aux_stream) cudaStreamDestroy(p->aux_stream);
+  if (p->bp_stream) cudaStreamDestroy(p->bp_stream);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_counts) cudaEventDestroy(p->ev_counts);
   if (p->ev_post) cudaEventDestroy(p->ev_post);
@@ -1216,6 +1219,7 @@ int vate_pool_destroy(vate_pool* p) {
   for (int i = 0; i < 2; ++i) {
     if (p->lat_a[i]) cudaEventDestroy(p->lat_a[i]);
     if (i == 0 && p->ev_bp) cudaEventDestroy(p->ev_bp);
+    if (i == 0 && p->ev_bp_fork) cudaEventDestroy(p->ev_bp_fork);
     if (p->lat_b[i]) cudaEventDestroy(p->lat_b[i]);
   }
   if (p->d_done) cudaFree(p->d_done);
@@ -1295,6 +1299,12 @@ int vate_pool_sync(vate_pool* p) {
   VATE_CUDA(cudaStreamSynchronize(p->h2d_stream));
   VATE_CUDA(cudaStreamSynchronize(p->d2h_stream));
   return sync_small(p);
+}
+
+int vate_api_calls(uint64_t* n) {
+  if (!n) return set_error(VATE_EVALUE, "null argument");
+  *n = vate::g_api_calls;
+  return VATE_OK;
 }
 
 int vate_pool_launches(const vate_pool* p, uint64_t* n) {

@@ -1,5 +1,6 @@
-"""Device timeline of the cfg 2 slice step (TL_C/TL_K/TL_N/TL_HOSTS: another shape): every launch (CUDA events around
-each kernel) and the idle gaps between them, for a few steady-state slices."""
+"""Device timeline of the slice step (cfg 2 by default; TL_C/TL_K/TL_N/TL_HOSTS/TL_WARM: another
+shape): the host cost of a call, then every launch (CUDA events around each kernel) and the idle
+gaps between them, for a few steady-state slices."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -22,11 +23,28 @@ for i in range(NB):
     check(lib.vate_synth_packets(pool.handle, i, n, HOSTS, 0x0A000000, 0, bufs[i].data_ptr()))
 lagged = os.environ.get("TL_LAGGED", "1") == "1"
 step = pipe.step_lagged if lagged else pipe.step_fast
-for t in range(130):
-    step(t, bufs[t].data_ptr(), n, "device", None)
+import time
+WARM = int(os.environ.get("TL_WARM", 130))
+for t in range(WARM):
+    step(t, bufs[t % NB].data_ptr(), n, "device", None)
+pool.synchronize()
+import ctypes as C
+host_us = []
+api0, l0 = C.c_uint64(), pool.launches()
+check(lib.vate_api_calls(C.byref(api0)))
+for t in range(WARM, WARM + 30):   # untimed: the host cost of a call
+    a = time.perf_counter()
+    step(t, bufs[t % NB].data_ptr(), n, "device", None)
+    host_us.append((time.perf_counter() - a) * 1e6)
+pool.synchronize()
+api1 = C.c_uint64()
+check(lib.vate_api_calls(C.byref(api1)))
+print("host us per step call (30 calls, no kernel timing): median %.1f; per call %.1f launches, "
+      "%.1f other CUDA calls" % (np.median(host_us), (pool.launches() - l0) / 30,
+                                 (api1.value - api0.value) / 30))
 pool.set_timing(True)
-for t in range(130, 136):
-    step(t, bufs[t].data_ptr(), n, "device", None)
+for t in range(WARM + 30, WARM + 36):
+    step(t, bufs[t % NB].data_ptr(), n, "device", None)
 if lagged:
     pipe.flush_lagged(None)
 pipe.wait_reports()
