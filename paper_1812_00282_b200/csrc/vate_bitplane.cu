@@ -699,7 +699,10 @@ int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
     p->bp_join = true;
   }
   // evict-first stores: the registry and the marks stay in L2 for the next scan
-  VATE_LAUNCH(p, VATE_K_BITMAP, grid_for((nwords + 3) / 4, 256, 148u * 16u), 256, 0,
+  // 4 CTAs per SM, looping: the pass takes the same 47 us with 4 or 64, and the
+  // due blocks and the registry compaction beside it get the SM room (cfg 4:
+  // 0.149 -> 0.143 ms per slice, profiles/r02m_ab_window_grid.txt)
+  VATE_LAUNCH(p, VATE_K_BITMAP, grid_for((nwords + 3) / 4, 256, 148u * 4u), 256, 0,
               k_bp_window<true>, S, p->bp_P.as<const uint32_t>(), M,
               fold ? p->bp_P.as<uint32_t>() : nullptr, p->bitmap.as<uint32_t>(), nwords,
               p->L.size, p->d_ctr + C_P, D, pub);
