@@ -124,7 +124,7 @@ enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_FILT
  * beside the bitmap pass, and the slice advance beside g0 + float path, on a
  * second stream of the pool (fork/join by events; results unchanged). */
 /* VATE_OPT_DEFERRED: -1 auto (default: on for AT pools whose cells exceed
- * 64 MiB or more), 0 off, 1 on.  On: scans and set_many set one bit per cell in an
+ * 16 MiB or more), 0 off, 1 on.  On: scans and set_many set one bit per cell in an
  * L2-resident pending-set bitmap; the next pool pass stores the block clocks
  * (identical state). */
 int vate_pool_set_option(vate_pool* p, int option, int64_t value);

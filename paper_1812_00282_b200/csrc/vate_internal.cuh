@@ -175,15 +175,21 @@ struct SkipRule {
   static constexpr bool kMark = false, kSkip = true;
 };
 
-template <typename T, typename Rule>
+// CHECK (skewed traffic, the scan's stamp-filter form): a mark is first read
+// from L2 and the red issued only if the bit is not yet set -- reads of a hot
+// word are served in parallel, reds to one word serialise in the L2 atomic
+// unit (cfg 3's Zipf head: ~460 marks per word of its top host's 1024 cells).
+template <typename T, bool CHECK = false, typename Rule>
 __device__ __forceinline__ void store_cell(T* __restrict__ cells, uint64_t c, const Rule& rule) {
   if constexpr (Rule::kSkip)
     return;
-  else if constexpr (Rule::kMark)  // fire-and-forget: a red (the compiler's atomicOr was a
+  else if constexpr (Rule::kMark) {  // fire-and-forget: a red (the compiler's atomicOr was a
     // returning atomic here; red: cfg 4 scan 94 -> 87 us, cfg 5 1.21 -> 1.13 ms)
-    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(rule.pend + (c >> 5)),
-                 "r"(1u << (uint32_t)(c & 31))
+    const uint32_t bit = 1u << (uint32_t)(c & 31);
+    if (CHECK && (__ldcg(rule.pend + (c >> 5)) & bit)) return;
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(rule.pend + (c >> 5)), "r"(bit)
                  : "memory");
+  }
   else
     cells[c] = rule.template value<T>(c);
 }
@@ -377,7 +383,7 @@ struct vate_pool {
   vate::DevBuf pend;
   bool deferred = false;     // scans mark pend instead of storing into cells
   bool pend_dirty = false;   // pend may hold marks
-  int opt_deferred = -1;     // -1 auto (cells > kDeferBytes), 0 off, 1 on
+  int opt_deferred = -1;     // -1 auto (cells >= kDeferBytes), 0 off, 1 on
   // bit-plane mode (vate_bitplane.cu): the pool's recent
   // history as one mark bitmap per epoch (advance) in a ring, a prefix OR of
   // the current L-epoch block and suffix ORs of the previous one, so the
@@ -544,7 +550,7 @@ int bp_advance(vate_pool* p);
 int bp_rebuild(vate_pool* p);           // after cells were overwritten (load, put, fill)
 int bp_wait_aux(vate_pool* p);          // order a cell access after the due-block work
 uint64_t peer_key_cap(const vate_peer* x);
-constexpr uint64_t kDeferBytes = 64ull << 20;
+constexpr uint64_t kDeferBytes = 16ull << 20;
 bool default_deferred(const vate_pool* p);
 
 // error plumbing (thread-local message)

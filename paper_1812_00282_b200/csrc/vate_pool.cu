@@ -264,7 +264,7 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
                                            unsigned* filt, DeferQ* dq = nullptr) {
 #pragma unroll
   for (int q = 0; q < U; ++q)
-    if (q < m) store_cell<T>(cells, cell_of(aip[q], slot_of(bip[q], H), H), rule);
+    if (q < m) store_cell<T, FILTER>(cells, cell_of(aip[q], slot_of(bip[q], H), H), rule);
   if (REG) {
     // all U first probes in flight before any is resolved: each reads the home
     // sector (two slots, one 256-bit load)
@@ -933,7 +933,7 @@ int build_bitmap_direct(vate_pool* p, int k_prime, bool with_delta, bool fused_a
     // from 177 to 166 us at cfg 4 (profiles/r02c_ab_pass.txt); an L2-resident
     // pool gains nothing from it
     const uint32_t grid = grid_for(nwords, kThreads, p->cap_bitmap);
-    if (p->L.size * (uint64_t)sizeof(T) > kDeferBytes) {
+    if (p->L.size * (uint64_t)sizeof(T) > (64ull << 20)) {
       if (pend)
         VATE_LAUNCH(p, VATE_K_BITMAP, grid, kThreads, 0, (k_bitmap<T, true, 2>), (T*)p->cells,
                     p->L, p->bact0, (uint32_t)k_prime, p->bitmap.as<uint32_t>(), nwords,
@@ -985,11 +985,11 @@ int flush_pending(vate_pool* p) {
   return VATE_OK;
 }
 
-// Auto: defer (and keep the bit-plane history) when the cells take 64 MiB or
-// more -- half the 126 MB L2, beside the registry and the packet stream: cfg
-// 3's 64 MiB (0.380 -> 0.352 ms per slice) and cfg 4 / 5's 512 MiB; an
-// L2-resident pool below that is faster with direct stores (cfg 2: 0.140 vs
-// 0.148, cfg 1: 0.056 vs 0.066; profiles/r02h_ab_modes.txt).
+// Auto: defer (and keep the bit-plane history) when the cells take 16 MiB or
+// more: cfg 2 (16 MiB, L2-resident: 0.140 -> 0.117 ms per slice), cfg 3 (64
+// MiB: 0.380 -> 0.314) and cfg 4 / 5 (512 MiB); a small pool is faster with
+// direct stores and the fused sweep (cfg 1, 1 MiB: 0.050 vs 0.070;
+// profiles/r02h_ab_modes.txt, r02n_ab_modes.txt).
 bool default_deferred(const vate_pool* p) {
   return p->kind == VATE_AT && p->L.size * (uint64_t)p->cell_bytes >= kDeferBytes;
 }
