@@ -578,8 +578,9 @@ def run_gpu(args, rank, world, local_rank):
     # the dominant kernel: largest event time among the main-stream kernels (the
     # aux-stream ones run beside them; profiles/*launches* has the serialised view)
     main_stream = ("scan", "bitmap", "g0") if not inc_on else ("scan", "bitmap")
+    checked = pool.scan_form() == 1
     rooflines = {k: _roofline(k, per_kind[k], alg_bytes[k], hbm, peak_src, l2, n, S, cb, w,
-                              deferred, args.config, bitplane)
+                              deferred, args.config, bitplane, checked)
                  for k in main_stream if alg_bytes.get(k) and per_kind[k]["ms_per_launch"]}
     dom = max(rooflines, key=lambda k: per_kind[k]["ms_total"])
     step_ms = max_ms / args.steps
@@ -653,7 +654,8 @@ def run_gpu(args, rank, world, local_rank):
     _teardown(dist)
 
 
-def _roofline(kind, k, alg, hbm, peak_src, l2, n, S, cb, w, deferred, cfg, bitplane=False):
+def _roofline(kind, k, alg, hbm, peak_src, l2, n, S, cb, w, deferred, cfg, bitplane=False,
+              checked=False):
     """One kernel's roofline: HBM (algorithmic bytes / launch time against the
     measured copy bandwidth; `bound` stays "hbm", the contract's memory bound)
     and, for work L2 serves, `l2`: the time the L2 probes need for the
@@ -668,16 +670,24 @@ def _roofline(kind, k, alg, hbm, peak_src, l2, n, S, cb, w, deferred, cfg, bitpl
          "algorithmic_bytes_per_launch": alg}
     pool_in_l2 = S * cb <= (64 << 20)
     if kind == "scan":
-        # per packet: its cell write (a red.or into the L2-resident mark bitmap when
-        # deferred, a random store into an L2-resident pool otherwise -- beyond L2 it
-        # is the HBM sector above) and one random sector read of the host registry
-        write_rate = l2["random_red_or_G_per_s"] if deferred else l2["random_u16_stores_G_per_s"]
-        t_l2 = n / (l2["random_sector_reads_G_per_s"] * 1e9)
+        # per packet: one random sector read of the host registry and its cell
+        # write -- a red.or into the L2-resident mark bitmap when deferred (for
+        # skewed traffic the stamp-filter form reads the mark word first and
+        # issues the red only for a new mark: counted as a read, a lower bound),
+        # a random store into an L2-resident pool otherwise; beyond L2 a direct
+        # store is the HBM sector above
+        reads = l2["random_sector_reads_G_per_s"] * 1e9
+        if deferred:
+            write_rate = reads if checked else l2["random_red_or_G_per_s"] * 1e9
+        else:
+            write_rate = l2["random_u16_stores_G_per_s"] * 1e9
+        t_l2 = n / reads
         if deferred or pool_in_l2:
-            t_l2 += n / (write_rate * 1e9)
+            t_l2 += n / write_rate
         r["l2"] = {"ceiling_ms": t_l2 * 1e3, "frac": t_l2 / t,
                    "model": "n random 32-B registry reads + n random cell writes "
-                            "(red.or marks when deferred) at the probed L2 rates",
+                            "(red.or marks when deferred; mark-word reads in the "
+                            "stamp-filter form) at the probed L2 rates",
                    "binding": bool(deferred or pool_in_l2)}
     elif kind == "bitmap" and pool_in_l2:
         t_l2 = (S * cb + 3 * S // 8) / (l2["stream_read_GB_per_s"] * 1e9)

@@ -78,8 +78,10 @@ int vate_pool_latency(vate_pool* p, double out[4]);
 /* The same marks for a slice driven by separate calls (scan, then the
  * estimate's begin/finish): which = 0 after the scan, 1 after the finish. */
 int vate_pool_lat_mark(vate_pool* p, int64_t t, int which);
-/* out = [deferred scatter on, bit-plane mode on, its window k', its ring slots]. */
-int vate_pool_mode(const vate_pool* p, int32_t out[4]);
+/* out = [deferred scatter on, bit-plane mode on, its window k', its ring
+ * slots, the last packed scan's form (1: the per-CTA stamp filter + mark-word
+ * check for skewed traffic, 0: plain)]. */
+int vate_pool_mode(const vate_pool* p, int32_t out[5]);
 /* CUDA runtime calls other than launches made by this thread so far (the
  * library's host cost per slice, with vate_pool_launches). */
 int vate_api_calls(uint64_t* n);

@@ -799,11 +799,12 @@ static int bp_next_epoch(vate_pool* p) {
 
 }  // namespace vate
 
-extern "C" int vate_pool_mode(const vate_pool* p, int32_t out[4]) {
+extern "C" int vate_pool_mode(const vate_pool* p, int32_t out[5]) {
   if (!p || !out) return set_error(VATE_EVALUE, "null argument");
   out[0] = p->deferred ? 1 : 0;
   out[1] = p->bp ? 1 : 0;
   out[2] = (int32_t)p->bp_L;
   out[3] = (int32_t)p->bp_R;
+  out[4] = p->scan_form_used;
   return VATE_OK;
 }

@@ -21,13 +21,19 @@ __device__ __forceinline__ uint32_t rnd32(uint32_t x) {
   return x ^ (x >> 13);
 }
 
+// Four independent accesses per thread per step (memory-level parallelism as
+// the scan has it: two packets, each a registry read and a cell write).
 __global__ void __launch_bounds__(256) k_l2_gather(const uint4* __restrict__ buf, uint32_t nsec_mask,
                                                    uint64_t n, uint32_t seed, unsigned* out) {
   unsigned acc = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t s = rnd32((uint32_t)i ^ seed) & nsec_mask;
-    acc += __ldcg(buf + 2 * (uint64_t)s).x;  // one 32-byte sector
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * 4; i < n; i += 4 * stride) {
+    uint32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = i + u < n ? __ldcg(buf + 2 * (uint64_t)(rnd32((uint32_t)(i + u) ^ seed) & nsec_mask)).x : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += v[u];
   }
   if (acc == 0x9E3779B9u) *out = acc;
 }
@@ -35,16 +41,25 @@ __global__ void __launch_bounds__(256) k_l2_gather(const uint4* __restrict__ buf
 __global__ void __launch_bounds__(256) k_l2_store(uint16_t* __restrict__ buf, uint32_t cell_mask,
                                                   uint64_t n, uint32_t seed) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    buf[rnd32((uint32_t)i ^ seed) & cell_mask] = (uint16_t)i;
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * 4; i < n; i += 4 * stride) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u < n) buf[rnd32((uint32_t)(i + u) ^ seed) & cell_mask] = (uint16_t)i;
+  }
 }
 
 __global__ void __launch_bounds__(256) k_l2_red(uint32_t* __restrict__ buf, uint32_t bit_mask,
                                                 uint64_t n, uint32_t seed) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t b = rnd32((uint32_t)i ^ seed) & bit_mask;
-    atomicOr(buf + (b >> 5), 1u << (b & 31));
+  for (uint64_t i = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * 4; i < n; i += 4 * stride) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i + u >= n) break;
+      const uint32_t b = rnd32((uint32_t)(i + u) ^ seed) & bit_mask;
+      asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(buf + (b >> 5)),
+                   "r"(1u << (b & 31))
+                   : "memory");
+    }
   }
 }
 
@@ -64,8 +79,8 @@ __global__ void __launch_bounds__(256) k_l2_stream(const uint4* __restrict__ buf
 using namespace vate;
 
 // out[0] random 32-B sector reads (G sectors/s), out[1] random 2-byte stores
-// (G stores/s = G sectors/s), out[2] random red.or (G ops/s), out[3]
-// streaming read (GB/s), all over a buf_bytes (power of two) buffer.
+// (G stores/s = G sectors/s), out[2] random red.or (G ops/s, the scan's mark),
+// out[3] streaming read (GB/s), all over a buf_bytes (power of two) buffer.
 extern "C" int vate_bench_l2(vate_pool* p, uint64_t buf_bytes, uint64_t n, int reps,
                              double out[4]) {
   int rc = enter(p);
@@ -80,7 +95,7 @@ extern "C" int vate_bench_l2(vate_pool* p, uint64_t buf_bytes, uint64_t n, int r
   cudaEvent_t a, b;
   VATE_CUDA(cudaEventCreate(&a));
   VATE_CUDA(cudaEventCreate(&b));
-  const uint32_t grid = 148u * 16u;
+  const uint32_t grid = 148u * 32u;
   const uint32_t nsec = (uint32_t)(buf_bytes / 32);
   double ms[4] = {0, 0, 0, 0};
   for (int probe = 0; probe < 4; ++probe) {

@@ -238,10 +238,14 @@ class _DevicePool:
 
     def mode(self) -> dict:
         """The pool's storage mode: deferred scatter, bit-plane mode and its window."""
-        out = (C.c_int32 * 4)()
+        out = (C.c_int32 * 5)()
         check(lib.vate_pool_mode(self._h, out))
         return {"deferred": bool(out[0]), "bitplane": bool(out[1]), "window": out[2],
-                "ring_slots": out[3]}
+                "ring_slots": out[3], "scan_filter": bool(out[4])}
+
+    def scan_form(self) -> int:
+        """1 if the last packed scan took the skewed-traffic form (stamp filter)."""
+        return int(self.mode()["scan_filter"])
 
     @property
     def deferred(self) -> bool:

@@ -13,4 +13,10 @@ for k in ${KERNELS:-k_bitmap k_scan_packed16}; do
   VATE_PROFILE_REGION=1 timeout 900 ncu --set full --clock-control none --import-source on \
     --profile-from-start off -k regex:"$k" -s 1 -c 1 -o gpurun_out/${TAG}_${CFG}_$k \
     python bench.py --config $CFG --steps 4 --warmup 3 ${BENCH_ARGS} > gpurun_out/${TAG}_${CFG}_$k.log 2>&1
+  # summaries on the box (gpurun_out comes back only under 64 MiB): metrics,
+  # opcode mix; the report itself only with KEEP_REP=1
+  python scripts/ncu_summary.py gpurun_out/${TAG}_${CFG}_$k.ncu-rep >> gpurun_out/${TAG}_ncu_kernels.txt 2>&1
+  python scripts/ncu_ops.py gpurun_out/${TAG}_${CFG}_$k.ncu-rep 16 > gpurun_out/${TAG}_${CFG}_${k}_ops.txt 2>&1
+  [ "${KEEP_REP:-0}" = "1" ] || rm -f gpurun_out/${TAG}_${CFG}_$k.ncu-rep
 done
+python scripts/launch_summary.py gpurun_out/${TAG}_${CFG}_launches.csv > gpurun_out/${TAG}_${CFG}_launches_summary.txt 2>&1
