@@ -800,6 +800,8 @@ def main():
     ap.add_argument("--deferred", type=int, choices=(-1, 0, 1), default=-1,
                     help="deferred scatter: scans mark an L2-resident pending-set bitmap and "
                          "the pool pass stores the clocks (VATE_OPT_DEFERRED; auto: cells > 64 MiB)")
+    ap.add_argument("--hosts", type=int, default=0,
+                    help="override the workload's host count (experiments; not a BASELINE shape)")
     ap.add_argument("--bitplane", type=int, choices=(-1, 0, 1), default=-1,
                     help="bit-plane mode for deferred pools (VATE_OPT_BITPLANE; auto: on)")
     ap.add_argument("--opt", action="append", default=[],
@@ -829,7 +831,10 @@ def main():
     if args.warmup < 3:
         ap.error("--warmup must be at least 3")
     global WORKLOAD
-    WORKLOAD = WORKLOADS[args.config]
+    WORKLOAD = dict(WORKLOADS[args.config])
+    if args.hosts:   # experiments only: the line then names a non-BASELINE workload
+        WORKLOAD["hosts"] = args.hosts
+        WORKLOAD["name"] += f"-hosts{args.hosts}"
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

@@ -1298,6 +1298,8 @@ int vate_pool_sync(vate_pool* p) {
   if (rc) return rc;
   VATE_CUDA(cudaStreamSynchronize(p->h2d_stream));
   VATE_CUDA(cudaStreamSynchronize(p->d2h_stream));
+  for (cudaStream_t s : {p->aux_stream, p->bp_stream})
+    if (s) VATE_CUDA(cudaStreamSynchronize(s));
   return sync_small(p);
 }
 
