@@ -621,19 +621,27 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
   const bool incremental = p->opt_inc_sort && was_valid &&
                            p->sorted_owner == h && na <= h->flip_cap && nd <= h->flip_cap &&
                            p->sorted_n + na - nd == *n && (na + nd) * 8 <= *n;
+  // radix-sort only the key bits in use: arrivals are at most this compaction's
+  // largest active key, departures at most the previous one's (u32 addresses:
+  // 4 digit passes instead of 8)
+  const unsigned long long maxkey_now = h->h_count[H_MAXKEY];
+  const unsigned long long maxkey_both = std::max(maxkey_now, h->prev_maxkey);
+  h->prev_maxkey = maxkey_now;
+  int inc_bits = 64;
+  while (inc_bits > 1 && !((maxkey_both >> (inc_bits - 1)) & 1ull)) --inc_bits;
   if (incremental) {
     unsigned long long* arr = h->flips.as<unsigned long long>();
     unsigned long long* dep = arr + h->flip_cap;
     unsigned long long* arr_s = dep + h->flip_cap;
     unsigned long long* dep_s = arr_s + h->flip_cap;
     if (na > 1) {
-      rc = sort_keys(p, (uint64_t*)arr, (uint64_t*)arr_s, na, 64);
+      rc = sort_keys(p, (uint64_t*)arr, (uint64_t*)arr_s, na, inc_bits);
       if (rc) return rc;
     } else if (na == 1) {
       VATE_CUDA(cudaMemcpyAsync(arr_s, arr, 8, cudaMemcpyDeviceToDevice, p->stream));
     }
     if (nd > 1) {
-      rc = sort_keys(p, (uint64_t*)dep, (uint64_t*)dep_s, nd, 64);
+      rc = sort_keys(p, (uint64_t*)dep, (uint64_t*)dep_s, nd, inc_bits);
       if (rc) return rc;
     } else if (nd == 1) {
       VATE_CUDA(cudaMemcpyAsync(dep_s, dep, 8, cudaMemcpyDeviceToDevice, p->stream));

@@ -508,6 +508,7 @@ struct vate_pool {
 
 struct vate_hosts {
   vate_pool* pool = nullptr;
+  unsigned long long prev_maxkey = ~0ull;  // largest active key of the previous compaction
   int k = 1;
   uint64_t cap = 0;
   vate::DevBuf table, ovf, scratch;
