@@ -165,7 +165,7 @@ class ClockSampler:
 # CPU arm: the oracle port on the box's host cores
 # ----------------------------------------------------------------------------------
 
-def cpu_sample(w, steps=1, host_sample=100_000, kind="at", warmup=0):
+def cpu_sample(w, steps=1, host_sample=250_000, kind="at", warmup=0):
     """The reference algorithm on the host cores, per slice of the workload.
 
     AT pools: the oracle's C half (oracle/native.py, OpenMP over every host

@@ -394,21 +394,6 @@ int vate_peer_info(const vate_peer* x, uint64_t* window_bytes, uint64_t* nvlink_
                    int* two_shot);
 int vate_peer_destroy(vate_peer* x);
 
-/* ---- trace ingest: traceio._read_binary + slice_stream (traceio.py:77-106,
- *      :188-230) -------------------------------------------------------
- * n 16-byte records {u64 ts_us, u32 aip, u32 bip} (host or device) are packed
- * into pairs_dev[pairs_off + i] ({aip, bip}); starts[q] (host, nslices
- * entries) receives the pair index where slice first_slice + q begins (empty
- * slices share their successor's start); *violation = index of the first
- * record whose timestamp is below its predecessor's (prev_ts for record 0
- * when has_prev), or -1. */
-int vate_trace_bucket(vate_pool* p, const uint8_t* records, uint64_t n, int where,
-                      uint64_t slice_us, int64_t first_slice, uint64_t prev_ts, int has_prev,
-                      uint32_t* pairs_dev, uint64_t pairs_off, uint64_t nslices,
-                      uint64_t* starts, int64_t* violation);
-
-/* stream-ordered device-to-device copy on the pool's stream (ingest carry) */
-int vate_copy_device(vate_pool* p, void* dst, const void* src, uint64_t bytes);
 
 /* ---- line-rate trace ingest (traceio.DeviceSlices; traceio.py:77-106,
  * :188-230): two pinned staging buffers the reader fills from the file, async

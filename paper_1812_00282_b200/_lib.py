@@ -133,9 +133,6 @@ _SIGS = {
     "vate_peer_exchange": ([_p, _i64, _pu64], _int),
     "vate_peer_info": ([_p, _pu64, _pu64, C.POINTER(_int)], _int),
     "vate_peer_destroy": ([_p], _int),
-    "vate_trace_bucket": ([_p, _p, _u64, _int, _u64, _i64, _u64, _int, _p, _u64, _u64, _p,
-                           C.POINTER(_i64)], _int),
-    "vate_copy_device": ([_p, _p, _p, _u64], _int),
     "vate_synth_zipf": ([_p, _i64, _u64, _u64, _u64, _u64, _p, _p, _u64, C.c_uint32, _p], _int),
     "vate_bench_sol_scatter": ([_p, _u64, _u64, _int, _pdbl], _int),
     "vate_synth_packets": ([_p, _i64, _u64, _u64, _u64, _u64, _p], _int),

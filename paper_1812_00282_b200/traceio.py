@@ -6,10 +6,11 @@ Formats are the reference's: 16-byte little-endian binary records
 must be non-decreasing; violations raise the reference's TraceOrderError /
 TraceParseError with the same messages and positions.
 
-``DeviceSlices`` is the fast path: record chunks go to the GPU, one kernel
-(``vate_trace_bucket``) packs them to 8-byte pairs and finds every slice start
-(``ts // slice_us - base``, empty slices included, traceio.py:188-230), and
-each slice is handed to the pipeline as a device pointer.  ``read_batches`` /
+``DeviceSlices`` is the fast path (the ``vate_tracer_*`` ABI): record chunks
+go to the GPU from pinned buffers, one kernel packs them to 8-byte pairs and
+emits one run per slice change (``ts // slice_us - base``, empty slices
+yielded lazily, traceio.py:188-230), and each slice is handed to the pipeline
+as a device pointer.  ``read_batches`` /
 ``slice_stream`` keep the reference's host API for callers that want arrays.
 """
 
