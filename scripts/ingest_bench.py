@@ -46,6 +46,20 @@ def drop_caches():
         return False
 
 
+def _steady(stamps, start, records, skip=3):
+    """One-time setup (pinned staging buffers, the pool's log table, incremental
+    index and bit-plane ring) lands on the first slices: report the time to the
+    end of slice `skip` apart and the rate over the slices after it (uniform
+    slices: records per slice = records / slices)."""
+    if len(stamps) <= skip + 1:
+        return {}
+    per = records / len(stamps)
+    span = stamps[-1] - stamps[skip]
+    return {"first_slices_s": stamps[skip] - start, "first_slices": skip + 1,
+            "after_last_slice_s": time.perf_counter() - stamps[-1],
+            "steady_GB_per_s": 16 * per * (len(stamps) - skip - 1) / span / 1e9}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--records", type=int, default=134_217_728)
@@ -58,6 +72,7 @@ def main():
 
     t0 = time.perf_counter()
     write_trace(args.path, args.records, args.per_slice, 1_000_000)
+    subprocess.run(["sync"], check=False)   # no dirty-page write-back under the warm runs
     size = os.path.getsize(args.path)
     print(json.dumps({"trace_bytes": size, "records": args.records,
                       "write_s": time.perf_counter() - t0}), flush=True)
@@ -71,14 +86,16 @@ def main():
         torch.cuda.synchronize()
         a = time.perf_counter()
         slices = pairs = 0
+        stamps = []
         for t, dptr, n in traceio.DeviceSlices(pool, args.path, traceio.BINARY, 1_000_000):
             slices += 1
             pairs += n
+            stamps.append(time.perf_counter())
         pool.synchronize()
         dt = time.perf_counter() - a
         print(json.dumps({"cache": cache, "mode": "ingest only", "slices": slices, "records": pairs,
-                          "s": dt, "GB_per_s": size / dt / 1e9, "Mrecords_per_s": pairs / dt / 1e6}),
-              flush=True)
+                          "s": dt, "GB_per_s": size / dt / 1e9, "Mrecords_per_s": pairs / dt / 1e6,
+                          **_steady(stamps, a, pairs)}), flush=True)
         if cache == "dropped":
             drop_caches()
         # (b) ingest feeding the slice step (scan, estimate of ~1M hosts, advance)
@@ -87,8 +104,19 @@ def main():
                 for _ in range(2)]
         a = time.perf_counter()
         slices = pairs = 0
-        for t, dptr, n in traceio.DeviceSlices(pool, args.path, traceio.BINARY, 1_000_000):
+        stamps = []
+        marks = []          # (t_wait: next slice handed over, t_step: step call returned)
+        it = iter(traceio.DeviceSlices(pool, args.path, traceio.BINARY, 1_000_000))
+        while True:
+            w0 = time.perf_counter()
+            try:
+                t, dptr, n = next(it)
+            except StopIteration:
+                break
+            w1 = time.perf_counter()
             pipe.step_fast(t, dptr, n, "device", outs[t % 2])
+            marks.append((w1 - w0, time.perf_counter() - w1))
+            stamps.append(time.perf_counter())
             slices += 1
             pairs += n
         pipe.wait_reports()
@@ -96,7 +124,9 @@ def main():
         dt = time.perf_counter() - a
         print(json.dumps({"cache": cache, "mode": "ingest + slice step (cfg 2 pool, 1M hosts)",
                           "slices": slices, "records": pairs, "s": dt,
-                          "GB_per_s": size / dt / 1e9, "Mrecords_per_s": pairs / dt / 1e6}),
+                          "GB_per_s": size / dt / 1e9, "Mrecords_per_s": pairs / dt / 1e6,
+                          **_steady(stamps, a, pairs),
+                          "per_slice_ms": [[round(1e3 * x, 2), round(1e3 * y, 2)] for x, y in marks]}),
               flush=True)
         pipe.close()
         pool.close()
