@@ -535,9 +535,14 @@ def run_gpu(args, rank, world, local_rank):
     sol_ms = C.c_double()
     check(lib.vate_bench_sol_scatter(scratch_pool.handle, n, table_bytes, 10, C.byref(sol_ms)))
     l2 = scratch_pool.l2_ceilings()
+    # the deferred scan's own skeleton: the packet stream, one red.or into the
+    # 2^c-bit mark bitmap and one registry home-sector read per packet, on the
+    # scan's grid (vate_bench_scan_skeleton)
+    skel_ms = scratch_pool.scan_skeleton_ms(w["c"], table_bytes, n - n % 2)
     scratch_pool.close()
     sol = {"ms_per_slice_of_packets": sol_ms.value, "registry_table_bytes": table_bytes,
-           "pool_bytes": (1 << w["c"]) * pool.cell_bytes}
+           "pool_bytes": (1 << w["c"]) * pool.cell_bytes,
+           "deferred_skeleton_ms": skel_ms}
 
     peaks, peak_src = _peaks()
     hbm = float(peaks["hbm_gbs"])
@@ -624,10 +629,15 @@ def run_gpu(args, rank, world, local_rank):
         "l2_ceilings": l2,
         "scan_speed_of_light": dict(sol, scan_ms_per_launch=per_kind["scan"]["ms_per_launch"],
                                     scan_over_sol=per_kind["scan"]["ms_per_launch"]
-                                    / sol["ms_per_slice_of_packets"],
-                                    note="random 32-B load (registry-sized table) + random "
-                                         "cell store per packet, no hashing or packet "
-                                         "stream: the L2/HBM random-access ceiling"),
+                                    / (skel_ms if deferred else sol["ms_per_slice_of_packets"]),
+                                    note="direct pools: random 32-B load (registry-sized "
+                                         "table) + random cell store per packet, no hashing "
+                                         "or packet stream; deferred pools "
+                                         "(deferred_skeleton_ms): the packet stream + one "
+                                         "random red.or into the 2^c-bit mark bitmap + one "
+                                         "random registry sector read per packet on the "
+                                         "scan's grid, i.e. the scan's memory operations "
+                                         "without its hashing and compare chain"),
         "active_set_ordering": pool.sort_stats(),
         "incremental": {"enabled": inc_on,
                         **{k: inc1[k] - inc0[k] for k in ("rebuilds", "delta_slices",

@@ -416,6 +416,15 @@ int vate_tracer_release(vate_tracer* x, int slot);
  * reads G/s, random 2-byte stores G/s, random 32-bit red.or G/s, streaming
  * read GB/s]. */
 int vate_bench_l2(vate_pool* p, uint64_t buf_bytes, uint64_t n, int reps, double out[4]);
+/* Measurement only: ms per launch of the scan's memory skeleton (per packet one
+ * streamed 8-B read, one random red.or into a 2^mark_log2-bit bitmap, one random
+ * 32-B read of a table_bytes table) on the scan's grid. */
+int vate_bench_scan_skeleton(vate_pool* p, int mark_log2, uint64_t table_bytes, uint64_t n,
+                             int reps, double* ms_out);
+/* The same with ablation flags (vate_probe.cu): 1 the scan's 64-bit hashing,
+ * 2 stamp stores, 4 dependent second reads, 8 256-bit loads. */
+int vate_bench_scan_ablation(vate_pool* p, int mark_log2, uint64_t table_bytes, uint64_t n,
+                             int reps, int flags, double* ms_out);
 
 /* ---- speed-of-light probe (bench only) -----------------------------------
  * n "packets" of the scan's memory pattern without its arithmetic or input

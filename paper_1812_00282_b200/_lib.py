@@ -67,6 +67,8 @@ _SIGS = {
     "vate_tracer_collect": ([_p, _int, _p, _u64, _p, _p, _p], _int),
     "vate_tracer_release": ([_p, _int], _int),
     "vate_bench_l2": ([_p, _u64, _u64, _int, _p], _int),
+    "vate_bench_scan_skeleton": ([_p, _int, _u64, _u64, _int, _p], _int),
+    "vate_bench_scan_ablation": ([_p, _int, _u64, _u64, _int, _int, _p], _int),
     "vate_pool_latency": ([_p, _p], _int),
     "vate_pool_lat_mark": ([_p, _i64, _int], _int),
     "vate_pool_destroy": ([_p], _int),

@@ -756,6 +756,7 @@ int vate_hosts_update(vate_hosts* h, const uint64_t* aips, uint64_t n, int64_t t
   if (rc || n == 0) return rc;
   rc = hosts_prepare_insert(h, n);
   if (rc) return rc;
+  h->note_t(t);
   const void* d_keys;
   rc = stage_in(p, p->in_a, aips, n * 8, where, &d_keys);
   if (rc) return rc;

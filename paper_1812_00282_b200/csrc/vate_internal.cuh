@@ -13,6 +13,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <climits>
 
 #include <string>
 #include <vector>
@@ -313,6 +314,10 @@ struct RegRef {
   uint64_t ovf_cap;
   unsigned int* special;  // 1 if the special entry is present
   int enabled;
+  // stamps as red.max (fire-and-forget; a plain store costs the scan more in L2):
+  // set only when this call's t is at least every slice the registry has seen,
+  // where max and the reference's overwrite (pipeline.py:50-52) agree
+  int stamp_max;
 };
 
 // A growable device buffer (one stream per pool, so growth may sync).
@@ -525,8 +530,15 @@ struct vate_hosts {
   bool member_valid = false;
   vate::DevBuf flips;      // arrivals, departures and their sorted copies (4 x flip_cap)
   uint64_t flip_cap = 0;
+  long long t_hi = LLONG_MIN;  // largest slice index any write path has stamped
 
   vate::RegRef ref() const;
+  // Record a write with slice t; true when t >= every earlier one (stamp_max ok).
+  bool note_t(long long t) {
+    const bool mono = t >= t_hi;
+    if (mono) t_hi = t;
+    return mono;
+  }
 };
 
 namespace vate {

@@ -399,6 +399,7 @@ int vate_peer_exchange(vate_peer* x, int64_t t, uint64_t* touched_total) {
   x->nvlink_bytes = two_shot ? 2 * (wb / x->world) * (x->world - 1) : wb * (x->world - 1);
 
   // 3. the peers' touched hosts into this registry (the barrier above ordered them)
+  h->note_t(t);
   for (int attempt = 0; attempt < 3; ++attempt) {
     VATE_LAUNCH(p, VATE_K_REGISTRY, 148u * 16u, kThreads, 0, k_absorb_peers, x->d_bases,
                 W.count + 8 * par, W.keys[par], x->rank, x->world, x->key_cap, h->ref(), (long long)t);

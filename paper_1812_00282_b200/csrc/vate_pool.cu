@@ -235,15 +235,19 @@ __device__ __forceinline__ void touch_last(const RegRef& R, unsigned* filt, uint
   // one shared-memory exchange: exactly one thread of a racing group sees a
   // different previous tag and stamps (race-free under compute-sanitizer)
   if (atomicExch(filt + (slot & (kTouchSlots - 1)), tag) == tag) return;
-  R.table[slot].last = t;
+  reg_stamp(R, slot, t);
 }
 
 // Registry misses of the home sector are deferred to a per-CTA shared-memory
 // queue and inserted after the CTA's packets, by dense threads: in-line, a
 // warp would run the probe loop as long as its slowest of 64 packets.
+// A key is queued with bit 0 of `skip` set when the home sector held two other
+// keys (the walk resumes at the next sector) -- the common case; a home
+// sector with an empty slot means a new key, inserted from the home sector.
 constexpr int kDeferCap = 1024;
 struct DeferQ {
   unsigned long long keys[kDeferCap];
+  unsigned char skip[kDeferCap];
   unsigned n;
 };
 
@@ -254,7 +258,8 @@ __device__ __forceinline__ void defer_init(DeferQ* dq) {
 __device__ __forceinline__ void defer_drain(DeferQ* dq, const RegRef& R, long long t) {
   __syncthreads();
   const unsigned n = min(dq->n, (unsigned)kDeferCap);
-  for (unsigned i = threadIdx.x; i < n; i += blockDim.x) reg_insert(R, dq->keys[i], t, false);
+  for (unsigned i = threadIdx.x; i < n; i += blockDim.x)
+    reg_insert(R, dq->keys[i], t, false, dq->skip[i] != 0);
 }
 
 template <typename T, bool REG, int U, bool FILTER, typename Rule>
@@ -281,18 +286,19 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
       if (aip[q] != kEmptyKey && e[q].key == aip[q]) {
         if (e[q].last != t) {
           if (FILTER) touch_last(R, filt, slot[q], t);
-          else R.table[slot[q]].last = t;
+          else reg_stamp(R, slot[q], t);
         }
       } else if (aip[q] != kEmptyKey && f[q].key == aip[q]) {
         if (f[q].last != t) {
           if (FILTER) touch_last(R, filt, slot[q] + 1, t);
-          else R.table[slot[q] + 1].last = t;
+          else reg_stamp(R, slot[q] + 1, t);
         }
       } else {
         if (dq) {
           const unsigned pos = atomicAdd(&dq->n, 1u);
           if (pos < (unsigned)kDeferCap) {
             dq->keys[pos] = aip[q];
+            dq->skip[pos] = (aip[q] != kEmptyKey && e[q].key != kEmptyKey && f[q].key != kEmptyKey);
             continue;
           }
         }
@@ -1488,6 +1494,7 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     rc = hosts_prepare_insert(hosts, n);
     if (rc) return rc;
     R = hosts->ref();
+    R.stamp_max = hosts->note_t(t) ? 1 : 0;
   }
   // registry-stamp filter: auto takes it for skewed traffic -- when the last
   // compacted slice saw 8 or more packets per distinct host (Zipf-like heads

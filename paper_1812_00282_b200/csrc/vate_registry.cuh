@@ -32,6 +32,15 @@ __device__ __forceinline__ void ld_pair(const RegEntry* p, RegEntry& a, RegEntry
   b.last = (long long)l1;
 }
 
+// The scan's stamp of a found key (its loaded `last` differed from t).
+__device__ __forceinline__ void reg_stamp(const RegRef& R, uint64_t slot, long long t) {
+  if (R.stamp_max)
+    asm volatile("red.relaxed.gpu.global.max.s64 [%0], %1;" ::"l"(&R.table[slot].last), "l"(t)
+                 : "memory");
+  else
+    R.table[slot].last = t;
+}
+
 __device__ __forceinline__ void reg_touch(RegEntry* e, long long t, bool use_max) {
   if (use_max) {
     atomicMax(&e->last, t);
@@ -64,8 +73,13 @@ __device__ __forceinline__ bool reg_claim(const RegRef& R, RegEntry* e, uint64_t
 // draining the overflow list, where entries of several calls meet (identical
 // to overwrite whenever slice indices are non-decreasing, as Pipeline.run
 // feeds them).
+//
+// skip_home: the caller's own load saw the home sector full of other keys, so
+// the walk starts at the next sector (non-empty keys never change).  Without
+// use_max a found key is stamped from the loaded `last` (a stale read only
+// repeats a store of the same t), with no second dependent load.
 __device__ __forceinline__ void reg_insert(const RegRef& R, uint64_t key, long long t,
-                                           bool use_max) {
+                                           bool use_max, bool skip_home = false) {
   if (key == kEmptyKey) {  // the one key that collides with the empty marker
     RegEntry* e = R.table + (R.mask + 1);
     if (atomicExch(R.special, 1u) == 0u) atomicAdd(R.count, 1ull);
@@ -73,18 +87,21 @@ __device__ __forceinline__ void reg_insert(const RegRef& R, uint64_t key, long l
     return;
   }
   uint64_t h = reg_home(key, R.mask);
+  if (skip_home) h = (h + 2) & R.mask;
 #pragma unroll 1
-  for (int step = 0; step < kMaxProbe / 2; ++step) {
+  for (int step = skip_home ? 1 : 0; step < kMaxProbe / 2; ++step) {
     RegEntry a, b;
     ld_pair(R.table + h, a, b);
     if (a.key == key) {
-      reg_touch(R.table + h, t, use_max);
+      if (use_max) reg_touch(R.table + h, t, true);
+      else if (a.last != t) reg_stamp(R, h, t);
       return;
     }
     if (a.key == kEmptyKey && reg_claim(R, R.table + h, key, t, use_max)) return;
     // slot h is (now) some other key: b is next in the probe sequence
     if (b.key == key) {
-      reg_touch(R.table + h + 1, t, use_max);
+      if (use_max) reg_touch(R.table + h + 1, t, true);
+      else if (b.last != t) reg_stamp(R, h + 1, t);
       return;
     }
     if (b.key == kEmptyKey && reg_claim(R, R.table + h + 1, key, t, use_max)) return;

@@ -324,6 +324,15 @@ class _DevicePool:
                 "random_u16_stores_G_per_s": out[1], "random_red_or_G_per_s": out[2],
                 "stream_read_GB_per_s": out[3]}
 
+    def scan_skeleton_ms(self, mark_log2: int, table_bytes: int, n: int, reps: int = 5) -> float:
+        """ms per launch of the scan's memory skeleton (vate_bench_scan_skeleton;
+        measurement only): n streamed packets, each one random red.or into a
+        2^mark_log2-bit bitmap and one random 32-B read of a table_bytes table."""
+        ms = C.c_double()
+        check(lib.vate_bench_scan_skeleton(self._h, int(mark_log2), int(table_bytes), int(n),
+                                           int(reps), C.byref(ms)))
+        return ms.value
+
     def set_timing(self, on: bool) -> None:
         check(lib.vate_pool_set_timing(self._h, int(on)))
 
