@@ -526,6 +526,7 @@ def run_gpu(args, rank, world, local_rank):
     if world == 1 and args.counter == "at":
         extra = after_timing(args, w, vb, pipe, pool, n, t, dslices, n_dev, di, out_sets, lagged)
         t = extra.pop("_t")
+    pcie = pcie_ceiling(torch, dev, hslices[0], int(e2e_rows / e2e_steps * 25), n)
 
     # speed of light of the scan's memory pattern on this pool shape: one random
     # 32-B registry-sized load + one random cell store per packet, no hashing,
@@ -609,7 +610,8 @@ def run_gpu(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": slice_bytes,
                 "d2h_bytes_per_step": int(e2e_rows / e2e_steps * 25),
                 "steps": e2e_steps,
-                "host_ms_per_step": {k: v / e2e_steps for k, v in host_ms.items()}},
+                "host_ms_per_step": {k: v / e2e_steps for k, v in host_ms.items()},
+                "pcie": dict(pcie, frac=e2e_value / pcie["ceiling_value"])},
         "gpu_launches": int(launches),
         **extra,
         "scan_update_mpps": n / ((per_kind["scan"]["ms_total"] + per_kind["sweep"]["ms_total"])
@@ -789,6 +791,47 @@ def after_timing(args, w, vb, pipe, pool, n, t, dslices, n_dev, di, out_sets, la
                 "EstimateReport objects are the reference's own output type"}
     res["_t"] = t
     return res
+
+
+def pcie_ceiling(torch, dev, src_pinned, d2h_bytes, n, reps=8):
+    """What PCIe alone allows the e2e line: the step's H2D (this slice's packets
+    from pinned memory) and D2H (its report rows into pinned memory) bytes as
+    bare copies, alone and on two streams at once (CUDA events, no kernels).
+    The concurrent pair bounds an e2e slice from below."""
+    nbytes = src_pinned.numel() * src_pinned.element_size()
+    h_src = src_pinned.reshape(-1).view(torch.uint8)
+    d_dst = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dev}")
+    d_src = torch.empty(max(d2h_bytes, 1), dtype=torch.uint8, device=f"cuda:{dev}")
+    h_dst = torch.empty(max(d2h_bytes, 1), dtype=torch.uint8, pin_memory=True)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(h2d, d2h):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        torch.cuda.synchronize(dev)
+        cur = torch.cuda.current_stream(dev)
+        ev[0].record(cur)
+        s_in.wait_stream(cur)
+        s_out.wait_stream(cur)
+        for _ in range(reps):
+            if h2d:
+                with torch.cuda.stream(s_in):
+                    d_dst.copy_(h_src, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s_out):
+                    h_dst.copy_(d_src, non_blocking=True)
+        cur.wait_stream(s_in)
+        cur.wait_stream(s_out)
+        ev[1].record(cur)
+        torch.cuda.synchronize(dev)
+        return ev[0].elapsed_time(ev[1]) / reps
+
+    timed(True, True)  # warm
+    h2d_ms, d2h_ms, both_ms = timed(True, False), timed(False, True), timed(True, True)
+    return {"h2d_gbs": nbytes / h2d_ms / 1e6, "d2h_gbs": d2h_bytes / d2h_ms / 1e6,
+            "h2d_plus_d2h_ms_per_slice": both_ms,
+            "ceiling_value": n / (both_ms / 1e3) / 1e6,
+            "note": "bare pinned copies of one step's H2D and D2H bytes on two streams (CUDA "
+                    "events): the PCIe bound on the e2e value"}
 
 
 def _teardown(dist):

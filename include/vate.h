@@ -107,7 +107,10 @@ int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
  * (exact), 0 recomputes every g0 by a full gather. */
 enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_FILTER = 2,
                    VATE_OPT_CONCURRENT = 3, VATE_OPT_INC_SORT = 4, VATE_OPT_FUSE_SWEEP = 5,
-                   VATE_OPT_DEFERRED = 6, VATE_OPT_BITPLANE = 7 };
+                   VATE_OPT_DEFERRED = 6, VATE_OPT_BITPLANE = 7, VATE_OPT_L2_KEEP = 8 };
+/* VATE_OPT_L2_KEEP: -1 auto (default: on for deferred pools), 0 off, 1 on --
+ * the scan's registry sector loads, stamps and marks carry the L2 evict_last
+ * policy so the table and the marks outlive the slice's streaming passes. */
 /* VATE_OPT_BITPLANE: -1 auto (default: on for deferred pools, when the HBM
  * fits it), 0 off, 1 on.  On: the pool keeps one mark bitmap per epoch, the
  * estimate for k' = the first estimate's k' reads ~(S | P | M_e) instead of

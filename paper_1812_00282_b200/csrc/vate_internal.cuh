@@ -145,6 +145,14 @@ __device__ __forceinline__ void for_word_clocks(uint64_t i0, uint32_t cnt, const
   }
 }
 
+// L2 eviction-priority policy for loads / reds that should outlive streaming
+// traffic (createpolicy: fraction 1.0 of the accessed lines get evict_last).
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // What a scan / set_many stores into a cell: the AT pool stores the clock of
 // the cell's block (pools.py:164-178); the comparators store a constant.
 struct AtRule {
@@ -169,6 +177,7 @@ struct ConstRule {
 // before any other cell access and before every advance).
 struct MarkRule {
   uint32_t* pend;
+  int keep = 0;  // L2 evict_last on the marks (VATE_OPT_L2_KEEP)
   static constexpr bool kMark = true, kSkip = false;
 };
 // No cell write (a registry-only pass).
@@ -188,8 +197,12 @@ __device__ __forceinline__ void store_cell(T* __restrict__ cells, uint64_t c, co
     // returning atomic here; red: cfg 4 scan 94 -> 87 us, cfg 5 1.21 -> 1.13 ms)
     const uint32_t bit = 1u << (uint32_t)(c & 31);
     if (CHECK && (__ldcg(rule.pend + (c >> 5)) & bit)) return;
-    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(rule.pend + (c >> 5)), "r"(bit)
-                 : "memory");
+    if (rule.keep)
+      asm volatile("red.relaxed.gpu.global.or.L2::cache_hint.b32 [%0], %1, %2;"
+                   ::"l"(rule.pend + (c >> 5)), "r"(bit), "l"(l2_keep_policy()) : "memory");
+    else
+      asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(rule.pend + (c >> 5)), "r"(bit)
+                   : "memory");
   }
   else
     cells[c] = rule.template value<T>(c);
@@ -318,7 +331,11 @@ struct RegRef {
   // set only when this call's t is at least every slice the registry has seen,
   // where max and the reference's overwrite (pipeline.py:50-52) agree
   int stamp_max;
+  // registry sector loads and stamps with the L2 evict_last policy
+  // (VATE_OPT_L2_KEEP): the table stays in L2 across the slice's streaming passes
+  int l2_keep;
 };
+
 
 // A growable device buffer (one stream per pool, so growth may sync).
 struct DevBuf {
@@ -458,6 +475,7 @@ struct vate_pool {
   // options
   int opt_g0 = 0;
   int opt_inc = 1;            // incremental g0 through the inverse index
+  int opt_l2_keep = -1;      // L2 evict_last on registry + marks in the scan: -1 auto, 0, 1
   int opt_scan_check = -1;   // registry-stamp filter: -1 auto, 0 off, 1 on
   int scan_form_used = 0;     // the form the last packed scan ran (auto resolved)
   int opt_concurrent = 1;     // fork independent estimate phases onto aux_stream

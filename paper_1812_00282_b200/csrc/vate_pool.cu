@@ -168,11 +168,22 @@ static int with_cell(int bytes, F f) {
 // Cell type and store rule of a pool: AT stores its block clock; the DR / TS
 // comparators store a constant per slice (0, or the slice index).
 // A deferred AT pool marks the pending-set bitmap instead (MarkRule).
+// L2 evict_last on the scan's registry and mark accesses (VATE_OPT_L2_KEEP):
+// auto = deferred pools, whose slice also streams the bit-plane / cell passes
+// through L2 between two scans.  No persisting set-aside is configured: with
+// 16-96 MB set aside the window pass lost L2 room and the slice slowed (cfg 4
+// 0.137 -> 0.142-0.191 ms); the bare hint keeps the scan's DRAM write-back at
+// 17 vs 60 MB per launch and the slice 1.5 % faster (profiles/r02y_ab_l2keep.txt)
+static int l2_keep(const vate_pool* p) {
+  return p->opt_l2_keep == 1 || (p->opt_l2_keep == -1 && p->deferred) ? 1 : 0;
+}
+
 template <typename F>
 static int with_store(vate_pool* p, F f) {
   if (p->kind == VATE_AT && p->deferred) {
     p->pend_dirty = true;
-    return with_cell(p->cell_bytes, [&](auto tag) { return f(tag, MarkRule{pend_ptr(p)}); });
+    return with_cell(p->cell_bytes,
+                     [&](auto tag) { return f(tag, MarkRule{pend_ptr(p), l2_keep(p)}); });
   }
   if (p->kind == VATE_AT)
     return with_cell(p->cell_bytes, [&](auto tag) { return f(tag, AtRule{p->L, p->bact0}); });
@@ -278,7 +289,7 @@ __device__ __forceinline__ void scan_batch(const uint64_t (&aip)[U], const uint6
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       slot[q] = reg_home(aip[q], R.mask);
-      if (q < m) ld_pair(R.table + slot[q], e[q], f[q]);
+      if (q < m) ld_pair(R.table + slot[q], e[q], f[q], R.l2_keep);
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
@@ -1368,6 +1379,10 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_concurrent = (int)value;
     return VATE_OK;
   }
+  if (option == VATE_OPT_L2_KEEP && value >= -1 && value <= 1) {
+    p->opt_l2_keep = (int)value;
+    return VATE_OK;
+  }
   if (option == VATE_OPT_SCAN_FILTER && value >= -1 && value <= 1) {
     p->opt_scan_check = (int)value;
     return VATE_OK;
@@ -1495,6 +1510,7 @@ static int scan_common(vate_pool* p, HashParams H, const uint64_t* aips, const u
     if (rc) return rc;
     R = hosts->ref();
     R.stamp_max = hosts->note_t(t) ? 1 : 0;
+    R.l2_keep = l2_keep(p);
   }
   // registry-stamp filter: auto takes it for skewed traffic -- when the last
   // compacted slice saw 8 or more packets per distinct host (Zipf-like heads

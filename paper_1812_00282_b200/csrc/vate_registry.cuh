@@ -21,11 +21,17 @@ __device__ __forceinline__ uint64_t reg_home(uint64_t key, uint64_t mask) {
 }
 
 // Slots s and s+1 (s even: one aligned 32-byte sector) in one load.
-__device__ __forceinline__ void ld_pair(const RegEntry* p, RegEntry& a, RegEntry& b) {
+__device__ __forceinline__ void ld_pair(const RegEntry* p, RegEntry& a, RegEntry& b,
+                                        bool keep = false) {
   unsigned long long k0, l0, k1, l1;
-  asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];"
-               : "=l"(k0), "=l"(l0), "=l"(k1), "=l"(l1)
-               : "l"(p));
+  if (keep)
+    asm volatile("ld.global.L2::cache_hint.v4.u64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=l"(k0), "=l"(l0), "=l"(k1), "=l"(l1)
+                 : "l"(p), "l"(l2_keep_policy()));
+  else
+    asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(k0), "=l"(l0), "=l"(k1), "=l"(l1)
+                 : "l"(p));
   a.key = k0;
   a.last = (long long)l0;
   b.key = k1;
@@ -34,7 +40,10 @@ __device__ __forceinline__ void ld_pair(const RegEntry* p, RegEntry& a, RegEntry
 
 // The scan's stamp of a found key (its loaded `last` differed from t).
 __device__ __forceinline__ void reg_stamp(const RegRef& R, uint64_t slot, long long t) {
-  if (R.stamp_max)
+  if (R.stamp_max && R.l2_keep)
+    asm volatile("red.relaxed.gpu.global.max.L2::cache_hint.s64 [%0], %1, %2;"
+                 ::"l"(&R.table[slot].last), "l"(t), "l"(l2_keep_policy()) : "memory");
+  else if (R.stamp_max)
     asm volatile("red.relaxed.gpu.global.max.s64 [%0], %1;" ::"l"(&R.table[slot].last), "l"(t)
                  : "memory");
   else
@@ -91,7 +100,7 @@ __device__ __forceinline__ void reg_insert(const RegRef& R, uint64_t key, long l
 #pragma unroll 1
   for (int step = skip_home ? 1 : 0; step < kMaxProbe / 2; ++step) {
     RegEntry a, b;
-    ld_pair(R.table + h, a, b);
+    ld_pair(R.table + h, a, b, R.l2_keep);
     if (a.key == key) {
       if (use_max) reg_touch(R.table + h, t, true);
       else if (a.last != t) reg_stamp(R, h, t);

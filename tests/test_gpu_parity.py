@@ -1023,7 +1023,8 @@ def test_scan_forms_are_equivalent(form):
     (VATE_OPT_SCAN_FILTER), direct cell stores or the deferred pending-set
     marks (VATE_OPT_DEFERRED) or the bit-plane history (d = 2,
     VATE_OPT_BITPLANE), 16-byte aligned input (two packets per thread,
-    plus the odd last packet) or misaligned input (one packet per thread) --
+    plus the odd last packet) or misaligned input (one packet per thread),
+    with the L2 evict_last hints (VATE_OPT_L2_KEEP) paired with the filter --
     leaves the reference's cells and host set: ATP1 bytes, reports and the
     registry after skewed traffic (a heavy host, odd packet counts) equal the
     oracle's, slice by slice."""
@@ -1033,6 +1034,7 @@ def test_scan_forms_are_equivalent(form):
     ocfg = vo.OracleConfig(256, 16, 6, seed=5)
     pool = cfg.build_pool()
     pool.set_option("scan_filter", filt)
+    pool.set_option("l2_keep", filt)
     pool.set_option("deferred", min(deferred, 1))
     pool.set_option("bitplane", 1 if deferred == 2 else 0)
     pipe = vb.Pipeline(pool, cfg, 5)
