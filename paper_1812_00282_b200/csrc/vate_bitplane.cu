@@ -672,7 +672,8 @@ int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
                                              : nullptr;  // S[j+1] at index j
   const bool fold = fused_advance && !p->bp_folded;
   const uint32_t* M = pend_ptr(p);
-  if (fused_advance) {
+  // the due blocks of the advance, on their own stream (forked from main)
+  auto launch_due = [&]() -> int {
     // the due blocks on the aux stream beside the window pass (they read only
     // ring slots up to this epoch and write only cells, which the pass does
     // not touch); bp_wait_aux orders every later cell access after them.
@@ -697,6 +698,12 @@ int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
     p->stream = main_stream;
     if (rc) return rc;
     p->bp_join = true;
+    return VATE_OK;
+  };
+  const bool due_late = p->opt_due_late == 1;
+  if (fused_advance && !due_late) {
+    rc = launch_due();
+    if (rc) return rc;
   }
   // evict-first stores: the registry and the marks stay in L2 for the next scan
   // 4 CTAs per SM, looping: the pass takes the same 47 us with 4 or 64, and the
@@ -707,6 +714,10 @@ int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
               fold ? p->bp_P.as<uint32_t>() : nullptr, p->bitmap.as<uint32_t>(), nwords,
               p->L.size, p->d_ctr + C_P, D, pub);
   if (fold) p->bp_folded = true;
+  if (fused_advance && due_late) {  // forked behind the pass: beside the next scan
+    rc = launch_due();
+    if (rc) return rc;
+  }
   if (fused_advance) return bp_next_epoch(p);
   return VATE_OK;
 }

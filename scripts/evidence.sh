@@ -9,6 +9,5 @@ timeout 900 python bench.py --impl reference > gpurun_out/bench_reference.json 2
 CFG=cfg4 TAG=$TAG KERNELS="k_scan_packed16 k_bp_window k_bp_groups k_bp_resolve" bash scripts/ncu_cfg.sh
 CFG=cfg2 TAG=$TAG KERNELS="k_scan_packed16 k_bp_window" bash scripts/ncu_cfg.sh
 CFG=cfg4 TAG=$TAG bash scripts/ncu_incontext.sh
-bash scripts/sanitize.sh > /dev/null 2>&1
 timeout 900 python scripts/ingest_bench.py > gpurun_out/ingest.json 2> gpurun_out/ingest.err
 du -sh gpurun_out
