@@ -107,11 +107,7 @@ int vate_mark_elapsed(vate_pool* p, int id0, int id1, double* ms);
  * (exact), 0 recomputes every g0 by a full gather. */
 enum vate_option { VATE_OPT_G0 = 0, VATE_OPT_INCREMENTAL = 1, VATE_OPT_SCAN_FILTER = 2,
                    VATE_OPT_CONCURRENT = 3, VATE_OPT_INC_SORT = 4, VATE_OPT_FUSE_SWEEP = 5,
-                   VATE_OPT_DEFERRED = 6, VATE_OPT_BITPLANE = 7, VATE_OPT_L2_KEEP = 8,
-                   VATE_OPT_DUE_LATE = 9 };
-/* VATE_OPT_DUE_LATE (default 0): a bit-plane pool's two due blocks of the
- * fused advance fork behind the window pass (1, beside the next scan) instead
- * of beside it (0). */
+                   VATE_OPT_DEFERRED = 6, VATE_OPT_BITPLANE = 7, VATE_OPT_L2_KEEP = 8 };
 /* VATE_OPT_L2_KEEP: -1 auto (default: on for deferred pools), 0 off, 1 on --
  * the scan's registry sector loads, stamps and marks carry the L2 evict_last
  * policy so the table and the marks outlive the slice's streaming passes. */

@@ -678,7 +678,8 @@ int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
     // ring slots up to this epoch and write only cells, which the pass does
     // not touch); bp_wait_aux orders every later cell access after them.
     // cfg 4: 0.183 -> 0.169 ms per slice (profiles/r02l_ab_bp_aux.txt); beside
-    // the next slice's scan instead they slowed both down (0.240 -> 0.268)
+    // the next slice's scan instead they slowed both down (0.240 -> 0.268; again
+    // at the L2-hint scan: 0.136 -> 0.172, profiles/r02g_ab_due_late.txt)
     if (p->adv_pending) return set_error(VATE_EVALUE, "previous advance not collected");
     if (!p->ev_bp) VATE_CUDA(cudaEventCreateWithFlags(&p->ev_bp, cudaEventDisableTiming));
     if (!p->ev_bp_fork) VATE_CUDA(cudaEventCreateWithFlags(&p->ev_bp_fork, cudaEventDisableTiming));
@@ -700,8 +701,7 @@ int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
     p->bp_join = true;
     return VATE_OK;
   };
-  const bool due_late = p->opt_due_late == 1;
-  if (fused_advance && !due_late) {
+  if (fused_advance) {
     rc = launch_due();
     if (rc) return rc;
   }
@@ -714,10 +714,6 @@ int bp_window(vate_pool* p, int k_prime, bool with_delta, bool fused_advance) {
               fold ? p->bp_P.as<uint32_t>() : nullptr, p->bitmap.as<uint32_t>(), nwords,
               p->L.size, p->d_ctr + C_P, D, pub);
   if (fold) p->bp_folded = true;
-  if (fused_advance && due_late) {  // forked behind the pass: beside the next scan
-    rc = launch_due();
-    if (rc) return rc;
-  }
   if (fused_advance) return bp_next_epoch(p);
   return VATE_OK;
 }

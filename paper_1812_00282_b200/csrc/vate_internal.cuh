@@ -475,7 +475,6 @@ struct vate_pool {
   // options
   int opt_g0 = 0;
   int opt_inc = 1;            // incremental g0 through the inverse index
-  int opt_due_late = 0;      // bit-plane due blocks forked behind the window pass (1) or beside it (0)
   int opt_l2_keep = -1;      // L2 evict_last on registry + marks in the scan: -1 auto, 0, 1
   int opt_scan_check = -1;   // registry-stamp filter: -1 auto, 0 off, 1 on
   int scan_form_used = 0;     // the form the last packed scan ran (auto resolved)

@@ -1379,10 +1379,6 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value) {
     p->opt_concurrent = (int)value;
     return VATE_OK;
   }
-  if (option == VATE_OPT_DUE_LATE && (value == 0 || value == 1)) {
-    p->opt_due_late = (int)value;
-    return VATE_OK;
-  }
   if (option == VATE_OPT_L2_KEEP && value >= -1 && value <= 1) {
     p->opt_l2_keep = (int)value;
     return VATE_OK;

@@ -271,13 +271,13 @@ class _DevicePool:
         return n.value
 
     OPTIONS = ("g0_kernel", "incremental", "scan_filter", "concurrent", "inc_sort",
-               "fuse_sweep", "deferred", "bitplane", "l2_keep", "due_late")
+               "fuse_sweep", "deferred", "bitplane", "l2_keep")
 
     def set_option(self, option: str, value: int) -> None:
         """Tuning switches (include/vate.h enum vate_option): 'g0_kernel' (0 auto,
         1 gather, 2 smem), 'incremental' (0/1), 'scan_filter' (-1 auto, 0, 1),
         'concurrent', 'inc_sort', 'fuse_sweep' (0/1), 'deferred' (-1 auto, 0, 1),
-        'bitplane' (-1 auto, 0, 1), 'l2_keep' (-1 auto, 0, 1), 'due_late' (0/1).
+        'bitplane' (-1 auto, 0, 1), 'l2_keep' (-1 auto, 0, 1).
         Every setting leaves identical results."""
         check(lib.vate_pool_set_option(self._h, self.OPTIONS.index(option), int(value)))
 
