@@ -33,6 +33,10 @@ def test_bench_line_contract_cfg1():
     assert d["gpu_launches"] > 0 and d["roofline"]["peak"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 8 * d["config"]["packets_per_slice_per_gpu"]
     assert "cpu_baseline" in d and d["cpu_baseline"]["kind"] == "port"
+    # the PCIe ceiling beside e2e: bare pinned copies of the step's H2D + D2H bytes
+    pcie = d["e2e"]["pcie"]
+    assert pcie["h2d_gbs"] > 0 and pcie["d2h_gbs"] > 0 and pcie["ceiling_value"] > 0
+    assert abs(pcie["frac"] - d["e2e"]["value"] / pcie["ceiling_value"]) < 1e-9
 
 
 @pytest.mark.timeout(600)
