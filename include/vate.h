@@ -140,6 +140,8 @@ int vate_pool_set_option(vate_pool* p, int option, int64_t value);
 int vate_pool_inc_stats(vate_pool* p, uint64_t out[11]);
 /* active-set ordering work: [full radix sorts, incremental merges, reuses] */
 int vate_pool_sort_stats(const vate_pool* p, uint64_t out[3]);
+/* key sorts of the active set (radix): calls, keys sorted in total, the largest */
+int vate_pool_sort_sizes(const vate_pool* p, uint64_t out[3]);
 
 /* cudaProfilerStart/Stop, so `ncu --profile-from-start off` captures exactly a
  * timed region (bench.py with VATE_PROFILE_REGION=1). */

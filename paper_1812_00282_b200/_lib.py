@@ -80,6 +80,7 @@ _SIGS = {
     "vate_pool_set_option": ([_p, _int, _i64], _int),
     "vate_pool_inc_stats": ([_p, _pu64], _int),
     "vate_pool_sort_stats": ([_p, _pu64], _int),
+    "vate_pool_sort_sizes": ([_p, _pu64], _int),
     "vate_pool_timeline": ([_p, _p, _u64, _pu64], _int),
     "vate_profiler": ([_int], _int),
     "vate_mark": ([_p, _int], _int),

@@ -467,7 +467,46 @@ __global__ void k_merge_new(const unsigned long long* __restrict__ old, uint64_t
   }
 }
 
+// Small sorts (the slice's arrivals / departures, typically a few hundred
+// keys): one CTA, a bitonic network in shared memory -- one launch instead of
+// the radix sort's histogram + digit passes (~20 us of launch-bound work each).
+constexpr uint32_t kSmallSort = 4096;
+
+__global__ void __launch_bounds__(512) k_sort_small(const unsigned long long* __restrict__ in,
+                                                    unsigned long long* __restrict__ out,
+                                                    uint32_t n, uint32_t np2) {
+  extern __shared__ unsigned long long sk[];
+  for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x) sk[i] = i < n ? in[i] : ~0ull;
+  __syncthreads();
+  for (uint32_t k = 2; k <= np2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long a = sk[i], b = sk[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            sk[i] = b;
+            sk[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = sk[i];
+}
+
 static int sort_keys(vate_pool* p, uint64_t* in, uint64_t* out, uint64_t n, int end_bit) {
+  p->sort_keys_n += n;
+  p->sort_calls++;
+  p->sort_max_n = std::max<uint64_t>(p->sort_max_n, n);
+  if (n <= kSmallSort) {
+    uint32_t np2 = 2;
+    while (np2 < n) np2 <<= 1;
+    VATE_LAUNCH(p, VATE_K_SORT, 1, std::min<uint32_t>(512u, np2 / 2), np2 * 8, k_sort_small,
+                (const unsigned long long*)in, (unsigned long long*)out, (uint32_t)n, np2);
+    return VATE_OK;
+  }
   size_t bytes = 0;
   VATE_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const unsigned long long*)in,
                                            (unsigned long long*)out, (int64_t)n, 0, end_bit,

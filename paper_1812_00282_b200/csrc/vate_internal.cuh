@@ -505,6 +505,7 @@ struct vate_pool {
   const void* sorted_owner = nullptr;  // registry whose active set hosts_sorted holds
   uint64_t sorted_n = 0;
   uint64_t sorts_skipped = 0;
+  uint64_t sort_calls = 0, sort_keys_n = 0, sort_max_n = 0;  // key sorts: calls, keys, largest
   uint64_t sorts_full = 0, sorts_incremental = 0;
   uint64_t sweeps_fused = 0;
   int opt_inc_sort = 1;       // merge membership flips into the sorted active set

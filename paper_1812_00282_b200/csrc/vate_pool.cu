@@ -1429,6 +1429,14 @@ int vate_pool_sort_stats(const vate_pool* p, uint64_t out[3]) {
   return VATE_OK;
 }
 
+int vate_pool_sort_sizes(const vate_pool* p, uint64_t out[3]) {
+  if (!p) return set_error(VATE_EVALUE, "null pool handle");
+  out[0] = p->sort_calls;
+  out[1] = p->sort_keys_n;
+  out[2] = p->sort_max_n;
+  return VATE_OK;
+}
+
 int vate_pool_inc_stats(vate_pool* p, uint64_t out[11]) {
   int rc = enter(p);
   if (rc) return rc;

@@ -294,7 +294,11 @@ class _DevicePool:
         """How the sorted active set was produced: full sorts, merges, reuses."""
         out = (C.c_uint64 * 3)()
         check(lib.vate_pool_sort_stats(self._h, out))
-        return dict(zip(("full", "incremental", "reused"), list(out)))
+        d = dict(zip(("full", "incremental", "reused"), list(out)))
+        sz = (C.c_uint64 * 3)()
+        check(lib.vate_pool_sort_sizes(self._h, sz))
+        d["key_sorts"], d["keys_sorted"], d["largest_sort"] = list(sz)
+        return d
 
     def timeline(self):
         """(kind, start ms, end ms) of every timed launch since set_timing(True)."""
