@@ -3,7 +3,7 @@
 # lines for every config and the reference arm, the launch list and ncu
 # summaries of the headline's kernels, sanitizers, ingest throughput.
 mkdir -p gpurun_out
-TAG=${TAG:-r02f}
+TAG=${TAG:-r02i}
 LONG=1 SUITE_TIMEOUT=2400 BENCH_CFGS="cfg4 cfg2 cfg3 cfg1 cfg5" bash scripts/gpu_round.sh
 timeout 900 python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
 CFG=cfg4 TAG=$TAG KERNELS="k_scan_packed16 k_bp_window k_bp_groups k_bp_resolve" bash scripts/ncu_cfg.sh
