@@ -54,3 +54,19 @@ def test_reported_fractions_are_bounded_by_their_ceilings():
     assert abs(r["achieved"] - 2000.0) < 1e-6 and abs(r["frac"] - 2000.0 / 6500.0) < 1e-9
     # 5M reads at 200 G/s + 5M reds at 100 G/s = 75 us over 100 us
     assert abs(r["l2"]["frac"] - 0.75) < 1e-9 and r["l2"]["binding"]
+
+
+def test_gather_roofline_uses_the_l2_ceiling():
+    """The full-recompute g0 gathers an L2-resident bitmap: its fraction is taken
+    against the probed L2 random-sector rate (no fraction far above 1)."""
+    import bench
+    l2 = {"random_sector_reads_G_per_s": 250.0, "random_u16_stores_G_per_s": 100.0,
+          "random_red_or_G_per_s": 100.0, "stream_read_GB_per_s": 5000.0}
+    w = bench.WORKLOADS["cfg4"]
+    hosts = 1_000_000
+    alg = hosts * (32 * w["g"] + 12)
+    r = bench._roofline("g0", {"ms_per_launch": 4.0}, alg, 6500.0, "measured", l2, 5_000_000,
+                        1 << 28, 2, w, True, "cfg4", True)
+    assert abs(r["peak"] - 8000.0) < 1e-9 and abs(r["frac"] - r["achieved"] / 8000.0) < 1e-12
+    assert abs(r["hbm_frac"] - r["achieved"] / 6500.0) < 1e-12
+    assert r["frac"] < 1.2 and r["hbm_frac"] > 1.0
