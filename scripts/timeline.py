@@ -1,5 +1,5 @@
 """Device timeline of the slice step (cfg 2 by default; TL_C/TL_K/TL_N/TL_HOSTS/TL_WARM: another
-shape): the host cost of a call, then every launch (CUDA events around each kernel) and the idle
+shape; TL_ZIPF=1: cfg 3's Zipf traffic): the host cost of a call, then every launch (CUDA events around each kernel) and the idle
 gaps between them, for a few steady-state slices."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -19,8 +19,14 @@ n = int(os.environ.get("TL_N", 5_000_000))
 HOSTS = int(os.environ.get("TL_HOSTS", 1_000_000))
 NB = 140
 bufs = torch.empty((NB, n, 2), dtype=torch.int32, device="cuda:0")
-for i in range(NB):
-    check(lib.vate_synth_packets(pool.handle, i, n, HOSTS, 0x0A000000, 0, bufs[i].data_ptr()))
+if os.environ.get("TL_ZIPF") == "1":   # cfg 3's traffic (Zipf + super-spreaders)
+    from paper_1812_00282_b200.synth import ZipfTables
+    zt = ZipfTables(0, HOSTS)
+    for i in range(NB):
+        zt.packets(pool, i, n, 0x0A000000, 0, bufs[i].data_ptr())
+else:
+    for i in range(NB):
+        check(lib.vate_synth_packets(pool.handle, i, n, HOSTS, 0x0A000000, 0, bufs[i].data_ptr()))
 lagged = os.environ.get("TL_LAGGED", "1") == "1"
 step = pipe.step_lagged if lagged else pipe.step_fast
 import time
