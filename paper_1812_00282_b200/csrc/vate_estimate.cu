@@ -30,7 +30,9 @@ __global__ void __launch_bounds__(kThreads) k_g0(const uint64_t* __restrict__ ho
                                                  const uint32_t* __restrict__ bitmap,
                                                  HashParams H, int32_t* __restrict__ g0,
                                                  const uint32_t* __restrict__ idx = nullptr,
-                                                 const unsigned long long* count = nullptr) {
+                                                 const unsigned long long* count = nullptr,
+                                                 uint64_t* __restrict__ yk = nullptr,
+                                                 int32_t* __restrict__ yg = nullptr) {
   if (LIST) n = umin64(n, *count);
   const int lane = threadIdx.x & 31;
   const int sub = lane & (LPH - 1);
@@ -65,7 +67,13 @@ __global__ void __launch_bounds__(kThreads) k_g0(const uint64_t* __restrict__ ho
     }
 #pragma unroll
     for (int o = LPH / 2; o; o >>= 1) cnt += __shfl_xor_sync(gmask, cnt, o);
-    if (sub == 0) g0[hi] = (int32_t)cnt;
+    if (sub == 0) {
+      g0[hi] = (int32_t)cnt;
+      if (LIST && yk) {  // the list's hosts and g0 in list order (the index capture)
+        yk[h] = aip;
+        yg[h] = (int32_t)cnt;
+      }
+    }
   }
 }
 
@@ -231,19 +239,19 @@ int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H,
 
 int launch_g0_list(vate_pool* p, const uint64_t* hosts_dev, const uint32_t* idx_dev,
                    const unsigned long long* count_dev, uint64_t cap, HashParams H,
-                   int32_t* g0_dev) {
+                   int32_t* g0_dev, uint64_t* yk, int32_t* yg) {
   int lph = 1;
   while (lph < 32 && (uint64_t)lph < H.g) lph <<= 1;
   // the count lives on the device: size the grid for a modest list, grid-stride beyond
   const uint32_t grid = grid_for(umin64(cap, 1u << 16) * (uint64_t)lph, kThreads, 148u * 16u);
   const uint32_t* bm = p->bitmap.as<const uint32_t>();
   switch (lph) {
-    case 1: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<1, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
-    case 2: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<2, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
-    case 4: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<4, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
-    case 8: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<8, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
-    case 16: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<16, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
-    default: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<32, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev); break;
+    case 1: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<1, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev, yk, yg); break;
+    case 2: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<2, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev, yk, yg); break;
+    case 4: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<4, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev, yk, yg); break;
+    case 8: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<8, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev, yk, yg); break;
+    case 16: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<16, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev, yk, yg); break;
+    default: VATE_LAUNCH(p, VATE_K_G0, grid, kThreads, 0, (k_g0<32, true>), hosts_dev, cap, bm, H, g0_dev, idx_dev, count_dev, yk, yg); break;
   }
   return VATE_OK;
 }

@@ -125,21 +125,6 @@ __global__ void k_inc_lookup(const uint64_t* __restrict__ A, uint64_t n,
   }
 }
 
-// The hosts a lookup missed (positions in A) and their just-gathered g0, kept
-// so the next slice can merge them into X (their g0 matches bprev).
-__global__ void k_inc_capture(const uint64_t* __restrict__ A, const uint32_t* __restrict__ miss,
-                              const unsigned long long* nmiss, uint64_t cap,
-                              const int32_t* __restrict__ g0, uint64_t* __restrict__ yk,
-                              int32_t* __restrict__ yg) {
-  const uint64_t n = umin64(*nmiss, cap);
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += stride) {
-    const uint32_t i = miss[j];
-    yk[j] = A[i];
-    yg[j] = g0[i];
-  }
-}
-
 __device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* __restrict__ v, uint64_t n,
                                                     uint64_t key) {
   uint64_t lo = 0, hi = n;
@@ -413,13 +398,12 @@ int inc_compute_g0(vate_pool* p, const uint64_t* hosts, uint64_t n, HashParams H
                   k_inc_lookup, hosts,
                   n, I.X.as<const uint64_t>(), I.m, I.g0x.as<const int32_t>(), p->g0.as<int32_t>(),
                   I.miss.as<uint32_t>(), p->d_ctr + C_MISS);
-      if ((rc = launch_g0_list(p, hosts, I.miss.as<const uint32_t>(), p->d_ctr + C_MISS, n, H,
-                               p->g0.as<int32_t>())))
-        return rc;
+      // the misses' g0 gather also captures them (keys + g0, list order) so the
+      // next slice can merge them into X
       if ((rc = I.Ykeys.ensure(n * 8 + 8)) || (rc = I.Yg0.ensure(n * 4 + 4))) return rc;
-      VATE_LAUNCH(p, VATE_K_G0, grid_for(umin64(n, 1u << 16), kThreads, 148u * 8u), kThreads, 0,
-                  k_inc_capture, hosts, I.miss.as<const uint32_t>(), p->d_ctr + C_MISS, n,
-                  p->g0.as<const int32_t>(), I.Ykeys.as<uint64_t>(), I.Yg0.as<int32_t>());
+      if ((rc = launch_g0_list(p, hosts, I.miss.as<const uint32_t>(), p->d_ctr + C_MISS, n, H,
+                               p->g0.as<int32_t>(), I.Ykeys.as<uint64_t>(), I.Yg0.as<int32_t>())))
+        return rc;
       VATE_CUDA(cudaMemcpyAsync(p->h_ctr + C_MISS, p->d_ctr + C_MISS, 8, cudaMemcpyDeviceToHost,
                                 p->stream));
       I.lookup_pending = true;

@@ -613,7 +613,8 @@ enum Ctr { C_P = 0, C_CLEARED = 1, C_NSEL = 2, C_ERR = 3, C_DCNT = 4, C_DWORK = 
 // estimate helpers (vate_estimate.cu / vate_incremental.cu)
 int launch_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H, int32_t* g0_dev);
 int launch_g0_list(vate_pool* p, const uint64_t* hosts_dev, const uint32_t* idx_dev,
-                   const unsigned long long* count_dev, uint64_t cap, HashParams H, int32_t* g0_dev);
+                   const unsigned long long* count_dev, uint64_t cap, HashParams H, int32_t* g0_dev,
+                   uint64_t* yk = nullptr, int32_t* yg = nullptr);
 bool inc_delta_ready(vate_pool* p, uint64_t g, uint64_t cs, int kp);
 int inc_compute_g0(vate_pool* p, const uint64_t* hosts_dev, uint64_t n, HashParams H, int kp);
 int inc_apply_early(vate_pool* p, const unsigned long long* nhosts_dev, uint64_t g);
