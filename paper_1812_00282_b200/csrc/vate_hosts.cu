@@ -443,27 +443,25 @@ __device__ __forceinline__ uint64_t lower_bound_u64(const unsigned long long* a,
 // Incremental sorted-set update: new = (old \ dep) U arr, all sorted, arr and
 // old disjoint, dep a subset of old.  Every element's final rank is found by
 // binary search, so the merge is one scatter pass.
-__global__ void k_merge_old(const unsigned long long* __restrict__ old, uint64_t n_old,
-                            const unsigned long long* __restrict__ dep, uint64_t n_dep,
-                            const unsigned long long* __restrict__ arr, uint64_t n_arr,
-                            unsigned long long* __restrict__ out) {
+// Both halves in one launch: threads [0, n_old) place the old keys, the rest
+// the arrivals (one launch fewer in the churn tail).
+__global__ void k_merge_both(const unsigned long long* __restrict__ old, uint64_t n_old,
+                             const unsigned long long* __restrict__ dep, uint64_t n_dep,
+                             const unsigned long long* __restrict__ arr, uint64_t n_arr,
+                             unsigned long long* __restrict__ out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_old; i += stride) {
-    const unsigned long long x = old[i];
-    const uint64_t d = lower_bound_u64(dep, n_dep, x);
-    if (d < n_dep && dep[d] == x) continue;  // departed
-    out[i - d + lower_bound_u64(arr, n_arr, x)] = x;
-  }
-}
-
-__global__ void k_merge_new(const unsigned long long* __restrict__ old, uint64_t n_old,
-                            const unsigned long long* __restrict__ dep, uint64_t n_dep,
-                            const unsigned long long* __restrict__ arr, uint64_t n_arr,
-                            unsigned long long* __restrict__ out) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_arr; j += stride) {
-    const unsigned long long y = arr[j];
-    out[j + lower_bound_u64(old, n_old, y) - lower_bound_u64(dep, n_dep, y)] = y;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_old + n_arr;
+       i += stride) {
+    if (i < n_old) {
+      const unsigned long long x = old[i];
+      const uint64_t d = lower_bound_u64(dep, n_dep, x);
+      if (d < n_dep && dep[d] == x) continue;  // departed
+      out[i - d + lower_bound_u64(arr, n_arr, x)] = x;
+    } else {
+      const uint64_t j = i - n_old;
+      const unsigned long long y = arr[j];
+      out[j + lower_bound_u64(old, n_old, y) - lower_bound_u64(dep, n_dep, y)] = y;
+    }
   }
 }
 
@@ -472,9 +470,17 @@ __global__ void k_merge_new(const unsigned long long* __restrict__ old, uint64_t
 // the radix sort's histogram + digit passes (~20 us of launch-bound work each).
 constexpr uint32_t kSmallSort = 4096;
 
-__global__ void __launch_bounds__(512) k_sort_small(const unsigned long long* __restrict__ in,
-                                                    unsigned long long* __restrict__ out,
-                                                    uint32_t n, uint32_t np2) {
+struct SmallSort {
+  const unsigned long long* in;
+  unsigned long long* out;
+  uint32_t n, np2;
+};
+
+__global__ void __launch_bounds__(512) k_sort_small(SmallSort a, SmallSort b) {
+  const SmallSort& x = blockIdx.x == 0 ? a : b;
+  const unsigned long long* __restrict__ in = x.in;
+  unsigned long long* __restrict__ out = x.out;
+  const uint32_t n = x.n, np2 = x.np2;
   extern __shared__ unsigned long long sk[];
   for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x) sk[i] = i < n ? in[i] : ~0ull;
   __syncthreads();
@@ -503,8 +509,8 @@ static int sort_keys(vate_pool* p, uint64_t* in, uint64_t* out, uint64_t n, int 
   if (n <= kSmallSort) {
     uint32_t np2 = 2;
     while (np2 < n) np2 <<= 1;
-    VATE_LAUNCH(p, VATE_K_SORT, 1, std::min<uint32_t>(512u, np2 / 2), np2 * 8, k_sort_small,
-                (const unsigned long long*)in, (unsigned long long*)out, (uint32_t)n, np2);
+    const SmallSort a{(const unsigned long long*)in, (unsigned long long*)out, (uint32_t)n, np2};
+    VATE_LAUNCH(p, VATE_K_SORT, 1, std::min<uint32_t>(512u, np2 / 2), np2 * 8, k_sort_small, a, a);
     return VATE_OK;
   }
   size_t bytes = 0;
@@ -673,25 +679,35 @@ int hosts_active_finish(vate_hosts* h, int64_t t, int k_prime, uint64_t** keys_d
     unsigned long long* dep = arr + h->flip_cap;
     unsigned long long* arr_s = dep + h->flip_cap;
     unsigned long long* dep_s = arr_s + h->flip_cap;
-    if (na > 1) {
-      rc = sort_keys(p, (uint64_t*)arr, (uint64_t*)arr_s, na, inc_bits);
-      if (rc) return rc;
-    } else if (na == 1) {
-      VATE_CUDA(cudaMemcpyAsync(arr_s, arr, 8, cudaMemcpyDeviceToDevice, p->stream));
-    }
-    if (nd > 1) {
-      rc = sort_keys(p, (uint64_t*)dep, (uint64_t*)dep_s, nd, inc_bits);
-      if (rc) return rc;
-    } else if (nd == 1) {
-      VATE_CUDA(cudaMemcpyAsync(dep_s, dep, 8, cudaMemcpyDeviceToDevice, p->stream));
+    if (na && nd && na <= kSmallSort && nd <= kSmallSort) {
+      // both lists in one launch (one CTA each; a single key sorts as itself)
+      uint32_t pa = 2, pd = 2;
+      while (pa < na) pa <<= 1;
+      while (pd < nd) pd <<= 1;
+      const uint32_t np2 = std::max(pa, pd);
+      p->sort_keys_n += na + nd;
+      p->sort_calls += 2;
+      p->sort_max_n = std::max<uint64_t>(p->sort_max_n, std::max(na, nd));
+      VATE_LAUNCH(p, VATE_K_SORT, 2, std::min<uint32_t>(512u, np2 / 2), np2 * 8, k_sort_small,
+                  SmallSort{arr, arr_s, (uint32_t)na, pa}, SmallSort{dep, dep_s, (uint32_t)nd, pd});
+    } else {
+      if (na > 1) {
+        rc = sort_keys(p, (uint64_t*)arr, (uint64_t*)arr_s, na, inc_bits);
+        if (rc) return rc;
+      } else if (na == 1) {
+        VATE_CUDA(cudaMemcpyAsync(arr_s, arr, 8, cudaMemcpyDeviceToDevice, p->stream));
+      }
+      if (nd > 1) {
+        rc = sort_keys(p, (uint64_t*)dep, (uint64_t*)dep_s, nd, inc_bits);
+        if (rc) return rc;
+      } else if (nd == 1) {
+        VATE_CUDA(cudaMemcpyAsync(dep_s, dep, 8, cudaMemcpyDeviceToDevice, p->stream));
+      }
     }
     const auto* old = p->hosts_sorted.as<const unsigned long long>();
     auto* out = p->hosts_tmp.as<unsigned long long>();
-    VATE_LAUNCH(p, VATE_K_SORT, grid_for(p->sorted_n, 256, 148u * 16u), 256, 0, k_merge_old, old,
-                p->sorted_n, dep_s, nd, arr_s, na, out);
-    if (na)
-      VATE_LAUNCH(p, VATE_K_SORT, grid_for(na, 256, 148u * 16u), 256, 0, k_merge_new, old,
-                  p->sorted_n, dep_s, nd, arr_s, na, out);
+    VATE_LAUNCH(p, VATE_K_SORT, grid_for(p->sorted_n + na, 256, 148u * 16u), 256, 0,
+                k_merge_both, old, p->sorted_n, dep_s, nd, arr_s, na, out);
     std::swap(p->hosts_sorted.ptr, p->hosts_tmp.ptr);
     std::swap(p->hosts_sorted.bytes, p->hosts_tmp.bytes);
     *keys_dev = p->hosts_sorted.as<uint64_t>();
